@@ -1,0 +1,506 @@
+#!/usr/bin/env python
+"""SAMO step benchmark (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload gpt-2.7b] [--sparsity 0.9]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N   (N > 1)
+    python bench.py --impl reference ...      (the reference's CPU implementation)
+
+One step = one pass of the SAMO per-step parameter-state path over one batch of
+synthetic dense gradients: K1 gather+unscale+cast -> (NCCL allreduce of the
+compressed fp32 gradient when N > 1) -> K23 Adam + downcast + expand.  Every
+rank holds the full replicated compressed state (data parallelism), so the
+per-GPU work is fixed as N grows ("scaling": "weak") and `value` is
+N * phi / t_step (dense parameters stepped per second, whole job).
+
+Rank 0 prints ONE JSON line.  All timing is CUDA events on the launching
+stream; multi-GPU times are the max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "SAMO step params/sec (gather+allreduce+Adam+expand); HBM & bus GB/s vs peak"
+UNIT = "params/s"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["samo", "reference"], default="samo")
+    ap.add_argument("--workload", default="gpt-2.7b")
+    ap.add_argument("--sparsity", type=float, default=0.9)
+    ap.add_argument("--tile", type=int, default=0, help="dense elements per tile (0 = default)")
+    ap.add_argument("--seed", type=int, default=1234)
+    ap.add_argument("--e2e-steps", type=int, default=0, help="0 = min(steps, 10)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-blocks", type=int, default=0, help="GPT blocks in the CPU sample")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/CPU legs)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# helpers
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "src": "measured"}
+    return {"hbm_gbs": 6650.0, "src": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: str):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", self.gpu, f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def gpt_blocks_of(wl):
+    """Indices of tensors grouped per transformer block (for CPU samples)."""
+    blocks = {}
+    for i, t in enumerate(wl.tensors):
+        key = t.name.split(".")[0] if t.name.startswith("h") else "_other"
+        blocks.setdefault(key, []).append(i)
+    return [v for k, v in blocks.items() if k != "_other"] or [list(range(len(wl.tensors)))]
+
+
+def partition(sizes, nbins):
+    """Greedy LPT partition of layer indices into nbins by size."""
+    order = sorted(range(len(sizes)), key=lambda i: -sizes[i])
+    bins = [[] for _ in range(nbins)]
+    load = [0] * nbins
+    for i in order:
+        b = load.index(min(load))
+        bins[b].append(i)
+        load[b] += sizes[i]
+    return [sorted(b) for b in bins if b]
+
+
+def cpu_reference_sample(dense_len, idx_sets, theta_sets, grad_sets, cfg_vals, reps, warm=1):
+    """Times the UNMODIFIED reference (oracle/_ref) step — sink gather +
+    SamoTrainer::optimizer_step — on host threads, layers partitioned across
+    independent trainers (SURVEY §8(d) CPU baseline).  Returns (sec/step,
+    threads)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle.oracle import Cfg, RefLib, RefSession
+    ref = RefLib()
+    cfg = Cfg(*cfg_vals)
+    ncores = len(os.sched_getaffinity(0))
+    parts = partition(list(dense_len), min(ncores, len(dense_len)))
+    sessions = []
+    for part in parts:
+        s = RefSession(ref, [dense_len[i] for i in part], [idx_sets[i] for i in part],
+                       [theta_sets[i] for i in part], cfg)
+        s.wrap([grad_sets[i] for i in part])
+        sessions.append(s)
+    with ThreadPoolExecutor(max_workers=len(sessions)) as ex:
+        for _ in range(warm):
+            list(ex.map(lambda s: s.step_wrapped(), sessions))
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            list(ex.map(lambda s: s.step_wrapped(), sessions))
+        dt = (time.perf_counter() - t0) / reps
+    for s in sessions:
+        s.close()
+    return dt, len(sessions)
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    from oracle.oracle import Oracle, RefLib, build
+    from paper_2302_05045_b200 import workloads
+    build()
+    wl = workloads.get(args.workload, args.sparsity)
+    o = Oracle()
+    ref = RefLib()
+    ncores = len(os.sched_getaffinity(0))
+    blocks = gpt_blocks_of(wl)
+    nb = args.cpu_blocks or max(1, min(len(blocks), 8, ncores // 12 or 1))
+    sel = [i for b in blocks[:nb] for i in b]
+    dense_len = [wl.tensors[i].numel for i in sel]
+    # inputs: the same counter-hash synthetic values as the GPU arm
+    vals = [o.synth_f32(0, wl.tensors[i].numel, args.seed, 2 * i, wl.tensors[i].init_bound) for i in sel]
+    from concurrent.futures import ThreadPoolExecutor
+
+    def prune_one(j):
+        rc, s = ref.magnitude_prune([vals[j]], [wl.tensors[sel[j]].prunable], wl.sparsity, 0)
+        assert rc == 0
+        return s[0]
+    with ThreadPoolExecutor(max_workers=ncores) as ex:
+        idx = list(ex.map(prune_one, range(len(sel))))
+    theta = [o.compress(v, s) for v, s in zip(vals, idx)]
+    grads = [o.synth_f16(0, wl.tensors[i].numel, args.seed + 1, 2 * i + 1, 2.0**-7, 1024.0) for i in sel]
+    del vals
+    phi_s = sum(dense_len)
+    cfg = (1e-3, 0.9, 0.999, 1e-8, 1024.0, 0.0)
+    steps = max(1, args.steps)
+    dt, threads = cpu_reference_sample(dense_len, idx, theta, grads, cfg, reps=steps,
+                                       warm=max(1, min(args.warmup, 3)))
+    value = phi_s / dt
+    sample = (f"{nb} of {len(blocks)} transformer blocks of {wl.name} "
+              f"({len(sel)} tensors, {phi_s} params) per step; layers split over {threads} "
+              f"independent reference trainers")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 * wl.phi / phi_s,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": wl.name, "sparsity": wl.sparsity,
+                                        "phi": wl.phi, "parallelism": "cpu-threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# SAMO arm
+
+def run_samo(args) -> None:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2302_05045_b200 import _abi, samo, workloads
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+
+    wl = workloads.get(args.workload, args.sparsity)
+    L = len(wl.tensors)
+    t_setup = time.perf_counter()
+
+    # -- one-time: synthetic weights, K0 magnitude prune, model state ------
+    sets, shapes = [], []
+    init_vals = []
+    for i, t in enumerate(wl.tensors):
+        v = samo.synth_uniform_f32(t.numel, args.seed, 2 * i, t.init_bound)
+        init_vals.append(v)
+        shapes.append(t.shape)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    sets = samo.magnitude_prune([samo.LayerParams(t.name, v, t.prunable)
+                                 for t, v in zip(wl.tensors, init_vals)], wl.sparsity)
+    ev1.record()
+    torch.cuda.synchronize()
+    prune_ms = ev0.elapsed_time(ev1)
+    model = samo.SamoModel.from_index_sets(sets, shapes, args.tile)
+    for l, v in enumerate(init_vals):
+        model.init_layer(l, v)
+    cfg = samo.OptimizerConfig()
+    model.set_config(cfg)
+    phi, nnz, ntiles = model.totals()
+    torch.cuda.synchronize()
+    cpu_sample = None
+    if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.profile):
+        # keep what the CPU sample needs before freeing the dense init values
+        blocks = gpt_blocks_of(wl)
+        ncores = len(os.sched_getaffinity(0))
+        nb = args.cpu_blocks or max(1, min(len(blocks), 4, ncores // 16 or 1))
+        sel = [i for b in blocks[:nb] for i in b]
+        cpu_sample = {"sel": sel, "nb": nb, "nblocks": len(blocks),
+                      "idx": [sets[i].indices.cpu().numpy().view(np.uint32) for i in sel],
+                      "theta": [model.read(i, "theta32").cpu().numpy() for i in sel]}
+    del init_vals, sets
+    torch.cuda.empty_cache()
+
+    # -- dense binary16 gradients: one flat arena, 256-byte aligned segments --
+    offs, off = [], 0
+    for t in wl.tensors:
+        offs.append(off)
+        off += (t.numel + 127) // 128 * 128
+    grad_arena = torch.empty(off, dtype=torch.float16, device=dev)
+    grads = []
+    for i, t in enumerate(wl.tensors):
+        g = grad_arena[offs[i]:offs[i] + t.numel]
+        samo.synth_uniform_f16(t.numel, args.seed + 1 + rank, 2 * i + 1, 2.0**-7, 1024.0, out=g)
+        grads.append(g)
+    model.set_grads(grads)
+
+    comm = None
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            uid.copy_(torch.tensor(list(samo.Communicator.unique_id()), dtype=torch.uint8))
+        dist.broadcast(uid, 0)
+        comm = samo.Communicator(bytes(uid.cpu().tolist()), world, rank)
+        model.attach_comm(comm)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+
+    # -- warm-up (graph path: also validates the captured step) --------------
+    for _ in range(max(0, args.warmup)):
+        model.step(graph=True)
+    torch.cuda.synchronize()
+
+    # -- timed region: staged step with events between the stages -----------
+    K = max(1, args.steps)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    gpu_name = torch.cuda.get_device_properties(dev).name
+    smi_index = os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local] \
+        if os.environ.get("CUDA_VISIBLE_DEVICES") else str(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = samo.kernel_launch_count()
+    with ClockSampler(smi_index) as clk:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for s in range(K):
+            e = evs[s]
+            e[0].record()
+            model.gather()
+            e[1].record()
+            model.exchange()
+            e[2].record()
+            model.update()
+            e[3].record()
+        t1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        # keep sampling a little longer so short regions still get clock samples
+        if len(clk.lines) < 3:
+            time.sleep(0.35)
+    launches = samo.kernel_launch_count() - launches0
+    total_ms = t0.elapsed_time(t1)
+    k1 = [e[0].elapsed_time(e[1]) for e in evs]
+    ar = [e[1].elapsed_time(e[2]) for e in evs]
+    k23 = [e[2].elapsed_time(e[3]) for e in evs]
+    if world > 1:
+        tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_step = total_ms / K
+    rec = model.step_record()
+    value = world * phi / (ms_step * 1e-3)
+
+    pk = peaks()
+    bytes_k1 = 2 * phi + 8 * nnz
+    bytes_k23 = 2 * phi + 32 * nnz
+    k1_ms = statistics.mean(k1)
+    k23_ms = statistics.mean(k23)
+    ar_ms = statistics.mean(ar)
+    kern = {
+        "K1_gather_unscale": {"ms": k1_ms, "bytes": bytes_k1,
+                              "GBps": bytes_k1 / (k1_ms * 1e-3) / 1e9},
+        "K23_adam_downcast_expand": {"ms": k23_ms, "bytes": bytes_k23,
+                                     "GBps": bytes_k23 / (k23_ms * 1e-3) / 1e9},
+    }
+    for v in kern.values():
+        v["frac"] = v["GBps"] / pk["hbm_gbs"]
+    if world > 1:
+        msg = 4 * (nnz + 1)
+        kern["allreduce"] = {"ms": ar_ms, "bytes": msg, "algbw_GBps": msg / (ar_ms * 1e-3) / 1e9,
+                             "busbw_GBps": msg * 2 * (world - 1) / world / (ar_ms * 1e-3) / 1e9,
+                             "busbw_frac_of_900": msg * 2 * (world - 1) / world / (ar_ms * 1e-3) / 900e9}
+    dom = "K23_adam_downcast_expand" if k23_ms >= k1_ms else "K1_gather_unscale"
+    traffic = None
+    tp = ROOT / "profiles" / "traffic.json"
+    if tp.exists():
+        try:
+            traffic = json.loads(tp.read_text()).get(wl.name, {}).get(dom)
+        except (ValueError, AttributeError):
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["GBps"], "peak": pk["hbm_gbs"],
+                "peak_src": pk["src"], "unit": "GB/s", "frac": kern[dom]["frac"], "traffic": traffic,
+                "algorithmic_bytes_per_launch": kern[dom]["bytes"],
+                "step_bytes": bytes_k1 + bytes_k23,
+                "step_frac": (bytes_k1 + bytes_k23) / ((k1_ms + k23_ms) * 1e-3) / 1e9 / pk["hbm_gbs"]}
+
+    # -- e2e: public API with HOST buffers (pinned), copies inside the region --
+    e2e = None
+    if not (args.no_e2e or args.profile):
+        E = args.e2e_steps or min(K, 10)
+        host = torch.empty(off, dtype=torch.float16, pin_memory=True)
+        host.copy_(grad_arena)  # this rank's synthetic gradients, staged on the host
+        dbuf = [grad_arena, torch.empty_like(grad_arena)]
+        dgrads = [[d[offs[i]:offs[i] + t.numel] for i, t in enumerate(wl.tensors)] for d in dbuf]
+        rec_host = torch.empty(32, dtype=torch.uint8, pin_memory=True)
+        copy_stream = torch.cuda.Stream(device=dev)
+        h2d_done = [torch.cuda.Event() for _ in range(2)]
+        consumed = [torch.cuda.Event() for _ in range(2)]
+        for c in consumed:
+            c.record(stream)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+
+        def h2d(s):
+            b = s % 2
+            with torch.cuda.stream(copy_stream):
+                copy_stream.wait_event(consumed[b])
+                dbuf[b].copy_(host, non_blocking=True)
+                h2d_done[b].record(copy_stream)
+        h2d(0)
+        for s in range(E):
+            if s + 1 < E:
+                h2d(s + 1)
+            b = s % 2
+            stream.wait_event(h2d_done[b])
+            model.set_grads(dgrads[b])
+            model.gather()
+            consumed[b].record(stream)
+            model.exchange()
+            model.update()
+            _abi.call("samo_model_step_record_async", model.handle, C.c_void_p(rec_host.data_ptr()),
+                      C.c_void_p(stream.cuda_stream))
+        a1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = a0.elapsed_time(a1)
+        if world > 1:
+            tt = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_ms = float(tt.item())
+        e2e = {"value": world * phi / (e2e_ms / E * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(host.numel() * 2), "d2h_bytes_per_step": 32,
+               "steps": E, "ms_per_step": e2e_ms / E,
+               "note": "dense fp16 grads H2D from pinned host (double-buffered against the "
+                       "previous step) + step + D2H of the step record (grad norm, skip flag)"}
+        del host, dbuf, dgrads
+
+    # -- CPU baseline: the reference on this host, bounded sample ------------
+    cpu = None
+    if cpu_sample is not None:
+        sel = cpu_sample["sel"]
+        dl = [wl.tensors[i].numel for i in sel]
+        gr = [grads[i].cpu().numpy().view(np.uint16) for i in sel]
+        cfgv = (cfg.learning_rate, cfg.beta1, cfg.beta2, cfg.epsilon, cfg.loss_scale, cfg.weight_decay)
+        try:
+            dt, threads = cpu_reference_sample(dl, cpu_sample["idx"], cpu_sample["theta"], gr, cfgv,
+                                               reps=3, warm=1)
+            phi_s = sum(dl)
+            cpu = {"value": phi_s / dt, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"{cpu_sample['nb']} of {cpu_sample['nblocks']} transformer blocks "
+                             f"({len(sel)} tensors, {phi_s} params), sink gather + "
+                             f"SamoTrainer::optimizer_step of the unmodified reference, layers "
+                             f"split over {threads} host threads, 3 reps"}
+        except Exception as ex:  # the baseline must not kill the GPU measurement
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                   "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (counter-hash weights and loss-scaled fp16 grads; K0-pruned mask)",
+            "config": {"workload": wl.name, "description": wl.description,
+                       "sparsity": wl.sparsity, "phi": phi, "nnz": nnz, "tensors": L,
+                       "tiles": ntiles, "parallelism": f"dp{world}",
+                       "l2": "inputs (>= 16 GB per step) are larger than L2; no flush needed",
+                       "gpu": gpu_name},
+            "gpu_launches": int(launches),
+            "roofline": roofline,
+            "kernels": kern,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "step_record": {"t": int(rec.t), "skipped": int(rec.skipped_steps),
+                            "grad_norm": float(rec.grad_norm)},
+            "setup": {"seconds": setup_s, "k0_prune_ms": prune_ms,
+                      "model_device_bytes": model.device_bytes()},
+        }
+        print(json.dumps(line), flush=True)
+    model.close()
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_samo(args)
+
+
+if __name__ == "__main__":
+    main()

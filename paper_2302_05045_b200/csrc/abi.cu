@@ -1,0 +1,888 @@
+// abi.cu — the C ABI (include/samo_cuda.h): argument checks with the
+// reference's error taxonomy, the plain API-parity entry points, the model
+// state (flat device arenas + tile table + device scalars), the step driver
+// (gather -> NCCL exchange -> update, optionally as one CUDA graph) and the
+// NCCL communicator.
+#include <nccl.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstddef>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+// ---------------------------------------------------------------------------
+// Status plumbing.
+
+namespace samo_dev {
+
+static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+void set_error(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+int fail(int status, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return status;
+}
+
+int cuda_fail(cudaError_t err, const char* what) {
+  return fail(err == cudaErrorMemoryAllocation ? SAMO_E_NOMEM : SAMO_E_CUDA, "%s: %s (%s)", what,
+              cudaGetErrorString(err), cudaGetErrorName(err));
+}
+
+void note_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+int device_ok() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return fail(SAMO_E_CUDA, "no CUDA device available (the SAMO path has no CPU fallback)");
+  }
+  return SAMO_OK;
+}
+
+int num_sms() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+}  // namespace samo_dev
+
+using namespace samo_dev;
+
+#define SAMO_TRY(expr)             \
+  do {                             \
+    int rc_ = (expr);              \
+    if (rc_ != SAMO_OK) return rc_; \
+  } while (0)
+
+static int clear_ok() {
+  g_last_error.clear();
+  return SAMO_OK;
+}
+
+extern "C" {
+
+int samo_abi_version(void) { return SAMO_ABI_VERSION; }
+
+const char* samo_status_string(int status) {
+  switch (status) {
+    case SAMO_OK: return "ok";
+    case SAMO_E_DIMENSION: return "DimensionError";
+    case SAMO_E_PARAMETER: return "ParameterError";
+    case SAMO_E_INDEX: return "IndexError";
+    case SAMO_E_STATE: return "StateError";
+    case SAMO_E_CONFIG: return "ConfigError";
+    case SAMO_E_CUDA: return "CudaError";
+    case SAMO_E_NCCL: return "NcclError";
+    case SAMO_E_NOMEM: return "OutOfDeviceMemory";
+    default: return "unknown";
+  }
+}
+
+const char* samo_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t samo_kernel_launch_count(void) { return g_launches.load(); }
+
+// ---------------------------------------------------------------------------
+// half.hpp
+
+int samo_float_to_half(const float* in, uint16_t* out, uint64_t n, samo_stream_t stream) {
+  SAMO_TRY(device_ok());
+  if (n && (!in || !out)) return fail(SAMO_E_PARAMETER, "float_to_half: null pointer");
+  SAMO_TRY(launch_f2h(in, out, n, as_stream(stream)));
+  return clear_ok();
+}
+
+int samo_half_to_float(const uint16_t* in, float* out, uint64_t n, samo_stream_t stream) {
+  SAMO_TRY(device_ok());
+  if (n && (!in || !out)) return fail(SAMO_E_PARAMETER, "half_to_float: null pointer");
+  SAMO_TRY(launch_h2f(in, out, n, as_stream(stream)));
+  return clear_ok();
+}
+
+// ---------------------------------------------------------------------------
+// store.hpp: compress / expand
+
+}  // extern "C"
+
+template <typename T>
+static int compress_impl(const T* dense, uint64_t dense_len, const uint32_t* idx, uint64_t n,
+                         uint64_t ind_dense_len, T* out, samo_stream_t stream) {
+  SAMO_TRY(device_ok());
+  if (dense_len != ind_dense_len)  // store.hpp:60-62
+    return fail(SAMO_E_DIMENSION, "compress: dense length does not match index set");
+  if (n && (!dense || !idx || !out)) return fail(SAMO_E_PARAMETER, "compress: null pointer");
+  SAMO_TRY(launch_compress<T>(dense, idx, n, out, as_stream(stream)));
+  return clear_ok();
+}
+
+extern "C" {
+
+int samo_compress_u16(const uint16_t* dense, uint64_t dense_len, const uint32_t* idx, uint64_t n,
+                      uint64_t ind_dense_len, uint16_t* out, samo_stream_t stream) {
+  return compress_impl<uint16_t>(dense, dense_len, idx, n, ind_dense_len, out, stream);
+}
+
+int samo_compress_u32(const uint32_t* dense, uint64_t dense_len, const uint32_t* idx, uint64_t n,
+                      uint64_t ind_dense_len, uint32_t* out, samo_stream_t stream) {
+  return compress_impl<uint32_t>(dense, dense_len, idx, n, ind_dense_len, out, stream);
+}
+
+}  // extern "C"
+
+// Single-layer tile plan in stream-ordered scratch: tile table + a one-entry
+// layer table whose output pointer is `out`.
+struct ScratchPlan {
+  SamoTile* tiles = nullptr;
+  SamoLayerDev* layer = nullptr;
+  uint64_t* k_off = nullptr;
+  uint32_t ntiles = 0;
+  void* block = nullptr;
+  cudaStream_t s = nullptr;
+  ~ScratchPlan() {
+    if (block) cudaFreeAsync(block, s);
+  }
+};
+
+static int make_plan(ScratchPlan& p, const uint32_t* idx, uint64_t n, uint64_t dense_len, void* out,
+                     uint32_t tile_elems, cudaStream_t s) {
+  p.s = s;
+  const uint64_t ntiles = (dense_len + tile_elems - 1) / tile_elems;
+  if (ntiles > 0xFFFFFFFFull) return fail(SAMO_E_PARAMETER, "too many tiles");
+  p.ntiles = static_cast<uint32_t>(ntiles);
+  const size_t tiles_bytes = ntiles * sizeof(SamoTile);
+  const size_t total = tiles_bytes + sizeof(SamoLayerDev) + 2 * sizeof(uint64_t);
+  SAMO_CUDA_TRY(cudaMallocAsync(&p.block, total, s));
+  p.tiles = static_cast<SamoTile*>(p.block);
+  p.layer = reinterpret_cast<SamoLayerDev*>(static_cast<char*>(p.block) + tiles_bytes);
+  p.k_off = reinterpret_cast<uint64_t*>(p.layer + 1);
+  std::vector<SamoTile> host(ntiles);
+  for (uint64_t t = 0; t < ntiles; ++t) {
+    host[t].layer = 0;
+    host[t].dense_begin = static_cast<uint32_t>(t * tile_elems);
+    host[t].dense_count = static_cast<uint32_t>(std::min<uint64_t>(tile_elems, dense_len - t * tile_elems));
+    host[t].pad_ = 0;
+    host[t].k_begin = host[t].k_end = 0;
+  }
+  SamoLayerDev ld{};
+  ld.grad = nullptr;
+  ld.theta16 = static_cast<uint16_t*>(out);
+  ld.dense_len = dense_len;
+  ld.k_off = 0;
+  const uint64_t koff[2] = {0, n};
+  SAMO_CUDA_TRY(cudaMemcpyAsync(p.tiles, host.data(), tiles_bytes, cudaMemcpyHostToDevice, s));
+  SAMO_CUDA_TRY(cudaMemcpyAsync(p.layer, &ld, sizeof(ld), cudaMemcpyHostToDevice, s));
+  SAMO_CUDA_TRY(cudaMemcpyAsync(p.k_off, koff, sizeof(koff), cudaMemcpyHostToDevice, s));
+  SAMO_TRY(launch_tiles_fill(p.tiles, p.ntiles, p.k_off, idx, s));
+  // Pageable sources: the copies above are staged before returning, but keep
+  // the host vectors alive until the stream has consumed them.
+  SAMO_CUDA_TRY(cudaStreamSynchronize(s));
+  return SAMO_OK;
+}
+
+constexpr uint32_t kDefaultTile = 8192;
+
+template <typename T>
+static int expand_impl(const T* values, uint64_t n_values, const uint32_t* idx, uint64_t n,
+                       uint64_t ind_dense_len, uint64_t shape_numel, T* dense_out,
+                       samo_stream_t stream) {
+  SAMO_TRY(device_ok());
+  if (n_values != n)  // store.hpp:75-77
+    return fail(SAMO_E_DIMENSION, "expand: value count does not match index set");
+  if (shape_numel != ind_dense_len)  // store.hpp:78-80
+    return fail(SAMO_E_DIMENSION, "expand: shape does not match index set dense length");
+  if (shape_numel == 0) return fail(SAMO_E_DIMENSION, "tensor extents must be positive");
+  if (!dense_out || (n && (!values || !idx))) return fail(SAMO_E_PARAMETER, "expand: null pointer");
+  if (ind_dense_len > 0xFFFFFFFFull)
+    return fail(SAMO_E_PARAMETER, "layer too large for 32-bit indices");
+  cudaStream_t s = as_stream(stream);
+  ScratchPlan plan;
+  SAMO_TRY(make_plan(plan, idx, n, ind_dense_len, dense_out, kDefaultTile, s));
+  ExpandArgs a{};
+  a.tiles = plan.tiles;
+  a.ntiles = plan.ntiles;
+  a.tile_elems = kDefaultTile;
+  a.layers = plan.layer;
+  a.idx = idx;
+  a.values = values;
+  a.use_bulk = (reinterpret_cast<uintptr_t>(dense_out) % 16) == 0;
+  SAMO_TRY((launch_expand<kModeValues, T>(a, 0, s)));
+  return clear_ok();
+}
+
+extern "C" {
+
+int samo_expand_u16(const uint16_t* values, uint64_t n_values, const uint32_t* idx, uint64_t n,
+                    uint64_t ind_dense_len, uint64_t shape_numel, uint16_t* dense_out,
+                    samo_stream_t stream) {
+  return expand_impl<uint16_t>(values, n_values, idx, n, ind_dense_len, shape_numel, dense_out,
+                               stream);
+}
+
+int samo_expand_u32(const uint32_t* values, uint64_t n_values, const uint32_t* idx, uint64_t n,
+                    uint64_t ind_dense_len, uint64_t shape_numel, uint32_t* dense_out,
+                    samo_stream_t stream) {
+  return expand_impl<uint32_t>(values, n_values, idx, n, ind_dense_len, shape_numel, dense_out,
+                               stream);
+}
+
+int samo_downcast_expand(const float* theta32, uint64_t n, const uint32_t* idx, uint64_t dense_len,
+                         uint16_t* theta16_dense, samo_stream_t stream) {
+  SAMO_TRY(device_ok());
+  if (dense_len == 0) return fail(SAMO_E_DIMENSION, "tensor extents must be positive");
+  if (n > dense_len) return fail(SAMO_E_DIMENSION, "expand: more values than dense slots");
+  if (!theta16_dense || (n && (!theta32 || !idx)))
+    return fail(SAMO_E_PARAMETER, "downcast_expand: null pointer");
+  if (dense_len > 0xFFFFFFFFull) return fail(SAMO_E_PARAMETER, "layer too large for 32-bit indices");
+  cudaStream_t s = as_stream(stream);
+  ScratchPlan plan;
+  SAMO_TRY(make_plan(plan, idx, n, dense_len, theta16_dense, kDefaultTile, s));
+  ExpandArgs a{};
+  a.tiles = plan.tiles;
+  a.ntiles = plan.ntiles;
+  a.tile_elems = kDefaultTile;
+  a.layers = plan.layer;
+  a.idx = idx;
+  a.theta = const_cast<float*>(theta32);
+  a.use_bulk = (reinterpret_cast<uintptr_t>(theta16_dense) % 16) == 0;
+  SAMO_TRY((launch_expand<kModeDowncast, uint16_t>(a, 0, s)));
+  return clear_ok();
+}
+
+// ---------------------------------------------------------------------------
+// train.hpp: OptimizerConfig + adam_update
+
+void samo_optimizer_config_default(samo_optimizer_config* cfg) {
+  if (!cfg) return;
+  cfg->learning_rate = 1e-3f;
+  cfg->beta1 = 0.9f;
+  cfg->beta2 = 0.999f;
+  cfg->epsilon = 1e-8f;
+  cfg->loss_scale = 1024.0f;
+  cfg->weight_decay = 0.0f;
+}
+
+int samo_optimizer_config_validate(const samo_optimizer_config* cfg) {
+  if (!cfg) return fail(SAMO_E_PARAMETER, "null config");
+  // train.hpp:78-86
+  if (!(cfg->beta1 >= 0.0f && cfg->beta1 < 1.0f) || !(cfg->beta2 >= 0.0f && cfg->beta2 < 1.0f))
+    return fail(SAMO_E_PARAMETER, "betas must lie in [0, 1)");
+  uint32_t bits;
+  std::memcpy(&bits, &cfg->loss_scale, 4);
+  if (!(cfg->loss_scale >= 1.0f) || (bits & 0x007FFFFFu) != 0)
+    return fail(SAMO_E_PARAMETER, "loss_scale must be a power of two >= 1");
+  return clear_ok();
+}
+
+static SamoAdamParams adam_params(const samo_optimizer_config* cfg) {
+  SamoAdamParams p;
+  p.lr = cfg->learning_rate;
+  p.beta1 = cfg->beta1;
+  p.beta2 = cfg->beta2;
+  p.eps = cfg->epsilon;
+  p.wd = cfg->weight_decay;
+  return p;
+}
+
+int samo_adam_update(float* theta, float* m, float* v, const float* g, uint64_t n,
+                     const samo_optimizer_config* cfg, float bias1, float bias2,
+                     samo_stream_t stream) {
+  SAMO_TRY(device_ok());
+  if (!cfg) return fail(SAMO_E_PARAMETER, "null config");
+  if (n && (!theta || !m || !v || !g)) return fail(SAMO_E_PARAMETER, "adam_update: null pointer");
+  SAMO_TRY(launch_adam(theta, m, v, g, n, adam_params(cfg), bias1, bias2, as_stream(stream)));
+  return clear_ok();
+}
+
+int samo_copy_async(void* dst, const void* src, uint64_t bytes, samo_stream_t stream) {
+  if (bytes == 0) return clear_ok();
+  if (!dst || !src) return fail(SAMO_E_PARAMETER, "copy: null pointer");
+  SAMO_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, as_stream(stream)));
+  return clear_ok();
+}
+
+int samo_stream_synchronize(samo_stream_t stream) {
+  SAMO_CUDA_TRY(cudaStreamSynchronize(as_stream(stream)));
+  return clear_ok();
+}
+
+// ---------------------------------------------------------------------------
+// Synthetic data
+
+int samo_synth_uniform_f32(float* out, uint64_t n, uint64_t seed, uint64_t stream_id, float bound,
+                           samo_stream_t stream) {
+  SAMO_TRY(device_ok());
+  if (n && !out) return fail(SAMO_E_PARAMETER, "synth: null pointer");
+  SAMO_TRY(launch_synth_f32(out, n, seed, stream_id, bound, as_stream(stream)));
+  return clear_ok();
+}
+
+int samo_synth_uniform_f16(uint16_t* out, uint64_t n, uint64_t seed, uint64_t stream_id, float bound,
+                           float scale, samo_stream_t stream) {
+  SAMO_TRY(device_ok());
+  if (n && !out) return fail(SAMO_E_PARAMETER, "synth: null pointer");
+  SAMO_TRY(launch_synth_f16(out, n, seed, stream_id, bound, scale, as_stream(stream)));
+  return clear_ok();
+}
+
+// ---------------------------------------------------------------------------
+// NCCL communicator
+
+}  // extern "C"
+
+struct samo_comm {
+  ncclComm_t comm = nullptr;
+  int nranks = 1;
+  int rank = 0;
+};
+
+static int nccl_fail(ncclResult_t r, const char* what) {
+  return fail(SAMO_E_NCCL, "%s: %s", what, ncclGetErrorString(r));
+}
+
+extern "C" {
+
+int samo_comm_unique_id(uint8_t id_out[SAMO_UNIQUE_ID_BYTES]) {
+  static_assert(sizeof(ncclUniqueId) == SAMO_UNIQUE_ID_BYTES, "ncclUniqueId size");
+  if (!id_out) return fail(SAMO_E_PARAMETER, "null id buffer");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+  std::memcpy(id_out, &id, sizeof(id));
+  return clear_ok();
+}
+
+int samo_comm_create(const uint8_t id[SAMO_UNIQUE_ID_BYTES], int nranks, int rank, samo_comm** out) {
+  SAMO_TRY(device_ok());
+  if (!id || !out) return fail(SAMO_E_PARAMETER, "null argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(SAMO_E_PARAMETER, "bad rank/size");
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  auto* c = new samo_comm();
+  c->nranks = nranks;
+  c->rank = rank;
+  ncclResult_t r = ncclCommInitRank(&c->comm, nranks, uid, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return nccl_fail(r, "ncclCommInitRank");
+  }
+  *out = c;
+  return clear_ok();
+}
+
+int samo_comm_destroy(samo_comm* comm) {
+  if (!comm) return clear_ok();
+  if (comm->comm) ncclCommDestroy(comm->comm);
+  delete comm;
+  return clear_ok();
+}
+
+int samo_comm_size(const samo_comm* comm) { return comm ? comm->nranks : 0; }
+
+int samo_allreduce_sum_f32(samo_comm* comm, float* buf, uint64_t n, samo_stream_t stream) {
+  if (!comm || (n && !buf)) return fail(SAMO_E_PARAMETER, "allreduce: null argument");
+  if (n == 0) return clear_ok();
+  ncclResult_t r = ncclAllReduce(buf, buf, n, ncclFloat32, ncclSum, comm->comm, as_stream(stream));
+  if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");
+  return clear_ok();
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Model state + step driver
+
+struct samo_model {
+  int nlayers = 0;
+  uint32_t tile_elems = kDefaultTile;
+  std::vector<uint64_t> dense_len, nnz, k_off, d_off;
+  std::vector<uint8_t> idx_set;
+  uint64_t phi = 0, n_tot = 0, d_tot = 0;
+  uint32_t ntiles = 0;
+  // device arenas
+  void* block = nullptr;  // one allocation for every arena/table
+  uint64_t block_bytes = 0;
+  float* theta = nullptr;
+  float* m = nullptr;
+  float* v = nullptr;
+  float* g = nullptr;          // n_tot + 1: the last slot carries the non-finite indicator
+  uint32_t* idx = nullptr;
+  uint16_t* theta16 = nullptr;
+  SamoTile* tiles = nullptr;
+  SamoLayerDev* layers_dev = nullptr;
+  uint64_t* k_off_dev = nullptr;
+  SamoStepState* st = nullptr;
+  float* norm_partials = nullptr;
+  std::vector<SamoLayerDev> layers_host;
+  std::vector<SamoTile> tiles_host;
+  samo_optimizer_config cfg{};
+  samo_comm* comm = nullptr;
+  bool finalized = false;
+  bool grads_set = false;
+  int grid_gather = 0, grid_update = 0;
+  // CUDA graph of one step
+  cudaGraphExec_t graph = nullptr;
+  samo_comm* graph_comm = nullptr;
+  uint64_t graph_kernels = 0;
+};
+
+static uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+extern "C" {
+
+int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_elems,
+                      samo_model** out) {
+  SAMO_TRY(device_ok());
+  if (!out || (nlayers > 0 && !layers)) return fail(SAMO_E_PARAMETER, "null argument");
+  if (nlayers < 0) return fail(SAMO_E_PARAMETER, "negative layer count");
+  if (tile_elems == 0) tile_elems = kDefaultTile;
+  if (tile_elems < 1024 || tile_elems > 65536 || (tile_elems & (tile_elems - 1)))
+    return fail(SAMO_E_PARAMETER, "tile_elems must be a power of two in [1024, 65536]");
+  auto* md = new samo_model();
+  md->nlayers = nlayers;
+  md->tile_elems = tile_elems;
+  md->dense_len.resize(nlayers);
+  md->nnz.resize(nlayers);
+  md->k_off.resize(nlayers + 1);
+  md->d_off.resize(nlayers);
+  md->idx_set.assign(nlayers, 0);
+  uint64_t ntiles = 0;
+  for (int l = 0; l < nlayers; ++l) {
+    const uint64_t dl = layers[l].dense_len, nz = layers[l].nnz;
+    if (dl == 0) {
+      delete md;
+      return fail(SAMO_E_DIMENSION, "tensor extents must be positive (layer %d)", l);
+    }
+    if (dl >= (1ull << 32)) {
+      delete md;
+      return fail(SAMO_E_PARAMETER, "layer too large for 32-bit indices (layer %d)", l);
+    }
+    if (nz > dl) {
+      delete md;
+      return fail(SAMO_E_DIMENSION, "layer %d keeps more indices than it has elements", l);
+    }
+    md->dense_len[l] = dl;
+    md->nnz[l] = nz;
+    md->k_off[l] = md->n_tot;
+    md->n_tot += nz;
+    md->d_off[l] = md->d_tot;
+    md->d_tot += align_up(dl, 128);  // 256-byte aligned dense segments
+    md->phi += dl;
+    ntiles += (dl + tile_elems - 1) / tile_elems;
+  }
+  md->k_off[nlayers] = md->n_tot;
+  if (ntiles > 0xFFFFFFFFull) {
+    delete md;
+    return fail(SAMO_E_PARAMETER, "too many tiles");
+  }
+  md->ntiles = static_cast<uint32_t>(ntiles);
+
+  md->grid_gather = gather_grid(tile_elems);
+  md->grid_update = expand_grid<kModeAdam, uint16_t>(tile_elems);
+  const int max_grid = std::max(md->grid_gather, md->grid_update);
+
+  // Carve one allocation.
+  const uint64_t n_al = align_up(md->n_tot, 64);
+  uint64_t off = 0;
+  auto carve = [&](uint64_t bytes) {
+    const uint64_t o = off;
+    off = align_up(off + bytes, 256);
+    return o;
+  };
+  const uint64_t o_theta = carve(n_al * 4), o_m = carve(n_al * 4), o_v = carve(n_al * 4);
+  const uint64_t o_g = carve((n_al + 64) * 4), o_idx = carve(n_al * 4);
+  const uint64_t o_t16 = carve(md->d_tot * 2), o_tiles = carve(ntiles * sizeof(SamoTile));
+  const uint64_t o_layers = carve(std::max(1, nlayers) * sizeof(SamoLayerDev));
+  const uint64_t o_koff = carve((nlayers + 1) * sizeof(uint64_t));
+  const uint64_t o_st = carve(sizeof(SamoStepState)), o_np = carve(max_grid * sizeof(float));
+  md->block_bytes = off;
+  cudaError_t e = cudaMalloc(&md->block, off);
+  if (e != cudaSuccess) {
+    delete md;
+    return cuda_fail(e, "cudaMalloc(model arenas)");
+  }
+  char* b = static_cast<char*>(md->block);
+  md->theta = reinterpret_cast<float*>(b + o_theta);
+  md->m = reinterpret_cast<float*>(b + o_m);
+  md->v = reinterpret_cast<float*>(b + o_v);
+  md->g = reinterpret_cast<float*>(b + o_g);
+  md->idx = reinterpret_cast<uint32_t*>(b + o_idx);
+  md->theta16 = reinterpret_cast<uint16_t*>(b + o_t16);
+  md->tiles = reinterpret_cast<SamoTile*>(b + o_tiles);
+  md->layers_dev = reinterpret_cast<SamoLayerDev*>(b + o_layers);
+  md->k_off_dev = reinterpret_cast<uint64_t*>(b + o_koff);
+  md->st = reinterpret_cast<SamoStepState*>(b + o_st);
+  md->norm_partials = reinterpret_cast<float*>(b + o_np);
+  e = cudaMemset(md->block, 0, off);
+  if (e != cudaSuccess) {
+    cudaFree(md->block);
+    delete md;
+    return cuda_fail(e, "cudaMemset(model arenas)");
+  }
+  SamoStepState st0{};
+  st0.beta1_pow = 1.0f;  // AdamScalars (train.hpp:320-323)
+  st0.beta2_pow = 1.0f;
+  cudaMemcpy(md->st, &st0, sizeof(st0), cudaMemcpyHostToDevice);
+
+  md->layers_host.resize(nlayers);
+  md->tiles_host.resize(ntiles);
+  uint64_t t = 0;
+  for (int l = 0; l < nlayers; ++l) {
+    md->layers_host[l].grad = nullptr;
+    md->layers_host[l].theta16 = md->theta16 + md->d_off[l];
+    md->layers_host[l].dense_len = md->dense_len[l];
+    md->layers_host[l].k_off = md->k_off[l];
+    for (uint64_t d = 0; d < md->dense_len[l]; d += tile_elems, ++t) {
+      SamoTile& td = md->tiles_host[t];
+      td.layer = static_cast<uint32_t>(l);
+      td.dense_begin = static_cast<uint32_t>(d);
+      td.dense_count = static_cast<uint32_t>(std::min<uint64_t>(tile_elems, md->dense_len[l] - d));
+      td.pad_ = 0;
+      td.k_begin = td.k_end = 0;
+    }
+  }
+  if (nlayers > 0) {
+    cudaMemcpy(md->layers_dev, md->layers_host.data(), nlayers * sizeof(SamoLayerDev),
+               cudaMemcpyHostToDevice);
+  }
+  cudaMemcpy(md->k_off_dev, md->k_off.data(), (nlayers + 1) * sizeof(uint64_t),
+             cudaMemcpyHostToDevice);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    cudaFree(md->block);
+    delete md;
+    return cuda_fail(e, "model setup");
+  }
+  samo_optimizer_config_default(&md->cfg);
+  *out = md;
+  return clear_ok();
+}
+
+int samo_model_destroy(samo_model* md) {
+  if (!md) return clear_ok();
+  if (md->graph) cudaGraphExecDestroy(md->graph);
+  if (md->block) cudaFree(md->block);
+  delete md;
+  return clear_ok();
+}
+
+int samo_model_num_layers(const samo_model* md) { return md ? md->nlayers : 0; }
+
+int samo_model_layer_view(const samo_model* md, int l, samo_layer_view* out) {
+  if (!md || !out) return fail(SAMO_E_PARAMETER, "null argument");
+  if (l < 0 || l >= md->nlayers) return fail(SAMO_E_INDEX, "layer %d out of range", l);
+  const uint64_t k = md->k_off[l];
+  out->theta16 = md->theta16 + md->d_off[l];
+  out->theta32 = md->theta + k;
+  out->adam_m = md->m + k;
+  out->adam_v = md->v + k;
+  out->grad32 = md->g + k;
+  out->indices = md->idx + k;
+  out->dense_len = md->dense_len[l];
+  out->nnz = md->nnz[l];
+  out->k_offset = k;
+  return clear_ok();
+}
+
+int samo_model_totals(const samo_model* md, uint64_t* phi, uint64_t* nnz, uint64_t* ntiles) {
+  if (!md) return fail(SAMO_E_PARAMETER, "null model");
+  if (phi) *phi = md->phi;
+  if (nnz) *nnz = md->n_tot;
+  if (ntiles) *ntiles = md->ntiles;
+  return clear_ok();
+}
+
+uint64_t samo_model_device_bytes(const samo_model* md) { return md ? md->block_bytes : 0; }
+
+int samo_model_set_indices(samo_model* md, int l, const uint32_t* idx, uint64_t n, int src_on_host,
+                           samo_stream_t stream) {
+  if (!md) return fail(SAMO_E_PARAMETER, "null model");
+  if (l < 0 || l >= md->nlayers) return fail(SAMO_E_INDEX, "layer %d out of range", l);
+  if (n != md->nnz[l]) return fail(SAMO_E_DIMENSION, "layer %d: %llu indices, expected %llu", l,
+                                   (unsigned long long)n, (unsigned long long)md->nnz[l]);
+  if (n && !idx) return fail(SAMO_E_PARAMETER, "null index pointer");
+  cudaStream_t s = as_stream(stream);
+  uint32_t* dst = md->idx + md->k_off[l];
+  if (n) {
+    SAMO_CUDA_TRY(cudaMemcpyAsync(dst, idx, n * 4,
+                                  src_on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+  }
+  // Validate on the device: strictly ascending, < dense_len.
+  uint32_t* bad = reinterpret_cast<uint32_t*>(md->norm_partials);  // scratch (idle outside a step)
+  SAMO_CUDA_TRY(cudaMemsetAsync(bad, 0, 4, s));
+  SAMO_TRY(launch_check_indices(dst, n, md->dense_len[l], bad, s));
+  uint32_t hbad = 0;
+  SAMO_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, s));
+  SAMO_CUDA_TRY(cudaStreamSynchronize(s));
+  if (hbad) return fail(SAMO_E_INDEX, "layer %d: indices must be strictly ascending and < dense_len", l);
+  md->idx_set[l] = 1;
+  md->finalized = false;
+  return clear_ok();
+}
+
+int samo_model_finalize(samo_model* md, samo_stream_t stream) {
+  if (!md) return fail(SAMO_E_PARAMETER, "null model");
+  for (int l = 0; l < md->nlayers; ++l)
+    if (!md->idx_set[l] && md->nnz[l] > 0)
+      return fail(SAMO_E_STATE, "layer %d has no index set", l);
+  cudaStream_t s = as_stream(stream);
+  if (md->ntiles) {
+    SAMO_CUDA_TRY(cudaMemcpyAsync(md->tiles, md->tiles_host.data(), md->ntiles * sizeof(SamoTile),
+                                  cudaMemcpyHostToDevice, s));
+    SAMO_TRY(launch_tiles_fill(md->tiles, md->ntiles, md->k_off_dev, md->idx, s));
+  }
+  SAMO_CUDA_TRY(cudaStreamSynchronize(s));
+  md->finalized = true;
+  if (md->graph) {
+    cudaGraphExecDestroy(md->graph);
+    md->graph = nullptr;
+  }
+  return clear_ok();
+}
+
+int samo_model_init_layer(samo_model* md, int l, const float* init, uint64_t dense_len,
+                          samo_stream_t stream) {
+  if (!md) return fail(SAMO_E_PARAMETER, "null model");
+  if (l < 0 || l >= md->nlayers) return fail(SAMO_E_INDEX, "layer %d out of range", l);
+  if (!md->finalized) return fail(SAMO_E_STATE, "init_layer requires finalize()");
+  if (dense_len != md->dense_len[l])  // compress() length check, store.hpp:60-62
+    return fail(SAMO_E_DIMENSION, "compress: dense length does not match index set");
+  if (!init) return fail(SAMO_E_PARAMETER, "null init");
+  cudaStream_t s = as_stream(stream);
+  const uint64_t k = md->k_off[l], n = md->nnz[l];
+  // theta32 = compress(init) (store.hpp:156); moments and grad32 zero (157-160)
+  SAMO_TRY(launch_compress<uint32_t>(reinterpret_cast<const uint32_t*>(init), md->idx + k, n,
+                                     reinterpret_cast<uint32_t*>(md->theta + k), s));
+  if (n) {
+    SAMO_CUDA_TRY(cudaMemsetAsync(md->m + k, 0, n * 4, s));
+    SAMO_CUDA_TRY(cudaMemsetAsync(md->v + k, 0, n * 4, s));
+    SAMO_CUDA_TRY(cudaMemsetAsync(md->g + k, 0, n * 4, s));
+  }
+  // theta16 = expand(half(theta32)) (store.hpp:162-166): this layer's tiles only.
+  uint64_t t0 = 0;
+  for (int j = 0; j < l; ++j) t0 += (md->dense_len[j] + md->tile_elems - 1) / md->tile_elems;
+  const uint64_t nt = (md->dense_len[l] + md->tile_elems - 1) / md->tile_elems;
+  ExpandArgs a{};
+  a.tiles = md->tiles + t0;
+  a.ntiles = static_cast<uint32_t>(nt);
+  a.tile_elems = md->tile_elems;
+  a.layers = md->layers_dev;
+  a.idx = md->idx;
+  a.theta = md->theta;
+  a.use_bulk = 1;
+  SAMO_TRY((launch_expand<kModeDowncast, uint16_t>(a, 0, s)));
+  return clear_ok();
+}
+
+int samo_model_set_config(samo_model* md, const samo_optimizer_config* cfg) {
+  if (!md) return fail(SAMO_E_PARAMETER, "null model");
+  SAMO_TRY(samo_optimizer_config_validate(cfg));
+  md->cfg = *cfg;
+  if (md->graph) {  // scalars are baked into the graph's kernel nodes
+    cudaGraphExecDestroy(md->graph);
+    md->graph = nullptr;
+  }
+  return clear_ok();
+}
+
+int samo_model_attach_comm(samo_model* md, samo_comm* comm) {
+  if (!md) return fail(SAMO_E_PARAMETER, "null model");
+  md->comm = comm;
+  return clear_ok();
+}
+
+int samo_model_set_grads(samo_model* md, const uint16_t* const* ptrs, samo_stream_t stream) {
+  if (!md || (md->nlayers && !ptrs)) return fail(SAMO_E_PARAMETER, "null argument");
+  for (int l = 0; l < md->nlayers; ++l) {
+    if (!ptrs[l]) return fail(SAMO_E_PARAMETER, "layer %d: null gradient pointer", l);
+    if (reinterpret_cast<uintptr_t>(ptrs[l]) % 16)
+      return fail(SAMO_E_PARAMETER, "layer %d: gradient pointer must be 16-byte aligned", l);
+    md->layers_host[l].grad = ptrs[l];
+  }
+  if (md->nlayers) {
+    SAMO_CUDA_TRY(cudaMemcpyAsync(md->layers_dev, md->layers_host.data(),
+                                  md->nlayers * sizeof(SamoLayerDev), cudaMemcpyHostToDevice,
+                                  as_stream(stream)));
+  }
+  md->grads_set = true;
+  return clear_ok();
+}
+
+static int comm_size(const samo_model* md) { return md->comm ? md->comm->nranks : 1; }
+
+static int step_ready(samo_model* md) {
+  if (!md) return fail(SAMO_E_PARAMETER, "null model");
+  if (!md->finalized) return fail(SAMO_E_STATE, "model not finalized");
+  return SAMO_OK;
+}
+
+int samo_model_gather(samo_model* md, samo_stream_t stream) {
+  SAMO_TRY(step_ready(md));
+  if (!md->grads_set) return fail(SAMO_E_STATE, "optimizer_step requires backward (no gradients set)");
+  // inv_scale = 1/loss_scale exactly as train.hpp:619; 1/G folded in (exact
+  // for power-of-two G).
+  float inv_scale = 1.0f / md->cfg.loss_scale;
+  const int G = comm_size(md);
+  if (G > 1) inv_scale = inv_scale * (1.0f / static_cast<float>(G));
+  SAMO_TRY(launch_gather_unscale(md->tiles, md->ntiles, md->tile_elems, md->layers_dev, md->idx,
+                                 md->g, inv_scale, md->g + md->n_tot, md->grid_gather,
+                                 as_stream(stream)));
+  return clear_ok();
+}
+
+int samo_model_exchange(samo_model* md, samo_stream_t stream) {
+  SAMO_TRY(step_ready(md));
+  if (comm_size(md) > 1) {
+    // grad32 arena plus the non-finite indicator slot, one in-place sum.
+    SAMO_TRY(samo_allreduce_sum_f32(md->comm, md->g, md->n_tot + 1, stream));
+  }
+  return clear_ok();
+}
+
+int samo_model_update(samo_model* md, samo_stream_t stream) {
+  SAMO_TRY(step_ready(md));
+  ExpandArgs a{};
+  a.tiles = md->tiles;
+  a.ntiles = md->ntiles;
+  a.tile_elems = md->tile_elems;
+  a.layers = md->layers_dev;
+  a.idx = md->idx;
+  a.theta = md->theta;
+  a.m = md->m;
+  a.v = md->v;
+  a.g = md->g;
+  a.prm = adam_params(&md->cfg);
+  a.st = md->st;
+  a.flag_slot = md->g + md->n_tot;
+  a.norm_partials = md->norm_partials;
+  a.use_bulk = 1;
+  if (md->ntiles == 0) return clear_ok();
+  SAMO_TRY((launch_expand<kModeAdam, uint16_t>(a, md->grid_update, as_stream(stream))));
+  return clear_ok();
+}
+
+int samo_model_step(samo_model* md, samo_stream_t stream) {
+  SAMO_TRY(samo_model_gather(md, stream));
+  SAMO_TRY(samo_model_exchange(md, stream));
+  SAMO_TRY(samo_model_update(md, stream));
+  return clear_ok();
+}
+
+int samo_model_step_graph(samo_model* md, samo_stream_t stream) {
+  SAMO_TRY(step_ready(md));
+  if (!md->grads_set) return fail(SAMO_E_STATE, "optimizer_step requires backward (no gradients set)");
+  cudaStream_t s = as_stream(stream);
+  if (md->graph && md->graph_comm != md->comm) {
+    cudaGraphExecDestroy(md->graph);
+    md->graph = nullptr;
+  }
+  if (!md->graph) {
+    if (s == nullptr) return fail(SAMO_E_PARAMETER, "graph steps need a non-default stream");
+    const uint64_t before = samo_kernel_launch_count();
+    SAMO_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    int rc = samo_model_step(md, stream);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(s, &graph);
+    if (rc != SAMO_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+    e = cudaGraphInstantiate(&md->graph, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+      md->graph = nullptr;
+      return cuda_fail(e, "cudaGraphInstantiate");
+    }
+    md->graph_kernels = samo_kernel_launch_count() - before;
+    g_launches.fetch_sub(md->graph_kernels);  // captured, not launched
+    md->graph_comm = md->comm;
+  }
+  SAMO_CUDA_TRY(cudaGraphLaunch(md->graph, s));
+  note_launch(md->graph_kernels);
+  return clear_ok();
+}
+
+int samo_model_step_record(samo_model* md, samo_step_record* out, samo_stream_t stream) {
+  if (!md || !out) return fail(SAMO_E_PARAMETER, "null argument");
+  SamoStepState st{};
+  cudaStream_t s = as_stream(stream);
+  SAMO_CUDA_TRY(cudaMemcpyAsync(&st, md->st, sizeof(st), cudaMemcpyDeviceToHost, s));
+  SAMO_CUDA_TRY(cudaStreamSynchronize(s));
+  out->t = st.t;
+  out->skipped_steps = st.skipped_steps;
+  out->beta1_pow = st.beta1_pow;
+  out->beta2_pow = st.beta2_pow;
+  out->grad_norm = st.grad_norm;
+  out->last_skipped = st.last_skipped;
+  return clear_ok();
+}
+
+int samo_model_step_record_async(samo_model* md, samo_step_record* out, samo_stream_t stream) {
+  static_assert(sizeof(samo_step_record) == 32, "record layout");
+  static_assert(offsetof(SamoStepState, last_skipped) == offsetof(samo_step_record, last_skipped),
+                "SamoStepState starts with a samo_step_record");
+  if (!md || !out) return fail(SAMO_E_PARAMETER, "null argument");
+  SAMO_CUDA_TRY(cudaMemcpyAsync(out, md->st, sizeof(samo_step_record), cudaMemcpyDeviceToHost,
+                                as_stream(stream)));
+  return clear_ok();
+}
+
+int samo_model_set_step_record(samo_model* md, const samo_step_record* rec, samo_stream_t stream) {
+  if (!md || !rec) return fail(SAMO_E_PARAMETER, "null argument");
+  SamoStepState st{};
+  st.t = rec->t;
+  st.skipped_steps = rec->skipped_steps;
+  st.beta1_pow = rec->beta1_pow;
+  st.beta2_pow = rec->beta2_pow;
+  st.grad_norm = rec->grad_norm;
+  st.last_skipped = rec->last_skipped;
+  cudaStream_t s = as_stream(stream);
+  SAMO_CUDA_TRY(cudaMemcpyAsync(md->st, &st, sizeof(st), cudaMemcpyHostToDevice, s));
+  SAMO_CUDA_TRY(cudaStreamSynchronize(s));
+  return clear_ok();
+}
+
+int samo_model_check_invariants(samo_model* md, samo_stream_t stream) {
+  SAMO_TRY(step_ready(md));
+  cudaStream_t s = as_stream(stream);
+  uint32_t* bad = reinterpret_cast<uint32_t*>(md->norm_partials);
+  SAMO_CUDA_TRY(cudaMemsetAsync(bad, 0, 4, s));
+  ExpandArgs a{};
+  a.tiles = md->tiles;
+  a.ntiles = md->ntiles;
+  a.tile_elems = md->tile_elems;
+  a.layers = md->layers_dev;
+  a.idx = md->idx;
+  a.theta = md->theta;
+  a.mismatch = bad;
+  SAMO_TRY((launch_expand<kModeCheck, uint16_t>(a, 0, s)));
+  uint32_t hbad = 0;
+  SAMO_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, s));
+  SAMO_CUDA_TRY(cudaStreamSynchronize(s));
+  if (hbad) return fail(SAMO_E_STATE, "theta16 disagrees with expand(half(theta32))");
+  return clear_ok();
+}
+
+}  // extern "C"

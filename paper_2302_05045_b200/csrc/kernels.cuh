@@ -1,0 +1,70 @@
+// kernels.cuh — launch interfaces of the SAMO step kernels (kernels_step.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace samo_dev {
+
+constexpr int kThreads = 256;       // threads per CTA for the tile kernels
+constexpr int kGatherStages = 3;    // TMA ring depth of the gather kernel
+
+enum ExpandMode : int {
+  kModeAdam = 0,      // K23: Adam + downcast + expand (train.hpp:640-651)
+  kModeDowncast = 1,  // K3 : downcast + expand (train.hpp:647-651)
+  kModeValues = 2,    // expand<T> of given values (store.hpp:72-87)
+  kModeCheck = 3      // check_state_invariants (store.hpp:171-197)
+};
+
+struct ExpandArgs {
+  const SamoTile* tiles;
+  uint32_t ntiles;
+  uint32_t tile_elems;
+  const SamoLayerDev* layers;  // per-layer dense output (theta16) pointers
+  const uint32_t* idx;         // index arena (layer-local indices)
+  float* theta;                // compressed fp32 master weights
+  float* m;
+  float* v;
+  const float* g;              // exchanged grad32
+  const void* values;          // kModeValues: compressed values (u16/u32)
+  SamoAdamParams prm;
+  SamoStepState* st;           // kModeAdam: device scalars
+  float* flag_slot;            // kModeAdam: non-finite indicator (reset here)
+  float* norm_partials;        // kModeAdam: one per CTA
+  uint32_t* mismatch;          // kModeCheck: set to nonzero on violation
+  int use_bulk;                // 1 when every dense output is 16-byte aligned
+};
+
+// Fills k_begin/k_end of every tile (layer/dense fields preset) by binary
+// search in the layer's ascending index segment.
+int launch_tiles_fill(SamoTile* tiles, uint32_t ntiles, const uint64_t* k_off,
+                      const uint32_t* idx, cudaStream_t s);
+
+// K1: gather + unscale + cast + finite flag.
+int launch_gather_unscale(const SamoTile* tiles, uint32_t ntiles, uint32_t tile_elems,
+                          const SamoLayerDev* layers, const uint32_t* idx, float* g32,
+                          float inv_scale, float* flag_slot, int grid, cudaStream_t s);
+int gather_grid(uint32_t tile_elems);
+
+template <int MODE, typename OutT>
+int launch_expand(const ExpandArgs& a, int grid, cudaStream_t s);
+template <int MODE, typename OutT>
+int expand_grid(uint32_t tile_elems);
+
+// Plain gather out[k] = dense[idx[k]] (compress<T>, store.hpp:58-69).
+template <typename T>
+int launch_compress(const T* dense, const uint32_t* idx, uint64_t n, T* out, cudaStream_t s);
+
+int launch_adam(float* theta, float* m, float* v, const float* g, uint64_t n,
+                SamoAdamParams prm, float bias1, float bias2, cudaStream_t s);
+
+int launch_f2h(const float* in, uint16_t* out, uint64_t n, cudaStream_t s);
+int launch_h2f(const uint16_t* in, float* out, uint64_t n, cudaStream_t s);
+int launch_synth_f32(float* out, uint64_t n, uint64_t seed, uint64_t stream_id, float bound,
+                     cudaStream_t s);
+int launch_synth_f16(uint16_t* out, uint64_t n, uint64_t seed, uint64_t stream_id, float bound,
+                     float scale, cudaStream_t s);
+// Strictly-ascending and < dense_len check of one index segment.
+int launch_check_indices(const uint32_t* idx, uint64_t n, uint64_t dense_len, uint32_t* bad,
+                         cudaStream_t s);
+
+}  // namespace samo_dev

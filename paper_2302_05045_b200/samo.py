@@ -1,0 +1,422 @@
+"""Python mirror of the reference operator interface for the SAMO step path.
+
+Same names, argument meaning and error behaviour as the reference's C++ API
+(/root/reference/proj/include/samo): `compress`, `expand`, `adam_update`,
+`magnitude_prune`, `unpruned_count`, `make_layer_state`-style model init and a
+`SamoTrainer`-style step driver — over CUDA tensors, every call going through
+the C ABI of libsamo_cuda.so (include/samo_cuda.h).  torch is used only for
+device memory and streams.
+
+binary16 data is carried in torch.float16 / torch.int16 tensors and handled as
+raw 16-bit patterns (the reference's `Half` is a storage type, half.hpp:75-103);
+fp32 data in torch.float32; index sets in torch.int32 holding uint32 values.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Iterable, Sequence
+
+import torch
+
+from . import _abi
+from ._abi import (DimensionError, ParameterError, SamoIndexError, StateError,  # noqa: F401
+                   ConfigError, CudaError, NcclError, OptimizerConfig, StepRecord)
+
+PER_LAYER = 0   # PruneScope::per_layer (prune.hpp:61)
+GLOBAL = 1      # PruneScope::global
+
+
+def _vp(t: torch.Tensor | None) -> C.c_void_p:
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _stream(stream: torch.cuda.Stream | None = None) -> C.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _require_cuda(*ts: torch.Tensor) -> None:
+    for t in ts:
+        if t is not None and (not t.is_cuda or not t.is_contiguous()):
+            raise ParameterError("expected contiguous CUDA tensors (the SAMO path has no CPU fallback)")
+
+
+def _bits16(t: torch.Tensor) -> torch.Tensor:
+    if t.element_size() != 2:
+        raise ParameterError("expected a 16-bit tensor")
+    return t
+
+
+# ---------------------------------------------------------------------------
+# half.hpp
+
+
+def float_to_half_bits(x: torch.Tensor) -> torch.Tensor:
+    """Half(float) for every element (half.hpp:13-49); returns int16 bit patterns."""
+    _require_cuda(x)
+    out = torch.empty(x.shape, dtype=torch.int16, device=x.device)
+    _abi.call("samo_float_to_half", _vp(x), _vp(out), x.numel(), _stream())
+    return out
+
+
+def half_bits_to_float(h: torch.Tensor) -> torch.Tensor:
+    """float(Half) for every element (half.hpp:52-71)."""
+    _require_cuda(h)
+    _bits16(h)
+    out = torch.empty(h.shape, dtype=torch.float32, device=h.device)
+    _abi.call("samo_half_to_float", _vp(h), _vp(out), h.numel(), _stream())
+    return out
+
+
+# ---------------------------------------------------------------------------
+# prune.hpp
+
+
+@dataclass
+class PrunedIndexSet:
+    """prune.hpp:21-27: strictly ascending uint32 linear indices (< dense_len)."""
+    layer_id: str
+    dense_len: int
+    indices: torch.Tensor  # int32 CUDA tensor carrying uint32 values
+
+    def count(self) -> int:
+        return int(self.indices.numel())
+
+
+@dataclass
+class LayerParams:
+    """prune.hpp:65-69."""
+    layer_id: str
+    values: torch.Tensor  # fp32 CUDA tensor, any shape
+    prunable: bool = True
+
+
+def unpruned_count(p: float, n: int) -> int:
+    """detail::unpruned_count (prune.hpp:76-79)."""
+    return int(_abi.load().samo_unpruned_count(float(p), int(n)))
+
+
+def magnitude_prune(layers: Sequence[LayerParams], p: float,
+                    scope: int = PER_LAYER) -> list[PrunedIndexSet]:
+    """magnitude_prune (prune.hpp:99-170), on the device (kernel K0)."""
+    n = len(layers)
+    for lp in layers:
+        _require_cuda(lp.values)
+        if lp.values.dtype != torch.float32:
+            raise ParameterError("magnitude_prune expects fp32 values")
+    outs = [torch.empty(max(1, lp.values.numel()), dtype=torch.int32, device=lp.values.device)
+            for lp in layers]
+    vals = (C.c_void_p * max(1, n))(*[lp.values.data_ptr() for lp in layers])
+    lens = (C.c_uint64 * max(1, n))(*[lp.values.numel() for lp in layers])
+    prun = (C.c_uint8 * max(1, n))(*[1 if lp.prunable else 0 for lp in layers])
+    optr = (C.c_void_p * max(1, n))(*[o.data_ptr() for o in outs])
+    counts = (C.c_uint64 * max(1, n))()
+    _abi.call("samo_magnitude_prune", vals, lens, prun, n, float(p), int(scope), optr, counts,
+              _stream())
+    return [PrunedIndexSet(lp.layer_id, lp.values.numel(), outs[i][: counts[i]].clone())
+            for i, lp in enumerate(layers)]
+
+
+# ---------------------------------------------------------------------------
+# store.hpp
+
+
+def compress(dense: torch.Tensor, ind: PrunedIndexSet) -> torch.Tensor:
+    """compress<T> (store.hpp:58-69): out[k] = dense.flat[ind.indices[k]]."""
+    _require_cuda(dense, ind.indices)
+    out = torch.empty(ind.count(), dtype=dense.dtype, device=dense.device)
+    name = {2: "samo_compress_u16", 4: "samo_compress_u32"}.get(dense.element_size())
+    if name is None:
+        raise ParameterError("compress supports 16- and 32-bit elements")
+    _abi.call(name, _vp(dense), dense.numel(), _vp(ind.indices), ind.count(), ind.dense_len,
+              _vp(out), _stream())
+    return out
+
+
+def expand(values: torch.Tensor, ind: PrunedIndexSet, shape: Sequence[int]) -> torch.Tensor:
+    """expand<T> (store.hpp:72-87): zeros except out.flat[ind.indices[k]] = values[k]."""
+    _require_cuda(values, ind.indices)
+    numel = 1
+    for e in shape:
+        if int(e) <= 0:
+            raise DimensionError("tensor extents must be positive")
+        numel *= int(e)
+    out = torch.empty(tuple(int(e) for e in shape), dtype=values.dtype, device=values.device)
+    name = {2: "samo_expand_u16", 4: "samo_expand_u32"}.get(values.element_size())
+    if name is None:
+        raise ParameterError("expand supports 16- and 32-bit elements")
+    _abi.call(name, _vp(values), values.numel(), _vp(ind.indices), ind.count(), ind.dense_len,
+              numel, _vp(out), _stream())
+    return out
+
+
+def downcast_expand(theta32: torch.Tensor, ind: PrunedIndexSet,
+                    shape: Sequence[int]) -> torch.Tensor:
+    """expand<Half>(Half(theta32), ind, shape) (train.hpp:647-651) in one pass."""
+    _require_cuda(theta32, ind.indices)
+    numel = 1
+    for e in shape:
+        numel *= int(e)
+    if numel != ind.dense_len:
+        raise DimensionError("expand: shape does not match index set dense length")
+    if theta32.numel() != ind.count():
+        raise DimensionError("expand: value count does not match index set")
+    out = torch.empty(tuple(int(e) for e in shape), dtype=torch.float16, device=theta32.device)
+    _abi.call("samo_downcast_expand", _vp(theta32), ind.count(), _vp(ind.indices), ind.dense_len,
+              _vp(out), _stream())
+    return out
+
+
+# ---------------------------------------------------------------------------
+# train.hpp
+
+
+def validate(cfg: OptimizerConfig) -> None:
+    """OptimizerConfig::validate (train.hpp:78-86)."""
+    _abi.call("samo_optimizer_config_validate", C.byref(cfg))
+
+
+def adam_update(theta: torch.Tensor, m: torch.Tensor, v: torch.Tensor, g: torch.Tensor,
+                cfg: OptimizerConfig, bias1: float, bias2: float) -> None:
+    """adam_update (train.hpp:332-347), in place on device spans."""
+    _require_cuda(theta, m, v, g)
+    n = theta.numel()
+    if not (m.numel() == v.numel() == g.numel() == n):
+        raise DimensionError("adam_update: span lengths differ")
+    _abi.call("samo_adam_update", _vp(theta), _vp(m), _vp(v), _vp(g), n, C.byref(cfg),
+              C.c_float(bias1), C.c_float(bias2), _stream())
+
+
+# ---------------------------------------------------------------------------
+# Gradient exchange communicator
+
+
+class Communicator:
+    """NCCL communicator for the compressed-gradient exchange (one per rank)."""
+
+    def __init__(self, unique_id: bytes, nranks: int, rank: int):
+        if len(unique_id) != 128:
+            raise ParameterError("unique id must be 128 bytes")
+        buf = (C.c_uint8 * 128)(*unique_id)
+        h = C.c_void_p()
+        _abi.call("samo_comm_create", buf, int(nranks), int(rank), C.byref(h))
+        self._h = h
+        self.nranks = int(nranks)
+        self.rank = int(rank)
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _abi.call("samo_comm_unique_id", buf)
+        return bytes(buf)
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def allreduce_sum_(self, t: torch.Tensor) -> torch.Tensor:
+        _require_cuda(t)
+        if t.dtype != torch.float32:
+            raise ParameterError("allreduce expects fp32")
+        _abi.call("samo_allreduce_sum_f32", self._h, _vp(t), t.numel(), _stream())
+        return t
+
+    def close(self) -> None:
+        if self._h:
+            _abi.load().samo_comm_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------
+# Model state + step driver (store.hpp:22-55, 150-197; train.hpp:574-704)
+
+
+@dataclass
+class LayerSpec:
+    layer_id: str
+    shape: tuple[int, ...]
+    nnz: int
+
+    @property
+    def dense_len(self) -> int:
+        n = 1
+        for e in self.shape:
+            n *= int(e)
+        return n
+
+
+class SamoModel:
+    """Device-resident compressed model state with the fused step driver.
+
+    Mirrors ModelState (store.hpp:42-55) + SamoTrainer::optimizer_step
+    (train.hpp:617-656): flat arenas for theta32/m/v/grad32/indices, a dense
+    binary16 theta16 per layer, device-resident Adam scalars.  The step is
+    K1 gather+unscale -> NCCL exchange (when a communicator is attached) -> K23
+    Adam+downcast+expand, with no host synchronisation.
+    """
+
+    def __init__(self, layers: Sequence[LayerSpec], tile_elems: int = 0):
+        self.layers = list(layers)
+        descs = (_abi.LayerDesc * max(1, len(self.layers)))(
+            *[_abi.LayerDesc(l.dense_len, l.nnz) for l in self.layers])
+        h = C.c_void_p()
+        _abi.call("samo_model_create", descs, len(self.layers), int(tile_elems), C.byref(h))
+        self._h = h
+        self._grads_keepalive: list[torch.Tensor] = []
+
+    # -- construction ------------------------------------------------------
+    @classmethod
+    def from_index_sets(cls, sets: Sequence[PrunedIndexSet], shapes: Sequence[Sequence[int]],
+                        tile_elems: int = 0) -> "SamoModel":
+        specs = [LayerSpec(s.layer_id, tuple(int(e) for e in shp), s.count())
+                 for s, shp in zip(sets, shapes)]
+        model = cls(specs, tile_elems)
+        for l, s in enumerate(sets):
+            model.set_indices(l, s.indices)
+        model.finalize()
+        return model
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def close(self) -> None:
+        if self._h:
+            _abi.load().samo_model_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_indices(self, layer: int, idx: torch.Tensor) -> None:
+        on_host = not idx.is_cuda
+        idx = idx.contiguous()
+        _abi.call("samo_model_set_indices", self._h, int(layer), _vp(idx), idx.numel(),
+                  1 if on_host else 0, _stream())
+
+    def finalize(self) -> None:
+        _abi.call("samo_model_finalize", self._h, _stream())
+
+    def init_layer(self, layer: int, dense_init: torch.Tensor) -> None:
+        """make_layer_state (store.hpp:150-168) from dense fp32 initial values."""
+        _require_cuda(dense_init)
+        if dense_init.dtype != torch.float32:
+            raise ParameterError("init values must be fp32")
+        _abi.call("samo_model_init_layer", self._h, int(layer), _vp(dense_init),
+                  dense_init.numel(), _stream())
+
+    def set_config(self, cfg: OptimizerConfig) -> None:
+        _abi.call("samo_model_set_config", self._h, C.byref(cfg))
+
+    def attach_comm(self, comm: Communicator | None) -> None:
+        _abi.call("samo_model_attach_comm", self._h, comm.handle if comm else C.c_void_p())
+
+    # -- step ----------------------------------------------------------------
+    def set_grads(self, grads: Sequence[torch.Tensor]) -> None:
+        """Dense binary16 gradients of the step (the backward sink's input)."""
+        if len(grads) != len(self.layers):
+            raise DimensionError("one dense gradient per layer required")
+        for g, l in zip(grads, self.layers):
+            _require_cuda(g)
+            _bits16(g)
+            if g.numel() != l.dense_len:
+                raise DimensionError(f"{l.layer_id}: gradient length does not match layer")
+        ptrs = (C.c_void_p * max(1, len(grads)))(*[g.data_ptr() for g in grads])
+        _abi.call("samo_model_set_grads", self._h, ptrs, _stream())
+        self._grads_keepalive = list(grads)
+
+    def gather(self) -> None:
+        _abi.call("samo_model_gather", self._h, _stream())
+
+    def exchange(self) -> None:
+        _abi.call("samo_model_exchange", self._h, _stream())
+
+    def update(self) -> None:
+        _abi.call("samo_model_update", self._h, _stream())
+
+    def step(self, graph: bool = False) -> None:
+        """gather + exchange + Adam/downcast/expand; device-resident, async."""
+        _abi.call("samo_model_step_graph" if graph else "samo_model_step", self._h, _stream())
+
+    def step_record(self) -> StepRecord:
+        rec = StepRecord()
+        _abi.call("samo_model_step_record", self._h, C.byref(rec), _stream())
+        return rec
+
+    def set_step_record(self, rec: StepRecord) -> None:
+        _abi.call("samo_model_set_step_record", self._h, C.byref(rec), _stream())
+
+    def check_invariants(self) -> None:
+        """check_state_invariants (store.hpp:171-197) -> StateError."""
+        _abi.call("samo_model_check_invariants", self._h, _stream())
+
+    # -- views -----------------------------------------------------------------
+    def view(self, layer: int) -> _abi.LayerView:
+        v = _abi.LayerView()
+        _abi.call("samo_model_layer_view", self._h, int(layer), C.byref(v))
+        return v
+
+    def totals(self) -> tuple[int, int, int]:
+        phi, nnz, nt = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _abi.call("samo_model_totals", self._h, C.byref(phi), C.byref(nnz), C.byref(nt))
+        return phi.value, nnz.value, nt.value
+
+    def device_bytes(self) -> int:
+        return int(_abi.load().samo_model_device_bytes(self._h))
+
+    _FIELDS = {"theta16": (torch.float16, "dense"), "theta32": (torch.float32, "nnz"),
+               "adam_m": (torch.float32, "nnz"), "adam_v": (torch.float32, "nnz"),
+               "grad32": (torch.float32, "nnz"), "indices": (torch.int32, "nnz")}
+
+    def read(self, layer: int, name: str) -> torch.Tensor:
+        """Copy of one per-layer buffer (device tensor)."""
+        v = self.view(layer)
+        dtype, kind = self._FIELDS[name]
+        n = v.dense_len if kind == "dense" else v.nnz
+        out = torch.empty(int(n), dtype=dtype, device="cuda")
+        if n:
+            _abi.call("samo_copy_async", _vp(out), C.c_void_p(getattr(v, name)),
+                      int(n) * out.element_size(), _stream())
+        return out.view(self.layers[layer].shape) if kind == "dense" else out
+
+    def write(self, layer: int, name: str, src: torch.Tensor) -> None:
+        """Overwrite one per-layer buffer (e.g. warm Adam moments on resume)."""
+        v = self.view(layer)
+        dtype, kind = self._FIELDS[name]
+        n = v.dense_len if kind == "dense" else v.nnz
+        if src.numel() != n or src.element_size() != torch.empty(0, dtype=dtype).element_size():
+            raise DimensionError(f"write {name}: size mismatch")
+        src = src.contiguous()
+        if n:
+            _abi.call("samo_copy_async", C.c_void_p(getattr(v, name)), _vp(src),
+                      int(n) * src.element_size(), _stream())
+
+
+def kernel_launch_count() -> int:
+    return int(_abi.load().samo_kernel_launch_count())
+
+
+def synth_uniform_f32(n: int, seed: int, stream_id: int, bound: float,
+                      out: torch.Tensor | None = None) -> torch.Tensor:
+    out = out if out is not None else torch.empty(n, dtype=torch.float32, device="cuda")
+    _abi.call("samo_synth_uniform_f32", _vp(out), int(n), int(seed), int(stream_id),
+              C.c_float(bound), _stream())
+    return out
+
+
+def synth_uniform_f16(n: int, seed: int, stream_id: int, bound: float, scale: float,
+                      out: torch.Tensor | None = None) -> torch.Tensor:
+    out = out if out is not None else torch.empty(n, dtype=torch.float16, device="cuda")
+    _abi.call("samo_synth_uniform_f16", _vp(out), int(n), int(seed), int(stream_id),
+              C.c_float(bound), C.c_float(scale), _stream())
+    return out

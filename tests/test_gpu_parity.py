@@ -1,0 +1,316 @@
+"""GPU parity: the CUDA path (through the C ABI) against the golden vectors of
+the reference and the oracle, bit-exact for every integer/byte/IEEE-per-op
+result.  Tolerances appear only where the summation order differs from the
+reference's serial fp32 loop (the gradient norm: rel 1e-5 vs fp64)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def T(a, dtype=None):
+    """numpy -> contiguous CUDA tensor (uint16/uint32 carried as int16/int32)."""
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.uint16:
+        a = a.view(np.int16)
+    elif a.dtype == np.uint32:
+        a = a.view(np.int32)
+    t = torch.from_numpy(a.copy()).cuda()
+    return t if dtype is None else t.view(dtype)
+
+
+def N(t, dtype):
+    return t.detach().cpu().contiguous().numpy().view(dtype)
+
+
+def bits(x):
+    return np.asarray(x, dtype=np.float32).view(np.uint32)
+
+
+@pytest.fixture(scope="module")
+def S(cuda):
+    from paper_2302_05045_b200 import samo
+    return samo
+
+
+# --------------------------------------------------------------------------
+# half.hpp
+
+def test_half_conversions_golden(S, golden):
+    g = golden("half")
+    got = N(S.float_to_half_bits(T(g["f2h_in"])), np.uint16)
+    assert np.array_equal(got, g["f2h_out"])
+    got = N(S.half_bits_to_float(T(g["h2f_in"])), np.uint32)
+    assert np.array_equal(got, g["h2f_out_bits"])
+
+
+# --------------------------------------------------------------------------
+# store.hpp
+
+def _set(S, idx, dense_len):
+    return S.PrunedIndexSet("w", int(dense_len), T(np.asarray(idx, np.uint32)))
+
+
+def test_compress_expand_kats(S):
+    d = T(np.array([1, 2, 3, 4], np.float32))
+    ind = _set(S, [0, 3], 4)
+    assert S.compress(d, ind).cpu().tolist() == [1.0, 4.0]              # store_test.cpp:29-33
+    assert S.compress(d, _set(S, [0, 1, 2, 3], 4)).cpu().tolist() == [1, 2, 3, 4]
+    with pytest.raises(S.DimensionError):                                # store_test.cpp:60-64
+        S.compress(T(np.zeros(3, np.float32)), _set(S, [0], 4))
+    e = S.expand(T(np.array([1, 4], np.float32)), ind, (2, 2))          # store_test.cpp:66-71
+    assert e.cpu().tolist() == [[1, 0], [0, 4]]
+    z = S.expand(T(np.array([], np.float32)), _set(S, [], 4), (4,))     # store_test.cpp:73-77
+    assert z.cpu().tolist() == [0, 0, 0, 0]
+    with pytest.raises(S.DimensionError):
+        S.expand(T(np.array([1.0], np.float32)), ind, (2, 2))
+    with pytest.raises(S.DimensionError):
+        S.expand(T(np.array([1, 4], np.float32)), ind, (5,))
+
+
+def test_store_golden_round_trips(S, golden):
+    g = golden("store")
+    off_d = off_i = 0
+    for t, (n, k) in enumerate(g["rt_meta"].astype(np.int64)):
+        dense = g["rt_dense"][off_d:off_d + n]
+        idx = g["rt_idx"][off_i:off_i + k]
+        off_d += n
+        off_i += k
+        ind = _set(S, idx, n)
+        vals = S.compress(T(dense), ind)
+        assert np.array_equal(N(vals, np.uint16), g[f"rt{t}_vals"])
+        exp = S.expand(vals, ind, (int(n),))
+        assert np.array_equal(N(exp, np.uint16), g[f"rt{t}_exp"])
+
+
+@pytest.mark.parametrize("dense_len,density", [(4096 * 4096, 0.1), (8192 * 3 + 7, 0.5),
+                                               (100_003, 0.05), (65536, 1.0), (1, 1.0)])
+def test_expand_large_vs_oracle(S, oracle, dense_len, density):
+    rng = np.random.default_rng(dense_len)
+    idx = np.nonzero(rng.random(dense_len) < density)[0].astype(np.uint32)
+    vals32 = rng.standard_normal(idx.size).astype(np.float32)
+    want16 = oracle.expand(oracle.f2h(vals32), idx, (dense_len,))
+    ind = _set(S, idx, dense_len)
+    got = S.downcast_expand(T(vals32), ind, (dense_len,))
+    assert np.array_equal(N(got, np.uint16), want16)
+    want32 = oracle.expand(vals32, idx, (dense_len,))
+    got32 = S.expand(T(vals32), ind, (dense_len,))
+    assert np.array_equal(N(got32, np.uint32), bits(want32))
+    dense = rng.integers(0, 65536, size=dense_len).astype(np.uint16)
+    assert np.array_equal(N(S.compress(T(dense), ind), np.uint16), oracle.compress(dense, idx))
+
+
+def test_expand_unaligned_output(S, oracle):
+    """Outputs that are not 16-byte aligned take the non-bulk store path."""
+    n = 50_001
+    rng = np.random.default_rng(3)
+    idx = np.nonzero(rng.random(n) < 0.2)[0].astype(np.uint32)
+    v = rng.integers(0, 65536, size=idx.size).astype(np.uint16)
+    from paper_2302_05045_b200 import _abi
+    import ctypes as C
+    big = torch.zeros(n + 8, dtype=torch.int16, device="cuda")
+    out = big[1:n + 1]
+    vt = T(v)
+    it = T(idx)
+    _abi.call("samo_expand_u16", C.c_void_p(vt.data_ptr()), idx.size, C.c_void_p(it.data_ptr()),
+              idx.size, n, n, C.c_void_p(out.data_ptr()), C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert np.array_equal(N(out, np.uint16), oracle.expand(v, idx, (n,)))
+    assert int(big[0]) == 0 and int(big[n + 1]) == 0
+
+
+# --------------------------------------------------------------------------
+# train.hpp: adam
+
+def test_adam_golden(S, golden):
+    g = golden("adam")
+    for tag in ("plain", "wd", "late"):
+        c = g[f"{tag}_cfg"]
+        cfg = S.OptimizerConfig(float(c[0]), float(c[1]), float(c[2]), float(c[3]), float(c[4]),
+                                float(c[5]))
+        th, m, v = T(g["th"]), T(g["m"]), T(g["v"])
+        S.adam_update(th, m, v, T(g["g"]), cfg, float(c[6]), float(c[7]))
+        assert np.array_equal(N(th, np.uint32), bits(g[f"{tag}_th"]))
+        assert np.array_equal(N(m, np.uint32), bits(g[f"{tag}_m"]))
+        assert np.array_equal(N(v, np.uint32), bits(g[f"{tag}_v"]))
+
+
+def test_config_validation(S):
+    S.validate(S.OptimizerConfig())
+    for bad in (S.OptimizerConfig(loss_scale=3.0), S.OptimizerConfig(loss_scale=0.5),
+                S.OptimizerConfig(beta1=1.0), S.OptimizerConfig(beta2=-0.1)):
+        with pytest.raises(S.ParameterError):
+            S.validate(bad)
+
+
+# --------------------------------------------------------------------------
+# prune.hpp (K0)
+
+def test_prune_kats(S):
+    def lp(vals, prunable=True):
+        return S.LayerParams("w", T(np.asarray(vals, np.float32)), prunable)
+    got = S.magnitude_prune([lp([3.0, -1.0, 0.5, -4.0])], 0.5)
+    assert got[0].indices.cpu().tolist() == [0, 3] and got[0].dense_len == 4
+    assert S.magnitude_prune([lp([0.1, -0.2, 0.0])], 0.0)[0].indices.cpu().tolist() == [0, 1, 2]
+    assert S.magnitude_prune([lp([1.0] * 4)], 0.5)[0].indices.cpu().tolist() == [0, 1]
+    for p in (1.0, -0.1):
+        with pytest.raises(S.ParameterError):
+            S.magnitude_prune([lp([1.0])], p)
+    sets = S.magnitude_prune([lp([5, 1, 2, 3]), lp([0, 0], False)], 0.75)
+    assert sets[0].count() == 1 and sets[1].indices.cpu().tolist() == [0, 1]
+    g = S.magnitude_prune([lp([10, 9, 8, 7]), lp([1, 0.9, 0.8, 0.7])], 0.5, S.GLOBAL)
+    assert g[0].indices.cpu().tolist() == [0, 1, 2, 3] and g[1].count() == 0
+
+
+def test_prune_golden(S, golden):
+    g = golden("prune")
+    for c, row in enumerate(g["cases"]):
+        L, p = int(row[0]), float(row[1])
+        layers = [S.LayerParams(f"l{l}", T(g[f"c{c}_val{l}"]), bool(row[2 + l])) for l in range(L)]
+        for scope in (0, 1):
+            got = S.magnitude_prune(layers, p, scope)
+            for l in range(L):
+                assert np.array_equal(N(got[l].indices, np.uint32), g[f"c{c}_s{scope}_idx{l}"]), \
+                    (c, scope, l)
+
+
+def test_prune_golden_big(S, oracle, golden):
+    g = golden("prune")
+    vals = oracle.mt64_uniform(int(g["big_seed"][0]), 4096 * 1024, 1.0 / 64.0)
+    got = S.magnitude_prune([S.LayerParams("w", T(vals))], 0.9)[0]
+    assert np.array_equal(N(got.indices, np.uint32), g["big_idx"])
+
+
+def test_prune_multi_layer_vs_oracle(S, oracle):
+    """Per-layer and global scope on a few million params with a non-prunable
+    layer in the middle (global tie order crosses layers)."""
+    rng = np.random.default_rng(9)
+    lens = [2_000_003, 17, 640_000, 1_000_000]
+    vals = [(rng.integers(-2000, 2000, size=n) * 2.0**-12).astype(np.float32) for n in lens]
+    prunable = [True, False, True, True]
+    layers = [S.LayerParams(f"l{i}", T(v), pr) for i, (v, pr) in enumerate(zip(vals, prunable))]
+    for scope in (0, 1):
+        for p in (0.9, 0.5, 0.95):
+            want = oracle.magnitude_prune(vals, prunable, p, scope)
+            got = S.magnitude_prune(layers, p, scope)
+            for l in range(len(lens)):
+                assert np.array_equal(N(got[l].indices, np.uint32), want[l]), (scope, p, l)
+
+
+# --------------------------------------------------------------------------
+# Model state + step (SamoTrainer::optimizer_step)
+
+def _model_from_golden(S, g, tile_elems=0):
+    dense_len = g["dense_len"].astype(np.int64)
+    L = len(dense_len)
+    sets = [S.PrunedIndexSet(f"l{l}", int(dense_len[l]), T(g[f"idx{l}"])) for l in range(L)]
+    model = S.SamoModel.from_index_sets(sets, [(int(d),) for d in dense_len], tile_elems)
+    for l in range(L):
+        model.init_layer(l, T(g[f"val{l}"]))
+    model.set_config(S.OptimizerConfig(learning_rate=1e-2, loss_scale=1024.0))
+    return model, L
+
+
+@pytest.mark.parametrize("graph", [False, True])
+@pytest.mark.parametrize("tile_elems", [0, 1024])
+def test_model_step_golden(S, golden, graph, tile_elems):
+    """Five reference optimizer steps incl. one skipped on +inf: theta32/m/v/
+    theta16 bit-exact, skip counter exact, grad norm within rel 1e-5."""
+    g = golden("step")
+    model, L = _model_from_golden(S, g, tile_elems)
+    model.check_invariants()
+    for s in range(int(g["steps"][0])):
+        grads = [T(g[f"s{s}_grad{l}"]) for l in range(L)]
+        model.set_grads(grads)
+        model.step(graph=graph)
+        rec = model.step_record()
+        assert rec.skipped_steps == int(g[f"s{s}_skipped"][0])
+        assert rec.last_skipped == (0 if g[f"s{s}_applied"][0] else 1)
+        want_norm = float(g[f"s{s}_norm"][0])
+        if np.isfinite(want_norm):
+            assert abs(rec.grad_norm - want_norm) <= 1e-5 * abs(want_norm)
+        for l in range(L):
+            for k in ("theta32", "adam_m", "adam_v"):
+                assert np.array_equal(N(model.read(l, k), np.uint32), bits(g[f"s{s}_{k}{l}"])), (s, l, k)
+            assert np.array_equal(N(model.read(l, "theta16"), np.uint16), g[f"s{s}_theta16{l}"]), (s, l)
+        model.check_invariants()
+    model.close()
+
+
+def test_model_invariant_violation_detected(S, golden):
+    g = golden("step")
+    model, L = _model_from_golden(S, g)
+    t16 = model.read(0, "theta16")
+    idx = N(model.read(0, "indices"), np.uint32)
+    pruned = int(np.setdiff1d(np.arange(t16.numel()), idx)[0])
+    t16.view(-1)[pruned] = 1.0
+    model.write(0, "theta16", t16.view(-1))
+    with pytest.raises(S.StateError):
+        model.check_invariants()
+
+
+def test_model_errors(S):
+    m = S.SamoModel([S.LayerSpec("w", (4,), 2)])
+    with pytest.raises(S.SamoIndexError):
+        m.set_indices(0, torch.tensor([3, 1], dtype=torch.int32))
+    with pytest.raises(S.SamoIndexError):
+        m.set_indices(0, torch.tensor([1, 4], dtype=torch.int32))
+    with pytest.raises(S.DimensionError):
+        m.set_indices(0, torch.tensor([1], dtype=torch.int32))
+    with pytest.raises(S.StateError):
+        m.finalize()                     # no index set yet
+    m.set_indices(0, torch.tensor([0, 3], dtype=torch.int32))
+    m.finalize()
+    with pytest.raises(S.StateError):
+        m.step()                         # optimizer_step requires backward (train.hpp:618)
+    with pytest.raises(S.ParameterError):
+        m.set_config(S.OptimizerConfig(loss_scale=1000.0))
+    with pytest.raises(S.DimensionError):
+        m.init_layer(0, torch.zeros(5, device="cuda"))
+    with pytest.raises(S.DimensionError):
+        S.SamoModel([S.LayerSpec("w", (4,), 5)])
+    m.close()
+
+
+def test_config1_fc4096_vs_oracle(S, oracle):
+    """BASELINE config 1: one 4096x4096 FC layer, init_params(seed 7), 90%
+    magnitude mask, loss-scaled binary16 grads, three steps bit-exact."""
+    n = 4096 * 4096
+    w = oracle.mt64_uniform(7, n, np.float32(1.0) / np.float32(64.0))  # 1/sqrt(4096)
+    idx = oracle.magnitude_prune([w], [True], 0.9)[0]
+    assert idx.size == 1_677_722
+    layers = [S.LayerParams("fc0.weight", T(w))]
+    got_idx = S.magnitude_prune(layers, 0.9)[0]
+    assert np.array_equal(N(got_idx.indices, np.uint32), idx)
+    model = S.SamoModel.from_index_sets([got_idx], [(4096, 4096)])
+    model.init_layer(0, T(w))
+    cfg = S.OptimizerConfig()
+    model.set_config(cfg)
+    from oracle.oracle import Cfg, StepState
+    ocfg = Cfg()
+    theta = oracle.compress(w, idx)
+    m, v, g32 = (np.zeros_like(theta) for _ in range(3))
+    t16 = [np.zeros(n, np.uint16)]
+    st = StepState()
+    for s in range(3):
+        grad = oracle.synth_f16(0, n, 5, s, 2.0**-7, 1024.0)
+        gt = T(grad)
+        model.set_grads([gt])
+        model.step(graph=(s > 0))
+        oracle.optimizer_step([n], [idx.size], idx, [grad], theta, m, v, g32, t16, ocfg, st)
+        assert np.array_equal(N(model.read(0, "theta32"), np.uint32), bits(theta))
+        assert np.array_equal(N(model.read(0, "adam_v"), np.uint32), bits(v))
+        assert np.array_equal(N(model.read(0, "theta16").view(-1), np.uint16), t16[0])
+    rec = model.step_record()
+    assert rec.t == 3 and rec.skipped_steps == 0
+    assert abs(rec.grad_norm - st.grad_norm) <= 1e-5 * st.grad_norm
+
+
+def test_synth_matches_oracle(S, oracle):
+    a = N(S.synth_uniform_f32(100_000, 3, 17, 0.25), np.uint32)
+    assert np.array_equal(a, bits(oracle.synth_f32(0, 100_000, 3, 17, 0.25)))
+    h = N(S.synth_uniform_f16(100_000, 3, 18, 2.0**-7, 1024.0), np.uint16)
+    assert np.array_equal(h, oracle.synth_f16(0, 100_000, 3, 18, 2.0**-7, 1024.0))
