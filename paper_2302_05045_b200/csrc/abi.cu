@@ -445,6 +445,7 @@ struct samo_model {
   cudaGraphExec_t graph = nullptr;
   samo_comm* graph_comm = nullptr;
   uint64_t graph_kernels = 0;
+  cudaStream_t capture_stream = nullptr;
 };
 
 static uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
@@ -582,6 +583,7 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
 int samo_model_destroy(samo_model* md) {
   if (!md) return clear_ok();
   if (md->graph) cudaGraphExecDestroy(md->graph);
+  if (md->capture_stream) cudaStreamDestroy(md->capture_stream);
   if (md->block) cudaFree(md->block);
   delete md;
   return clear_ok();
@@ -798,12 +800,15 @@ int samo_model_step_graph(samo_model* md, samo_stream_t stream) {
     md->graph = nullptr;
   }
   if (!md->graph) {
-    if (s == nullptr) return fail(SAMO_E_PARAMETER, "graph steps need a non-default stream");
+    // Capture on a private stream (the legacy default stream cannot be
+    // captured); the instantiated graph is then launched on the caller's.
+    if (!md->capture_stream)
+      SAMO_CUDA_TRY(cudaStreamCreateWithFlags(&md->capture_stream, cudaStreamNonBlocking));
     const uint64_t before = samo_kernel_launch_count();
-    SAMO_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    int rc = samo_model_step(md, stream);
+    SAMO_CUDA_TRY(cudaStreamBeginCapture(md->capture_stream, cudaStreamCaptureModeThreadLocal));
+    int rc = samo_model_step(md, md->capture_stream);
     cudaGraph_t graph = nullptr;
-    cudaError_t e = cudaStreamEndCapture(s, &graph);
+    cudaError_t e = cudaStreamEndCapture(md->capture_stream, &graph);
     if (rc != SAMO_OK) {
       if (graph) cudaGraphDestroy(graph);
       return rc;

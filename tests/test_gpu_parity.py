@@ -306,7 +306,14 @@ def test_config1_fc4096_vs_oracle(S, oracle):
         assert np.array_equal(N(model.read(0, "theta16").view(-1), np.uint16), t16[0])
     rec = model.step_record()
     assert rec.t == 3 and rec.skipped_steps == 0
-    assert abs(rec.grad_norm - st.grad_norm) <= 1e-5 * st.grad_norm
+    # Grad norm: the reference sums g*g serially in fp32 (train.hpp:627), whose
+    # own error grows like n*2^-24; the device sums fixed per-CTA fp32 trees in
+    # double.  Both are checked against the exact (fp64) norm: device within
+    # rel 1e-5, reference within its serial-summation bound.
+    g = oracle.h2f(grad[idx]).astype(np.float64) / 1024.0
+    exact = float(np.sqrt(np.sum(g * g)))
+    assert abs(rec.grad_norm - exact) <= 1e-5 * exact
+    assert abs(st.grad_norm - exact) <= idx.size * 2.0**-24 * exact
 
 
 def test_synth_matches_oracle(S, oracle):
