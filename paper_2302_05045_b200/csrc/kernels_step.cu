@@ -21,6 +21,7 @@
 //       of the freshly updated weights) and writes it back with one bulk
 //       store, double-buffered against the next tile's Adam work.
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -432,10 +433,17 @@ int launch_tiles_fill(SamoTile* tiles, uint32_t ntiles, const uint64_t* k_off,
 }
 
 static int occupancy_grid(const void* fn, int threads, size_t smem) {
+  const char* env = getenv("SAMO_CARVEOUT");  // tuning override (percent shared)
+  if (env && *env)
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(env));
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
+  if (const char* env = getenv("SAMO_CTAS_PER_SM")) {  // tuning override
+    const int want = atoi(env);
+    if (want > 0 && want < per_sm) per_sm = want;
+  }
   return per_sm * num_sms();
 }
 
