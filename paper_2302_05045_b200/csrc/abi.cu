@@ -428,6 +428,7 @@ struct samo_model {
   float* v = nullptr;
   float* g = nullptr;          // n_tot + 1: the last slot carries the non-finite indicator
   uint32_t* idx = nullptr;
+  uint32_t* bitmap = nullptr;  // tile t owns words [t*T/32, (t+1)*T/32)
   uint16_t* theta16 = nullptr;
   SamoTile* tiles = nullptr;
   SamoLayerDev* layers_dev = nullptr;
@@ -440,7 +441,7 @@ struct samo_model {
   samo_comm* comm = nullptr;
   bool finalized = false;
   bool grads_set = false;
-  int grid_gather = 0, grid_update = 0;
+  int grid_gather16 = 0, grid_gather32 = 0, grid_update16 = 0, grid_update32 = 0;
   // CUDA graph of one step
   cudaGraphExec_t graph = nullptr;
   samo_comm* graph_comm = nullptr;
@@ -499,12 +500,20 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   }
   md->ntiles = static_cast<uint32_t>(ntiles);
 
-  md->grid_gather = gather_grid(tile_elems);
-  md->grid_update = expand_grid<kModeAdam, uint16_t>(tile_elems);
-  const int max_grid = std::max(md->grid_gather, md->grid_update);
+  if (tile_elems > 16384) {
+    delete md;
+    return fail(SAMO_E_PARAMETER, "the step kernels support tile_elems <= 16384");
+  }
+  md->grid_gather16 = step_grid(0, false, tile_elems);
+  md->grid_gather32 = step_grid(0, true, tile_elems);
+  md->grid_update16 = step_grid(1, false, tile_elems);
+  md->grid_update32 = step_grid(1, true, tile_elems);
+  const int max_grid = std::max(md->grid_update16, md->grid_update32);
 
   // Carve one allocation.
-  const uint64_t n_al = align_up(md->n_tot, 64);
+  // +64 elements of slack: the update kernel's 16-byte aligned bulk loads may
+  // read up to 7 elements past the last kept one.
+  const uint64_t n_al = align_up(md->n_tot + 64, 64);
   uint64_t off = 0;
   auto carve = [&](uint64_t bytes) {
     const uint64_t o = off;
@@ -513,6 +522,7 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   };
   const uint64_t o_theta = carve(n_al * 4), o_m = carve(n_al * 4), o_v = carve(n_al * 4);
   const uint64_t o_g = carve((n_al + 64) * 4), o_idx = carve(n_al * 4);
+  const uint64_t o_bm = carve(static_cast<uint64_t>(ntiles) * (tile_elems / 8));
   const uint64_t o_t16 = carve(md->d_tot * 2), o_tiles = carve(ntiles * sizeof(SamoTile));
   const uint64_t o_layers = carve(std::max(1, nlayers) * sizeof(SamoLayerDev));
   const uint64_t o_koff = carve((nlayers + 1) * sizeof(uint64_t));
@@ -529,6 +539,7 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   md->v = reinterpret_cast<float*>(b + o_v);
   md->g = reinterpret_cast<float*>(b + o_g);
   md->idx = reinterpret_cast<uint32_t*>(b + o_idx);
+  md->bitmap = reinterpret_cast<uint32_t*>(b + o_bm);
   md->theta16 = reinterpret_cast<uint16_t*>(b + o_t16);
   md->tiles = reinterpret_cast<SamoTile*>(b + o_tiles);
   md->layers_dev = reinterpret_cast<SamoLayerDev*>(b + o_layers);
@@ -653,6 +664,7 @@ int samo_model_finalize(samo_model* md, samo_stream_t stream) {
     SAMO_CUDA_TRY(cudaMemcpyAsync(md->tiles, md->tiles_host.data(), md->ntiles * sizeof(SamoTile),
                                   cudaMemcpyHostToDevice, s));
     SAMO_TRY(launch_tiles_fill(md->tiles, md->ntiles, md->k_off_dev, md->idx, s));
+    SAMO_TRY(launch_build_bitmap(md->tiles, md->ntiles, md->tile_elems, md->idx, md->bitmap, s));
   }
   SAMO_CUDA_TRY(cudaStreamSynchronize(s));
   md->finalized = true;
@@ -739,17 +751,44 @@ static int step_ready(samo_model* md) {
   return SAMO_OK;
 }
 
-int samo_model_gather(samo_model* md, samo_stream_t stream) {
-  SAMO_TRY(step_ready(md));
-  if (!md->grads_set) return fail(SAMO_E_STATE, "optimizer_step requires backward (no gradients set)");
-  // inv_scale = 1/loss_scale exactly as train.hpp:619; 1/G folded in (exact
-  // for power-of-two G).
+}  // extern "C"
+
+// The gradient arena holds unscaled fp32 when it is exchanged between ranks,
+// and the raw compressed binary16 gradient (the reference's grad16) otherwise.
+static bool wide_grads(const samo_model* md) { return comm_size(md) > 1; }
+
+static StepArgs step_args(samo_model* md) {
+  StepArgs a{};
+  a.tiles = md->tiles;
+  a.ntiles = md->ntiles;
+  a.tile_elems = md->tile_elems;
+  a.layers = md->layers_dev;
+  a.bitmap = md->bitmap;
+  a.g = md->g;
+  a.theta = md->theta;
+  a.m = md->m;
+  a.v = md->v;
+  // inv_scale = 1/loss_scale exactly as train.hpp:619; with an fp32 exchange
+  // 1/G is folded in (exact for power-of-two G).
   float inv_scale = 1.0f / md->cfg.loss_scale;
   const int G = comm_size(md);
   if (G > 1) inv_scale = inv_scale * (1.0f / static_cast<float>(G));
-  SAMO_TRY(launch_gather_unscale(md->tiles, md->ntiles, md->tile_elems, md->layers_dev, md->idx,
-                                 md->g, inv_scale, md->g + md->n_tot, md->grid_gather,
-                                 as_stream(stream)));
+  a.inv_scale = inv_scale;
+  a.prm = adam_params(&md->cfg);
+  a.st = md->st;
+  a.flag_slot = md->g + md->n_tot;
+  a.norm_partials = md->norm_partials;
+  return a;
+}
+
+extern "C" {
+
+int samo_model_gather(samo_model* md, samo_stream_t stream) {
+  SAMO_TRY(step_ready(md));
+  if (!md->grads_set) return fail(SAMO_E_STATE, "optimizer_step requires backward (no gradients set)");
+  const bool wide = wide_grads(md);
+  SAMO_TRY(launch_gather(step_args(md), wide, wide ? md->grid_gather32 : md->grid_gather16,
+                         as_stream(stream)));
   return clear_ok();
 }
 
@@ -764,23 +803,9 @@ int samo_model_exchange(samo_model* md, samo_stream_t stream) {
 
 int samo_model_update(samo_model* md, samo_stream_t stream) {
   SAMO_TRY(step_ready(md));
-  ExpandArgs a{};
-  a.tiles = md->tiles;
-  a.ntiles = md->ntiles;
-  a.tile_elems = md->tile_elems;
-  a.layers = md->layers_dev;
-  a.idx = md->idx;
-  a.theta = md->theta;
-  a.m = md->m;
-  a.v = md->v;
-  a.g = md->g;
-  a.prm = adam_params(&md->cfg);
-  a.st = md->st;
-  a.flag_slot = md->g + md->n_tot;
-  a.norm_partials = md->norm_partials;
-  a.use_bulk = 1;
-  if (md->ntiles == 0) return clear_ok();
-  SAMO_TRY((launch_expand<kModeAdam, uint16_t>(a, md->grid_update, as_stream(stream))));
+  const bool wide = wide_grads(md);
+  SAMO_TRY(launch_update(step_args(md), wide, wide ? md->grid_update32 : md->grid_update16,
+                         as_stream(stream)));
   return clear_ok();
 }
 

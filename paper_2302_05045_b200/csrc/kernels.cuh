@@ -1,15 +1,15 @@
 // kernels.cuh — launch interfaces of the SAMO step kernels (kernels_step.cu).
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace samo_dev {
 
 constexpr int kThreads = 256;       // threads per CTA for the tile kernels
-constexpr int kGatherStages = 3;    // TMA ring depth of the gather kernel
 
 enum ExpandMode : int {
-  kModeAdam = 0,      // K23: Adam + downcast + expand (train.hpp:640-651)
   kModeDowncast = 1,  // K3 : downcast + expand (train.hpp:647-651)
   kModeValues = 2,    // expand<T> of given values (store.hpp:72-87)
   kModeCheck = 3      // check_state_invariants (store.hpp:171-197)
@@ -22,14 +22,7 @@ struct ExpandArgs {
   const SamoLayerDev* layers;  // per-layer dense output (theta16) pointers
   const uint32_t* idx;         // index arena (layer-local indices)
   float* theta;                // compressed fp32 master weights
-  float* m;
-  float* v;
-  const float* g;              // exchanged grad32
   const void* values;          // kModeValues: compressed values (u16/u32)
-  SamoAdamParams prm;
-  SamoStepState* st;           // kModeAdam: device scalars
-  float* flag_slot;            // kModeAdam: non-finite indicator (reset here)
-  float* norm_partials;        // kModeAdam: one per CTA
   uint32_t* mismatch;          // kModeCheck: set to nonzero on violation
   int use_bulk;                // 1 when every dense output is 16-byte aligned
 };
@@ -39,11 +32,32 @@ struct ExpandArgs {
 int launch_tiles_fill(SamoTile* tiles, uint32_t ntiles, const uint64_t* k_off,
                       const uint32_t* idx, cudaStream_t s);
 
-// K1: gather + unscale + cast + finite flag.
-int launch_gather_unscale(const SamoTile* tiles, uint32_t ntiles, uint32_t tile_elems,
-                          const SamoLayerDev* layers, const uint32_t* idx, float* g32,
-                          float inv_scale, float* flag_slot, int grid, cudaStream_t s);
-int gather_grid(uint32_t tile_elems);
+// Arguments of the two per-step kernels (kernels_fused.cu).
+struct StepArgs {
+  const SamoTile* tiles;
+  uint32_t ntiles;
+  uint32_t tile_elems;
+  const SamoLayerDev* layers;  // dense gradient inputs / theta16 outputs
+  const uint32_t* bitmap;      // tile t owns words [t*T/32, (t+1)*T/32)
+  void* g;                     // compressed gradient arena: fp32 or binary16
+  float* theta;
+  float* m;
+  float* v;
+  float inv_scale;             // 1/loss_scale (and 1/G when exchanging fp32)
+  SamoAdamParams prm;
+  SamoStepState* st;
+  float* flag_slot;            // non-finite indicator (summed across ranks)
+  float* norm_partials;        // one per K23 CTA
+};
+
+// K1 gather: out_f32 -> unscaled fp32 for the exchange, else raw binary16.
+int launch_gather(const StepArgs& a, bool out_f32, int grid, cudaStream_t s);
+// K23 update: g_f32 selects the gradient arena type written by K1.
+int launch_update(const StepArgs& a, bool g_f32, int grid, cudaStream_t s);
+// which: 0 = gather, 1 = update; wide = fp32 gradient arena.
+int step_grid(int which, bool wide, uint32_t tile_elems);
+int launch_build_bitmap(const SamoTile* tiles, uint32_t ntiles, uint32_t tile_elems,
+                        const uint32_t* idx, uint32_t* bitmap, cudaStream_t s);
 
 template <int MODE, typename OutT>
 int launch_expand(const ExpandArgs& a, int grid, cudaStream_t s);
