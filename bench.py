@@ -358,8 +358,13 @@ def run_samo(args) -> None:
     value = world * phi / (ms_step * 1e-3)
 
     pk = peaks()
-    bytes_k1 = 2 * phi + 8 * nnz
-    bytes_k23 = 2 * phi + 32 * nnz
+    # Algorithmic bytes per launch: dense grad read 2phi + off16
+    # 2n + compressed grad write (fp32 4n when exchanged, binary16 2n
+    # otherwise); K23: grad read + off16 2n + theta/m/v read+write 24n + dense
+    # theta16 write 2phi.
+    gb = 4 if world > 1 else 2
+    bytes_k1 = 2 * phi + 2 * nnz + gb * nnz
+    bytes_k23 = 2 * phi + 2 * nnz + gb * nnz + 24 * nnz
     k1_ms = statistics.mean(k1)
     k23_ms = statistics.mean(k23)
     ar_ms = statistics.mean(ar)

@@ -428,7 +428,7 @@ struct samo_model {
   float* v = nullptr;
   float* g = nullptr;          // n_tot + 1: the last slot carries the non-finite indicator
   uint32_t* idx = nullptr;
-  uint32_t* bitmap = nullptr;  // tile t owns words [t*T/32, (t+1)*T/32)
+  uint16_t* off16 = nullptr;   // idx[k] - dense_begin of k's tile (step kernels)
   uint16_t* theta16 = nullptr;
   SamoTile* tiles = nullptr;
   SamoLayerDev* layers_dev = nullptr;
@@ -500,7 +500,7 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   }
   md->ntiles = static_cast<uint32_t>(ntiles);
 
-  if (tile_elems > 16384) {
+  if (tile_elems > 16384) {  // two dense out tiles + the stage ring must fit in shared memory
     delete md;
     return fail(SAMO_E_PARAMETER, "the step kernels support tile_elems <= 16384");
   }
@@ -522,7 +522,7 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   };
   const uint64_t o_theta = carve(n_al * 4), o_m = carve(n_al * 4), o_v = carve(n_al * 4);
   const uint64_t o_g = carve((n_al + 64) * 4), o_idx = carve(n_al * 4);
-  const uint64_t o_bm = carve(static_cast<uint64_t>(ntiles) * (tile_elems / 8));
+  const uint64_t o_off = carve(n_al * 2);
   const uint64_t o_t16 = carve(md->d_tot * 2), o_tiles = carve(ntiles * sizeof(SamoTile));
   const uint64_t o_layers = carve(std::max(1, nlayers) * sizeof(SamoLayerDev));
   const uint64_t o_koff = carve((nlayers + 1) * sizeof(uint64_t));
@@ -539,7 +539,7 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   md->v = reinterpret_cast<float*>(b + o_v);
   md->g = reinterpret_cast<float*>(b + o_g);
   md->idx = reinterpret_cast<uint32_t*>(b + o_idx);
-  md->bitmap = reinterpret_cast<uint32_t*>(b + o_bm);
+  md->off16 = reinterpret_cast<uint16_t*>(b + o_off);
   md->theta16 = reinterpret_cast<uint16_t*>(b + o_t16);
   md->tiles = reinterpret_cast<SamoTile*>(b + o_tiles);
   md->layers_dev = reinterpret_cast<SamoLayerDev*>(b + o_layers);
@@ -664,7 +664,7 @@ int samo_model_finalize(samo_model* md, samo_stream_t stream) {
     SAMO_CUDA_TRY(cudaMemcpyAsync(md->tiles, md->tiles_host.data(), md->ntiles * sizeof(SamoTile),
                                   cudaMemcpyHostToDevice, s));
     SAMO_TRY(launch_tiles_fill(md->tiles, md->ntiles, md->k_off_dev, md->idx, s));
-    SAMO_TRY(launch_build_bitmap(md->tiles, md->ntiles, md->tile_elems, md->idx, md->bitmap, s));
+    SAMO_TRY(launch_build_off16(md->tiles, md->ntiles, md->idx, md->off16, s));
   }
   SAMO_CUDA_TRY(cudaStreamSynchronize(s));
   md->finalized = true;
@@ -763,7 +763,7 @@ static StepArgs step_args(samo_model* md) {
   a.ntiles = md->ntiles;
   a.tile_elems = md->tile_elems;
   a.layers = md->layers_dev;
-  a.bitmap = md->bitmap;
+  a.off16 = md->off16;
   a.g = md->g;
   a.theta = md->theta;
   a.m = md->m;

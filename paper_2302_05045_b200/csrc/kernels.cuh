@@ -38,7 +38,7 @@ struct StepArgs {
   uint32_t ntiles;
   uint32_t tile_elems;
   const SamoLayerDev* layers;  // dense gradient inputs / theta16 outputs
-  const uint32_t* bitmap;      // tile t owns words [t*T/32, (t+1)*T/32)
+  const uint16_t* off16;       // kept index relative to its tile's dense_begin
   void* g;                     // compressed gradient arena: fp32 or binary16
   float* theta;
   float* m;
@@ -56,8 +56,8 @@ int launch_gather(const StepArgs& a, bool out_f32, int grid, cudaStream_t s);
 int launch_update(const StepArgs& a, bool g_f32, int grid, cudaStream_t s);
 // which: 0 = gather, 1 = update; wide = fp32 gradient arena.
 int step_grid(int which, bool wide, uint32_t tile_elems);
-int launch_build_bitmap(const SamoTile* tiles, uint32_t ntiles, uint32_t tile_elems,
-                        const uint32_t* idx, uint32_t* bitmap, cudaStream_t s);
+int launch_build_off16(const SamoTile* tiles, uint32_t ntiles, const uint32_t* idx,
+                       uint16_t* off16, cudaStream_t s);
 
 template <int MODE, typename OutT>
 int launch_expand(const ExpandArgs& a, int grid, cudaStream_t s);

@@ -3,35 +3,31 @@
 // Data layout (per rank, HBM):
 //   dense side : per-layer binary16 gradients (inputs) and theta16 (outputs),
 //                cut into tiles of T dense elements (T = tile_elems, 8192 by
-//                default); tile t also owns T/32 bitmap words at
-//                bitmap[t * T/32] — bit (d & 31) of word (d >> 5) set iff
-//                dense element dense_begin + d is kept.  The bitmap is derived
-//                once from the reference's ascending u32 index set
-//                (PrunedIndexSet, prune.hpp:21-27) and carries the same
-//                information in T/8 bytes per tile instead of 4 bytes per kept
-//                element.
-//   compressed : flat arenas theta32 / adam_m / adam_v / grad (layer
-//                segments concatenated in layer order); the kept elements of
-//                tile t are the contiguous range [k_begin, k_end).
+//                default, <= 65536).
+//   compressed : flat arenas theta32 / adam_m / adam_v / grad and the tile-
+//                local index arena off16 (layer segments concatenated in layer
+//                order).  The kept elements of tile t are the contiguous range
+//                [k_begin, k_end); off16[k] = idx[k] - dense_begin is the
+//                reference index (PrunedIndexSet, prune.hpp:21-27) relative to
+//                its tile — derived once, 2 bytes per kept element instead of
+//                the 4 of the u32 index set, and directly usable as a shared-
+//                memory offset by both kernels.
 //
 // K1 gather (train.hpp:598-611 sink + 619-629 unscale/finite):
-//   TMA ring: each stage = one dense gradient tile + its bitmap (cp.async.bulk,
-//   mbarrier complete_tx).  The consumer ranks the set bits with a block
-//   exclusive scan, gathers the kept halves out of shared memory into a
-//   compacted shared buffer (converted and unscaled when the exchange needs
-//   fp32; raw binary16 — the reference's grad16 — otherwise) and writes it
-//   with coalesced stores.  Non-finite gradients raise the step's skip flag.
+//   TMA ring of dense gradient tiles (cp.async.bulk + mbarrier complete_tx);
+//   kept elements gathered out of shared memory through off16, written with
+//   coalesced stores — unscaled fp32 when the gradient is exchanged between
+//   ranks, the raw compressed binary16 (the reference's grad16) otherwise.
+//   Non-finite gradients raise the step's skip flag.
 //
 // K23 update (train.hpp:632-654, adam_update 332-347, expand store.hpp:72-87):
-//   TMA ring over chunks of <= kChunk kept elements: each stage holds the
-//   16-byte aligned superset of theta32/m/v/grad for the chunk (+ the tile's
-//   bitmap on a tile's first chunk).  Per tile the bitmap is decoded into a
-//   u16 list of dense offsets, the dense theta16 tile is built in shared
-//   memory (zero fill + scatter of half_rn(theta)) and written back with one
-//   bulk store, double-buffered against the next tile.  theta/m/v are written
-//   straight from registers with coalesced stores.  The last CTA to finish
-//   reduces the per-CTA grad-norm partials in CTA order and advances the
-//   device-resident Adam scalars.
+//   TMA ring over chunks of <= kChunk kept elements; a stage holds the
+//   16-byte aligned superset of theta32/m/v/grad/off16 of the chunk.  Per tile
+//   the dense theta16 tile is built in shared memory (zero fill + scatter of
+//   half_rn(theta) at off16) and written back with one bulk store,
+//   double-buffered against the next tile.  theta/m/v are written straight
+//   from registers with coalesced stores.  The last CTA reduces the per-CTA
+//   grad-norm partials in CTA order and advances the device Adam scalars.
 //
 // Both kernels are persistent (grid = resident CTAs x SMs) and HBM-bound.
 #include <cstdio>
@@ -45,35 +41,10 @@ namespace {
 constexpr int kChunk = 1024;  // kept elements per K23 stage
 constexpr int kK1Stages = 3;
 constexpr int kK23Stages = 3;
+constexpr int kU = 4;         // independent elements per thread and pass (ILP)
 
 __device__ __forceinline__ bool finite_f32(float x) {
   return (__float_as_uint(x) & 0x7F800000u) != 0x7F800000u;
-}
-
-// Block-wide exclusive scan of one uint32 per thread.  `ws` must hold
-// kThreads/32 words; callers separate consecutive scans by a __syncthreads.
-__device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* ws, uint32_t& total) {
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t incl = x;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-    if (lane >= static_cast<uint32_t>(o)) incl += y;
-  }
-  if (lane == 31) ws[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t v = lane < kThreads / 32 ? ws[lane] : 0u;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, v, o);
-      if (lane >= static_cast<uint32_t>(o)) v += y;
-    }
-    if (lane < kThreads / 32) ws[lane] = v;
-  }
-  __syncthreads();
-  total = ws[kThreads / 32 - 1];
-  return incl - x + (warp ? ws[warp - 1] : 0u);
 }
 
 __device__ __forceinline__ void st_na_f32(float* p, float v) {
@@ -84,25 +55,15 @@ __device__ __forceinline__ void st_na_u16(uint16_t* p, uint16_t v) {
 }
 
 // ---------------------------------------------------------------------------
-// Bitmap construction (one CTA per tile, once at finalize).
+// off16 construction (once, at finalize).
 
 __global__ void __launch_bounds__(kThreads)
-k_build_bitmap(const SamoTile* __restrict__ tiles, uint32_t ntiles, uint32_t tile_elems,
-               const uint32_t* __restrict__ idx, uint32_t* __restrict__ bitmap) {
-  extern __shared__ uint32_t words[];
-  const uint32_t nw = tile_elems / 32;
+k_build_off16(const SamoTile* __restrict__ tiles, uint32_t ntiles, const uint32_t* __restrict__ idx,
+              uint16_t* __restrict__ off16) {
   for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const SamoTile td = tiles[t];
-    for (uint32_t i = threadIdx.x; i < nw; i += kThreads) words[i] = 0u;
-    __syncthreads();
-    for (uint64_t k = td.k_begin + threadIdx.x; k < td.k_end; k += kThreads) {
-      const uint32_t d = idx[k] - td.dense_begin;
-      atomicOr(&words[d >> 5], 1u << (d & 31));
-    }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < nw; i += kThreads)
-      bitmap[static_cast<uint64_t>(t) * nw + i] = words[i];
-    __syncthreads();
+    for (uint64_t k = td.k_begin + threadIdx.x; k < td.k_end; k += kThreads)
+      off16[k] = static_cast<uint16_t>(idx[k] - td.dense_begin);
   }
 }
 
@@ -111,14 +72,10 @@ k_build_bitmap(const SamoTile* __restrict__ tiles, uint32_t ntiles, uint32_t til
 
 template <bool OUT_F32>
 __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
-  using OutT = typename std::conditional<OUT_F32, float, uint16_t>::type;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[kK1Stages];
-  __shared__ uint32_t ws[kThreads / 32];
 
-  const uint32_t T = a.tile_elems, NW = T / 32;
-  const uint32_t stage_bytes = T * 2 + NW * 4;
-  OutT* cbuf = reinterpret_cast<OutT*>(smem + kK1Stages * stage_bytes);
+  const uint32_t T = a.tile_elems;
   const uint32_t tid = threadIdx.x;
   const uint64_t policy = policy_evict_first();
   if (tid == 0) {
@@ -129,11 +86,14 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
 
   auto issue = [&](uint32_t t, int s) {
     const SamoTile td = a.tiles[t];
-    uint8_t* st = smem + s * stage_bytes;
-    const uint32_t gbytes = (td.dense_count * 2u) & ~15u;
-    mbar_arrive_expect_tx(&full[s], gbytes + NW * 4);
-    if (gbytes) bulk_g2s(st, a.layers[td.layer].grad + td.dense_begin, gbytes, &full[s], policy);
-    bulk_g2s(st + T * 2, a.bitmap + static_cast<uint64_t>(t) * NW, NW * 4, &full[s], policy);
+    const uint32_t bytes = (td.dense_count * 2u) & ~15u;
+    if (bytes) {
+      mbar_arrive_expect_tx(&full[s], bytes);
+      bulk_g2s(smem + static_cast<size_t>(s) * T * 2, a.layers[td.layer].grad + td.dense_begin,
+               bytes, &full[s], policy);
+    } else {
+      mbar_arrive(&full[s]);
+    }
   };
   if (tid == 0) {
     for (int s = 0; s < kK1Stages; ++s) {
@@ -142,7 +102,6 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
     }
   }
 
-  const uint32_t W = (NW + kThreads - 1) / kThreads;  // bitmap words per thread
   bool bad = false;
   uint32_t it = 0;
   for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++it) {
@@ -150,34 +109,34 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
     const SamoTile td = a.tiles[t];
     const uint16_t* gsrc = a.layers[td.layer].grad + td.dense_begin;
     const uint32_t staged = ((td.dense_count * 2u) & ~15u) >> 1;
-    const uint8_t* st = smem + s * stage_bytes;
-    const uint16_t* sg = reinterpret_cast<const uint16_t*>(st);
-    const uint32_t* bm = reinterpret_cast<const uint32_t*>(st + T * 2);
+    const uint16_t* sg = reinterpret_cast<const uint16_t*>(smem + static_cast<size_t>(s) * T * 2);
     mbar_wait(&full[s], (it / kK1Stages) & 1u);
 
-    const uint32_t w0 = tid * W;
-    uint32_t cnt = 0;
-    for (uint32_t w = w0; w < w0 + W && w < NW; ++w) cnt += __popc(bm[w]);
-    uint32_t total;
-    uint32_t pos = block_excl_scan(cnt, ws, total);
-    for (uint32_t w = w0; w < w0 + W && w < NW; ++w) {
-      uint32_t bits = bm[w];
-      while (bits) {
-        const uint32_t j = __ffs(bits) - 1;
-        bits &= bits - 1;
-        const uint32_t d = w * 32 + j;
-        const uint16_t h = d < staged ? sg[d] : gsrc[d];
-        if constexpr (OUT_F32) {
-          const float gk = mul_x86(f16_bits_to_f32(h), a.inv_scale);
-          bad |= !finite_f32(gk);
-          cbuf[pos++] = gk;
-        } else {
-          bad |= (h & 0x7C00u) == 0x7C00u;  // |h * 2^-k| is finite iff h is
-          cbuf[pos++] = h;
+#pragma unroll 1
+    for (uint64_t kb = td.k_begin + tid; kb < td.k_end; kb += kU * kThreads) {
+      uint16_t off[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint64_t k = kb + static_cast<uint64_t>(u) * kThreads;
+        off[u] = k < td.k_end ? ld_stream_u16(a.off16 + k) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const uint64_t k = kb + static_cast<uint64_t>(u) * kThreads;
+        if (k < td.k_end) {
+          const uint16_t h = off[u] < staged ? sg[off[u]] : gsrc[off[u]];
+          if constexpr (OUT_F32) {
+            const float gk = mul_x86(f16_bits_to_f32(h), a.inv_scale);
+            bad |= !finite_f32(gk);
+            st_na_f32(reinterpret_cast<float*>(a.g) + k, gk);
+          } else {
+            bad |= (h & 0x7C00u) == 0x7C00u;  // |h * 2^-s| is finite iff h is
+            st_na_u16(reinterpret_cast<uint16_t*>(a.g) + k, h);
+          }
         }
       }
     }
-    __syncthreads();  // stage s fully read, cbuf complete
+    __syncthreads();  // every thread is done reading stage s
     if (tid == 0) {
       const uint64_t tn = t + static_cast<uint64_t>(kK1Stages) * gridDim.x;
       if (tn < a.ntiles) {
@@ -185,24 +144,12 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
         issue(static_cast<uint32_t>(tn), s);
       }
     }
-    OutT* dst = reinterpret_cast<OutT*>(a.g) + td.k_begin;
-    for (uint32_t i = tid; i < total; i += kThreads) {
-      if constexpr (OUT_F32) st_na_f32(dst + i, cbuf[i]);
-      else st_na_u16(dst + i, cbuf[i]);
-    }
-    // the next tile's scan (which begins with a barrier) orders these reads of
-    // cbuf before it is overwritten
   }
   if (__syncthreads_or(bad) && tid == 0) atomicAdd(a.flag_slot, 1.0f);
 }
 
 // ---------------------------------------------------------------------------
 // K23
-
-struct ChunkPlan {
-  uint64_t kc0, kc1;  // kept-element range of the chunk
-  uint32_t j, nch;    // chunk index within its tile, chunks in the tile
-};
 
 __device__ __forceinline__ uint32_t tile_chunks(const SamoTile& td) {
   const uint64_t n = td.k_end - td.k_begin;
@@ -211,8 +158,10 @@ __device__ __forceinline__ uint32_t tile_chunks(const SamoTile& td) {
 
 template <bool G16>
 struct K23Layout {
-  static constexpr uint32_t kF32 = (kChunk + 8) * 4;                  // theta/m/v/g32 slot
-  static constexpr uint32_t kG = G16 ? (kChunk + 16) * 2 : kF32;     // grad slot
+  static constexpr uint32_t kF32 = (kChunk + 8) * 4;                 // theta/m/v/g32 slot
+  static constexpr uint32_t kG = G16 ? (kChunk + 16) * 2 : kF32;    // grad slot
+  static constexpr uint32_t kOff = (kChunk + 16) * 2;               // off16 slot
+  static constexpr uint32_t kStage = 3 * kF32 + kG + kOff;
 };
 
 template <bool G16>
@@ -220,15 +169,11 @@ __global__ void __launch_bounds__(kThreads) k23_update(StepArgs a) {
   using L = K23Layout<G16>;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[kK23Stages];
-  __shared__ uint32_t ws[kThreads / 32];
   __shared__ float red[kThreads / 32];
   __shared__ int last_cta;
 
-  const uint32_t T = a.tile_elems, NW = T / 32;
-  const uint32_t stage_bytes = 3 * L::kF32 + L::kG + NW * 4;
-  uint8_t* lst_raw = smem + kK23Stages * stage_bytes;
-  uint16_t* lst = reinterpret_cast<uint16_t*>(lst_raw);               // T entries
-  uint16_t* outb = reinterpret_cast<uint16_t*>(lst_raw + T * 2);      // 2 x T halves
+  const uint32_t T = a.tile_elems;
+  uint16_t* outb = reinterpret_cast<uint16_t*>(smem + kK23Stages * L::kStage);  // 2 x T halves
   const uint32_t tid = threadIdx.x;
 
   // Step scalars (train.hpp:640-642), identical float ops in every CTA.
@@ -253,31 +198,25 @@ __global__ void __launch_bounds__(kThreads) k23_update(StepArgs a) {
     const SamoTile td = a.tiles[pt];
     const uint64_t kc0 = td.k_begin + static_cast<uint64_t>(pj) * kChunk;
     const uint64_t kc1 = min(td.k_end, kc0 + kChunk);
-    uint8_t* st = smem + s * stage_bytes;
-    const uint64_t f0 = kc0 & ~3ull, f1 = (kc1 + 3) & ~3ull;
-    const uint32_t fb = static_cast<uint32_t>((f1 - f0) * 4);
-    uint32_t gb;
-    uint64_t g0;
-    if (G16) {
-      g0 = kc0 & ~7ull;
-      gb = static_cast<uint32_t>((((kc1 + 7) & ~7ull) - g0) * 2);
-    } else {
-      g0 = f0;
-      gb = fb;
-    }
-    const uint32_t bmb = pj == 0 ? NW * 4 : 0u;
-    mbar_arrive_expect_tx(&full[s], 3 * fb + gb + bmb);
+    uint8_t* st = smem + s * L::kStage;
+    const uint64_t f0 = kc0 & ~3ull;
+    const uint32_t fb = static_cast<uint32_t>((((kc1 + 3) & ~3ull) - f0) * 4);
+    const uint64_t h0 = kc0 & ~7ull;
+    const uint32_t hb = static_cast<uint32_t>((((kc1 + 7) & ~7ull) - h0) * 2);
+    const uint32_t gb = G16 ? hb : fb;
+    mbar_arrive_expect_tx(&full[s], 3 * fb + gb + hb);
     if (fb) {
       bulk_g2s(st, a.theta + f0, fb, &full[s], policy);
       bulk_g2s(st + L::kF32, a.m + f0, fb, &full[s], policy);
       bulk_g2s(st + 2 * L::kF32, a.v + f0, fb, &full[s], policy);
     }
     if (gb) {
-      const uint8_t* gsrc = reinterpret_cast<const uint8_t*>(a.g) + g0 * (G16 ? 2 : 4);
+      const void* gsrc = G16 ? static_cast<const void*>(reinterpret_cast<const uint16_t*>(a.g) + h0)
+                             : static_cast<const void*>(reinterpret_cast<const float*>(a.g) + f0);
       bulk_g2s(st + 3 * L::kF32, gsrc, gb, &full[s], policy);
     }
-    if (bmb) bulk_g2s(st + 3 * L::kF32 + L::kG, a.bitmap + static_cast<uint64_t>(pt) * NW, bmb,
-                      &full[s], policy);
+    if (hb) bulk_g2s(st + 3 * L::kF32 + L::kG, a.off16 + h0, hb, &full[s], policy);
+    if (!(fb | hb)) mbar_arrive(&full[s]);  // unreachable: ranges are never empty
     if (++pj >= tile_chunks(td)) {
       pj = 0;
       pt += gridDim.x;
@@ -287,73 +226,78 @@ __global__ void __launch_bounds__(kThreads) k23_update(StepArgs a) {
     for (int s = 0; s < kK23Stages && pt < a.ntiles; ++s) issue(s);
   }
 
-  const uint32_t W = (NW + kThreads - 1) / kThreads;
   float nacc = 0.0f;
   uint32_t it = 0, tile_it = 0;
   for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++tile_it) {
     const SamoTile td = a.tiles[t];
     const uint32_t nch = tile_chunks(td);
     uint16_t* out = outb + (tile_it & 1u) * T;
+    if (!skip) {
+      // The out buffer was last bulk-stored two tiles ago.
+      if (tid == 0 && tile_it >= 2) bulk_wait_read<1>();
+      __syncthreads();
+      uint4* o4 = reinterpret_cast<uint4*>(out);
+      const uint32_t n16 = (td.dense_count * 2u + 15u) >> 4;
+      for (uint32_t i = tid; i < n16; i += kThreads) o4[i] = make_uint4(0u, 0u, 0u, 0u);
+      __syncthreads();
+    }
     for (uint32_t j = 0; j < nch; ++j, ++it) {
       const int s = static_cast<int>(it % kK23Stages);
-      const uint8_t* st = smem + s * stage_bytes;
+      const uint8_t* st = smem + s * L::kStage;
       const uint64_t kc0 = td.k_begin + static_cast<uint64_t>(j) * kChunk;
       const uint64_t kc1 = min(td.k_end, kc0 + kChunk);
+      const uint32_t n = static_cast<uint32_t>(kc1 - kc0);
+      const uint32_t fo = static_cast<uint32_t>(kc0 & 3ull);  // chunk offset in the f32 slots
+      const uint32_t ho = static_cast<uint32_t>(kc0 & 7ull);  // ... in the 16-bit slots
+      const float* sth = reinterpret_cast<const float*>(st) + fo;
+      const float* smv = reinterpret_cast<const float*>(st + L::kF32) + fo;
+      const float* svv = reinterpret_cast<const float*>(st + 2 * L::kF32) + fo;
+      const uint16_t* soff = reinterpret_cast<const uint16_t*>(st + 3 * L::kF32 + L::kG) + ho;
       mbar_wait(&full[s], (it / kK23Stages) & 1u);
 
-      if (j == 0 && !skip) {
-        // New tile: its out buffer was last bulk-stored two tiles ago.
-        if (tid == 0 && tile_it >= 2) bulk_wait_read<1>();
-        const uint32_t* bm = reinterpret_cast<const uint32_t*>(st + 3 * L::kF32 + L::kG);
-        const uint32_t w0 = tid * W;
-        uint32_t cnt = 0;
-        for (uint32_t w = w0; w < w0 + W && w < NW; ++w) cnt += __popc(bm[w]);
-        uint32_t total;
-        uint32_t pos = block_excl_scan(cnt, ws, total);  // has barriers: bulk wait visible
-        for (uint32_t w = w0; w < w0 + W && w < NW; ++w) {
-          uint32_t bits = bm[w];
-          while (bits) {
-            const uint32_t b = __ffs(bits) - 1;
-            bits &= bits - 1;
-            lst[pos++] = static_cast<uint16_t>(w * 32 + b);
+#pragma unroll 1
+      for (uint32_t ib = tid; ib < n; ib += kU * kThreads) {
+        float gv[kU], tv[kU], mv[kU], vv[kU];
+        uint16_t ov[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const uint32_t i = ib + u * kThreads;
+          if (i < n) {
+            if constexpr (G16) {
+              const uint16_t h = reinterpret_cast<const uint16_t*>(st + 3 * L::kF32)[ho + i];
+              gv[u] = mul_x86(f16_bits_to_f32(h), a.inv_scale);
+            } else {
+              gv[u] = reinterpret_cast<const float*>(st + 3 * L::kF32)[fo + i];
+            }
+            tv[u] = sth[i];
+            mv[u] = smv[i];
+            vv[u] = svv[i];
+            ov[u] = soff[i];
           }
         }
-        uint4* o4 = reinterpret_cast<uint4*>(out);
-        const uint32_t n16 = (td.dense_count * 2u + 15u) >> 4;
-        for (uint32_t i = tid; i < n16; i += kThreads) o4[i] = make_uint4(0u, 0u, 0u, 0u);
-        __syncthreads();
-      }
-
-      const float* sth = reinterpret_cast<const float*>(st);
-      const float* smv = reinterpret_cast<const float*>(st + L::kF32);
-      const float* svv = reinterpret_cast<const float*>(st + 2 * L::kF32);
-      const uint64_t f0 = kc0 & ~3ull;
-      const uint64_t g0 = G16 ? (kc0 & ~7ull) : f0;
-      for (uint64_t k = kc0 + tid; k < kc1; k += kThreads) {
-        const uint32_t i = static_cast<uint32_t>(k - f0);
-        const uint32_t ig = static_cast<uint32_t>(k - g0);
-        float gk;
-        if constexpr (G16) {
-          const uint16_t h = reinterpret_cast<const uint16_t*>(st + 3 * L::kF32)[ig];
-          gk = mul_x86(f16_bits_to_f32(h), a.inv_scale);
-        } else {
-          gk = reinterpret_cast<const float*>(st + 3 * L::kF32)[ig];
-        }
-        nacc = __fadd_rn(nacc, __fmul_rn(gk, gk));
-        if (!skip) {
-          // adam_update (train.hpp:338-345): IEEE per op, no contraction.
-          const float mk = __fadd_rn(__fmul_rn(a.prm.beta1, smv[i]), __fmul_rn(omb1, gk));
-          const float vk =
-              __fadd_rn(__fmul_rn(a.prm.beta2, svv[i]), __fmul_rn(omb2, __fmul_rn(gk, gk)));
-          const float mh = __fdiv_rn(mk, bias1);
-          const float vh = __fdiv_rn(vk, bias2);
-          float tk = __fsub_rn(
-              sth[i], __fmul_rn(a.prm.lr, __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), a.prm.eps))));
-          if (a.prm.wd != 0.0f) tk = __fsub_rn(tk, __fmul_rn(lrwd, tk));
-          st_na_f32(a.m + k, mk);
-          st_na_f32(a.v + k, vk);
-          st_na_f32(a.theta + k, tk);
-          out[lst[k - td.k_begin]] = f32_to_f16_bits(tk);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const uint32_t i = ib + u * kThreads;
+          if (i < n) {
+            const float gk = gv[u];
+            nacc = __fadd_rn(nacc, __fmul_rn(gk, gk));
+            if (!skip) {
+              // adam_update (train.hpp:338-345): IEEE per op, no contraction.
+              const float mk = __fadd_rn(__fmul_rn(a.prm.beta1, mv[u]), __fmul_rn(omb1, gk));
+              const float vk =
+                  __fadd_rn(__fmul_rn(a.prm.beta2, vv[u]), __fmul_rn(omb2, __fmul_rn(gk, gk)));
+              const float mh = __fdiv_rn(mk, bias1);
+              const float vh = __fdiv_rn(vk, bias2);
+              float tk = __fsub_rn(
+                  tv[u], __fmul_rn(a.prm.lr, __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), a.prm.eps))));
+              if (a.prm.wd != 0.0f) tk = __fsub_rn(tk, __fmul_rn(lrwd, tk));
+              const uint64_t k = kc0 + i;
+              st_na_f32(a.m + k, mk);
+              st_na_f32(a.v + k, vk);
+              st_na_f32(a.theta + k, tk);
+              out[ov[u]] = f32_to_f16_bits(tk);
+            }
+          }
         }
       }
       const bool last = (j + 1 == nch);
@@ -419,6 +363,9 @@ template <typename F>
 int grid_for(F fn, size_t smem) {
   SAMO_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
+  const char* carve = getenv("SAMO_CARVEOUT");  // tuning override (percent shared)
+  if (carve && *carve)
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(carve));
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem) != cudaSuccess ||
       per_sm < 1)
@@ -430,14 +377,11 @@ int grid_for(F fn, size_t smem) {
 
 }  // namespace
 
-size_t gather_smem(uint32_t tile_elems, bool f32) {
-  return kK1Stages * (tile_elems * 2u + tile_elems / 8u) + tile_elems * (f32 ? 4u : 2u);
-}
+size_t gather_smem(uint32_t tile_elems, bool) { return kK1Stages * tile_elems * 2u; }
 
 size_t update_smem(uint32_t tile_elems, bool g16) {
-  const uint32_t fs = (kChunk + 8) * 4, gs = g16 ? (kChunk + 16) * 2 : fs;
-  return kK23Stages * (3 * fs + gs + tile_elems / 8u) + tile_elems * 2u /*lst*/ +
-         tile_elems * 4u /*2 out tiles*/;
+  return kK23Stages * (g16 ? K23Layout<true>::kStage : K23Layout<false>::kStage) +
+         tile_elems * 4u /* two dense out tiles */;
 }
 
 int step_grid(int which, bool wide, uint32_t tile_elems) {
@@ -449,48 +393,39 @@ int step_grid(int which, bool wide, uint32_t tile_elems) {
   return wide ? grid_for(k23_update<false>, sm) : grid_for(k23_update<true>, sm);
 }
 
+template <typename F>
+static int launch_persistent(F fn, const StepArgs& a, size_t sm, int grid, cudaStream_t s,
+                             const char* what) {
+  SAMO_CUDA_TRY(
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
+  if (static_cast<uint32_t>(grid) > a.ntiles) grid = static_cast<int>(a.ntiles);
+  fn<<<grid, kThreads, sm, s>>>(a);
+  SAMO_LAUNCH_CHECK(what);
+  return SAMO_OK;
+}
+
 int launch_gather(const StepArgs& a, bool out_f32, int grid, cudaStream_t s) {
   if (a.ntiles == 0) return SAMO_OK;
-  const size_t sm = gather_smem(a.tile_elems, out_f32);
   if (grid <= 0) grid = step_grid(0, out_f32, a.tile_elems);
-  if (static_cast<uint32_t>(grid) > a.ntiles) grid = static_cast<int>(a.ntiles);
-  if (out_f32) {
-    SAMO_CUDA_TRY(cudaFuncSetAttribute(k1_gather<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(sm)));
-    k1_gather<true><<<grid, kThreads, sm, s>>>(a);
-  } else {
-    SAMO_CUDA_TRY(cudaFuncSetAttribute(k1_gather<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(sm)));
-    k1_gather<false><<<grid, kThreads, sm, s>>>(a);
-  }
-  SAMO_LAUNCH_CHECK("k1_gather");
-  return SAMO_OK;
+  const size_t sm = gather_smem(a.tile_elems, out_f32);
+  return out_f32 ? launch_persistent(k1_gather<true>, a, sm, grid, s, "k1_gather<f32>")
+                 : launch_persistent(k1_gather<false>, a, sm, grid, s, "k1_gather<f16>");
 }
 
 int launch_update(const StepArgs& a, bool g_f32, int grid, cudaStream_t s) {
   if (a.ntiles == 0) return SAMO_OK;
-  const size_t sm = update_smem(a.tile_elems, !g_f32);
   if (grid <= 0) grid = step_grid(1, g_f32, a.tile_elems);
-  if (static_cast<uint32_t>(grid) > a.ntiles) grid = static_cast<int>(a.ntiles);
-  if (g_f32) {
-    SAMO_CUDA_TRY(cudaFuncSetAttribute(k23_update<false>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-    k23_update<false><<<grid, kThreads, sm, s>>>(a);
-  } else {
-    SAMO_CUDA_TRY(cudaFuncSetAttribute(k23_update<true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-    k23_update<true><<<grid, kThreads, sm, s>>>(a);
-  }
-  SAMO_LAUNCH_CHECK("k23_update");
-  return SAMO_OK;
+  const size_t sm = update_smem(a.tile_elems, !g_f32);
+  return g_f32 ? launch_persistent(k23_update<false>, a, sm, grid, s, "k23_update<f32>")
+               : launch_persistent(k23_update<true>, a, sm, grid, s, "k23_update<f16>");
 }
 
-int launch_build_bitmap(const SamoTile* tiles, uint32_t ntiles, uint32_t tile_elems,
-                        const uint32_t* idx, uint32_t* bitmap, cudaStream_t s) {
+int launch_build_off16(const SamoTile* tiles, uint32_t ntiles, const uint32_t* idx,
+                       uint16_t* off16, cudaStream_t s) {
   if (ntiles == 0) return SAMO_OK;
-  const int grid = static_cast<int>(ntiles < 4096u ? ntiles : 4096u);
-  k_build_bitmap<<<grid, kThreads, tile_elems / 8, s>>>(tiles, ntiles, tile_elems, idx, bitmap);
-  SAMO_LAUNCH_CHECK("k_build_bitmap");
+  const int grid = static_cast<int>(ntiles < 8192u ? ntiles : 8192u);
+  k_build_off16<<<grid, kThreads, 0, s>>>(tiles, ntiles, idx, off16);
+  SAMO_LAUNCH_CHECK("k_build_off16");
   return SAMO_OK;
 }
 
