@@ -165,17 +165,77 @@ struct K23Layout {
 };
 
 template <bool G16>
-__global__ void __launch_bounds__(kThreads) k23_update(StepArgs a) {
+__global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
   using L = K23Layout<G16>;
+  constexpr uint32_t kConsumerWarps = kThreads / 32;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[kK23Stages];
-  __shared__ float red[kThreads / 32];
+  __shared__ __align__(8) uint64_t empty[kK23Stages];
+  __shared__ float red[kConsumerWarps];
   __shared__ int last_cta;
 
   const uint32_t T = a.tile_elems;
   uint16_t* outb = reinterpret_cast<uint16_t*>(smem + kK23Stages * L::kStage);  // 2 x T halves
-  const uint32_t tid = threadIdx.x;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
+  // Both dense out tiles start zeroed; afterwards the copy-out clears each
+  // tile as it reads it, so no separate zero-fill phase is needed.
+  {
+    uint4* o4 = reinterpret_cast<uint4*>(outb);
+    for (uint32_t i = tid; i < T * 4u / 16u; i += blockDim.x) o4[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  if (tid == 0) {
+    for (int s = 0; s < kK23Stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();  // the only CTA-wide barrier
+
+  if (warp == kConsumerWarps) {
+    // ---- producer warp: one elected lane walks the CTA's chunks and keeps
+    // the ring full (16-byte aligned supersets of theta/m/v/grad/off16).
+    if (lane == 0) {
+      const uint64_t policy = policy_evict_first();
+      uint32_t it = 0;
+      SamoTile nxt{};
+      if (blockIdx.x < a.ntiles) nxt = a.tiles[blockIdx.x];
+      for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+        const SamoTile td = nxt;
+        if (t + gridDim.x < a.ntiles) nxt = a.tiles[t + gridDim.x];
+        const uint32_t nch = tile_chunks(td);
+        for (uint32_t j = 0; j < nch; ++j, ++it) {
+          const int s = static_cast<int>(it % kK23Stages);
+          if (it >= static_cast<uint32_t>(kK23Stages))
+            mbar_wait(&empty[s], ((it / kK23Stages) - 1) & 1u);
+          const uint64_t kc0 = td.k_begin + static_cast<uint64_t>(j) * kChunk;
+          const uint64_t kc1 = min(td.k_end, kc0 + kChunk);
+          uint8_t* st = smem + s * L::kStage;
+          const uint64_t f0 = kc0 & ~3ull;
+          const uint32_t fb = static_cast<uint32_t>((((kc1 + 3) & ~3ull) - f0) * 4);
+          const uint64_t h0 = kc0 & ~7ull;
+          const uint32_t hb = static_cast<uint32_t>((((kc1 + 7) & ~7ull) - h0) * 2);
+          const uint32_t gb = G16 ? hb : fb;
+          if (!(fb | hb)) {  // empty tile: nothing to move, just publish the slot
+            mbar_arrive(&full[s]);
+            continue;
+          }
+          mbar_arrive_expect_tx(&full[s], 3 * fb + gb + hb);
+          bulk_g2s(st, a.theta + f0, fb, &full[s], policy);
+          bulk_g2s(st + L::kF32, a.m + f0, fb, &full[s], policy);
+          bulk_g2s(st + 2 * L::kF32, a.v + f0, fb, &full[s], policy);
+          const void* gsrc = G16 ? static_cast<const void*>(reinterpret_cast<const uint16_t*>(a.g) + h0)
+                                 : static_cast<const void*>(reinterpret_cast<const float*>(a.g) + f0);
+          bulk_g2s(st + 3 * L::kF32, gsrc, gb, &full[s], policy);
+          bulk_g2s(st + 3 * L::kF32 + L::kG, a.off16 + h0, hb, &full[s], policy);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumer warps ------------------------------------------------------
   // Step scalars (train.hpp:640-642), identical float ops in every CTA.
   const bool skip = *reinterpret_cast<volatile float*>(a.flag_slot) != 0.0f;
   const float b1p = __fmul_rn(a.st->beta1_pow, a.prm.beta1);
@@ -185,62 +245,16 @@ __global__ void __launch_bounds__(kThreads) k23_update(StepArgs a) {
   const float omb2 = __fsub_rn(1.0f, a.prm.beta2);  // train.hpp:336
   const float lrwd = __fmul_rn(a.prm.lr, a.prm.wd);
 
-  const uint64_t policy = policy_evict_first();
-  if (tid == 0) {
-    for (int s = 0; s < kK23Stages; ++s) mbar_init(&full[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  // Producer cursor (thread 0 only) — runs kK23Stages chunks ahead.
-  uint32_t pt = blockIdx.x, pj = 0;
-  auto issue = [&](int s) {
-    const SamoTile td = a.tiles[pt];
-    const uint64_t kc0 = td.k_begin + static_cast<uint64_t>(pj) * kChunk;
-    const uint64_t kc1 = min(td.k_end, kc0 + kChunk);
-    uint8_t* st = smem + s * L::kStage;
-    const uint64_t f0 = kc0 & ~3ull;
-    const uint32_t fb = static_cast<uint32_t>((((kc1 + 3) & ~3ull) - f0) * 4);
-    const uint64_t h0 = kc0 & ~7ull;
-    const uint32_t hb = static_cast<uint32_t>((((kc1 + 7) & ~7ull) - h0) * 2);
-    const uint32_t gb = G16 ? hb : fb;
-    mbar_arrive_expect_tx(&full[s], 3 * fb + gb + hb);
-    if (fb) {
-      bulk_g2s(st, a.theta + f0, fb, &full[s], policy);
-      bulk_g2s(st + L::kF32, a.m + f0, fb, &full[s], policy);
-      bulk_g2s(st + 2 * L::kF32, a.v + f0, fb, &full[s], policy);
-    }
-    if (gb) {
-      const void* gsrc = G16 ? static_cast<const void*>(reinterpret_cast<const uint16_t*>(a.g) + h0)
-                             : static_cast<const void*>(reinterpret_cast<const float*>(a.g) + f0);
-      bulk_g2s(st + 3 * L::kF32, gsrc, gb, &full[s], policy);
-    }
-    if (hb) bulk_g2s(st + 3 * L::kF32 + L::kG, a.off16 + h0, hb, &full[s], policy);
-    if (!(fb | hb)) mbar_arrive(&full[s]);  // unreachable: ranges are never empty
-    if (++pj >= tile_chunks(td)) {
-      pj = 0;
-      pt += gridDim.x;
-    }
-  };
-  if (tid == 0) {
-    for (int s = 0; s < kK23Stages && pt < a.ntiles; ++s) issue(s);
-  }
-
   float nacc = 0.0f;
   uint32_t it = 0, tile_it = 0;
+  SamoTile ntd{};
+  if (blockIdx.x < a.ntiles) ntd = a.tiles[blockIdx.x];
   for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++tile_it) {
-    const SamoTile td = a.tiles[t];
+    const SamoTile td = ntd;
+    if (t + gridDim.x < a.ntiles) ntd = a.tiles[t + gridDim.x];  // prefetch
     const uint32_t nch = tile_chunks(td);
     uint16_t* out = outb + (tile_it & 1u) * T;
-    if (!skip) {
-      // The out buffer was last bulk-stored two tiles ago.
-      if (tid == 0 && tile_it >= 2) bulk_wait_read<1>();
-      __syncthreads();
-      uint4* o4 = reinterpret_cast<uint4*>(out);
-      const uint32_t n16 = (td.dense_count * 2u + 15u) >> 4;
-      for (uint32_t i = tid; i < n16; i += kThreads) o4[i] = make_uint4(0u, 0u, 0u, 0u);
-      __syncthreads();
-    }
+    uint16_t* dst = a.layers[td.layer].theta16 + td.dense_begin;
     for (uint32_t j = 0; j < nch; ++j, ++it) {
       const int s = static_cast<int>(it % kK23Stages);
       const uint8_t* st = smem + s * L::kStage;
@@ -300,43 +314,46 @@ __global__ void __launch_bounds__(kThreads) k23_update(StepArgs a) {
           }
         }
       }
-      const bool last = (j + 1 == nch);
-      if (last && !skip) fence_proxy_async_smem();
-      __syncthreads();  // stage s consumed; on the last chunk the tile is complete
-      if (tid == 0) {
-        if (pt < a.ntiles) {
-          fence_proxy_async_smem();
-          issue(s);
-        }
-        if (last && !skip) {
-          const uint32_t bytes = td.dense_count * 2u;
-          const uint32_t bulk = bytes & ~15u;
-          uint16_t* dst = a.layers[td.layer].theta16 + td.dense_begin;
-          if (bulk) bulk_s2g(dst, out, bulk);
-          bulk_commit();
-          for (uint32_t i = bulk / 2; i < td.dense_count; ++i) dst[i] = out[i];
-        }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
+    }
+    // All consumer warps have scattered into `out`.
+    asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+    if (!skip) {
+      // Copy the finished dense tile out with 128-bit stores (layer segments
+      // are 256-byte aligned, tiles start at multiples of T) and clear it for
+      // its next use two tiles later.
+      uint4* o4 = reinterpret_cast<uint4*>(out);
+      uint4* d4 = reinterpret_cast<uint4*>(dst);
+      const uint32_t full16 = td.dense_count >> 3;
+      for (uint32_t i = tid; i < full16; i += kThreads) {
+        const uint4 v = o4[i];
+        o4[i] = make_uint4(0u, 0u, 0u, 0u);
+        d4[i] = v;
+      }
+      for (uint32_t i = full16 * 8 + tid; i < td.dense_count; i += kThreads) {
+        dst[i] = out[i];
+        out[i] = 0;
       }
     }
   }
-  if (tid == 0) bulk_wait<0>();
 
   // Grad norm partial per CTA (fixed schedule -> deterministic), finalised by
   // the last CTA in CTA order (double).
   float x = nacc;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) x = __fadd_rn(x, __shfl_xor_sync(0xFFFFFFFFu, x, o));
-  if ((tid & 31) == 0) red[tid >> 5] = x;
-  __syncthreads();
+  if (lane == 0) red[warp] = x;
+  asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
   if (tid == 0) {
     float s = 0.f;
-    for (int w = 0; w < kThreads / 32; ++w) s = __fadd_rn(s, red[w]);
+    for (uint32_t w = 0; w < kConsumerWarps; ++w) s = __fadd_rn(s, red[w]);
     a.norm_partials[blockIdx.x] = s;
     __threadfence();
     const uint32_t ticket = atomicAdd(&a.st->done_ctas, 1u);
     last_cta = (ticket == gridDim.x - 1);
   }
-  __syncthreads();
+  asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
   if (last_cta && tid == 0) {
     __threadfence();
     double acc = 0.0;
@@ -360,14 +377,14 @@ __global__ void __launch_bounds__(kThreads) k23_update(StepArgs a) {
 }
 
 template <typename F>
-int grid_for(F fn, size_t smem) {
+int grid_for(F fn, size_t smem, int threads = kThreads) {
   SAMO_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
   const char* carve = getenv("SAMO_CARVEOUT");  // tuning override (percent shared)
   if (carve && *carve)
     cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(carve));
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem) != cudaSuccess ||
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess ||
       per_sm < 1)
     per_sm = 1;
   const char* env = getenv("SAMO_CTAS_PER_SM");  // tuning override
@@ -390,16 +407,16 @@ int step_grid(int which, bool wide, uint32_t tile_elems) {
     return wide ? grid_for(k1_gather<true>, sm) : grid_for(k1_gather<false>, sm);
   }
   const size_t sm = update_smem(tile_elems, !wide);
-  return wide ? grid_for(k23_update<false>, sm) : grid_for(k23_update<true>, sm);
+  return wide ? grid_for(k23_update<false>, sm, kThreads + 32) : grid_for(k23_update<true>, sm, kThreads + 32);
 }
 
 template <typename F>
-static int launch_persistent(F fn, const StepArgs& a, size_t sm, int grid, cudaStream_t s,
+static int launch_persistent(F fn, const StepArgs& a, size_t sm, int grid, cudaStream_t s, int threads,
                              const char* what) {
   SAMO_CUDA_TRY(
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
   if (static_cast<uint32_t>(grid) > a.ntiles) grid = static_cast<int>(a.ntiles);
-  fn<<<grid, kThreads, sm, s>>>(a);
+  fn<<<grid, threads, sm, s>>>(a);
   SAMO_LAUNCH_CHECK(what);
   return SAMO_OK;
 }
@@ -408,16 +425,16 @@ int launch_gather(const StepArgs& a, bool out_f32, int grid, cudaStream_t s) {
   if (a.ntiles == 0) return SAMO_OK;
   if (grid <= 0) grid = step_grid(0, out_f32, a.tile_elems);
   const size_t sm = gather_smem(a.tile_elems, out_f32);
-  return out_f32 ? launch_persistent(k1_gather<true>, a, sm, grid, s, "k1_gather<f32>")
-                 : launch_persistent(k1_gather<false>, a, sm, grid, s, "k1_gather<f16>");
+  return out_f32 ? launch_persistent(k1_gather<true>, a, sm, grid, s, kThreads, "k1_gather<f32>")
+                 : launch_persistent(k1_gather<false>, a, sm, grid, s, kThreads, "k1_gather<f16>");
 }
 
 int launch_update(const StepArgs& a, bool g_f32, int grid, cudaStream_t s) {
   if (a.ntiles == 0) return SAMO_OK;
   if (grid <= 0) grid = step_grid(1, g_f32, a.tile_elems);
   const size_t sm = update_smem(a.tile_elems, !g_f32);
-  return g_f32 ? launch_persistent(k23_update<false>, a, sm, grid, s, "k23_update<f32>")
-               : launch_persistent(k23_update<true>, a, sm, grid, s, "k23_update<f16>");
+  return g_f32 ? launch_persistent(k23_update<false>, a, sm, grid, s, kThreads + 32, "k23_update<f32>")
+               : launch_persistent(k23_update<true>, a, sm, grid, s, kThreads + 32, "k23_update<f16>");
 }
 
 int launch_build_off16(const SamoTile* tiles, uint32_t ntiles, const uint32_t* idx,
