@@ -184,6 +184,8 @@ static int make_plan(ScratchPlan& p, const uint32_t* idx, uint64_t n, uint64_t d
     host[t].dense_count = static_cast<uint32_t>(std::min<uint64_t>(tile_elems, dense_len - t * tile_elems));
     host[t].pad_ = 0;
     host[t].k_begin = host[t].k_end = 0;
+    host[t].out_off = t * tile_elems;  // relative to the caller's dense output
+    host[t].pad2_ = 0;
   }
   SamoLayerDev ld{};
   ld.grad = nullptr;
@@ -201,7 +203,8 @@ static int make_plan(ScratchPlan& p, const uint32_t* idx, uint64_t n, uint64_t d
   return SAMO_OK;
 }
 
-constexpr uint32_t kDefaultTile = 8192;
+constexpr uint32_t kDefaultTile = 8192;   // single-layer API-parity plans
+constexpr uint32_t kModelTile = 16384;    // model step (measured best)
 
 template <typename T>
 static int expand_impl(const T* values, uint64_t n_values, const uint32_t* idx, uint64_t n,
@@ -223,7 +226,7 @@ static int expand_impl(const T* values, uint64_t n_values, const uint32_t* idx, 
   a.tiles = plan.tiles;
   a.ntiles = plan.ntiles;
   a.tile_elems = kDefaultTile;
-  a.layers = plan.layer;
+  a.out_base = dense_out;
   a.idx = idx;
   a.values = values;
   a.use_bulk = (reinterpret_cast<uintptr_t>(dense_out) % 16) == 0;
@@ -262,7 +265,7 @@ int samo_downcast_expand(const float* theta32, uint64_t n, const uint32_t* idx, 
   a.tiles = plan.tiles;
   a.ntiles = plan.ntiles;
   a.tile_elems = kDefaultTile;
-  a.layers = plan.layer;
+  a.out_base = theta16_dense;
   a.idx = idx;
   a.theta = const_cast<float*>(theta32);
   a.use_bulk = (reinterpret_cast<uintptr_t>(theta16_dense) % 16) == 0;
@@ -458,7 +461,7 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   SAMO_TRY(device_ok());
   if (!out || (nlayers > 0 && !layers)) return fail(SAMO_E_PARAMETER, "null argument");
   if (nlayers < 0) return fail(SAMO_E_PARAMETER, "negative layer count");
-  if (tile_elems == 0) tile_elems = kDefaultTile;
+  if (tile_elems == 0) tile_elems = kModelTile;
   if (tile_elems < 1024 || tile_elems > 65536 || (tile_elems & (tile_elems - 1)))
     return fail(SAMO_E_PARAMETER, "tile_elems must be a power of two in [1024, 65536]");
   auto* md = new samo_model();
@@ -572,6 +575,8 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
       td.dense_count = static_cast<uint32_t>(std::min<uint64_t>(tile_elems, md->dense_len[l] - d));
       td.pad_ = 0;
       td.k_begin = td.k_end = 0;
+      td.out_off = md->d_off[l] + d;  // into the model's theta16 arena
+      td.pad2_ = 0;
     }
   }
   if (nlayers > 0) {
@@ -701,7 +706,7 @@ int samo_model_init_layer(samo_model* md, int l, const float* init, uint64_t den
   a.tiles = md->tiles + t0;
   a.ntiles = static_cast<uint32_t>(nt);
   a.tile_elems = md->tile_elems;
-  a.layers = md->layers_dev;
+  a.out_base = md->theta16;
   a.idx = md->idx;
   a.theta = md->theta;
   a.use_bulk = 1;
@@ -763,6 +768,7 @@ static StepArgs step_args(samo_model* md) {
   a.ntiles = md->ntiles;
   a.tile_elems = md->tile_elems;
   a.layers = md->layers_dev;
+  a.theta16 = md->theta16;
   a.off16 = md->off16;
   a.g = md->g;
   a.theta = md->theta;
@@ -903,7 +909,7 @@ int samo_model_check_invariants(samo_model* md, samo_stream_t stream) {
   a.tiles = md->tiles;
   a.ntiles = md->ntiles;
   a.tile_elems = md->tile_elems;
-  a.layers = md->layers_dev;
+  a.out_base = md->theta16;
   a.idx = md->idx;
   a.theta = md->theta;
   a.mismatch = bad;

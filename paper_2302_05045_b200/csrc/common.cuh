@@ -196,7 +196,8 @@ __host__ __device__ __forceinline__ uint64_t synth_mix64(uint64_t seed, uint64_t
 
 // One dense tile of one layer: dense elements [dense_begin, dense_begin +
 // dense_count) of layer `layer`, whose kept indices occupy the compressed
-// arena range [k_begin, k_end).
+// arena range [k_begin, k_end).  out_off is the element offset of the tile's
+// first dense element in the output (theta16) buffer the kernels write.
 struct SamoTile {
   uint32_t layer;
   uint32_t dense_begin;
@@ -204,8 +205,10 @@ struct SamoTile {
   uint32_t pad_;
   uint64_t k_begin;
   uint64_t k_end;
+  uint64_t out_off;
+  uint64_t pad2_;
 };
-static_assert(sizeof(SamoTile) == 32, "tile descriptor is 32 bytes");
+static_assert(sizeof(SamoTile) == 48, "tile descriptor is 48 bytes");
 
 struct SamoLayerDev {
   const uint16_t* grad;  // dense binary16 gradient of the current step

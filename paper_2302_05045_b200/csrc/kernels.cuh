@@ -19,7 +19,7 @@ struct ExpandArgs {
   const SamoTile* tiles;
   uint32_t ntiles;
   uint32_t tile_elems;
-  const SamoLayerDev* layers;  // per-layer dense output (theta16) pointers
+  void* out_base;              // dense output buffer; tile t writes at out_base + out_off
   const uint32_t* idx;         // index arena (layer-local indices)
   float* theta;                // compressed fp32 master weights
   const void* values;          // kModeValues: compressed values (u16/u32)
@@ -37,7 +37,8 @@ struct StepArgs {
   const SamoTile* tiles;
   uint32_t ntiles;
   uint32_t tile_elems;
-  const SamoLayerDev* layers;  // dense gradient inputs / theta16 outputs
+  const SamoLayerDev* layers;  // dense gradient inputs (per layer)
+  uint16_t* theta16;           // dense output arena; tile t writes at theta16 + out_off
   const uint16_t* off16;       // kept index relative to its tile's dense_begin
   void* g;                     // compressed gradient arena: fp32 or binary16
   float* theta;

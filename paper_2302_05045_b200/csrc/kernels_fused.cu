@@ -38,9 +38,6 @@
 namespace samo_dev {
 namespace {
 
-constexpr int kChunk = 1024;  // kept elements per K23 stage
-constexpr int kK1Stages = 3;
-constexpr int kK23Stages = 3;
 constexpr int kU = 4;         // independent elements per thread and pass (ILP)
 
 __device__ __forceinline__ bool finite_f32(float x) {
@@ -70,16 +67,16 @@ k_build_off16(const SamoTile* __restrict__ tiles, uint32_t ntiles, const uint32_
 // ---------------------------------------------------------------------------
 // K1
 
-template <bool OUT_F32>
+template <bool OUT_F32, int NS>
 __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[kK1Stages];
+  __shared__ __align__(8) uint64_t full[NS];
 
   const uint32_t T = a.tile_elems;
   const uint32_t tid = threadIdx.x;
   const uint64_t policy = policy_evict_first();
   if (tid == 0) {
-    for (int s = 0; s < kK1Stages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -96,7 +93,7 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
     }
   };
   if (tid == 0) {
-    for (int s = 0; s < kK1Stages; ++s) {
+    for (int s = 0; s < NS; ++s) {
       const uint64_t t = blockIdx.x + static_cast<uint64_t>(s) * gridDim.x;
       if (t < a.ntiles) issue(static_cast<uint32_t>(t), s);
     }
@@ -105,12 +102,12 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
   bool bad = false;
   uint32_t it = 0;
   for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++it) {
-    const int s = static_cast<int>(it % kK1Stages);
+    const int s = static_cast<int>(it % NS);
     const SamoTile td = a.tiles[t];
     const uint16_t* gsrc = a.layers[td.layer].grad + td.dense_begin;
     const uint32_t staged = ((td.dense_count * 2u) & ~15u) >> 1;
     const uint16_t* sg = reinterpret_cast<const uint16_t*>(smem + static_cast<size_t>(s) * T * 2);
-    mbar_wait(&full[s], (it / kK1Stages) & 1u);
+    mbar_wait(&full[s], (it / NS) & 1u);
 
 #pragma unroll 1
     for (uint64_t kb = td.k_begin + tid; kb < td.k_end; kb += kU * kThreads) {
@@ -138,7 +135,7 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
     }
     __syncthreads();  // every thread is done reading stage s
     if (tid == 0) {
-      const uint64_t tn = t + static_cast<uint64_t>(kK1Stages) * gridDim.x;
+      const uint64_t tn = t + static_cast<uint64_t>(NS) * gridDim.x;
       if (tn < a.ntiles) {
         fence_proxy_async_smem();
         issue(static_cast<uint32_t>(tn), s);
@@ -151,31 +148,50 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
 // ---------------------------------------------------------------------------
 // K23
 
-__device__ __forceinline__ uint32_t tile_chunks(const SamoTile& td) {
-  const uint64_t n = td.k_end - td.k_begin;
-  return n == 0 ? 1u : static_cast<uint32_t>((n + kChunk - 1) / kChunk);
+template <int CH>
+__device__ __forceinline__ uint32_t tile_chunks(uint64_t k_begin, uint64_t k_end) {
+  const uint64_t n = k_end - k_begin;
+  return n == 0 ? 1u : static_cast<uint32_t>((n + CH - 1) / CH);
 }
 
-template <bool G16>
+// The fields of a tile descriptor the update kernel needs, loaded with three
+// 16-byte read-only loads straight into registers.
+struct TileRegs {
+  uint64_t k_begin, k_end, out_off;
+  uint32_t dense_count;
+};
+
+__device__ __forceinline__ TileRegs load_tile(const SamoTile* p) {
+  const uint4* q = reinterpret_cast<const uint4*>(p);
+  const uint4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+  TileRegs r;
+  r.dense_count = a.z;
+  r.k_begin = (static_cast<uint64_t>(b.y) << 32) | b.x;
+  r.k_end = (static_cast<uint64_t>(b.w) << 32) | b.z;
+  r.out_off = (static_cast<uint64_t>(c.y) << 32) | c.x;
+  return r;
+}
+
+template <bool G16, int CH>
 struct K23Layout {
-  static constexpr uint32_t kF32 = (kChunk + 8) * 4;                 // theta/m/v/g32 slot
-  static constexpr uint32_t kG = G16 ? (kChunk + 16) * 2 : kF32;    // grad slot
-  static constexpr uint32_t kOff = (kChunk + 16) * 2;               // off16 slot
+  static constexpr uint32_t kF32 = (CH + 8) * 4;                 // theta/m/v/g32 slot
+  static constexpr uint32_t kG = G16 ? (CH + 16) * 2 : kF32;    // grad slot
+  static constexpr uint32_t kOff = (CH + 16) * 2;               // off16 slot
   static constexpr uint32_t kStage = 3 * kF32 + kG + kOff;
 };
 
-template <bool G16>
+template <bool G16, int CH, int NS>
 __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
-  using L = K23Layout<G16>;
+  using L = K23Layout<G16, CH>;
   constexpr uint32_t kConsumerWarps = kThreads / 32;
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[kK23Stages];
-  __shared__ __align__(8) uint64_t empty[kK23Stages];
+  __shared__ __align__(8) uint64_t full[NS];
+  __shared__ __align__(8) uint64_t empty[NS];
   __shared__ float red[kConsumerWarps];
   __shared__ int last_cta;
 
   const uint32_t T = a.tile_elems;
-  uint16_t* outb = reinterpret_cast<uint16_t*>(smem + kK23Stages * L::kStage);  // 2 x T halves
+  uint16_t* outb = reinterpret_cast<uint16_t*>(smem + NS * L::kStage);  // 2 x T halves
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   // Both dense out tiles start zeroed; afterwards the copy-out clears each
@@ -185,7 +201,7 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
     for (uint32_t i = tid; i < T * 4u / 16u; i += blockDim.x) o4[i] = make_uint4(0u, 0u, 0u, 0u);
   }
   if (tid == 0) {
-    for (int s = 0; s < kK23Stages; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumerWarps);
     }
@@ -199,18 +215,18 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
     if (lane == 0) {
       const uint64_t policy = policy_evict_first();
       uint32_t it = 0;
-      SamoTile nxt{};
-      if (blockIdx.x < a.ntiles) nxt = a.tiles[blockIdx.x];
+      TileRegs nxt{};
+      if (blockIdx.x < a.ntiles) nxt = load_tile(a.tiles + blockIdx.x);
       for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
-        const SamoTile td = nxt;
-        if (t + gridDim.x < a.ntiles) nxt = a.tiles[t + gridDim.x];
-        const uint32_t nch = tile_chunks(td);
+        const TileRegs td = nxt;
+        if (t + gridDim.x < a.ntiles) nxt = load_tile(a.tiles + t + gridDim.x);
+        const uint32_t nch = tile_chunks<CH>(td.k_begin, td.k_end);
         for (uint32_t j = 0; j < nch; ++j, ++it) {
-          const int s = static_cast<int>(it % kK23Stages);
-          if (it >= static_cast<uint32_t>(kK23Stages))
-            mbar_wait(&empty[s], ((it / kK23Stages) - 1) & 1u);
-          const uint64_t kc0 = td.k_begin + static_cast<uint64_t>(j) * kChunk;
-          const uint64_t kc1 = min(td.k_end, kc0 + kChunk);
+          const int s = static_cast<int>(it % NS);
+          if (it >= static_cast<uint32_t>(NS))
+            mbar_wait(&empty[s], ((it / NS) - 1) & 1u);
+          const uint64_t kc0 = td.k_begin + static_cast<uint64_t>(j) * CH;
+          const uint64_t kc1 = min(td.k_end, kc0 + CH);
           uint8_t* st = smem + s * L::kStage;
           const uint64_t f0 = kc0 & ~3ull;
           const uint32_t fb = static_cast<uint32_t>((((kc1 + 3) & ~3ull) - f0) * 4);
@@ -247,19 +263,19 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
 
   float nacc = 0.0f;
   uint32_t it = 0, tile_it = 0;
-  SamoTile ntd{};
-  if (blockIdx.x < a.ntiles) ntd = a.tiles[blockIdx.x];
+  TileRegs nxt{};
+  if (blockIdx.x < a.ntiles) nxt = load_tile(a.tiles + blockIdx.x);
   for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++tile_it) {
-    const SamoTile td = ntd;
-    if (t + gridDim.x < a.ntiles) ntd = a.tiles[t + gridDim.x];  // prefetch
-    const uint32_t nch = tile_chunks(td);
+    const TileRegs td = nxt;
+    if (t + gridDim.x < a.ntiles) nxt = load_tile(a.tiles + t + gridDim.x);  // prefetch
+    const uint32_t nch = tile_chunks<CH>(td.k_begin, td.k_end);
     uint16_t* out = outb + (tile_it & 1u) * T;
-    uint16_t* dst = a.layers[td.layer].theta16 + td.dense_begin;
+    uint16_t* dst = a.theta16 + td.out_off;
     for (uint32_t j = 0; j < nch; ++j, ++it) {
-      const int s = static_cast<int>(it % kK23Stages);
+      const int s = static_cast<int>(it % NS);
       const uint8_t* st = smem + s * L::kStage;
-      const uint64_t kc0 = td.k_begin + static_cast<uint64_t>(j) * kChunk;
-      const uint64_t kc1 = min(td.k_end, kc0 + kChunk);
+      const uint64_t kc0 = td.k_begin + static_cast<uint64_t>(j) * CH;
+      const uint64_t kc1 = min(td.k_end, kc0 + CH);
       const uint32_t n = static_cast<uint32_t>(kc1 - kc0);
       const uint32_t fo = static_cast<uint32_t>(kc0 & 3ull);  // chunk offset in the f32 slots
       const uint32_t ho = static_cast<uint32_t>(kc0 & 7ull);  // ... in the 16-bit slots
@@ -267,7 +283,7 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
       const float* smv = reinterpret_cast<const float*>(st + L::kF32) + fo;
       const float* svv = reinterpret_cast<const float*>(st + 2 * L::kF32) + fo;
       const uint16_t* soff = reinterpret_cast<const uint16_t*>(st + 3 * L::kF32 + L::kG) + ho;
-      mbar_wait(&full[s], (it / kK23Stages) & 1u);
+      mbar_wait(&full[s], (it / NS) & 1u);
 
 #pragma unroll 1
       for (uint32_t ib = tid; ib < n; ib += kU * kThreads) {
@@ -326,10 +342,21 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
       uint4* o4 = reinterpret_cast<uint4*>(out);
       uint4* d4 = reinterpret_cast<uint4*>(dst);
       const uint32_t full16 = td.dense_count >> 3;
-      for (uint32_t i = tid; i < full16; i += kThreads) {
-        const uint4 v = o4[i];
-        o4[i] = make_uint4(0u, 0u, 0u, 0u);
-        d4[i] = v;
+      for (uint32_t i0 = tid; i0 < full16; i0 += 4 * kThreads) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t i = i0 + u * kThreads;
+          if (i < full16) v[u] = o4[i];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t i = i0 + u * kThreads;
+          if (i < full16) {
+            o4[i] = make_uint4(0u, 0u, 0u, 0u);
+            d4[i] = v[u];
+          }
+        }
       }
       for (uint32_t i = full16 * 8 + tid; i < td.dense_count; i += kThreads) {
         dst[i] = out[i];
@@ -394,20 +421,57 @@ int grid_for(F fn, size_t smem, int threads = kThreads) {
 
 }  // namespace
 
-size_t gather_smem(uint32_t tile_elems, bool) { return kK1Stages * tile_elems * 2u; }
+// K1 ring depth: three dense tiles up to T = 8192, two above (keeps three
+// CTAs resident per SM at T = 16384).
+static int k1_stages(uint32_t tile_elems) { return tile_elems <= 8192 ? 3 : 2; }
 
-size_t update_smem(uint32_t tile_elems, bool g16) {
-  return kK23Stages * (g16 ? K23Layout<true>::kStage : K23Layout<false>::kStage) +
-         tile_elems * 4u /* two dense out tiles */;
+size_t gather_smem(uint32_t tile_elems, bool) { return k1_stages(tile_elems) * tile_elems * 2u; }
+
+template <bool F32, typename F>
+static int with_k1(uint32_t tile_elems, F f) {
+  const size_t sm = gather_smem(tile_elems, F32);
+  return k1_stages(tile_elems) == 3 ? f(k1_gather<F32, 3>, sm) : f(k1_gather<F32, 2>, sm);
+}
+
+// K23 variants (kept elements per stage, ring depth): trades stage depth for
+// resident CTAs.  SAMO_K23_VARIANT selects one for tuning.
+struct K23Variant {
+  int chunk, stages;
+};
+constexpr K23Variant kK23Variants[] = {{1024, 3}, {1024, 2}, {512, 3}, {512, 4}, {2048, 2}};
+constexpr int kK23Default = 0;
+
+static int k23_variant() {
+  const char* env = getenv("SAMO_K23_VARIANT");
+  const int v = (env && *env) ? atoi(env) : kK23Default;
+  return (v >= 0 && v < static_cast<int>(sizeof(kK23Variants) / sizeof(kK23Variants[0]))) ? v
+                                                                                           : kK23Default;
+}
+
+template <bool G16, int CH, int NS>
+static size_t k23_smem(uint32_t tile_elems) {
+  return NS * K23Layout<G16, CH>::kStage + tile_elems * 4u /* two dense out tiles */;
+}
+
+// Calls f(kernel, smem) for the selected variant.
+template <bool G16, typename F>
+static int with_k23(uint32_t tile_elems, F f) {
+  switch (k23_variant()) {
+    case 1: return f(k23_update<G16, 1024, 2>, k23_smem<G16, 1024, 2>(tile_elems));
+    case 2: return f(k23_update<G16, 512, 3>, k23_smem<G16, 512, 3>(tile_elems));
+    case 3: return f(k23_update<G16, 512, 4>, k23_smem<G16, 512, 4>(tile_elems));
+    case 4: return f(k23_update<G16, 2048, 2>, k23_smem<G16, 2048, 2>(tile_elems));
+    default: return f(k23_update<G16, 1024, 3>, k23_smem<G16, 1024, 3>(tile_elems));
+  }
 }
 
 int step_grid(int which, bool wide, uint32_t tile_elems) {
   if (which == 0) {
-    const size_t sm = gather_smem(tile_elems, wide);
-    return wide ? grid_for(k1_gather<true>, sm) : grid_for(k1_gather<false>, sm);
+    auto g = [](auto fn, size_t sm) { return grid_for(fn, sm); };
+    return wide ? with_k1<true>(tile_elems, g) : with_k1<false>(tile_elems, g);
   }
-  const size_t sm = update_smem(tile_elems, !wide);
-  return wide ? grid_for(k23_update<false>, sm, kThreads + 32) : grid_for(k23_update<true>, sm, kThreads + 32);
+  auto g = [](auto fn, size_t sm) { return grid_for(fn, sm, kThreads + 32); };
+  return wide ? with_k23<false>(tile_elems, g) : with_k23<true>(tile_elems, g);
 }
 
 template <typename F>
@@ -424,17 +488,19 @@ static int launch_persistent(F fn, const StepArgs& a, size_t sm, int grid, cudaS
 int launch_gather(const StepArgs& a, bool out_f32, int grid, cudaStream_t s) {
   if (a.ntiles == 0) return SAMO_OK;
   if (grid <= 0) grid = step_grid(0, out_f32, a.tile_elems);
-  const size_t sm = gather_smem(a.tile_elems, out_f32);
-  return out_f32 ? launch_persistent(k1_gather<true>, a, sm, grid, s, kThreads, "k1_gather<f32>")
-                 : launch_persistent(k1_gather<false>, a, sm, grid, s, kThreads, "k1_gather<f16>");
+  auto go = [&](auto fn, size_t sm) {
+    return launch_persistent(fn, a, sm, grid, s, kThreads, "k1_gather");
+  };
+  return out_f32 ? with_k1<true>(a.tile_elems, go) : with_k1<false>(a.tile_elems, go);
 }
 
 int launch_update(const StepArgs& a, bool g_f32, int grid, cudaStream_t s) {
   if (a.ntiles == 0) return SAMO_OK;
   if (grid <= 0) grid = step_grid(1, g_f32, a.tile_elems);
-  const size_t sm = update_smem(a.tile_elems, !g_f32);
-  return g_f32 ? launch_persistent(k23_update<false>, a, sm, grid, s, kThreads + 32, "k23_update<f32>")
-               : launch_persistent(k23_update<true>, a, sm, grid, s, kThreads + 32, "k23_update<f16>");
+  auto go = [&](auto fn, size_t sm) {
+    return launch_persistent(fn, a, sm, grid, s, kThreads + 32, "k23_update");
+  };
+  return g_f32 ? with_k23<false>(a.tile_elems, go) : with_k23<true>(a.tile_elems, go);
 }
 
 int launch_build_off16(const SamoTile* tiles, uint32_t ntiles, const uint32_t* idx,

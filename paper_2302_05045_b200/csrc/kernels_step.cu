@@ -51,11 +51,6 @@ __global__ void k_tiles_fill(SamoTile* tiles, uint32_t ntiles, const uint64_t* _
 // Tile expand kernels: per-tile shared-memory expand (downcast / values /
 // invariant check).  The per-step update kernel lives in kernels_fused.cu.
 
-template <typename OutT>
-__device__ __forceinline__ OutT* layer_out(const SamoLayerDev* layers, uint32_t l) {
-  return reinterpret_cast<OutT*>(layers[l].theta16);
-}
-
 template <int MODE, typename OutT>
 __global__ void __launch_bounds__(kThreads) k_expand_tiles(ExpandArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -103,7 +98,7 @@ __global__ void __launch_bounds__(kThreads) k_expand_tiles(ExpandArgs a) {
     }
 
     {
-      OutT* dst = layer_out<OutT>(a.layers, td.layer) + td.dense_begin;
+      OutT* dst = reinterpret_cast<OutT*>(a.out_base) + td.out_off;
       if (MODE == kModeCheck) {
         __syncthreads();
         bool bad = false;
