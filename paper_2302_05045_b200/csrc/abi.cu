@@ -5,11 +5,13 @@
 // NCCL communicator.
 #include <nccl.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstddef>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -355,7 +357,8 @@ int samo_synth_uniform_f16(uint16_t* out, uint64_t n, uint64_t seed, uint64_t st
 }  // extern "C"
 
 struct samo_comm {
-  ncclComm_t comm = nullptr;
+  ncclComm_t comm = nullptr;  // gradient buckets
+  ncclComm_t flag = nullptr;  // the skip indicator, concurrently with the buckets
   int nranks = 1;
   int rank = 0;
 };
@@ -390,12 +393,21 @@ int samo_comm_create(const uint8_t id[SAMO_UNIQUE_ID_BYTES], int nranks, int ran
     delete c;
     return nccl_fail(r, "ncclCommInitRank");
   }
+  // A second communicator carries the one-float skip indicator, so that it can
+  // be reduced while gradient buckets are still in flight on the first.
+  r = ncclCommSplit(c->comm, 0, rank, &c->flag, nullptr);
+  if (r != ncclSuccess) {
+    ncclCommDestroy(c->comm);
+    delete c;
+    return nccl_fail(r, "ncclCommSplit");
+  }
   *out = c;
   return clear_ok();
 }
 
 int samo_comm_destroy(samo_comm* comm) {
   if (!comm) return clear_ok();
+  if (comm->flag) ncclCommDestroy(comm->flag);
   if (comm->comm) ncclCommDestroy(comm->comm);
   delete comm;
   return clear_ok();
@@ -450,7 +462,17 @@ struct samo_model {
   samo_comm* graph_comm = nullptr;
   uint64_t graph_kernels = 0;
   cudaStream_t capture_stream = nullptr;
+  // Overlapped data-parallel step: tile-range buckets whose allreduce runs on
+  // a side stream while later buckets gather and earlier ones update.
+  int nbuckets = 0;
+  std::vector<uint32_t> bucket_t;       // tile boundaries, nbuckets + 1
+  cudaStream_t s_comm = nullptr, s_flag = nullptr;
+  std::vector<cudaEvent_t> ev_k1, ev_ar;
+  cudaEvent_t ev_fork = nullptr, ev_flag = nullptr;
+  int reserve_sms = 16;                 // SMs left to NCCL while our kernels run
 };
+
+constexpr int kMaxBuckets = 32;
 
 static uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
@@ -529,7 +551,8 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   const uint64_t o_t16 = carve(md->d_tot * 2), o_tiles = carve(ntiles * sizeof(SamoTile));
   const uint64_t o_layers = carve(std::max(1, nlayers) * sizeof(SamoLayerDev));
   const uint64_t o_koff = carve((nlayers + 1) * sizeof(uint64_t));
-  const uint64_t o_st = carve(sizeof(SamoStepState)), o_np = carve(max_grid * sizeof(float));
+  const uint64_t o_st = carve(sizeof(SamoStepState));
+  const uint64_t o_np = carve(static_cast<uint64_t>(max_grid) * kMaxBuckets * sizeof(float));
   md->block_bytes = off;
   cudaError_t e = cudaMalloc(&md->block, off);
   if (e != cudaSuccess) {
@@ -600,6 +623,12 @@ int samo_model_destroy(samo_model* md) {
   if (!md) return clear_ok();
   if (md->graph) cudaGraphExecDestroy(md->graph);
   if (md->capture_stream) cudaStreamDestroy(md->capture_stream);
+  if (md->s_comm) cudaStreamDestroy(md->s_comm);
+  if (md->s_flag) cudaStreamDestroy(md->s_flag);
+  for (auto e : md->ev_k1) cudaEventDestroy(e);
+  for (auto e : md->ev_ar) cudaEventDestroy(e);
+  if (md->ev_fork) cudaEventDestroy(md->ev_fork);
+  if (md->ev_flag) cudaEventDestroy(md->ev_flag);
   if (md->block) cudaFree(md->block);
   delete md;
   return clear_ok();
@@ -670,6 +699,9 @@ int samo_model_finalize(samo_model* md, samo_stream_t stream) {
                                   cudaMemcpyHostToDevice, s));
     SAMO_TRY(launch_tiles_fill(md->tiles, md->ntiles, md->k_off_dev, md->idx, s));
     SAMO_TRY(launch_build_off16(md->tiles, md->ntiles, md->idx, md->off16, s));
+    // k ranges back on the host: bucket planning for the overlapped step.
+    SAMO_CUDA_TRY(cudaMemcpyAsync(md->tiles_host.data(), md->tiles, md->ntiles * sizeof(SamoTile),
+                                  cudaMemcpyDeviceToHost, s));
   }
   SAMO_CUDA_TRY(cudaStreamSynchronize(s));
   md->finalized = true;
@@ -784,7 +816,104 @@ static StepArgs step_args(samo_model* md) {
   a.st = md->st;
   a.flag_slot = md->g + md->n_tot;
   a.norm_partials = md->norm_partials;
+  a.norm_all = md->norm_partials;
+  a.norm_count = 0;
+  a.finalize = 1;
   return a;
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return (e && *e) ? atoi(e) : dflt;
+}
+
+// Splits the tiles into contiguous buckets of about equal kept-element count.
+static int plan_buckets(samo_model* md) {
+  if (md->nbuckets > 0) return SAMO_OK;
+  int B = env_int("SAMO_BUCKETS", 8);
+  B = std::max(1, std::min({B, kMaxBuckets, static_cast<int>(md->ntiles)}));
+  md->bucket_t.assign(1, 0);
+  const uint64_t n = md->n_tot;
+  uint64_t done = 0;
+  for (uint32_t t = 0; t < md->ntiles && static_cast<int>(md->bucket_t.size()) < B; ++t) {
+    done = md->tiles_host[t].k_end;
+    const uint64_t target = n * md->bucket_t.size() / B;
+    if (done >= target && t + 1 < md->ntiles) md->bucket_t.push_back(t + 1);
+  }
+  md->bucket_t.push_back(md->ntiles);
+  md->nbuckets = static_cast<int>(md->bucket_t.size()) - 1;
+  md->reserve_sms = std::max(0, std::min(env_int("SAMO_NCCL_SMS", 16), num_sms() - 8));
+  SAMO_CUDA_TRY(cudaStreamCreateWithFlags(&md->s_comm, cudaStreamNonBlocking));
+  SAMO_CUDA_TRY(cudaStreamCreateWithFlags(&md->s_flag, cudaStreamNonBlocking));
+  md->ev_k1.resize(md->nbuckets);
+  md->ev_ar.resize(md->nbuckets);
+  for (int b = 0; b < md->nbuckets; ++b) {
+    SAMO_CUDA_TRY(cudaEventCreateWithFlags(&md->ev_k1[b], cudaEventDisableTiming));
+    SAMO_CUDA_TRY(cudaEventCreateWithFlags(&md->ev_ar[b], cudaEventDisableTiming));
+  }
+  SAMO_CUDA_TRY(cudaEventCreateWithFlags(&md->ev_fork, cudaEventDisableTiming));
+  SAMO_CUDA_TRY(cudaEventCreateWithFlags(&md->ev_flag, cudaEventDisableTiming));
+  return SAMO_OK;
+}
+
+// One data-parallel step with the exchange overlapped:
+//   S (caller):  K1[0] K1[1] ... K1[B-1]  |wait flag|  wait AR[0] K23[0] ... wait AR[B-1] K23[B-1]
+//   s_comm:          AR[0]  AR[1] ...  AR[B-1]          (bucket b after K1[b])
+//   s_flag:                               AR(flag)      (after K1[B-1], second communicator)
+// Persistent grids leave `reserve_sms` SMs free so the NCCL kernels run
+// concurrently with ours.
+static int step_overlapped(samo_model* md, cudaStream_t S) {
+  SAMO_TRY(plan_buckets(md));
+  const int B = md->nbuckets;
+  const int sms = num_sms();
+  const int per_g = std::max(1, md->grid_gather32 / sms), per_u = std::max(1, md->grid_update32 / sms);
+  const int gg = per_g * (sms - md->reserve_sms), gu = per_u * (sms - md->reserve_sms);
+  const StepArgs base = step_args(md);
+  SAMO_CUDA_TRY(cudaEventRecord(md->ev_fork, S));
+  SAMO_CUDA_TRY(cudaStreamWaitEvent(md->s_comm, md->ev_fork, 0));
+  SAMO_CUDA_TRY(cudaStreamWaitEvent(md->s_flag, md->ev_fork, 0));
+  uint32_t norm_total = 0;
+  for (int b = 0; b < B; ++b) {
+    const uint32_t t0 = md->bucket_t[b], t1 = md->bucket_t[b + 1];
+    StepArgs a = base;
+    a.tiles = md->tiles + t0;
+    a.ntiles = t1 - t0;
+    SAMO_TRY(launch_gather(a, true, std::min<int>(gg, a.ntiles), S));
+    SAMO_CUDA_TRY(cudaEventRecord(md->ev_k1[b], S));
+    SAMO_CUDA_TRY(cudaStreamWaitEvent(md->s_comm, md->ev_k1[b], 0));
+    const uint64_t k0 = md->tiles_host[t0].k_begin, k1 = md->tiles_host[t1 - 1].k_end;
+    if (k1 > k0) {
+      const ncclResult_t r = ncclAllReduce(md->g + k0, md->g + k0, k1 - k0, ncclFloat32, ncclSum,
+                                           md->comm->comm, md->s_comm);
+      if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce(bucket)");
+    }
+    SAMO_CUDA_TRY(cudaEventRecord(md->ev_ar[b], md->s_comm));
+    norm_total += std::min<uint32_t>(gu, a.ntiles);
+  }
+  SAMO_CUDA_TRY(cudaStreamWaitEvent(md->s_flag, md->ev_k1[B - 1], 0));
+  {
+    float* flag = md->g + md->n_tot;
+    const ncclResult_t r = ncclAllReduce(flag, flag, 1, ncclFloat32, ncclSum, md->comm->flag, md->s_flag);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce(flag)");
+  }
+  SAMO_CUDA_TRY(cudaEventRecord(md->ev_flag, md->s_flag));
+  SAMO_CUDA_TRY(cudaStreamWaitEvent(S, md->ev_flag, 0));
+  uint32_t norm_off = 0;
+  for (int b = 0; b < B; ++b) {
+    const uint32_t t0 = md->bucket_t[b], t1 = md->bucket_t[b + 1];
+    SAMO_CUDA_TRY(cudaStreamWaitEvent(S, md->ev_ar[b], 0));
+    StepArgs a = base;
+    a.tiles = md->tiles + t0;
+    a.ntiles = t1 - t0;
+    const int grid = std::min<int>(gu, a.ntiles);
+    a.norm_partials = md->norm_partials + norm_off;
+    a.norm_all = md->norm_partials;
+    a.norm_count = norm_total;
+    a.finalize = (b == B - 1) ? 1u : 0u;
+    norm_off += grid;
+    SAMO_TRY(launch_update(a, true, grid, S));
+  }
+  return SAMO_OK;
 }
 
 extern "C" {
@@ -810,12 +939,20 @@ int samo_model_exchange(samo_model* md, samo_stream_t stream) {
 int samo_model_update(samo_model* md, samo_stream_t stream) {
   SAMO_TRY(step_ready(md));
   const bool wide = wide_grads(md);
-  SAMO_TRY(launch_update(step_args(md), wide, wide ? md->grid_update32 : md->grid_update16,
-                         as_stream(stream)));
+  StepArgs a = step_args(md);
+  const int grid = std::min<int>(wide ? md->grid_update32 : md->grid_update16, md->ntiles);
+  a.norm_count = static_cast<uint32_t>(grid);
+  SAMO_TRY(launch_update(a, wide, grid, as_stream(stream)));
   return clear_ok();
 }
 
 int samo_model_step(samo_model* md, samo_stream_t stream) {
+  SAMO_TRY(step_ready(md));
+  if (!md->grads_set) return fail(SAMO_E_STATE, "optimizer_step requires backward (no gradients set)");
+  if (comm_size(md) > 1 && env_int("SAMO_OVERLAP", 1)) {
+    SAMO_TRY(step_overlapped(md, as_stream(stream)));
+    return clear_ok();
+  }
   SAMO_TRY(samo_model_gather(md, stream));
   SAMO_TRY(samo_model_exchange(md, stream));
   SAMO_TRY(samo_model_update(md, stream));

@@ -48,7 +48,10 @@ struct StepArgs {
   SamoAdamParams prm;
   SamoStepState* st;
   float* flag_slot;            // non-finite indicator (summed across ranks)
-  float* norm_partials;        // one per K23 CTA
+  float* norm_partials;        // this launch's per-CTA grad-norm partials
+  const float* norm_all;       // every partial of the step (read when finalize)
+  uint32_t norm_count;
+  uint32_t finalize;           // 1 on the step's last update launch
 };
 
 // K1 gather: out_f32 -> unscaled fp32 for the exchange, else raw binary16.

@@ -382,23 +382,25 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
   }
   asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
   if (last_cta && tid == 0) {
-    __threadfence();
-    double acc = 0.0;
-    const volatile float* np = a.norm_partials;
-    for (uint32_t b = 0; b < gridDim.x; ++b) acc += static_cast<double>(np[b]);
     SamoStepState* stt = a.st;
-    stt->grad_norm = static_cast<float>(sqrt(acc));
-    if (skip) {  // train.hpp:632-639
-      stt->skipped_steps += 1;
-      stt->last_skipped = 1u;
-    } else {     // AdamScalars::advance, train.hpp:325-329
-      stt->t += 1;
-      stt->beta1_pow = b1p;
-      stt->beta2_pow = b2p;
-      stt->last_skipped = 0u;
+    if (a.finalize) {  // the step's last update launch
+      __threadfence();
+      double acc = 0.0;
+      const volatile float* np = a.norm_all;
+      for (uint32_t b = 0; b < a.norm_count; ++b) acc += static_cast<double>(np[b]);
+      stt->grad_norm = static_cast<float>(sqrt(acc));
+      if (skip) {  // train.hpp:632-639
+        stt->skipped_steps += 1;
+        stt->last_skipped = 1u;
+      } else {     // AdamScalars::advance, train.hpp:325-329
+        stt->t += 1;
+        stt->beta1_pow = b1p;
+        stt->beta2_pow = b2p;
+        stt->last_skipped = 0u;
+      }
+      *a.flag_slot = 0.0f;  // every CTA of every launch has read it
     }
     stt->done_ctas = 0u;
-    *a.flag_slot = 0.0f;  // every CTA has read it; ready for the next gather
     __threadfence();
   }
 }

@@ -1,0 +1,84 @@
+"""Data-parallel parity on >= 2 GPUs: the NCCL exchange of the compressed
+gradient arena, bucketed and overlapped with the step kernels.
+
+Tolerance: none at G = 2 — a two-operand fp32 sum is order-independent, so
+every replica must equal the oracle (rank-ascending fp32 sum, then the
+reference's Adam / downcast / expand) bit for bit, including the step skipped
+because one rank saw +inf.  Skipped when fewer than two GPUs are visible."""
+from __future__ import annotations
+
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+HERE = Path(__file__).resolve().parent
+
+
+def _port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _expected(oracle, world):
+    sys.path.insert(0, str(HERE))
+    import dp_worker as W
+    from oracle.oracle import Cfg
+    vals, sets, grads = W.inputs(oracle, world)
+    L = len(W.DENSE_LEN)
+    theta = [oracle.compress(v, s) for v, s in zip(vals, sets)]
+    m = [np.zeros_like(t) for t in theta]
+    v = [np.zeros_like(t) for t in theta]
+    cfg = Cfg(lr=1e-2)
+    b1p = b2p = np.float32(1.0)
+    t = skipped = 0
+    inv = np.float32(1.0) / np.float32(1024.0) * (np.float32(1.0) / np.float32(world))
+    for s in range(W.STEPS):
+        g = []
+        for l in range(L):
+            per_rank = [(oracle.h2f(oracle.compress(grads[(r, s, l)], sets[l])) * inv).astype(np.float32)
+                        for r in range(world)]
+            g.append(oracle.dp_sum(per_rank)[0])
+        if not all(np.all(np.isfinite(x)) for x in g):
+            skipped += 1
+            continue
+        t += 1
+        b1p = np.float32(b1p * np.float32(0.9))
+        b2p = np.float32(b2p * np.float32(0.999))
+        for l in range(L):
+            oracle.adam_update(theta[l], m[l], v[l], g[l], cfg, float(np.float32(1) - b1p),
+                               float(np.float32(1) - b2p))
+    t16 = [oracle.expand(oracle.f2h(theta[l]), sets[l], (W.DENSE_LEN[l],)) for l in range(L)]
+    return theta, m, v, t16, t, skipped
+
+
+@pytest.mark.parametrize("mode", ["overlap", "staged", "graph"])
+def test_dp_two_gpus_bit_exact(tmp_path, oracle, mode):
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    env = dict(os.environ)
+    env["SAMO_OVERLAP"] = "0" if mode == "staged" else "1"
+    env["SAMO_DP_GRAPH"] = "1" if mode == "graph" else "0"
+    env["SAMO_BUCKETS"] = "5"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+           str(HERE / "dp_worker.py"), str(tmp_path)]
+    res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    r = [dict(np.load(tmp_path / f"dp_rank{i}.npz")) for i in range(2)]
+    theta, m, v, t16, t, skipped = _expected(oracle, 2)
+    for rr in r:
+        assert int(rr["t"][0]) == t and int(rr["skipped"][0]) == skipped == 1
+        for l in range(len(theta)):
+            assert np.array_equal(rr[f"theta32{l}"].view(np.uint32), theta[l].view(np.uint32)), l
+            assert np.array_equal(rr[f"adam_m{l}"].view(np.uint32), m[l].view(np.uint32)), l
+            assert np.array_equal(rr[f"adam_v{l}"].view(np.uint32), v[l].view(np.uint32)), l
+            assert np.array_equal(rr[f"theta16_{l}"], t16[l]), l
