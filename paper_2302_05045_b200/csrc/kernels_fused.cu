@@ -458,6 +458,14 @@ static size_t k23_smem(uint32_t tile_elems) {
 // Calls f(kernel, smem) for the selected variant.
 template <bool G16, typename F>
 static int with_k23(uint32_t tile_elems, F f) {
+  const char* env = getenv("SAMO_K23_VARIANT");
+  if (!(env && *env)) {
+    // Default: 1024-element chunks, three stages when two CTAs still fit per
+    // SM (227 KB of shared memory), else two.
+    if (k23_smem<G16, 1024, 3>(tile_elems) <= 113u * 1024u)
+      return f(k23_update<G16, 1024, 3>, k23_smem<G16, 1024, 3>(tile_elems));
+    return f(k23_update<G16, 1024, 2>, k23_smem<G16, 1024, 2>(tile_elems));
+  }
   switch (k23_variant()) {
     case 1: return f(k23_update<G16, 1024, 2>, k23_smem<G16, 1024, 2>(tile_elems));
     case 2: return f(k23_update<G16, 512, 3>, k23_smem<G16, 512, 3>(tile_elems));
