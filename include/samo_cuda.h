@@ -232,6 +232,27 @@ int samo_model_set_config(samo_model* model, const samo_optimizer_config* cfg);
  * Adam, with 1/nranks folded into the unscale. NULL detaches. */
 int samo_model_attach_comm(samo_model* model, samo_comm* comm);
 
+/* Gradient exchange of a data-parallel step (communicator size > 1):
+ *  SAMO_EXCHANGE_ALLREDUCE — every rank keeps the full compressed state; the
+ *    fp32 gradient arena is sum-allreduced (bucketed, overlapped with the
+ *    step kernels) and every rank runs the full update.
+ *  SAMO_EXCHANGE_SHARDED — ZeRO-1 on the compressed state: reduce-scatter of
+ *    the gradient arena, Adam on the rank's shard only, all-gather of the
+ *    compressed binary16 weights, local expand.  theta32/m/v are
+ *    authoritative only inside samo_model_shard_range(); theta16 everywhere.
+ * The default is SHARDED (environment SAMO_EXCHANGE=allreduce overrides);
+ * mode -1 restores the default. */
+enum samo_exchange_mode {
+  SAMO_EXCHANGE_NONE = 0,
+  SAMO_EXCHANGE_ALLREDUCE = 1,
+  SAMO_EXCHANGE_SHARDED = 2
+};
+int samo_model_set_exchange(samo_model* model, int mode);
+/* SAMO_EXCHANGE_NONE without a communicator of size > 1. */
+int samo_model_exchange_mode(const samo_model* model);
+/* Compressed-arena range [k0, k1) this rank updates (everything unless sharded). */
+int samo_model_shard_range(const samo_model* model, uint64_t* k0, uint64_t* k1);
+
 /* Per-layer dense binary16 gradients (device pointers, 16-byte aligned,
  * dense_len elements each) consumed by the next step. `ptrs` is a host array
  * of nlayers device pointers; it is copied to the device on `stream`. */

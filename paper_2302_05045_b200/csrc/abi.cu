@@ -441,7 +441,12 @@ struct samo_model {
   float* theta = nullptr;
   float* m = nullptr;
   float* v = nullptr;
-  float* g = nullptr;          // n_tot + 1: the last slot carries the non-finite indicator
+  float* g = nullptr;          // compressed gradient arena (+ skip-indicator slot)
+  uint16_t* c16 = nullptr;     // compressed binary16 weights (sharded exchange)
+  double* norm2 = nullptr;     // this rank's / the global sum of g^2 (sharded exchange)
+  uint32_t* done = nullptr;    // arrival counter of k_adam_shard
+  uint64_t n_al = 0;
+  int exchange = -1;           // SAMO_EXCHANGE_*; -1 = environment default
   uint32_t* idx = nullptr;
   uint16_t* off16 = nullptr;   // idx[k] - dense_begin of k's tile (step kernels)
   uint16_t* theta16 = nullptr;
@@ -473,6 +478,10 @@ struct samo_model {
 };
 
 constexpr int kMaxBuckets = 32;
+constexpr uint64_t kArenaSlack = 1024;  // elements: G * shard padding (G <= 128) + flag
+constexpr uint64_t kFlagOff = 1000;     // flag slot at g + n_al + kFlagOff
+
+static float* flag_ptr(const samo_model* md) { return md->g + md->n_al + kFlagOff; }
 
 static uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
@@ -539,6 +548,7 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   // +64 elements of slack: the update kernel's 16-byte aligned bulk loads may
   // read up to 7 elements past the last kept one.
   const uint64_t n_al = align_up(md->n_tot + 64, 64);
+  md->n_al = n_al;
   uint64_t off = 0;
   auto carve = [&](uint64_t bytes) {
     const uint64_t o = off;
@@ -546,7 +556,11 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
     return o;
   };
   const uint64_t o_theta = carve(n_al * 4), o_m = carve(n_al * 4), o_v = carve(n_al * 4);
-  const uint64_t o_g = carve((n_al + 64) * 4), o_idx = carve(n_al * 4);
+  // grad arena: n_al floats (the sharded exchange pads it to G * shard size,
+  // G <= 128) + the skip-indicator slot at n_al + kFlagOff.
+  const uint64_t o_g = carve((n_al + kArenaSlack) * 4), o_idx = carve(n_al * 4);
+  const uint64_t o_c16 = carve((n_al + kArenaSlack) * 2);
+  const uint64_t o_n2 = carve(64);
   const uint64_t o_off = carve(n_al * 2);
   const uint64_t o_t16 = carve(md->d_tot * 2), o_tiles = carve(ntiles * sizeof(SamoTile));
   const uint64_t o_layers = carve(std::max(1, nlayers) * sizeof(SamoLayerDev));
@@ -566,6 +580,9 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   md->g = reinterpret_cast<float*>(b + o_g);
   md->idx = reinterpret_cast<uint32_t*>(b + o_idx);
   md->off16 = reinterpret_cast<uint16_t*>(b + o_off);
+  md->c16 = reinterpret_cast<uint16_t*>(b + o_c16);
+  md->norm2 = reinterpret_cast<double*>(b + o_n2);
+  md->done = reinterpret_cast<uint32_t*>(b + o_n2 + 16);
   md->theta16 = reinterpret_cast<uint16_t*>(b + o_t16);
   md->tiles = reinterpret_cast<SamoTile*>(b + o_tiles);
   md->layers_dev = reinterpret_cast<SamoLayerDev*>(b + o_layers);
@@ -814,7 +831,7 @@ static StepArgs step_args(samo_model* md) {
   a.inv_scale = inv_scale;
   a.prm = adam_params(&md->cfg);
   a.st = md->st;
-  a.flag_slot = md->g + md->n_tot;
+  a.flag_slot = flag_ptr(md);
   a.norm_partials = md->norm_partials;
   a.norm_all = md->norm_partials;
   a.norm_count = 0;
@@ -892,7 +909,7 @@ static int step_overlapped(samo_model* md, cudaStream_t S) {
   }
   SAMO_CUDA_TRY(cudaStreamWaitEvent(md->s_flag, md->ev_k1[B - 1], 0));
   {
-    float* flag = md->g + md->n_tot;
+    float* flag = flag_ptr(md);
     const ncclResult_t r = ncclAllReduce(flag, flag, 1, ncclFloat32, ncclSum, md->comm->flag, md->s_flag);
     if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce(flag)");
   }
@@ -916,7 +933,98 @@ static int step_overlapped(samo_model* md, cudaStream_t S) {
   return SAMO_OK;
 }
 
+static int exchange_mode(const samo_model* md) {
+  if (md->exchange >= 0) return md->exchange;
+  const char* e = getenv("SAMO_EXCHANGE");
+  if (e && std::strcmp(e, "allreduce") == 0) return SAMO_EXCHANGE_ALLREDUCE;
+  return SAMO_EXCHANGE_SHARDED;
+}
+
+// Shard of the compressed arena owned by this rank in the sharded exchange:
+// [rank * cnt, min((rank + 1) * cnt, n)), cnt a multiple of 8.
+static uint64_t shard_count(const samo_model* md) {
+  const uint64_t G = comm_size(md);
+  return align_up((md->n_tot + G - 1) / G, 8);
+}
+
+// One data-parallel step, ZeRO-1 style on the compressed state:
+//   K1 (fp32, 1/G folded) -> allreduce(skip flag) -> reduce-scatter(grad)
+//   -> Adam on the own shard (theta32/m/v + compressed binary16 copy)
+//   -> all-gather(theta16c) + allreduce(norm^2) -> expand every tile -> scalars.
+// Link bytes per rank 6n(G-1)/G instead of 8n(G-1)/G, Adam HBM traffic / G.
+static int step_sharded(samo_model* md, cudaStream_t S) {
+  const int G = comm_size(md), r = md->comm->rank;
+  const uint64_t cnt = shard_count(md);
+  if (static_cast<uint64_t>(G) * cnt > md->n_al + kFlagOff)
+    return fail(SAMO_E_PARAMETER, "too many ranks for the arena padding");
+  SAMO_TRY(launch_gather(step_args(md), true, md->grid_gather32, S));
+  float* flag = flag_ptr(md);
+  ncclResult_t rr = ncclAllReduce(flag, flag, 1, ncclFloat32, ncclSum, md->comm->flag, S);
+  if (rr != ncclSuccess) return nccl_fail(rr, "ncclAllReduce(flag)");
+  rr = ncclReduceScatter(md->g, md->g + r * cnt, cnt, ncclFloat32, ncclSum, md->comm->comm, S);
+  if (rr != ncclSuccess) return nccl_fail(rr, "ncclReduceScatter");
+  ShardArgs sa{};
+  sa.g = md->g;
+  sa.theta = md->theta;
+  sa.m = md->m;
+  sa.v = md->v;
+  sa.theta16c = md->c16;
+  sa.k0 = std::min<uint64_t>(r * cnt, md->n_tot);
+  sa.k1 = std::min<uint64_t>((r + 1) * cnt, md->n_tot);
+  sa.prm = adam_params(&md->cfg);
+  sa.st = md->st;
+  sa.flag_slot = flag;
+  sa.norm_partials = md->norm_partials;
+  sa.norm2_out = md->norm2;
+  sa.done = md->done;
+  const uint64_t nv = (sa.k1 - sa.k0 + 3) / 4;
+  const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(num_sms() * 8, (nv + 255) / 256)));
+  if (sa.k1 > sa.k0) {
+    SAMO_TRY(launch_adam_shard(sa, grid, S));
+  } else {
+    SAMO_CUDA_TRY(cudaMemsetAsync(md->norm2, 0, sizeof(double), S));
+  }
+  rr = ncclAllGather(md->c16 + r * cnt, md->c16, cnt, ncclFloat16, md->comm->comm, S);
+  if (rr != ncclSuccess) return nccl_fail(rr, "ncclAllGather");
+  rr = ncclAllReduce(md->norm2, md->norm2, 1, ncclFloat64, ncclSum, md->comm->flag, S);
+  if (rr != ncclSuccess) return nccl_fail(rr, "ncclAllReduce(norm)");
+  StepArgs a = step_args(md);
+  a.g = md->c16;
+  SAMO_TRY(launch_expand_c16(a, std::min<int>(md->grid_update16, md->ntiles), S));
+  SAMO_TRY(launch_step_finalize(md->st, md->norm2, flag, md->cfg.beta1, md->cfg.beta2, S));
+  return SAMO_OK;
+}
+
 extern "C" {
+
+int samo_model_set_exchange(samo_model* md, int mode) {
+  if (!md) return fail(SAMO_E_PARAMETER, "null model");
+  if (mode != -1 && mode != SAMO_EXCHANGE_ALLREDUCE && mode != SAMO_EXCHANGE_SHARDED)
+    return fail(SAMO_E_PARAMETER, "unknown exchange mode %d", mode);
+  md->exchange = mode;
+  if (md->graph) {
+    cudaGraphExecDestroy(md->graph);
+    md->graph = nullptr;
+  }
+  return clear_ok();
+}
+
+int samo_model_exchange_mode(const samo_model* md) {
+  return md ? (comm_size(md) > 1 ? exchange_mode(md) : SAMO_EXCHANGE_NONE) : -1;
+}
+
+int samo_model_shard_range(const samo_model* md, uint64_t* k0, uint64_t* k1) {
+  if (!md || !k0 || !k1) return fail(SAMO_E_PARAMETER, "null argument");
+  if (comm_size(md) <= 1 || exchange_mode(md) != SAMO_EXCHANGE_SHARDED) {
+    *k0 = 0;
+    *k1 = md->n_tot;
+    return clear_ok();
+  }
+  const uint64_t cnt = shard_count(md);
+  *k0 = std::min<uint64_t>(md->comm->rank * cnt, md->n_tot);
+  *k1 = std::min<uint64_t>((md->comm->rank + 1) * cnt, md->n_tot);
+  return clear_ok();
+}
 
 int samo_model_gather(samo_model* md, samo_stream_t stream) {
   SAMO_TRY(step_ready(md));
@@ -930,8 +1038,9 @@ int samo_model_gather(samo_model* md, samo_stream_t stream) {
 int samo_model_exchange(samo_model* md, samo_stream_t stream) {
   SAMO_TRY(step_ready(md));
   if (comm_size(md) > 1) {
-    // grad32 arena plus the non-finite indicator slot, one in-place sum.
-    SAMO_TRY(samo_allreduce_sum_f32(md->comm, md->g, md->n_tot + 1, stream));
+    // grad32 arena through the non-finite indicator slot, one in-place sum
+    // (the zero padding in between is noise-free and < 1024 elements).
+    SAMO_TRY(samo_allreduce_sum_f32(md->comm, md->g, md->n_al + kFlagOff + 1, stream));
   }
   return clear_ok();
 }
@@ -949,6 +1058,10 @@ int samo_model_update(samo_model* md, samo_stream_t stream) {
 int samo_model_step(samo_model* md, samo_stream_t stream) {
   SAMO_TRY(step_ready(md));
   if (!md->grads_set) return fail(SAMO_E_STATE, "optimizer_step requires backward (no gradients set)");
+  if (comm_size(md) > 1 && exchange_mode(md) == SAMO_EXCHANGE_SHARDED) {
+    SAMO_TRY(step_sharded(md, as_stream(stream)));
+    return clear_ok();
+  }
   if (comm_size(md) > 1 && env_int("SAMO_OVERLAP", 1)) {
     SAMO_TRY(step_overlapped(md, as_stream(stream)));
     return clear_ok();

@@ -60,6 +60,26 @@ int launch_gather(const StepArgs& a, bool out_f32, int grid, cudaStream_t s);
 int launch_update(const StepArgs& a, bool g_f32, int grid, cudaStream_t s);
 // which: 0 = gather, 1 = update; wide = fp32 gradient arena.
 int step_grid(int which, bool wide, uint32_t tile_elems);
+// Sharded data-parallel step pieces.
+struct ShardArgs {
+  const float* g;              // reduce-scattered gradient (this rank's shard in place)
+  float* theta;
+  float* m;
+  float* v;
+  uint16_t* theta16c;          // compressed binary16 weights (all-gathered afterwards)
+  uint64_t k0, k1;             // this rank's shard, k0 a multiple of 8
+  SamoAdamParams prm;
+  const SamoStepState* st;
+  const float* flag_slot;      // global skip indicator (already reduced)
+  float* norm_partials;
+  double* norm2_out;           // this rank's sum of g^2
+  uint32_t* done;
+};
+int launch_adam_shard(const ShardArgs& a, int grid, cudaStream_t s);
+int launch_step_finalize(SamoStepState* st, const double* norm2, float* flag, float beta1,
+                         float beta2, cudaStream_t s);
+// Expand-only tile pass: a.g holds theta16c.
+int launch_expand_c16(const StepArgs& a, int grid, cudaStream_t s);
 int launch_build_off16(const SamoTile* tiles, uint32_t ntiles, const uint32_t* idx,
                        uint16_t* off16, cudaStream_t s);
 

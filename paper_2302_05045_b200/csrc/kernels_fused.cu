@@ -180,8 +180,12 @@ struct K23Layout {
   static constexpr uint32_t kStage = 3 * kF32 + kG + kOff;
 };
 
-template <bool G16, int CH, int NS>
+// EXPAND = true: expand-only pass of the sharded data-parallel step — the
+// grad slot carries the all-gathered compressed binary16 weights (theta16c),
+// no Adam, no theta/m/v traffic.
+template <bool G16, int CH, int NS, bool EXPAND = false>
 __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
+  static_assert(!EXPAND || G16, "expand-only reads 16-bit values");
   using L = K23Layout<G16, CH>;
   constexpr uint32_t kConsumerWarps = kThreads / 32;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -233,18 +237,22 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
           const uint64_t h0 = kc0 & ~7ull;
           const uint32_t hb = static_cast<uint32_t>((((kc1 + 7) & ~7ull) - h0) * 2);
           const uint32_t gb = G16 ? hb : fb;
-          if (!(fb | hb)) {  // empty tile: nothing to move, just publish the slot
+          const uint32_t fb3 = EXPAND ? 0u : fb;  // theta/m/v slots unused when expanding
+          const uint32_t total = 3 * fb3 + gb + hb;
+          if (total == 0) {  // empty, aligned tile: nothing to move, just publish the slot
             mbar_arrive(&full[s]);
             continue;
           }
-          mbar_arrive_expect_tx(&full[s], 3 * fb + gb + hb);
-          bulk_g2s(st, a.theta + f0, fb, &full[s], policy);
-          bulk_g2s(st + L::kF32, a.m + f0, fb, &full[s], policy);
-          bulk_g2s(st + 2 * L::kF32, a.v + f0, fb, &full[s], policy);
+          mbar_arrive_expect_tx(&full[s], total);
+          if (fb3) {
+            bulk_g2s(st, a.theta + f0, fb3, &full[s], policy);
+            bulk_g2s(st + L::kF32, a.m + f0, fb3, &full[s], policy);
+            bulk_g2s(st + 2 * L::kF32, a.v + f0, fb3, &full[s], policy);
+          }
           const void* gsrc = G16 ? static_cast<const void*>(reinterpret_cast<const uint16_t*>(a.g) + h0)
                                  : static_cast<const void*>(reinterpret_cast<const float*>(a.g) + f0);
-          bulk_g2s(st + 3 * L::kF32, gsrc, gb, &full[s], policy);
-          bulk_g2s(st + 3 * L::kF32 + L::kG, a.off16 + h0, hb, &full[s], policy);
+          if (gb) bulk_g2s(st + 3 * L::kF32, gsrc, gb, &full[s], policy);
+          if (hb) bulk_g2s(st + 3 * L::kF32 + L::kG, a.off16 + h0, hb, &full[s], policy);
         }
       }
     }
@@ -253,7 +261,7 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
 
   // ---- consumer warps ------------------------------------------------------
   // Step scalars (train.hpp:640-642), identical float ops in every CTA.
-  const bool skip = *reinterpret_cast<volatile float*>(a.flag_slot) != 0.0f;
+  const bool skip = !EXPAND && *reinterpret_cast<volatile float*>(a.flag_slot) != 0.0f;
   const float b1p = __fmul_rn(a.st->beta1_pow, a.prm.beta1);
   const float b2p = __fmul_rn(a.st->beta2_pow, a.prm.beta2);
   const float bias1 = __fsub_rn(1.0f, b1p), bias2 = __fsub_rn(1.0f, b2p);
@@ -285,6 +293,11 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
       const uint16_t* soff = reinterpret_cast<const uint16_t*>(st + 3 * L::kF32 + L::kG) + ho;
       mbar_wait(&full[s], (it / NS) & 1u);
 
+      if constexpr (EXPAND) {
+        const uint16_t* sval = reinterpret_cast<const uint16_t*>(st + 3 * L::kF32) + ho;
+#pragma unroll 4
+        for (uint32_t i = tid; i < n; i += kThreads) out[soff[i]] = sval[i];
+      } else {
 #pragma unroll 1
       for (uint32_t ib = tid; ib < n; ib += kU * kThreads) {
         float gv[kU], tv[kU], mv[kU], vv[kU];
@@ -330,6 +343,7 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
           }
         }
       }
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
     }
@@ -364,6 +378,8 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
       }
     }
   }
+
+  if constexpr (EXPAND) return;
 
   // Grad norm partial per CTA (fixed schedule -> deterministic), finalised by
   // the last CTA in CTA order (double).
@@ -403,6 +419,117 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
     stt->done_ctas = 0u;
     __threadfence();
   }
+}
+
+// ---------------------------------------------------------------------------
+// Sharded data-parallel step (ZeRO-1 on the compressed state): Adam on this
+// rank's shard of the reduce-scattered gradient, writing the updated weights
+// both as fp32 master copy and as compressed binary16 (theta16c) for the
+// all-gather; then the expand-only tile pass rebuilds every dense theta16.
+
+__device__ __forceinline__ float adam_one(float g, float& m, float& v, float t, const SamoAdamParams& p,
+                                          float omb1, float omb2, float bias1, float bias2,
+                                          float lrwd) {
+  m = __fadd_rn(__fmul_rn(p.beta1, m), __fmul_rn(omb1, g));
+  v = __fadd_rn(__fmul_rn(p.beta2, v), __fmul_rn(omb2, __fmul_rn(g, g)));
+  const float mh = __fdiv_rn(m, bias1);
+  const float vh = __fdiv_rn(v, bias2);
+  t = __fsub_rn(t, __fmul_rn(p.lr, __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), p.eps))));
+  if (p.wd != 0.0f) t = __fsub_rn(t, __fmul_rn(lrwd, t));
+  return t;
+}
+
+__global__ void __launch_bounds__(kThreads) k_adam_shard(ShardArgs a) {
+  __shared__ float red[kThreads / 32];
+  __shared__ int last_cta;
+  const bool skip = *reinterpret_cast<const volatile float*>(a.flag_slot) != 0.0f;
+  const float b1p = __fmul_rn(a.st->beta1_pow, a.prm.beta1);
+  const float b2p = __fmul_rn(a.st->beta2_pow, a.prm.beta2);
+  const float bias1 = __fsub_rn(1.0f, b1p), bias2 = __fsub_rn(1.0f, b2p);
+  const float omb1 = __fsub_rn(1.0f, a.prm.beta1), omb2 = __fsub_rn(1.0f, a.prm.beta2);
+  const float lrwd = __fmul_rn(a.prm.lr, a.prm.wd);
+  float nacc = 0.0f;
+  // k0 is a multiple of 8 (shard size), so 4-element vectors stay aligned.
+  const uint64_t nv = (a.k1 - a.k0) / 4;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kThreads;
+  for (uint64_t q = blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x; q < nv; q += stride) {
+    const uint64_t k = a.k0 + 4 * q;
+    const float4 g = *reinterpret_cast<const float4*>(a.g + k);
+    float4 t = *reinterpret_cast<const float4*>(a.theta + k);
+    float4 m = *reinterpret_cast<const float4*>(a.m + k);
+    float4 v = *reinterpret_cast<const float4*>(a.v + k);
+    nacc = __fadd_rn(nacc, __fmul_rn(g.x, g.x));
+    nacc = __fadd_rn(nacc, __fmul_rn(g.y, g.y));
+    nacc = __fadd_rn(nacc, __fmul_rn(g.z, g.z));
+    nacc = __fadd_rn(nacc, __fmul_rn(g.w, g.w));
+    if (!skip) {
+      t.x = adam_one(g.x, m.x, v.x, t.x, a.prm, omb1, omb2, bias1, bias2, lrwd);
+      t.y = adam_one(g.y, m.y, v.y, t.y, a.prm, omb1, omb2, bias1, bias2, lrwd);
+      t.z = adam_one(g.z, m.z, v.z, t.z, a.prm, omb1, omb2, bias1, bias2, lrwd);
+      t.w = adam_one(g.w, m.w, v.w, t.w, a.prm, omb1, omb2, bias1, bias2, lrwd);
+      *reinterpret_cast<float4*>(a.theta + k) = t;
+      *reinterpret_cast<float4*>(a.m + k) = m;
+      *reinterpret_cast<float4*>(a.v + k) = v;
+    }
+    uint2 h;
+    h.x = static_cast<uint32_t>(f32_to_f16_bits(t.x)) | (static_cast<uint32_t>(f32_to_f16_bits(t.y)) << 16);
+    h.y = static_cast<uint32_t>(f32_to_f16_bits(t.z)) | (static_cast<uint32_t>(f32_to_f16_bits(t.w)) << 16);
+    *reinterpret_cast<uint2*>(a.theta16c + k) = h;
+  }
+  // scalar tail (fewer than 4 elements)
+  if (blockIdx.x == 0 && threadIdx.x < (a.k1 - a.k0) % 4) {
+    const uint64_t k = a.k0 + 4 * nv + threadIdx.x;
+    const float g = a.g[k];
+    float t = a.theta[k], m = a.m[k], v = a.v[k];
+    nacc = __fadd_rn(nacc, __fmul_rn(g, g));
+    if (!skip) {
+      t = adam_one(g, m, v, t, a.prm, omb1, omb2, bias1, bias2, lrwd);
+      a.theta[k] = t;
+      a.m[k] = m;
+      a.v[k] = v;
+    }
+    a.theta16c[k] = f32_to_f16_bits(t);
+  }
+  float x = nacc;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = __fadd_rn(x, __shfl_xor_sync(0xFFFFFFFFu, x, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int w = 0; w < kThreads / 32; ++w) s = __fadd_rn(s, red[w]);
+    a.norm_partials[blockIdx.x] = s;
+    __threadfence();
+    last_cta = atomicAdd(a.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last_cta && threadIdx.x == 0) {
+    __threadfence();
+    double acc = 0.0;
+    const volatile float* np = a.norm_partials;
+    for (uint32_t b = 0; b < gridDim.x; ++b) acc += static_cast<double>(np[b]);
+    *a.norm2_out = acc;
+    *a.done = 0u;
+    __threadfence();
+  }
+}
+
+// One thread: the step's scalars once the global grad norm^2 and skip flag
+// are known (AdamScalars::advance, train.hpp:325-329; skip, 632-639).
+__global__ void k_step_finalize(SamoStepState* st, const double* norm2, float* flag, float beta1,
+                                float beta2) {
+  const bool skip = *flag != 0.0f;
+  st->grad_norm = static_cast<float>(sqrt(*norm2));
+  if (skip) {
+    st->skipped_steps += 1;
+    st->last_skipped = 1u;
+  } else {
+    st->t += 1;
+    st->beta1_pow = __fmul_rn(st->beta1_pow, beta1);
+    st->beta2_pow = __fmul_rn(st->beta2_pow, beta2);
+    st->last_skipped = 0u;
+  }
+  *flag = 0.0f;
 }
 
 template <typename F>
@@ -511,6 +638,32 @@ int launch_update(const StepArgs& a, bool g_f32, int grid, cudaStream_t s) {
     return launch_persistent(fn, a, sm, grid, s, kThreads + 32, "k23_update");
   };
   return g_f32 ? with_k23<false>(a.tile_elems, go) : with_k23<true>(a.tile_elems, go);
+}
+
+int launch_adam_shard(const ShardArgs& a, int grid, cudaStream_t s) {
+  if (a.k1 <= a.k0) return SAMO_OK;
+  k_adam_shard<<<grid, kThreads, 0, s>>>(a);
+  SAMO_LAUNCH_CHECK("k_adam_shard");
+  return SAMO_OK;
+}
+
+int launch_step_finalize(SamoStepState* st, const double* norm2, float* flag, float beta1,
+                         float beta2, cudaStream_t s) {
+  k_step_finalize<<<1, 1, 0, s>>>(st, norm2, flag, beta1, beta2);
+  SAMO_LAUNCH_CHECK("k_step_finalize");
+  return SAMO_OK;
+}
+
+int launch_expand_c16(const StepArgs& a, int grid, cudaStream_t s) {
+  if (a.ntiles == 0) return SAMO_OK;
+  const size_t sm = k23_smem<true, 1024, 3>(a.tile_elems) <= 113u * 1024u
+                        ? k23_smem<true, 1024, 3>(a.tile_elems)
+                        : k23_smem<true, 1024, 2>(a.tile_elems);
+  if (sm == k23_smem<true, 1024, 3>(a.tile_elems))
+    return launch_persistent(k23_update<true, 1024, 3, true>, a, sm, grid, s, kThreads + 32,
+                             "k23_expand");
+  return launch_persistent(k23_update<true, 1024, 2, true>, a, sm, grid, s, kThreads + 32,
+                           "k23_expand");
 }
 
 int launch_build_off16(const SamoTile* tiles, uint32_t ntiles, const uint32_t* idx,

@@ -321,6 +321,22 @@ class SamoModel:
     def attach_comm(self, comm: Communicator | None) -> None:
         _abi.call("samo_model_attach_comm", self._h, comm.handle if comm else C.c_void_p())
 
+    EXCHANGE_NONE, EXCHANGE_ALLREDUCE, EXCHANGE_SHARDED = 0, 1, 2
+
+    def set_exchange(self, mode: int) -> None:
+        """EXCHANGE_ALLREDUCE (replicated state) or EXCHANGE_SHARDED (ZeRO-1 on
+        the compressed state); -1 restores the default."""
+        _abi.call("samo_model_set_exchange", self._h, int(mode))
+
+    def exchange_mode(self) -> int:
+        return int(_abi.load().samo_model_exchange_mode(self._h))
+
+    def shard_range(self) -> tuple[int, int]:
+        """Compressed-arena range [k0, k1) this rank updates."""
+        k0, k1 = C.c_uint64(), C.c_uint64()
+        _abi.call("samo_model_shard_range", self._h, C.byref(k0), C.byref(k1))
+        return k0.value, k1.value
+
     # -- step ----------------------------------------------------------------
     def set_grads(self, grads: Sequence[torch.Tensor]) -> None:
         """Dense binary16 gradients of the step (the backward sink's input)."""

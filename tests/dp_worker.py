@@ -57,14 +57,18 @@ def main() -> None:
     model.set_config(samo.OptimizerConfig(learning_rate=1e-2))
     comm = sdist.make_communicator()
     model.attach_comm(comm)
+    mode = os.environ.get("SAMO_DP_MODE", "sharded")
+    model.set_exchange(model.EXCHANGE_SHARDED if mode == "sharded" else model.EXCHANGE_ALLREDUCE)
     for s in range(STEPS):
         g = [torch.from_numpy(grads[(rank, s, l)].view(np.int16)).cuda() for l in range(len(DENSE_LEN))]
         model.set_grads(g)
         model.step(graph=os.environ.get("SAMO_DP_GRAPH") == "1")
     torch.cuda.synchronize()
     rec = model.step_record()
+    k0, k1 = model.shard_range()
     out = {"t": np.array([rec.t]), "skipped": np.array([rec.skipped_steps]),
-           "norm": np.array([rec.grad_norm], np.float32)}
+           "norm": np.array([rec.grad_norm], np.float32), "shard": np.array([k0, k1], np.uint64),
+           "k_off": np.array([model.view(l).k_offset for l in range(len(DENSE_LEN))], np.uint64)}
     for l in range(len(DENSE_LEN)):
         for k in ("theta32", "adam_m", "adam_v"):
             out[f"{k}{l}"] = model.read(l, k).cpu().numpy()

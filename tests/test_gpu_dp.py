@@ -60,13 +60,14 @@ def _expected(oracle, world):
     return theta, m, v, t16, t, skipped
 
 
-@pytest.mark.parametrize("mode", ["overlap", "staged", "graph"])
+@pytest.mark.parametrize("mode", ["sharded", "sharded-graph", "overlap", "staged", "graph"])
 def test_dp_two_gpus_bit_exact(tmp_path, oracle, mode):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     env = dict(os.environ)
+    env["SAMO_DP_MODE"] = "sharded" if mode.startswith("sharded") else "allreduce"
     env["SAMO_OVERLAP"] = "0" if mode == "staged" else "1"
-    env["SAMO_DP_GRAPH"] = "1" if mode == "graph" else "0"
+    env["SAMO_DP_GRAPH"] = "1" if mode.endswith("graph") else "0"
     env["SAMO_BUCKETS"] = "5"
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
@@ -75,10 +76,21 @@ def test_dp_two_gpus_bit_exact(tmp_path, oracle, mode):
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     r = [dict(np.load(tmp_path / f"dp_rank{i}.npz")) for i in range(2)]
     theta, m, v, t16, t, skipped = _expected(oracle, 2)
+    covered = 0
     for rr in r:
         assert int(rr["t"][0]) == t and int(rr["skipped"][0]) == skipped == 1
+        k0, k1 = (int(x) for x in rr["shard"])
         for l in range(len(theta)):
-            assert np.array_equal(rr[f"theta32{l}"].view(np.uint32), theta[l].view(np.uint32)), l
-            assert np.array_equal(rr[f"adam_m{l}"].view(np.uint32), m[l].view(np.uint32)), l
-            assert np.array_equal(rr[f"adam_v{l}"].view(np.uint32), v[l].view(np.uint32)), l
+            # theta16 is complete on every rank; theta32/m/v are authoritative
+            # in the rank's shard (everything unless the exchange is sharded)
             assert np.array_equal(rr[f"theta16_{l}"], t16[l]), l
+            off = int(rr["k_off"][l])
+            lo, hi = max(k0 - off, 0), min(k1 - off, len(theta[l]))
+            if hi <= lo:
+                continue
+            covered += hi - lo
+            for name, want in (("theta32", theta), ("adam_m", m), ("adam_v", v)):
+                got = rr[f"{name}{l}"][lo:hi].view(np.uint32)
+                assert np.array_equal(got, want[l][lo:hi].view(np.uint32)), (name, l)
+    n = sum(len(x) for x in theta)
+    assert covered == (n if mode.startswith("sharded") else 2 * n)
