@@ -350,10 +350,24 @@ def run_samo(args) -> None:
             time.sleep(0.35)
     launches = samo.kernel_launch_count() - launches0
     total_ms = t0.elapsed_time(t1)
+    phases = None
     if world > 1:
         tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt.item())
+        # Phase breakdown of the production step (events inside the driver;
+        # sharded exchange only) — not the headline.
+        phases = None
+        if model.exchange_mode() == model.EXCHANGE_SHARDED:
+            _abi.call("samo_model_enable_phase_timing", model.handle, 1)
+            for _ in range(3):
+                model.step()
+            buf = (C.c_float * 16)()
+            cnt = _abi.load().samo_model_phase_times(model.handle, buf, 16)
+            _abi.call("samo_model_enable_phase_timing", model.handle, 0)
+            names = ["K1_gather", "flag_allreduce", "reduce_scatter", "shard_adam", "all_gather",
+                     "norm_allreduce", "expand", "finalize"]
+            phases = {names[i]: round(buf[i], 4) for i in range(max(0, cnt))}
         # Stage breakdown (not the headline): the same three stages run back
         # to back, the exchange as one allreduce of the whole arena.
         KB = min(K, 10)
@@ -503,8 +517,11 @@ def run_samo(args) -> None:
                        "l2": "inputs (>= 16 GB per step) are larger than L2; no flush needed",
                        "gpu": gpu_name},
             "gpu_launches": int(launches),
-            "step_mode": "staged K1|K23 (no exchange)" if world == 1 else
-                         "overlapped: bucketed NCCL allreduce concurrent with K1/K23",
+            "step_mode": "K1 | K23 (no exchange)" if world == 1 else
+                         ("sharded: K1 | NCCL reduce-scatter | shard Adam | NCCL all-gather of "
+                          "binary16 weights | expand" if model.exchange_mode() == model.EXCHANGE_SHARDED
+                          else "allreduce: bucketed NCCL allreduce overlapped with K1/K23"),
+            "phases_ms": phases,
             "roofline": roofline,
             "kernels": kern,
             "e2e": e2e,

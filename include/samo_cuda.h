@@ -253,6 +253,14 @@ int samo_model_exchange_mode(const samo_model* model);
 /* Compressed-arena range [k0, k1) this rank updates (everything unless sharded). */
 int samo_model_shard_range(const samo_model* model, uint64_t* k0, uint64_t* k1);
 
+/* Phase timing of the data-parallel step (CUDA events between its stages;
+ * off by default).  samo_model_phase_times writes the durations (ms) of the
+ * last step's phases and returns their count (sharded exchange: gather, skip
+ * flag allreduce, reduce-scatter, shard Adam, all-gather, norm allreduce,
+ * expand, finalize); it synchronises on the last phase. */
+int samo_model_enable_phase_timing(samo_model* model, int on);
+int samo_model_phase_times(samo_model* model, float* ms, int cap);
+
 /* Per-layer dense binary16 gradients (device pointers, 16-byte aligned,
  * dense_len elements each) consumed by the next step. `ptrs` is a host array
  * of nlayers device pointers; it is copied to the device on `stream`. */

@@ -475,6 +475,10 @@ struct samo_model {
   std::vector<cudaEvent_t> ev_k1, ev_ar;
   cudaEvent_t ev_fork = nullptr, ev_flag = nullptr;
   int reserve_sms = 16;                 // SMs left to NCCL while our kernels run
+  // Phase timing of the data-parallel step.
+  bool phase_timing = false;
+  cudaEvent_t phase_ev[16] = {};
+  int phase_count = 0;
 };
 
 constexpr int kMaxBuckets = 32;
@@ -482,6 +486,14 @@ constexpr uint64_t kArenaSlack = 1024;  // elements: G * shard padding (G <= 128
 constexpr uint64_t kFlagOff = 1000;     // flag slot at g + n_al + kFlagOff
 
 static float* flag_ptr(const samo_model* md) { return md->g + md->n_al + kFlagOff; }
+
+// Optional phase timing of the data-parallel step (samo_model_enable_phase_timing).
+static int phase_mark(samo_model* md, int i, cudaStream_t s) {
+  if (!md->phase_timing) return SAMO_OK;
+  if (!md->phase_ev[i]) SAMO_CUDA_TRY(cudaEventCreate(&md->phase_ev[i]));
+  SAMO_CUDA_TRY(cudaEventRecord(md->phase_ev[i], s));
+  return SAMO_OK;
+}
 
 static uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
@@ -646,6 +658,8 @@ int samo_model_destroy(samo_model* md) {
   for (auto e : md->ev_ar) cudaEventDestroy(e);
   if (md->ev_fork) cudaEventDestroy(md->ev_fork);
   if (md->ev_flag) cudaEventDestroy(md->ev_flag);
+  for (auto e : md->phase_ev)
+    if (e) cudaEventDestroy(e);
   if (md->block) cudaFree(md->block);
   delete md;
   return clear_ok();
@@ -957,12 +971,16 @@ static int step_sharded(samo_model* md, cudaStream_t S) {
   const uint64_t cnt = shard_count(md);
   if (static_cast<uint64_t>(G) * cnt > md->n_al + kFlagOff)
     return fail(SAMO_E_PARAMETER, "too many ranks for the arena padding");
+  SAMO_TRY(phase_mark(md, 0, S));
   SAMO_TRY(launch_gather(step_args(md), true, md->grid_gather32, S));
+  SAMO_TRY(phase_mark(md, 1, S));
   float* flag = flag_ptr(md);
   ncclResult_t rr = ncclAllReduce(flag, flag, 1, ncclFloat32, ncclSum, md->comm->flag, S);
   if (rr != ncclSuccess) return nccl_fail(rr, "ncclAllReduce(flag)");
+  SAMO_TRY(phase_mark(md, 2, S));
   rr = ncclReduceScatter(md->g, md->g + r * cnt, cnt, ncclFloat32, ncclSum, md->comm->comm, S);
   if (rr != ncclSuccess) return nccl_fail(rr, "ncclReduceScatter");
+  SAMO_TRY(phase_mark(md, 3, S));
   ShardArgs sa{};
   sa.g = md->g;
   sa.theta = md->theta;
@@ -984,14 +1002,20 @@ static int step_sharded(samo_model* md, cudaStream_t S) {
   } else {
     SAMO_CUDA_TRY(cudaMemsetAsync(md->norm2, 0, sizeof(double), S));
   }
+  SAMO_TRY(phase_mark(md, 4, S));
   rr = ncclAllGather(md->c16 + r * cnt, md->c16, cnt, ncclFloat16, md->comm->comm, S);
   if (rr != ncclSuccess) return nccl_fail(rr, "ncclAllGather");
+  SAMO_TRY(phase_mark(md, 5, S));
   rr = ncclAllReduce(md->norm2, md->norm2, 1, ncclFloat64, ncclSum, md->comm->flag, S);
   if (rr != ncclSuccess) return nccl_fail(rr, "ncclAllReduce(norm)");
+  SAMO_TRY(phase_mark(md, 6, S));
   StepArgs a = step_args(md);
   a.g = md->c16;
   SAMO_TRY(launch_expand_c16(a, std::min<int>(md->grid_update16, md->ntiles), S));
+  SAMO_TRY(phase_mark(md, 7, S));
   SAMO_TRY(launch_step_finalize(md->st, md->norm2, flag, md->cfg.beta1, md->cfg.beta2, S));
+  SAMO_TRY(phase_mark(md, 8, S));
+  md->phase_count = 8;
   return SAMO_OK;
 }
 
@@ -1007,6 +1031,22 @@ int samo_model_set_exchange(samo_model* md, int mode) {
     md->graph = nullptr;
   }
   return clear_ok();
+}
+
+int samo_model_enable_phase_timing(samo_model* md, int on) {
+  if (!md) return fail(SAMO_E_PARAMETER, "null model");
+  md->phase_timing = on != 0;
+  md->phase_count = 0;
+  return clear_ok();
+}
+
+int samo_model_phase_times(samo_model* md, float* ms, int cap) {
+  if (!md || (cap > 0 && !ms)) return -fail(SAMO_E_PARAMETER, "null argument");
+  const int n = std::min(cap, md->phase_count);
+  if (n <= 0) return 0;
+  if (cudaEventSynchronize(md->phase_ev[n]) != cudaSuccess) return -fail(SAMO_E_CUDA, "event sync");
+  for (int i = 0; i < n; ++i) cudaEventElapsedTime(&ms[i], md->phase_ev[i], md->phase_ev[i + 1]);
+  return n;
 }
 
 int samo_model_exchange_mode(const samo_model* md) {
