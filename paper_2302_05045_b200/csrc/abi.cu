@@ -482,8 +482,8 @@ struct samo_model {
 };
 
 constexpr int kMaxBuckets = 32;
-constexpr uint64_t kArenaSlack = 1024;  // elements: G * shard padding (G <= 128) + flag
-constexpr uint64_t kFlagOff = 1000;     // flag slot at g + n_al + kFlagOff
+constexpr uint64_t kArenaSlack = 64;    // elements: G * shard padding (G <= 8) + flag
+constexpr uint64_t kFlagOff = 48;       // flag slot at g + n_al + kFlagOff
 
 static float* flag_ptr(const samo_model* md) { return md->g + md->n_al + kFlagOff; }
 
@@ -571,14 +571,16 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   // grad arena: n_al floats (the sharded exchange pads it to G * shard size,
   // G <= 128) + the skip-indicator slot at n_al + kFlagOff.
   const uint64_t o_g = carve((n_al + kArenaSlack) * 4), o_idx = carve(n_al * 4);
-  const uint64_t o_c16 = carve((n_al + kArenaSlack) * 2);
-  const uint64_t o_n2 = carve(64);
   const uint64_t o_off = carve(n_al * 2);
   const uint64_t o_t16 = carve(md->d_tot * 2), o_tiles = carve(ntiles * sizeof(SamoTile));
   const uint64_t o_layers = carve(std::max(1, nlayers) * sizeof(SamoLayerDev));
   const uint64_t o_koff = carve((nlayers + 1) * sizeof(uint64_t));
   const uint64_t o_st = carve(sizeof(SamoStepState));
   const uint64_t o_np = carve(static_cast<uint64_t>(max_grid) * kMaxBuckets * sizeof(float));
+  // Buffers of the sharded exchange last: the step kernels' streams keep the
+  // relative placement measured best.
+  const uint64_t o_c16 = carve((n_al + kArenaSlack) * 2);
+  const uint64_t o_n2 = carve(64);
   md->block_bytes = off;
   cudaError_t e = cudaMalloc(&md->block, off);
   if (e != cudaSuccess) {

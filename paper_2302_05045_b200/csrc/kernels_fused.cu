@@ -237,22 +237,25 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
           const uint64_t h0 = kc0 & ~7ull;
           const uint32_t hb = static_cast<uint32_t>((((kc1 + 7) & ~7ull) - h0) * 2);
           const uint32_t gb = G16 ? hb : fb;
-          const uint32_t fb3 = EXPAND ? 0u : fb;  // theta/m/v slots unused when expanding
-          const uint32_t total = 3 * fb3 + gb + hb;
-          if (total == 0) {  // empty, aligned tile: nothing to move, just publish the slot
+          if (kc1 == kc0) {  // empty tile: nothing to move, just publish the slot
             mbar_arrive(&full[s]);
             continue;
           }
-          mbar_arrive_expect_tx(&full[s], total);
-          if (fb3) {
-            bulk_g2s(st, a.theta + f0, fb3, &full[s], policy);
-            bulk_g2s(st + L::kF32, a.m + f0, fb3, &full[s], policy);
-            bulk_g2s(st + 2 * L::kF32, a.v + f0, fb3, &full[s], policy);
-          }
           const void* gsrc = G16 ? static_cast<const void*>(reinterpret_cast<const uint16_t*>(a.g) + h0)
                                  : static_cast<const void*>(reinterpret_cast<const float*>(a.g) + f0);
-          if (gb) bulk_g2s(st + 3 * L::kF32, gsrc, gb, &full[s], policy);
-          if (hb) bulk_g2s(st + 3 * L::kF32 + L::kG, a.off16 + h0, hb, &full[s], policy);
+          if constexpr (EXPAND) {  // theta/m/v slots unused; hb > 0 here
+            mbar_arrive_expect_tx(&full[s], 2 * hb);
+            bulk_g2s(st + 3 * L::kF32, gsrc, hb, &full[s], policy);
+            bulk_g2s(st + 3 * L::kF32 + L::kG, a.off16 + h0, hb, &full[s], policy);
+          } else {
+            // kc1 > kc0, so every range rounded out to 16 bytes is non-empty.
+            mbar_arrive_expect_tx(&full[s], 3 * fb + gb + hb);
+            bulk_g2s(st, a.theta + f0, fb, &full[s], policy);
+            bulk_g2s(st + L::kF32, a.m + f0, fb, &full[s], policy);
+            bulk_g2s(st + 2 * L::kF32, a.v + f0, fb, &full[s], policy);
+            bulk_g2s(st + 3 * L::kF32, gsrc, gb, &full[s], policy);
+            bulk_g2s(st + 3 * L::kF32 + L::kG, a.off16 + h0, hb, &full[s], policy);
+          }
         }
       }
     }
@@ -269,6 +272,16 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
   const float omb2 = __fsub_rn(1.0f, a.prm.beta2);  // train.hpp:336
   const float lrwd = __fmul_rn(a.prm.lr, a.prm.wd);
 
+  // Hot-loop parameters in registers (see pin_f32).
+  const float p_beta1 = pin_f32(a.prm.beta1), p_beta2 = pin_f32(a.prm.beta2);
+  const float p_lr = pin_f32(a.prm.lr), p_eps = pin_f32(a.prm.eps), p_wd = pin_f32(a.prm.wd);
+  const float p_inv = pin_f32(a.inv_scale);
+  const uint32_t p_T = pin_u32(T);
+  float* const p_theta = pin_ptr(a.theta);
+  float* const p_m = pin_ptr(a.m);
+  float* const p_v = pin_ptr(a.v);
+  uint16_t* const p_t16 = pin_ptr(a.theta16);
+
   float nacc = 0.0f;
   uint32_t it = 0, tile_it = 0;
   TileRegs nxt{};
@@ -277,8 +290,8 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
     const TileRegs td = nxt;
     if (t + gridDim.x < a.ntiles) nxt = load_tile(a.tiles + t + gridDim.x);  // prefetch
     const uint32_t nch = tile_chunks<CH>(td.k_begin, td.k_end);
-    uint16_t* out = outb + (tile_it & 1u) * T;
-    uint16_t* dst = a.theta16 + td.out_off;
+    uint16_t* out = outb + (tile_it & 1u) * p_T;
+    uint16_t* dst = p_t16 + td.out_off;
     for (uint32_t j = 0; j < nch; ++j, ++it) {
       const int s = static_cast<int>(it % NS);
       const uint8_t* st = smem + s * L::kStage;
@@ -308,7 +321,7 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
           if (i < n) {
             if constexpr (G16) {
               const uint16_t h = reinterpret_cast<const uint16_t*>(st + 3 * L::kF32)[ho + i];
-              gv[u] = mul_x86(f16_bits_to_f32(h), a.inv_scale);
+              gv[u] = mul_x86(f16_bits_to_f32(h), p_inv);
             } else {
               gv[u] = reinterpret_cast<const float*>(st + 3 * L::kF32)[fo + i];
             }
@@ -326,18 +339,18 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
             nacc = __fadd_rn(nacc, __fmul_rn(gk, gk));
             if (!skip) {
               // adam_update (train.hpp:338-345): IEEE per op, no contraction.
-              const float mk = __fadd_rn(__fmul_rn(a.prm.beta1, mv[u]), __fmul_rn(omb1, gk));
+              const float mk = __fadd_rn(__fmul_rn(p_beta1, mv[u]), __fmul_rn(omb1, gk));
               const float vk =
-                  __fadd_rn(__fmul_rn(a.prm.beta2, vv[u]), __fmul_rn(omb2, __fmul_rn(gk, gk)));
+                  __fadd_rn(__fmul_rn(p_beta2, vv[u]), __fmul_rn(omb2, __fmul_rn(gk, gk)));
               const float mh = __fdiv_rn(mk, bias1);
               const float vh = __fdiv_rn(vk, bias2);
               float tk = __fsub_rn(
-                  tv[u], __fmul_rn(a.prm.lr, __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), a.prm.eps))));
-              if (a.prm.wd != 0.0f) tk = __fsub_rn(tk, __fmul_rn(lrwd, tk));
+                  tv[u], __fmul_rn(p_lr, __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), p_eps))));
+              if (p_wd != 0.0f) tk = __fsub_rn(tk, __fmul_rn(lrwd, tk));
               const uint64_t k = kc0 + i;
-              st_na_f32(a.m + k, mk);
-              st_na_f32(a.v + k, vk);
-              st_na_f32(a.theta + k, tk);
+              st_na_f32(p_m + k, mk);
+              st_na_f32(p_v + k, vk);
+              st_na_f32(p_theta + k, tk);
               out[ov[u]] = f32_to_f16_bits(tk);
             }
           }
