@@ -1,0 +1,291 @@
+// kat_test.cpp — the reference's own known-answer tests, restated against the
+// CUDA-backed drop-in API (include/samo_b200/samo.hpp).  Each block names the
+// reference test it ports (proj/tests/*.cpp).  Built by tests/test_cpp_kat.py;
+// prints one line per test and exits non-zero on the first failure group.
+#include <bit>
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <limits>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "samo_b200/samo.hpp"
+
+using namespace samo_b200;
+
+static int g_fail = 0, g_pass = 0;
+
+#define CHECK(cond)                                                              \
+  do {                                                                           \
+    if (!(cond)) {                                                               \
+      std::printf("  FAILED %s:%d: %s\n", __FILE__, __LINE__, #cond);            \
+      throw std::runtime_error("check failed");                                  \
+    }                                                                            \
+  } while (0)
+
+template <typename E, typename F>
+static bool throws(F f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+static void run(const char* name, const std::function<void()>& body) {
+  try {
+    body();
+    ++g_pass;
+    std::printf("PASS %s\n", name);
+  } catch (const std::exception& e) {
+    ++g_fail;
+    std::printf("FAIL %s (%s)\n", name, e.what());
+  }
+}
+
+static std::shared_ptr<const PrunedIndexSet> make_ind(std::uint64_t dense_len,
+                                                      std::vector<std::uint32_t> idx) {
+  PrunedIndexSet s;
+  s.layer_id = "w";
+  s.dense_len = dense_len;
+  s.indices = std::move(idx);
+  return std::make_shared<const PrunedIndexSet>(std::move(s));
+}
+
+static LayerParams layer(std::string id, std::vector<float> values, bool prunable = true) {
+  const std::size_t n = values.size();
+  return {std::move(id), Tensor<float>({n}, std::move(values)), prunable};
+}
+
+int main() {
+  // ---- half_test.cpp ------------------------------------------------------
+  run("Half.SpecExamples (half_test.cpp:54-59)", [] {
+    CHECK(static_cast<float>(Half(1.0f)) == 1.0f);
+    CHECK(static_cast<float>(Half(2049.0f)) == 2048.0f);
+    CHECK(static_cast<float>(Half(0.5f)) == 0.5f);
+  });
+  run("Half.ExhaustiveRoundTrip (half_test.cpp:61-68)", [] {
+    std::vector<Half> all;
+    for (std::uint32_t b = 0; b <= 0xFFFF; ++b) {
+      const Half h = Half::from_bits(static_cast<std::uint16_t>(b));
+      if (h.is_finite()) all.push_back(h);
+    }
+    const auto back = to_half(to_float(all));
+    for (std::size_t i = 0; i < all.size(); ++i) CHECK(back[i].bits() == all[i].bits());
+  });
+  run("Half.OverflowAndUnderflowEdges (half_test.cpp:83-94)", [] {
+    const std::vector<float> f = {65504.0f, 65519.996f, 65520.0f, 1.0e10f, -1.0e10f, 0x1.0p-24f,
+                                  0x1.0p-25f, std::nextafterf(0x1.0p-25f, 1.0f), -0.0f};
+    const std::vector<std::uint16_t> want = {0x7BFF, 0x7BFF, 0x7C00, 0x7C00, 0xFC00,
+                                             0x0001, 0x0000, 0x0001, 0x8000};
+    const auto got = to_half(f);
+    for (std::size_t i = 0; i < f.size(); ++i) CHECK(got[i].bits() == want[i]);
+  });
+  run("Half.InfinityAndNanSurvive (half_test.cpp:70-81)", [] {
+    CHECK(Half(static_cast<float>(Half::from_bits(0x7C00))).bits() == 0x7C00);
+    CHECK(Half(static_cast<float>(Half::from_bits(0xFC00))).bits() == 0xFC00);
+    CHECK(Half(std::numeric_limits<float>::quiet_NaN()).is_nan());
+    CHECK(std::isnan(static_cast<float>(Half::from_bits(0x7E01))));
+  });
+
+  // ---- store_test.cpp -----------------------------------------------------
+  run("Compress.GatherByDefinition (store_test.cpp:29-33)", [] {
+    const Tensor<float> dense({4}, {1.0f, 2.0f, 3.0f, 4.0f});
+    CHECK((compress(dense, *make_ind(4, {0, 3})) == std::vector<float>{1.0f, 4.0f}));
+  });
+  run("Compress.FullIndexSetIsIdentity (store_test.cpp:35-40)", [] {
+    const Tensor<float> dense({2, 2}, {1.0f, 2.0f, 3.0f, 4.0f});
+    CHECK((compress(dense, *make_ind(4, {0, 1, 2, 3})) == std::vector<float>{1, 2, 3, 4}));
+  });
+  run("Compress.MatchesGatherOracle (store_test.cpp:42-58)", [] {
+    std::mt19937_64 eng(41);
+    Tensor<float> dense({4, 4});
+    for (auto& v : dense.flat()) v = static_cast<float>(eng() >> 40) * 0x1.0p-24f;
+    std::vector<std::uint32_t> idx;
+    for (std::uint32_t i = 0; i < 16; ++i)
+      if (eng() % 2) idx.push_back(i);
+    const auto got = compress(dense, *make_ind(16, idx));
+    CHECK(got.size() == idx.size());
+    for (std::size_t k = 0; k < idx.size(); ++k) CHECK(got[k] == dense.flat()[idx[k]]);
+  });
+  run("Compress.LengthMismatch (store_test.cpp:60-64)", [] {
+    const Tensor<float> dense({3});
+    CHECK(throws<DimensionError>([&] { compress(dense, *make_ind(4, {0})); }));
+  });
+  run("Expand.ScatterByDefinition (store_test.cpp:66-71)", [] {
+    const std::vector<float> values = {1.0f, 4.0f};
+    const Tensor<float> got = expand<float>(values, *make_ind(4, {0, 3}), {2, 2});
+    CHECK((got == Tensor<float>({2, 2}, {1.0f, 0.0f, 0.0f, 4.0f})));
+  });
+  run("Expand.EmptyIndexSetGivesZeros (store_test.cpp:73-77)", [] {
+    const Tensor<float> got = expand<float>(std::vector<float>{}, *make_ind(4, {}), {4});
+    CHECK((got == Tensor<float>({4})));
+  });
+  run("Expand.RoundTripProperty (store_test.cpp:79-108, 1000 trials)", [] {
+    std::mt19937_64 eng(43);
+    for (int trial = 0; trial < 1000; ++trial) {
+      std::vector<std::size_t> shape(1 + eng() % 3);
+      for (auto& e : shape) e = 1 + eng() % 5;
+      const std::size_t n = numel(shape);
+      std::vector<std::uint32_t> idx;
+      for (std::uint32_t i = 0; i < n; ++i)
+        if (eng() % 3) idx.push_back(i);
+      const auto ind = make_ind(n, idx);
+      std::vector<float> xf(n);
+      for (auto& v : xf) v = (static_cast<float>(eng() >> 40) * 0x1.0p-24f - 0.5f) * 8.0f;
+      const Tensor<Half> x(shape, to_half(xf));
+      const auto values = compress(x, *ind);
+      const Tensor<Half> expanded = expand<Half>(values, *ind, shape);
+      Tensor<Half> masked(shape);
+      for (auto i : idx) masked.flat()[i] = x.flat()[i];
+      CHECK(bit_equal(expanded, masked));
+      const auto back = compress(expanded, *ind);
+      CHECK(back.size() == values.size());
+      for (std::size_t k = 0; k < back.size(); ++k) CHECK(back[k].bits() == values[k].bits());
+    }
+  });
+
+  // ---- prune_test.cpp -----------------------------------------------------
+  run("Linearize.PaperExample2x2 / RowMajorOracle / OutOfBounds (prune_test.cpp:24-47)", [] {
+    const std::vector<std::vector<std::uint64_t>> c = {{0, 0}, {1, 1}};
+    const std::vector<std::size_t> s22 = {2, 2};
+    CHECK((linearize(c, s22) == std::vector<std::uint64_t>{0, 3}));
+    const std::vector<std::vector<std::uint64_t>> c3 = {{1, 2, 3}};
+    const std::vector<std::size_t> s234 = {2, 3, 4};
+    CHECK((linearize(c3, s234) == std::vector<std::uint64_t>{23}));
+    const std::vector<std::vector<std::uint64_t>> bad = {{2, 0}};
+    CHECK(throws<IndexError>([&] { linearize(bad, s22); }));
+  });
+  run("MagnitudePrune.SortByMagnitudeOracle (prune_test.cpp:84-92)", [] {
+    const std::vector<LayerParams> layers = {layer("w", {3.0f, -1.0f, 0.5f, -4.0f})};
+    const auto sets = magnitude_prune(layers, 0.5);
+    CHECK(sets.size() == 1u);
+    CHECK((sets[0].indices == std::vector<std::uint32_t>{0, 3}));
+    CHECK(sets[0].dense_len == 4u && sets[0].layer_id == "w");
+  });
+  run("MagnitudePrune.ZeroSparsity / Ties / BadSparsity / NonPrunable (prune_test.cpp:94-118)", [] {
+    CHECK((magnitude_prune(std::vector<LayerParams>{layer("w", {0.1f, -0.2f, 0.0f})}, 0.0)[0].indices ==
+           std::vector<std::uint32_t>{0, 1, 2}));
+    CHECK((magnitude_prune(std::vector<LayerParams>{layer("w", {1.0f, 1.0f, 1.0f, 1.0f})}, 0.5)[0].indices ==
+           std::vector<std::uint32_t>{0, 1}));
+    const std::vector<LayerParams> one = {layer("w", {1.0f})};
+    CHECK(throws<ParameterError>([&] { magnitude_prune(one, 1.0); }));
+    CHECK(throws<ParameterError>([&] { magnitude_prune(one, -0.1); }));
+    const std::vector<LayerParams> two = {layer("w", {5.0f, 1.0f, 2.0f, 3.0f}), layer("b", {0.0f, 0.0f}, false)};
+    const auto sets = magnitude_prune(two, 0.75);
+    CHECK(sets[0].indices.size() == 1u);
+    CHECK((sets[1].indices == std::vector<std::uint32_t>{0, 1}));
+  });
+  run("MagnitudePrune.CountMatchesRoundingConvention (prune_test.cpp:127-147)", [] {
+    std::mt19937_64 eng(23);
+    for (int trial = 0; trial < 200; ++trial) {
+      const std::uint64_t den = 20, num = eng() % den;
+      const double p = static_cast<double>(num) / static_cast<double>(den);
+      const std::size_t n = 1 + eng() % 50;
+      std::vector<float> values(n);
+      for (auto& v : values) v = (static_cast<float>(eng() >> 40) * 0x1.0p-24f - 0.5f) * 2.0f;
+      const auto sets = magnitude_prune(std::vector<LayerParams>{layer("w", values)}, p);
+      const std::uint64_t q = (den - num) * n;
+      CHECK(sets[0].indices.size() == (2 * q + den) / (2 * den));
+      for (std::size_t i = 1; i < sets[0].indices.size(); ++i) CHECK(sets[0].indices[i - 1] < sets[0].indices[i]);
+      for (auto i : sets[0].indices) CHECK(i < n);
+    }
+  });
+  run("MagnitudePrune.ScaleInvariance (prune_test.cpp:149-168)", [] {
+    std::mt19937_64 eng(29);
+    for (int trial = 0; trial < 50; ++trial) {
+      const std::size_t n = 8 + eng() % 32;
+      std::vector<float> values(n);
+      for (auto& v : values) v = (static_cast<float>(eng() >> 40) * 0x1.0p-24f - 0.5f) * 2.0f;
+      const double p = 0.05 * static_cast<double>(eng() % 20);
+      const auto base = magnitude_prune(std::vector<LayerParams>{layer("w", values)}, p);
+      for (float c : {0.5f, 2.0f, 8.0f}) {
+        std::vector<float> scaled(values);
+        for (auto& v : scaled) v *= c;
+        CHECK(magnitude_prune(std::vector<LayerParams>{layer("w", scaled)}, p)[0].indices == base[0].indices);
+      }
+    }
+  });
+  run("MagnitudePrune.GlobalScope (prune_test.cpp:170-202)", [] {
+    const std::vector<LayerParams> layers = {layer("big", {10.0f, 9.0f, 8.0f, 7.0f}),
+                                             layer("small", {1.0f, 0.9f, 0.8f, 0.7f})};
+    const auto g = magnitude_prune(layers, 0.5, PruneScope::global);
+    CHECK((g[0].indices == std::vector<std::uint32_t>{0, 1, 2, 3}) && g[1].indices.empty());
+    const auto pl = magnitude_prune(layers, 0.5, PruneScope::per_layer);
+    CHECK(pl[0].indices.size() == 2u && pl[1].indices.size() == 2u);
+    std::mt19937_64 eng(31);
+    std::vector<LayerParams> ls;
+    std::uint64_t total = 0;
+    for (int l = 0; l < 3; ++l) {
+      const std::size_t n = 5 + eng() % 20;
+      total += n;
+      std::vector<float> v(n);
+      for (auto& x : v) x = (static_cast<float>(eng() >> 40) * 0x1.0p-24f - 0.5f) * 2.0f;
+      ls.push_back(layer("l" + std::to_string(l), v));
+    }
+    const auto sets = magnitude_prune(ls, 0.45, PruneScope::global);
+    std::uint64_t kept = 0;
+    for (const auto& s : sets) kept += s.indices.size();
+    CHECK(kept == (2 * 11 * total + 20) / 40);
+  });
+
+  // ---- train_test.cpp -----------------------------------------------------
+  run("OptimizerStep.ScalarAdamOracle (train_test.cpp:156-180)", [] {
+    std::vector<float> th = {0.5f}, m = {0.0f}, v = {0.0f};
+    const std::vector<float> g = {1.0f};
+    OptimizerConfig cfg;
+    cfg.learning_rate = 0.1f;
+    cfg.loss_scale = 1.0f;
+    adam_update(th, m, v, g, cfg, 1.0f - 0.9f, 1.0f - 0.999f);
+    CHECK(std::fabs(th[0] - 0.4f) <= 1e-6f);
+  });
+  run("Model.ScalarAdamOracle through the fused step (train_test.cpp:156-180)", [] {
+    Model model({*make_ind(1, {0})});
+    model.init_layer(0, Tensor<float>({1, 1}, {0.5f}));
+    OptimizerConfig cfg;
+    cfg.learning_rate = 0.1f;
+    cfg.loss_scale = 1.0f;
+    model.set_config(cfg);
+    DeviceBuffer<std::uint16_t> grad(1);
+    const std::uint16_t one = Half(1.0f).bits();
+    grad.upload(&one, 1);
+    model.set_grads({grad.get()});
+    model.step();
+    const auto rec = model.record();
+    CHECK(rec.t == 1 && rec.skipped_steps == 0);
+    CHECK(std::fabs(model.theta32(0)[0] - 0.4f) <= 1e-6f);
+    model.check_state_invariants();
+  });
+  run("OptimizerStep.NonFiniteGradientSkipsAndCounts (train_test.cpp:182-199)", [] {
+    Model model({*make_ind(1, {0})});
+    model.init_layer(0, Tensor<float>({1, 1}, {0.5f}));
+    OptimizerConfig cfg;
+    cfg.learning_rate = 0.1f;
+    cfg.loss_scale = 65536.0f;
+    model.set_config(cfg);
+    DeviceBuffer<std::uint16_t> grad(1);
+    const std::uint16_t inf = 0x7C00;
+    grad.upload(&inf, 1);
+    model.set_grads({grad.get()});
+    model.step();
+    const auto rec = model.record();
+    CHECK(rec.skipped_steps == 1 && rec.last_skipped && rec.t == 0);
+    CHECK(model.theta32(0)[0] == 0.5f);
+    CHECK(model.adam_m(0)[0] == 0.0f);
+  });
+  run("OptimizerStep.StateErrors (train_test.cpp: optimizer_step requires backward)", [] {
+    Model model({*make_ind(4, {0, 3})});
+    CHECK(throws<StateError>([&] { model.step(); }));
+    OptimizerConfig bad;
+    bad.loss_scale = 1000.0f;
+    CHECK(throws<ParameterError>([&] { model.set_config(bad); }));
+  });
+
+  std::printf("%d passed, %d failed\n", g_pass, g_fail);
+  return g_fail ? 1 : 0;
+}
