@@ -365,8 +365,9 @@ def run_samo(args) -> None:
             buf = (C.c_float * 16)()
             cnt = _abi.load().samo_model_phase_times(model.handle, buf, 16)
             _abi.call("samo_model_enable_phase_timing", model.handle, 0)
-            names = ["K1_gather", "flag_allreduce", "reduce_scatter", "shard_adam", "all_gather",
-                     "norm_allreduce", "expand", "finalize"]
+            names = ["K1_gather (reduce-scatter overlapped)",
+                     "skip flag + shard Adam + first all-gather bucket",
+                     "expand (all-gather overlapped)", "norm allreduce + finalize"]
             phases = {names[i]: round(buf[i], 4) for i in range(max(0, cnt))}
         # Stage breakdown (not the headline): the same three stages run back
         # to back, the exchange as one allreduce of the whole arena.
@@ -518,8 +519,8 @@ def run_samo(args) -> None:
                        "gpu": gpu_name},
             "gpu_launches": int(launches),
             "step_mode": "K1 | K23 (no exchange)" if world == 1 else
-                         ("sharded: K1 | NCCL reduce-scatter | shard Adam | NCCL all-gather of "
-                          "binary16 weights | expand" if model.exchange_mode() == model.EXCHANGE_SHARDED
+                         ("sharded (ZeRO-1), k-bucketed: K1 || NCCL reduce-scatter, shard Adam, "
+                          "NCCL all-gather of binary16 weights || expand" if model.exchange_mode() == model.EXCHANGE_SHARDED
                           else "allreduce: bucketed NCCL allreduce overlapped with K1/K23"),
             "phases_ms": phases,
             "roofline": roofline,

@@ -239,7 +239,9 @@ int samo_model_attach_comm(samo_model* model, samo_comm* comm);
  *  SAMO_EXCHANGE_SHARDED — ZeRO-1 on the compressed state: reduce-scatter of
  *    the gradient arena, Adam on the rank's shard only, all-gather of the
  *    compressed binary16 weights, local expand.  theta32/m/v are
- *    authoritative only inside samo_model_shard_range(); theta16 everywhere.
+ *    authoritative only on the rank's shard (samo_model_shard_layout);
+ *    theta16 everywhere.  The exchange is pipelined over k-buckets
+ *    (SAMO_SHARD_BUCKETS, default 4) behind the gather and expand kernels.
  * The default is SHARDED (environment SAMO_EXCHANGE=allreduce overrides);
  * mode -1 restores the default. */
 enum samo_exchange_mode {
@@ -250,8 +252,11 @@ enum samo_exchange_mode {
 int samo_model_set_exchange(samo_model* model, int mode);
 /* SAMO_EXCHANGE_NONE without a communicator of size > 1. */
 int samo_model_exchange_mode(const samo_model* model);
-/* Compressed-arena range [k0, k1) this rank updates (everything unless sharded). */
-int samo_model_shard_range(const samo_model* model, uint64_t* k0, uint64_t* k1);
+/* Compressed-arena elements this rank updates: for b in [0, buckets) the
+ * range [b*stride + rank*chunk, b*stride + (rank+1)*chunk) clipped to the
+ * arena (chunk = stride = nnz, buckets = 1, rank = 0 unless sharded). */
+int samo_model_shard_layout(samo_model* model, uint64_t* chunk, uint64_t* stride,
+                            int* buckets, int* rank);
 
 /* Phase timing of the data-parallel step (CUDA events between its stages;
  * off by default).  samo_model_phase_times writes the durations (ms) of the

@@ -120,7 +120,7 @@ _SIGS = {
     "samo_model_attach_comm": (C.c_int, [vp, vp]),
     "samo_model_set_exchange": (C.c_int, [vp, C.c_int]),
     "samo_model_exchange_mode": (C.c_int, [vp]),
-    "samo_model_shard_range": (C.c_int, [vp, u64p, u64p]),
+    "samo_model_shard_layout": (C.c_int, [vp, u64p, u64p, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "samo_model_enable_phase_timing": (C.c_int, [vp, C.c_int]),
     "samo_model_phase_times": (C.c_int, [vp, C.POINTER(C.c_float), C.c_int]),
     "samo_model_set_grads": (C.c_int, [vp, C.POINTER(vp), vp]),

@@ -428,6 +428,13 @@ int samo_allreduce_sum_f32(samo_comm* comm, float* buf, uint64_t n, samo_stream_
 // ---------------------------------------------------------------------------
 // Model state + step driver
 
+// Bucketing of the sharded (ZeRO-1) data-parallel step (step_sharded).
+struct ShardPlan {
+  int G = 0, B = 0;
+  uint64_t c = 0, C = 0;
+  std::vector<uint32_t> k1_t, ex_t;  // tile boundaries per bucket, B + 1 each
+};
+
 struct samo_model {
   int nlayers = 0;
   uint32_t tile_elems = kDefaultTile;
@@ -475,6 +482,9 @@ struct samo_model {
   std::vector<cudaEvent_t> ev_k1, ev_ar;
   cudaEvent_t ev_fork = nullptr, ev_flag = nullptr;
   int reserve_sms = 16;                 // SMs left to NCCL while our kernels run
+  ShardPlan shard_plan;
+  std::vector<cudaEvent_t> ev_sh;       // sharded pipeline: K1 and all-gather events
+  int grid_expand = 0;
   // Phase timing of the data-parallel step.
   bool phase_timing = false;
   cudaEvent_t phase_ev[16] = {};
@@ -482,8 +492,8 @@ struct samo_model {
 };
 
 constexpr int kMaxBuckets = 32;
-constexpr uint64_t kArenaSlack = 64;    // elements: G * shard padding (G <= 8) + flag
-constexpr uint64_t kFlagOff = 48;       // flag slot at g + n_al + kFlagOff
+constexpr uint64_t kArenaSlack = 2048;  // elements: bucket x rank padding of the sharded exchange + flag
+constexpr uint64_t kFlagOff = 2040;     // flag slot at g + n_al + kFlagOff
 
 static float* flag_ptr(const samo_model* md) { return md->g + md->n_al + kFlagOff; }
 
@@ -554,6 +564,7 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   md->grid_gather32 = step_grid(0, true, tile_elems);
   md->grid_update16 = step_grid(1, false, tile_elems);
   md->grid_update32 = step_grid(1, true, tile_elems);
+  md->grid_expand = expand_grid(tile_elems);
   const int max_grid = std::max(md->grid_update16, md->grid_update32);
 
   // Carve one allocation.
@@ -580,7 +591,7 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   // Buffers of the sharded exchange last: the step kernels' streams keep the
   // relative placement measured best.
   const uint64_t o_c16 = carve((n_al + kArenaSlack) * 2);
-  const uint64_t o_n2 = carve(64);
+  const uint64_t o_n2 = carve(256);  // 16 norm^2 slots + arrival counter
   md->block_bytes = off;
   cudaError_t e = cudaMalloc(&md->block, off);
   if (e != cudaSuccess) {
@@ -596,7 +607,7 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   md->off16 = reinterpret_cast<uint16_t*>(b + o_off);
   md->c16 = reinterpret_cast<uint16_t*>(b + o_c16);
   md->norm2 = reinterpret_cast<double*>(b + o_n2);
-  md->done = reinterpret_cast<uint32_t*>(b + o_n2 + 16);
+  md->done = reinterpret_cast<uint32_t*>(b + o_n2 + 16 * sizeof(double));
   md->theta16 = reinterpret_cast<uint16_t*>(b + o_t16);
   md->tiles = reinterpret_cast<SamoTile*>(b + o_tiles);
   md->layers_dev = reinterpret_cast<SamoLayerDev*>(b + o_layers);
@@ -660,6 +671,7 @@ int samo_model_destroy(samo_model* md) {
   for (auto e : md->ev_ar) cudaEventDestroy(e);
   if (md->ev_fork) cudaEventDestroy(md->ev_fork);
   if (md->ev_flag) cudaEventDestroy(md->ev_flag);
+  for (auto e : md->ev_sh) cudaEventDestroy(e);
   for (auto e : md->phase_ev)
     if (e) cudaEventDestroy(e);
   if (md->block) cudaFree(md->block);
@@ -963,61 +975,139 @@ static uint64_t shard_count(const samo_model* md) {
   return align_up((md->n_tot + G - 1) / G, 8);
 }
 
-// One data-parallel step, ZeRO-1 style on the compressed state:
-//   K1 (fp32, 1/G folded) -> allreduce(skip flag) -> reduce-scatter(grad)
-//   -> Adam on the own shard (theta32/m/v + compressed binary16 copy)
-//   -> all-gather(theta16c) + allreduce(norm^2) -> expand every tile -> scalars.
-// Link bytes per rank 6n(G-1)/G instead of 8n(G-1)/G, Adam HBM traffic / G.
-static int step_sharded(samo_model* md, cudaStream_t S) {
-  const int G = comm_size(md), r = md->comm->rank;
-  const uint64_t cnt = shard_count(md);
-  if (static_cast<uint64_t>(G) * cnt > md->n_al + kFlagOff)
-    return fail(SAMO_E_PARAMETER, "too many ranks for the arena padding");
-  SAMO_TRY(phase_mark(md, 0, S));
-  SAMO_TRY(launch_gather(step_args(md), true, md->grid_gather32, S));
-  SAMO_TRY(phase_mark(md, 1, S));
-  float* flag = flag_ptr(md);
-  ncclResult_t rr = ncclAllReduce(flag, flag, 1, ncclFloat32, ncclSum, md->comm->flag, S);
-  if (rr != ncclSuccess) return nccl_fail(rr, "ncclAllReduce(flag)");
-  SAMO_TRY(phase_mark(md, 2, S));
-  rr = ncclReduceScatter(md->g, md->g + r * cnt, cnt, ncclFloat32, ncclSum, md->comm->comm, S);
-  if (rr != ncclSuccess) return nccl_fail(rr, "ncclReduceScatter");
-  SAMO_TRY(phase_mark(md, 3, S));
-  ShardArgs sa{};
-  sa.g = md->g;
-  sa.theta = md->theta;
-  sa.m = md->m;
-  sa.v = md->v;
-  sa.theta16c = md->c16;
-  sa.k0 = std::min<uint64_t>(r * cnt, md->n_tot);
-  sa.k1 = std::min<uint64_t>((r + 1) * cnt, md->n_tot);
-  sa.prm = adam_params(&md->cfg);
-  sa.st = md->st;
-  sa.flag_slot = flag;
-  sa.norm_partials = md->norm_partials;
-  sa.norm2_out = md->norm2;
-  sa.done = md->done;
-  const uint64_t nv = (sa.k1 - sa.k0 + 3) / 4;
-  const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(num_sms() * 8, (nv + 255) / 256)));
-  if (sa.k1 > sa.k0) {
-    SAMO_TRY(launch_adam_shard(sa, grid, S));
-  } else {
-    SAMO_CUDA_TRY(cudaMemsetAsync(md->norm2, 0, sizeof(double), S));
+// One data-parallel step, ZeRO-1 style on the compressed state, pipelined
+// over B k-buckets (bucket b = arena range [b*C, (b+1)*C), C = G*c, rank r
+// owns [b*C + r*c, b*C + (r+1)*c) of every bucket):
+//
+//   S (caller):  K1[0] .. K1[B-1]                      wait AG[b] -> expand[b] ...   finalize
+//   s_comm:           RS[0] .. RS[B-1] | wait flag | Adam[b] AG[b] ...
+//   s_flag:                    flag allreduce (after K1[B-1])        norm allreduce
+//
+// K1[b] covers the tiles whose first kept element lies in bucket b (so RS[b]
+// only waits for K1[0..b]); expand[b] covers the tiles whose last kept element
+// lies in bucket b (so it only waits for AG[0..b]).  The reduce-scatter hides
+// behind the gather kernels and the all-gather behind the expand kernels.
+// Link bytes per rank 6n(G-1)/G instead of 8n(G-1)/G; Adam HBM traffic / G.
+static int plan_shards(samo_model* md, ShardPlan& p) {
+  const int G = comm_size(md);
+  int B = env_int("SAMO_SHARD_BUCKETS", 4);
+  B = std::max(1, std::min(B, 16));
+  if (p.G == G && p.B == B) return SAMO_OK;
+  p.G = G;
+  p.B = B;
+  p.c = align_up((md->n_tot + static_cast<uint64_t>(G) * B - 1) / (static_cast<uint64_t>(G) * B), 8);
+  p.C = p.c * G;
+  if (p.C * B > md->n_al + kFlagOff)
+    return fail(SAMO_E_PARAMETER, "too many ranks x buckets for the arena padding");
+  auto bucket_of = [&](uint64_t k) { return static_cast<int>(std::min<uint64_t>(k / p.C, B - 1)); };
+  p.k1_t.assign(B + 1, md->ntiles);
+  p.ex_t.assign(B + 1, md->ntiles);
+  p.k1_t[0] = p.ex_t[0] = 0;
+  // first tile of each bucket (keys are non-decreasing in tile order)
+  std::vector<int> k1_first(B + 1, -1), ex_first(B + 1, -1);
+  for (uint32_t t = 0; t < md->ntiles; ++t) {
+    const SamoTile& td = md->tiles_host[t];
+    const int b1 = bucket_of(td.k_begin);
+    const int be = bucket_of(td.k_end > 0 ? td.k_end - 1 : 0);
+    for (int b = 1; b <= b1; ++b)
+      if (p.k1_t[b] == md->ntiles) p.k1_t[b] = t;
+    for (int b = 1; b <= be; ++b)
+      if (p.ex_t[b] == md->ntiles) p.ex_t[b] = t;
   }
-  SAMO_TRY(phase_mark(md, 4, S));
-  rr = ncclAllGather(md->c16 + r * cnt, md->c16, cnt, ncclFloat16, md->comm->comm, S);
-  if (rr != ncclSuccess) return nccl_fail(rr, "ncclAllGather");
-  SAMO_TRY(phase_mark(md, 5, S));
-  rr = ncclAllReduce(md->norm2, md->norm2, 1, ncclFloat64, ncclSum, md->comm->flag, S);
+  (void)k1_first;
+  (void)ex_first;
+  for (int b = 1; b <= B; ++b) {  // monotone
+    p.k1_t[b] = std::max(p.k1_t[b], p.k1_t[b - 1]);
+    p.ex_t[b] = std::max(p.ex_t[b], p.ex_t[b - 1]);
+  }
+  p.k1_t[B] = p.ex_t[B] = md->ntiles;
+  return SAMO_OK;
+}
+
+static int step_sharded(samo_model* md, cudaStream_t S) {
+  SAMO_TRY(plan_buckets(md));  // side streams + events
+  ShardPlan& p = md->shard_plan;
+  SAMO_TRY(plan_shards(md, p));
+  const int r = md->comm->rank, B = p.B;
+  if (static_cast<int>(md->ev_sh.size()) < 2 * B) {
+    for (int i = static_cast<int>(md->ev_sh.size()); i < 2 * B; ++i) {
+      cudaEvent_t e;
+      SAMO_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      md->ev_sh.push_back(e);
+    }
+  }
+  cudaEvent_t* ev_k1 = md->ev_sh.data();
+  cudaEvent_t* ev_ag = md->ev_sh.data() + B;
+  cudaStream_t C = md->s_comm, F = md->s_flag;
+  float* flag = flag_ptr(md);
+  const StepArgs base = step_args(md);
+
+  SAMO_TRY(phase_mark(md, 0, S));
+  SAMO_CUDA_TRY(cudaEventRecord(md->ev_fork, S));
+  SAMO_CUDA_TRY(cudaStreamWaitEvent(C, md->ev_fork, 0));
+  SAMO_CUDA_TRY(cudaStreamWaitEvent(F, md->ev_fork, 0));
+  for (int b = 0; b < B; ++b) {
+    StepArgs a = base;
+    a.tiles = md->tiles + p.k1_t[b];
+    a.ntiles = p.k1_t[b + 1] - p.k1_t[b];
+    if (a.ntiles) SAMO_TRY(launch_gather(a, true, std::min<int>(md->grid_gather32, a.ntiles), S));
+    SAMO_CUDA_TRY(cudaEventRecord(ev_k1[b], S));
+    SAMO_CUDA_TRY(cudaStreamWaitEvent(C, ev_k1[b], 0));
+    float* gb = md->g + b * p.C;
+    const ncclResult_t rr = ncclReduceScatter(gb, gb + r * p.c, p.c, ncclFloat32, ncclSum, md->comm->comm, C);
+    if (rr != ncclSuccess) return nccl_fail(rr, "ncclReduceScatter");
+  }
+  SAMO_TRY(phase_mark(md, 1, S));
+  SAMO_CUDA_TRY(cudaStreamWaitEvent(F, ev_k1[B - 1], 0));
+  ncclResult_t rr = ncclAllReduce(flag, flag, 1, ncclFloat32, ncclSum, md->comm->flag, F);
+  if (rr != ncclSuccess) return nccl_fail(rr, "ncclAllReduce(flag)");
+  SAMO_CUDA_TRY(cudaEventRecord(md->ev_flag, F));
+  SAMO_CUDA_TRY(cudaStreamWaitEvent(C, md->ev_flag, 0));
+  for (int b = 0; b < B; ++b) {
+    ShardArgs sa{};
+    sa.g = md->g;
+    sa.theta = md->theta;
+    sa.m = md->m;
+    sa.v = md->v;
+    sa.theta16c = md->c16;
+    sa.k0 = std::min<uint64_t>(b * p.C + r * p.c, md->n_tot);
+    sa.k1 = std::min<uint64_t>(b * p.C + (r + 1) * p.c, md->n_tot);
+    sa.prm = adam_params(&md->cfg);
+    sa.st = md->st;
+    sa.flag_slot = flag;
+    sa.norm_partials = md->norm_partials;
+    sa.norm2_out = md->norm2 + b;
+    sa.done = md->done;
+    const uint64_t nv = (sa.k1 - sa.k0 + 3) / 4;
+    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(num_sms() * 8, (nv + 255) / 256)));
+    if (sa.k1 > sa.k0) {
+      SAMO_TRY(launch_adam_shard(sa, grid, C));
+    } else {
+      SAMO_CUDA_TRY(cudaMemsetAsync(md->norm2 + b, 0, sizeof(double), C));
+    }
+    uint16_t* cb = md->c16 + b * p.C;
+    rr = ncclAllGather(cb + r * p.c, cb, p.c, ncclFloat16, md->comm->comm, C);
+    if (rr != ncclSuccess) return nccl_fail(rr, "ncclAllGather");
+    SAMO_CUDA_TRY(cudaEventRecord(ev_ag[b], C));
+  }
+  SAMO_CUDA_TRY(cudaStreamWaitEvent(F, ev_ag[B - 1], 0));
+  rr = ncclAllReduce(md->norm2, md->norm2, B, ncclFloat64, ncclSum, md->comm->flag, F);
   if (rr != ncclSuccess) return nccl_fail(rr, "ncclAllReduce(norm)");
-  SAMO_TRY(phase_mark(md, 6, S));
-  StepArgs a = step_args(md);
-  a.g = md->c16;
-  SAMO_TRY(launch_expand_c16(a, std::min<int>(md->grid_update16, md->ntiles), S));
-  SAMO_TRY(phase_mark(md, 7, S));
-  SAMO_TRY(launch_step_finalize(md->st, md->norm2, flag, md->cfg.beta1, md->cfg.beta2, S));
-  SAMO_TRY(phase_mark(md, 8, S));
-  md->phase_count = 8;
+  SAMO_CUDA_TRY(cudaEventRecord(md->ev_flag, F));
+  for (int b = 0; b < B; ++b) {
+    SAMO_CUDA_TRY(cudaStreamWaitEvent(S, ev_ag[b], 0));
+    if (b == 0) SAMO_TRY(phase_mark(md, 2, S));
+    StepArgs a = base;
+    a.g = md->c16;
+    a.tiles = md->tiles + p.ex_t[b];
+    a.ntiles = p.ex_t[b + 1] - p.ex_t[b];
+    if (a.ntiles) SAMO_TRY(launch_expand_c16(a, std::min<int>(md->grid_expand, a.ntiles), S));
+  }
+  SAMO_TRY(phase_mark(md, 3, S));
+  SAMO_CUDA_TRY(cudaStreamWaitEvent(S, md->ev_flag, 0));
+  SAMO_TRY(launch_step_finalize(md->st, md->norm2, B, flag, md->cfg.beta1, md->cfg.beta2, S));
+  SAMO_TRY(phase_mark(md, 4, S));
+  md->phase_count = 4;
   return SAMO_OK;
 }
 
@@ -1055,16 +1145,21 @@ int samo_model_exchange_mode(const samo_model* md) {
   return md ? (comm_size(md) > 1 ? exchange_mode(md) : SAMO_EXCHANGE_NONE) : -1;
 }
 
-int samo_model_shard_range(const samo_model* md, uint64_t* k0, uint64_t* k1) {
-  if (!md || !k0 || !k1) return fail(SAMO_E_PARAMETER, "null argument");
+int samo_model_shard_layout(samo_model* md, uint64_t* chunk, uint64_t* stride, int* buckets,
+                            int* rank) {
+  if (!md || !chunk || !stride || !buckets || !rank) return fail(SAMO_E_PARAMETER, "null argument");
   if (comm_size(md) <= 1 || exchange_mode(md) != SAMO_EXCHANGE_SHARDED) {
-    *k0 = 0;
-    *k1 = md->n_tot;
+    *chunk = *stride = md->n_tot;
+    *buckets = 1;
+    *rank = 0;
     return clear_ok();
   }
-  const uint64_t cnt = shard_count(md);
-  *k0 = std::min<uint64_t>(md->comm->rank * cnt, md->n_tot);
-  *k1 = std::min<uint64_t>((md->comm->rank + 1) * cnt, md->n_tot);
+  if (!md->finalized) return fail(SAMO_E_STATE, "model not finalized");
+  SAMO_TRY(plan_shards(md, md->shard_plan));
+  *chunk = md->shard_plan.c;
+  *stride = md->shard_plan.C;
+  *buckets = md->shard_plan.B;
+  *rank = md->comm->rank;
   return clear_ok();
 }
 

@@ -76,10 +76,11 @@ struct ShardArgs {
   uint32_t* done;
 };
 int launch_adam_shard(const ShardArgs& a, int grid, cudaStream_t s);
-int launch_step_finalize(SamoStepState* st, const double* norm2, float* flag, float beta1,
-                         float beta2, cudaStream_t s);
+int launch_step_finalize(SamoStepState* st, const double* norm2, int nslots, float* flag,
+                         float beta1, float beta2, cudaStream_t s);
 // Expand-only tile pass: a.g holds theta16c.
 int launch_expand_c16(const StepArgs& a, int grid, cudaStream_t s);
+int expand_grid(uint32_t tile_elems);
 int launch_build_off16(const SamoTile* tiles, uint32_t ntiles, const uint32_t* idx,
                        uint16_t* off16, cudaStream_t s);
 

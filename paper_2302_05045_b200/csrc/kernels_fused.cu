@@ -172,9 +172,11 @@ __device__ __forceinline__ TileRegs load_tile(const SamoTile* p) {
   return r;
 }
 
-template <bool G16, int CH>
+template <bool G16, int CH, bool EXPAND = false>
 struct K23Layout {
-  static constexpr uint32_t kF32 = (CH + 8) * 4;                 // theta/m/v/g32 slot
+  // expand-only stages carry just the 16-bit values and off16 (compact, so
+  // NCCL kernels still fit on the SMs while the expand runs)
+  static constexpr uint32_t kF32 = EXPAND ? 0u : (CH + 8) * 4;    // theta/m/v/g32 slot
   static constexpr uint32_t kG = G16 ? (CH + 16) * 2 : kF32;    // grad slot
   static constexpr uint32_t kOff = (CH + 16) * 2;               // off16 slot
   static constexpr uint32_t kStage = 3 * kF32 + kG + kOff;
@@ -186,7 +188,7 @@ struct K23Layout {
 template <bool G16, int CH, int NS, bool EXPAND = false>
 __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
   static_assert(!EXPAND || G16, "expand-only reads 16-bit values");
-  using L = K23Layout<G16, CH>;
+  using L = K23Layout<G16, CH, EXPAND>;
   constexpr uint32_t kConsumerWarps = kThreads / 32;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[NS];
@@ -529,10 +531,12 @@ __global__ void __launch_bounds__(kThreads) k_adam_shard(ShardArgs a) {
 
 // One thread: the step's scalars once the global grad norm^2 and skip flag
 // are known (AdamScalars::advance, train.hpp:325-329; skip, 632-639).
-__global__ void k_step_finalize(SamoStepState* st, const double* norm2, float* flag, float beta1,
-                                float beta2) {
+__global__ void k_step_finalize(SamoStepState* st, const double* norm2, int nslots, float* flag,
+                                float beta1, float beta2) {
   const bool skip = *flag != 0.0f;
-  st->grad_norm = static_cast<float>(sqrt(*norm2));
+  double acc = 0.0;
+  for (int i = 0; i < nslots; ++i) acc += norm2[i];  // fixed order: deterministic
+  st->grad_norm = static_cast<float>(sqrt(acc));
   if (skip) {
     st->skipped_steps += 1;
     st->last_skipped = 1u;
@@ -590,9 +594,9 @@ static int k23_variant() {
                                                                                            : kK23Default;
 }
 
-template <bool G16, int CH, int NS>
+template <bool G16, int CH, int NS, bool EXPAND = false>
 static size_t k23_smem(uint32_t tile_elems) {
-  return NS * K23Layout<G16, CH>::kStage + tile_elems * 4u /* two dense out tiles */;
+  return NS * K23Layout<G16, CH, EXPAND>::kStage + tile_elems * 4u /* two dense out tiles */;
 }
 
 // Calls f(kernel, smem) for the selected variant.
@@ -660,23 +664,23 @@ int launch_adam_shard(const ShardArgs& a, int grid, cudaStream_t s) {
   return SAMO_OK;
 }
 
-int launch_step_finalize(SamoStepState* st, const double* norm2, float* flag, float beta1,
-                         float beta2, cudaStream_t s) {
-  k_step_finalize<<<1, 1, 0, s>>>(st, norm2, flag, beta1, beta2);
+int launch_step_finalize(SamoStepState* st, const double* norm2, int nslots, float* flag,
+                         float beta1, float beta2, cudaStream_t s) {
+  k_step_finalize<<<1, 1, 0, s>>>(st, norm2, nslots, flag, beta1, beta2);
   SAMO_LAUNCH_CHECK("k_step_finalize");
   return SAMO_OK;
 }
 
+int expand_grid(uint32_t tile_elems) {
+  return grid_for(k23_update<true, 1024, 3, true>, k23_smem<true, 1024, 3, true>(tile_elems),
+                  kThreads + 32);
+}
+
 int launch_expand_c16(const StepArgs& a, int grid, cudaStream_t s) {
   if (a.ntiles == 0) return SAMO_OK;
-  const size_t sm = k23_smem<true, 1024, 3>(a.tile_elems) <= 113u * 1024u
-                        ? k23_smem<true, 1024, 3>(a.tile_elems)
-                        : k23_smem<true, 1024, 2>(a.tile_elems);
-  if (sm == k23_smem<true, 1024, 3>(a.tile_elems))
-    return launch_persistent(k23_update<true, 1024, 3, true>, a, sm, grid, s, kThreads + 32,
-                             "k23_expand");
-  return launch_persistent(k23_update<true, 1024, 2, true>, a, sm, grid, s, kThreads + 32,
-                           "k23_expand");
+  if (grid <= 0) grid = expand_grid(a.tile_elems);
+  return launch_persistent(k23_update<true, 1024, 3, true>, a, k23_smem<true, 1024, 3, true>(a.tile_elems),
+                           grid, s, kThreads + 32, "k23_expand");
 }
 
 int launch_build_off16(const SamoTile* tiles, uint32_t ntiles, const uint32_t* idx,

@@ -331,11 +331,20 @@ class SamoModel:
     def exchange_mode(self) -> int:
         return int(_abi.load().samo_model_exchange_mode(self._h))
 
-    def shard_range(self) -> tuple[int, int]:
-        """Compressed-arena range [k0, k1) this rank updates."""
-        k0, k1 = C.c_uint64(), C.c_uint64()
-        _abi.call("samo_model_shard_range", self._h, C.byref(k0), C.byref(k1))
-        return k0.value, k1.value
+    def shard_ranges(self) -> list[tuple[int, int]]:
+        """Compressed-arena ranges [k0, k1) this rank updates (all of them
+        unless the exchange is sharded)."""
+        c, st, nb, rk = C.c_uint64(), C.c_uint64(), C.c_int(), C.c_int()
+        _abi.call("samo_model_shard_layout", self._h, C.byref(c), C.byref(st), C.byref(nb),
+                  C.byref(rk))
+        n = self.totals()[1]
+        out = []
+        for b in range(nb.value):
+            k0 = min(b * st.value + rk.value * c.value, n)
+            k1 = min(b * st.value + (rk.value + 1) * c.value, n)
+            if k1 > k0:
+                out.append((k0, k1))
+        return out
 
     # -- step ----------------------------------------------------------------
     def set_grads(self, grads: Sequence[torch.Tensor]) -> None:

@@ -65,9 +65,9 @@ def main() -> None:
         model.step(graph=os.environ.get("SAMO_DP_GRAPH") == "1")
     torch.cuda.synchronize()
     rec = model.step_record()
-    k0, k1 = model.shard_range()
+    ranges = np.array(model.shard_ranges(), np.uint64).reshape(-1, 2)
     out = {"t": np.array([rec.t]), "skipped": np.array([rec.skipped_steps]),
-           "norm": np.array([rec.grad_norm], np.float32), "shard": np.array([k0, k1], np.uint64),
+           "norm": np.array([rec.grad_norm], np.float32), "shard": ranges,
            "k_off": np.array([model.view(l).k_offset for l in range(len(DENSE_LEN))], np.uint64)}
     for l in range(len(DENSE_LEN)):
         for k in ("theta32", "adam_m", "adam_v"):

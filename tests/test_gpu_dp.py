@@ -79,18 +79,19 @@ def test_dp_two_gpus_bit_exact(tmp_path, oracle, mode):
     covered = 0
     for rr in r:
         assert int(rr["t"][0]) == t and int(rr["skipped"][0]) == skipped == 1
-        k0, k1 = (int(x) for x in rr["shard"])
         for l in range(len(theta)):
             # theta16 is complete on every rank; theta32/m/v are authoritative
             # in the rank's shard (everything unless the exchange is sharded)
             assert np.array_equal(rr[f"theta16_{l}"], t16[l]), l
-            off = int(rr["k_off"][l])
-            lo, hi = max(k0 - off, 0), min(k1 - off, len(theta[l]))
-            if hi <= lo:
-                continue
-            covered += hi - lo
-            for name, want in (("theta32", theta), ("adam_m", m), ("adam_v", v)):
-                got = rr[f"{name}{l}"][lo:hi].view(np.uint32)
-                assert np.array_equal(got, want[l][lo:hi].view(np.uint32)), (name, l)
+        for k0, k1 in (tuple(int(x) for x in row) for row in rr["shard"]):
+            for l in range(len(theta)):
+                off = int(rr["k_off"][l])
+                lo, hi = max(k0 - off, 0), min(k1 - off, len(theta[l]))
+                if hi <= lo:
+                    continue
+                covered += hi - lo
+                for name, want in (("theta32", theta), ("adam_m", m), ("adam_v", v)):
+                    got = rr[f"{name}{l}"][lo:hi].view(np.uint32)
+                    assert np.array_equal(got, want[l][lo:hi].view(np.uint32)), (name, l)
     n = sum(len(x) for x in theta)
     assert covered == (n if mode.startswith("sharded") else 2 * n)
