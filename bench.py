@@ -358,16 +358,20 @@ def run_samo(args) -> None:
         # Phase breakdown of the production step (events inside the driver;
         # sharded exchange only) — not the headline.
         phases = None
-        if model.exchange_mode() == model.EXCHANGE_SHARDED:
+        if model.exchange_mode() in (model.EXCHANGE_SHARDED, model.EXCHANGE_P2P):
             _abi.call("samo_model_enable_phase_timing", model.handle, 1)
             for _ in range(3):
                 model.step()
             buf = (C.c_float * 16)()
             cnt = _abi.load().samo_model_phase_times(model.handle, buf, 16)
             _abi.call("samo_model_enable_phase_timing", model.handle, 0)
-            names = ["K1_gather (reduce-scatter overlapped)",
-                     "skip flag + shard Adam + first all-gather bucket",
-                     "expand (all-gather overlapped)", "norm allreduce + finalize"]
+            names = (["K1_gather", "skip-flag allreduce (barrier)",
+                      "shard update: fused NVLink exchange + Adam", "norm allreduce (barrier)",
+                      "expand", "finalize"]
+                     if model.exchange_mode() == model.EXCHANGE_P2P else
+                     ["K1_gather (reduce-scatter overlapped)",
+                      "skip flag + shard Adam + first all-gather bucket",
+                      "expand (all-gather overlapped)", "norm allreduce + finalize"])
             phases = {names[i]: round(buf[i], 4) for i in range(max(0, cnt))}
         # Stage breakdown (not the headline): the same three stages run back
         # to back, the exchange as one allreduce of the whole arena.
@@ -519,8 +523,13 @@ def run_samo(args) -> None:
                        "gpu": gpu_name},
             "gpu_launches": int(launches),
             "step_mode": "K1 | K23 (no exchange)" if world == 1 else
-                         ("sharded (ZeRO-1), k-bucketed: K1 || NCCL reduce-scatter, shard Adam, "
-                          "NCCL all-gather of binary16 weights || expand" if model.exchange_mode() == model.EXCHANGE_SHARDED
+                         ("p2p (ZeRO-1, exchange fused over NVLink): K1 | shard kernel loads every "
+                          "rank's binary16 grads, rank-ordered fp32 sum, Adam, stores binary16 "
+                          "weights to every rank | expand"
+                          if model.exchange_mode() == model.EXCHANGE_P2P else
+                          "sharded (ZeRO-1), k-bucketed: K1 || NCCL reduce-scatter, shard Adam, "
+                          "NCCL all-gather of binary16 weights || expand"
+                          if model.exchange_mode() == model.EXCHANGE_SHARDED
                           else "allreduce: bucketed NCCL allreduce overlapped with K1/K23"),
             "phases_ms": phases,
             "roofline": roofline,

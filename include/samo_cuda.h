@@ -242,12 +242,21 @@ int samo_model_attach_comm(samo_model* model, samo_comm* comm);
  *    authoritative only on the rank's shard (samo_model_shard_layout);
  *    theta16 everywhere.  The exchange is pipelined over k-buckets
  *    (SAMO_SHARD_BUCKETS, default 4) behind the gather and expand kernels.
- * The default is SHARDED (environment SAMO_EXCHANGE=allreduce overrides);
- * mode -1 restores the default. */
+ *  SAMO_EXCHANGE_P2P — the sharded update with the exchange fused into it:
+ *    every rank's shard kernel loads its shard of all ranks' binary16
+ *    gradients over NVLink (CUDA IPC peer mappings made by
+ *    samo_model_attach_comm, which is then collective), sums them in rank
+ *    order in fp32 (deterministic, bit-exact with a rank-ordered sum for any
+ *    G), runs Adam and stores the binary16 weights into every rank.  NCCL
+ *    only carries two 4/8-byte allreduces that double as barriers.
+ * The default is P2P when the peer mappings succeeded on every rank, else
+ * SHARDED (environment SAMO_EXCHANGE=allreduce|sharded overrides); mode -1
+ * restores the default. */
 enum samo_exchange_mode {
   SAMO_EXCHANGE_NONE = 0,
   SAMO_EXCHANGE_ALLREDUCE = 1,
-  SAMO_EXCHANGE_SHARDED = 2
+  SAMO_EXCHANGE_SHARDED = 2,
+  SAMO_EXCHANGE_P2P = 3
 };
 int samo_model_set_exchange(samo_model* model, int mode);
 /* SAMO_EXCHANGE_NONE without a communicator of size > 1. */

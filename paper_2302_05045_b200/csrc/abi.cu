@@ -483,6 +483,10 @@ struct samo_model {
   cudaEvent_t ev_fork = nullptr, ev_flag = nullptr;
   int reserve_sms = 16;                 // SMs left to NCCL while our kernels run
   ShardPlan shard_plan;
+  // Peer mappings of the other ranks' model blocks (CUDA IPC) for the fused
+  // peer-to-peer exchange; p2p_ok is agreed by every rank.
+  void* peer_base[kMaxP2PRanks] = {};
+  bool p2p_ok = false;
   std::vector<cudaEvent_t> ev_sh;       // sharded pipeline: K1 and all-gather events
   int grid_expand = 0;
   // Phase timing of the data-parallel step.
@@ -506,6 +510,87 @@ static int phase_mark(samo_model* md, int i, cudaStream_t s) {
 }
 
 static uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+static void close_peers(samo_model* md) {
+  for (int q = 0; q < kMaxP2PRanks; ++q) {
+    if (md->peer_base[q] && md->peer_base[q] != md->block) cudaIpcCloseMemHandle(md->peer_base[q]);
+    md->peer_base[q] = nullptr;
+  }
+  md->p2p_ok = false;
+}
+
+// Collective over the attached communicator: exchanges the CUDA IPC handles
+// of every rank's model block (all ranks have the same arena layout) and maps
+// the peers.  Every rank ends with the same p2p_ok (min over ranks).
+static int open_peers(samo_model* md) {
+  samo_comm* c = md->comm;
+  const int G = c->nranks, r = c->rank;
+  if (G > kMaxP2PRanks) return SAMO_OK;
+  int ok = 1;
+  cudaIpcMemHandle_t mine{};
+  if (cudaIpcGetMemHandle(&mine, md->block) != cudaSuccess) {
+    cudaGetLastError();
+    ok = 0;
+  }
+  cudaStream_t s = nullptr;
+  SAMO_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  uint8_t* d = nullptr;
+  SAMO_CUDA_TRY(cudaMalloc(&d, G * sizeof(cudaIpcMemHandle_t) + 16));
+  int* dok = reinterpret_cast<int*>(d + G * sizeof(cudaIpcMemHandle_t));
+  std::vector<cudaIpcMemHandle_t> all(G);
+  int rc = SAMO_OK;
+  do {
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(d + r * sizeof(cudaIpcMemHandle_t), &mine, sizeof(mine), cudaMemcpyHostToDevice, s))) {
+      rc = cuda_fail(e, "ipc handle upload");
+      break;
+    }
+    ncclResult_t nr = ncclAllGather(d + r * sizeof(cudaIpcMemHandle_t), d, sizeof(cudaIpcMemHandle_t), ncclUint8,
+                                    c->comm, s);
+    if (nr != ncclSuccess) {
+      rc = nccl_fail(nr, "ncclAllGather(ipc handles)");
+      break;
+    }
+    if ((e = cudaMemcpyAsync(all.data(), d, G * sizeof(cudaIpcMemHandle_t), cudaMemcpyDeviceToHost, s)) ||
+        (e = cudaStreamSynchronize(s))) {
+      rc = cuda_fail(e, "ipc handle download");
+      break;
+    }
+    for (int q = 0; q < G && ok; ++q) {
+      if (q == r) {
+        md->peer_base[q] = md->block;
+        continue;
+      }
+      if (cudaIpcOpenMemHandle(&md->peer_base[q], all[q], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        md->peer_base[q] = nullptr;
+        ok = 0;
+      }
+    }
+    // every rank must take the same path
+    if ((e = cudaMemcpyAsync(dok, &ok, sizeof(int), cudaMemcpyHostToDevice, s))) {
+      rc = cuda_fail(e, "ok upload");
+      break;
+    }
+    nr = ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, c->comm, s);
+    if (nr != ncclSuccess) {
+      rc = nccl_fail(nr, "ncclAllReduce(p2p ok)");
+      break;
+    }
+    if ((e = cudaMemcpyAsync(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost, s)) || (e = cudaStreamSynchronize(s))) {
+      rc = cuda_fail(e, "ok download");
+      break;
+    }
+  } while (false);
+  cudaFree(d);
+  cudaStreamDestroy(s);
+  if (rc != SAMO_OK || !ok) {
+    close_peers(md);
+    return rc;
+  }
+  md->p2p_ok = true;
+  return SAMO_OK;
+}
 
 extern "C" {
 
@@ -664,6 +749,7 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
 int samo_model_destroy(samo_model* md) {
   if (!md) return clear_ok();
   if (md->graph) cudaGraphExecDestroy(md->graph);
+  close_peers(md);
   if (md->capture_stream) cudaStreamDestroy(md->capture_stream);
   if (md->s_comm) cudaStreamDestroy(md->s_comm);
   if (md->s_flag) cudaStreamDestroy(md->s_flag);
@@ -804,7 +890,9 @@ int samo_model_set_config(samo_model* md, const samo_optimizer_config* cfg) {
 
 int samo_model_attach_comm(samo_model* md, samo_comm* comm) {
   if (!md) return fail(SAMO_E_PARAMETER, "null model");
+  close_peers(md);
   md->comm = comm;
+  if (comm && comm->nranks > 1) SAMO_TRY(open_peers(md));
   return clear_ok();
 }
 
@@ -965,7 +1053,70 @@ static int exchange_mode(const samo_model* md) {
   if (md->exchange >= 0) return md->exchange;
   const char* e = getenv("SAMO_EXCHANGE");
   if (e && std::strcmp(e, "allreduce") == 0) return SAMO_EXCHANGE_ALLREDUCE;
-  return SAMO_EXCHANGE_SHARDED;
+  if (e && std::strcmp(e, "sharded") == 0) return SAMO_EXCHANGE_SHARDED;
+  return md->p2p_ok ? SAMO_EXCHANGE_P2P : SAMO_EXCHANGE_SHARDED;
+}
+
+// One data-parallel step with the fused peer-to-peer exchange (ZeRO-1 on the
+// compressed state, no NCCL on the data path):
+//   K1 (binary16 compressed grads, local)
+//   -> allreduce(skip flag)            [NCCL, 4 bytes: also the barrier]
+//   -> k_shard_p2p on the own shard    [peer loads of every rank's grad16,
+//                                       rank-ordered fp32 sum, Adam, peer
+//                                       stores of the binary16 weights]
+//   -> allreduce(norm^2)               [NCCL, 8 bytes: also the barrier]
+//   -> expand every tile from theta16c -> scalars.
+static int step_p2p(samo_model* md, cudaStream_t S) {
+  const int G = md->comm->nranks, r = md->comm->rank;
+  const uint64_t c = align_up((md->n_tot + G - 1) / G, 8);
+  if (static_cast<uint64_t>(G) * c + 8 > md->n_al + kFlagOff)
+    return fail(SAMO_E_PARAMETER, "too many ranks for the arena padding");
+  float* flag = flag_ptr(md);
+  SAMO_TRY(phase_mark(md, 0, S));
+  SAMO_TRY(launch_gather(step_args(md), false, md->grid_gather16, S));
+  SAMO_TRY(phase_mark(md, 1, S));
+  ncclResult_t rr = ncclAllReduce(flag, flag, 1, ncclFloat32, ncclSum, md->comm->flag, S);
+  if (rr != ncclSuccess) return nccl_fail(rr, "ncclAllReduce(flag)");
+  SAMO_TRY(phase_mark(md, 2, S));
+  P2PArgs pa{};
+  const char* base = static_cast<const char*>(md->block);
+  const size_t g_off = reinterpret_cast<const char*>(md->g) - base;
+  const size_t c_off = reinterpret_cast<const char*>(md->c16) - base;
+  for (int q = 0; q < G; ++q) {
+    pa.g16[q] = reinterpret_cast<const uint16_t*>(static_cast<const char*>(md->peer_base[q]) + g_off);
+    pa.c16[q] = reinterpret_cast<uint16_t*>(static_cast<char*>(md->peer_base[q]) + c_off);
+  }
+  pa.G = G;
+  pa.rank = r;
+  pa.theta = md->theta;
+  pa.m = md->m;
+  pa.v = md->v;
+  pa.k0 = std::min<uint64_t>(r * c, md->n_tot);
+  pa.k1 = std::min<uint64_t>((r + 1) * c, md->n_tot);
+  pa.scale = (1.0f / md->cfg.loss_scale) * (1.0f / static_cast<float>(G));
+  pa.prm = adam_params(&md->cfg);
+  pa.st = md->st;
+  pa.flag_slot = flag;
+  pa.norm_partials = md->norm_partials;
+  pa.norm2_out = md->norm2;
+  pa.done = md->done;
+  if (pa.k1 > pa.k0) {
+    SAMO_TRY(launch_shard_p2p(pa, S));
+  } else {
+    SAMO_CUDA_TRY(cudaMemsetAsync(md->norm2, 0, sizeof(double), S));
+  }
+  SAMO_TRY(phase_mark(md, 3, S));
+  rr = ncclAllReduce(md->norm2, md->norm2, 1, ncclFloat64, ncclSum, md->comm->flag, S);
+  if (rr != ncclSuccess) return nccl_fail(rr, "ncclAllReduce(norm)");
+  SAMO_TRY(phase_mark(md, 4, S));
+  StepArgs a = step_args(md);
+  a.g = md->c16;
+  SAMO_TRY(launch_expand_c16(a, std::min<int>(md->grid_expand, md->ntiles), S));
+  SAMO_TRY(phase_mark(md, 5, S));
+  SAMO_TRY(launch_step_finalize(md->st, md->norm2, 1, flag, md->cfg.beta1, md->cfg.beta2, S));
+  SAMO_TRY(phase_mark(md, 6, S));
+  md->phase_count = 6;
+  return SAMO_OK;
 }
 
 // Shard of the compressed arena owned by this rank in the sharded exchange:
@@ -1041,6 +1192,12 @@ static int step_sharded(samo_model* md, cudaStream_t S) {
   cudaStream_t C = md->s_comm, F = md->s_flag;
   float* flag = flag_ptr(md);
   const StepArgs base = step_args(md);
+  // Persistent grids leave SAMO_SHARD_NCCL_SMS SMs to the concurrent NCCL
+  // kernels (reduce-scatter behind K1, all-gather behind the expand).
+  const int sms = num_sms();
+  const int reserve = std::max(0, std::min(env_int("SAMO_SHARD_NCCL_SMS", 0), sms - 8));
+  const int gg = std::max(1, md->grid_gather32 / sms) * (sms - reserve);
+  const int ge = std::max(1, md->grid_expand / sms) * (sms - reserve);
 
   SAMO_TRY(phase_mark(md, 0, S));
   SAMO_CUDA_TRY(cudaEventRecord(md->ev_fork, S));
@@ -1050,7 +1207,7 @@ static int step_sharded(samo_model* md, cudaStream_t S) {
     StepArgs a = base;
     a.tiles = md->tiles + p.k1_t[b];
     a.ntiles = p.k1_t[b + 1] - p.k1_t[b];
-    if (a.ntiles) SAMO_TRY(launch_gather(a, true, std::min<int>(md->grid_gather32, a.ntiles), S));
+    if (a.ntiles) SAMO_TRY(launch_gather(a, true, std::min<int>(gg, a.ntiles), S));
     SAMO_CUDA_TRY(cudaEventRecord(ev_k1[b], S));
     SAMO_CUDA_TRY(cudaStreamWaitEvent(C, ev_k1[b], 0));
     float* gb = md->g + b * p.C;
@@ -1101,7 +1258,7 @@ static int step_sharded(samo_model* md, cudaStream_t S) {
     a.g = md->c16;
     a.tiles = md->tiles + p.ex_t[b];
     a.ntiles = p.ex_t[b + 1] - p.ex_t[b];
-    if (a.ntiles) SAMO_TRY(launch_expand_c16(a, std::min<int>(md->grid_expand, a.ntiles), S));
+    if (a.ntiles) SAMO_TRY(launch_expand_c16(a, std::min<int>(ge, a.ntiles), S));
   }
   SAMO_TRY(phase_mark(md, 3, S));
   SAMO_CUDA_TRY(cudaStreamWaitEvent(S, md->ev_flag, 0));
@@ -1115,7 +1272,8 @@ extern "C" {
 
 int samo_model_set_exchange(samo_model* md, int mode) {
   if (!md) return fail(SAMO_E_PARAMETER, "null model");
-  if (mode != -1 && mode != SAMO_EXCHANGE_ALLREDUCE && mode != SAMO_EXCHANGE_SHARDED)
+  if (mode != -1 && mode != SAMO_EXCHANGE_ALLREDUCE && mode != SAMO_EXCHANGE_SHARDED &&
+      mode != SAMO_EXCHANGE_P2P)
     return fail(SAMO_E_PARAMETER, "unknown exchange mode %d", mode);
   md->exchange = mode;
   if (md->graph) {
@@ -1148,10 +1306,18 @@ int samo_model_exchange_mode(const samo_model* md) {
 int samo_model_shard_layout(samo_model* md, uint64_t* chunk, uint64_t* stride, int* buckets,
                             int* rank) {
   if (!md || !chunk || !stride || !buckets || !rank) return fail(SAMO_E_PARAMETER, "null argument");
-  if (comm_size(md) <= 1 || exchange_mode(md) != SAMO_EXCHANGE_SHARDED) {
+  if (comm_size(md) <= 1 || exchange_mode(md) == SAMO_EXCHANGE_ALLREDUCE) {
     *chunk = *stride = md->n_tot;
     *buckets = 1;
     *rank = 0;
+    return clear_ok();
+  }
+  if (exchange_mode(md) == SAMO_EXCHANGE_P2P) {
+    const uint64_t G = comm_size(md);
+    *chunk = align_up((md->n_tot + G - 1) / G, 8);
+    *stride = *chunk * G;
+    *buckets = 1;
+    *rank = md->comm->rank;
     return clear_ok();
   }
   if (!md->finalized) return fail(SAMO_E_STATE, "model not finalized");
@@ -1195,6 +1361,11 @@ int samo_model_update(samo_model* md, samo_stream_t stream) {
 int samo_model_step(samo_model* md, samo_stream_t stream) {
   SAMO_TRY(step_ready(md));
   if (!md->grads_set) return fail(SAMO_E_STATE, "optimizer_step requires backward (no gradients set)");
+  if (comm_size(md) > 1 && exchange_mode(md) == SAMO_EXCHANGE_P2P) {
+    if (!md->p2p_ok) return fail(SAMO_E_STATE, "peer-to-peer exchange unavailable (IPC mapping failed)");
+    SAMO_TRY(step_p2p(md, as_stream(stream)));
+    return clear_ok();
+  }
   if (comm_size(md) > 1 && exchange_mode(md) == SAMO_EXCHANGE_SHARDED) {
     SAMO_TRY(step_sharded(md, as_stream(stream)));
     return clear_ok();

@@ -60,6 +60,30 @@ int launch_gather(const StepArgs& a, bool out_f32, int grid, cudaStream_t s);
 int launch_update(const StepArgs& a, bool g_f32, int grid, cudaStream_t s);
 // which: 0 = gather, 1 = update; wide = fp32 gradient arena.
 int step_grid(int which, bool wide, uint32_t tile_elems);
+// Fused peer-to-peer exchange + shard update (kernels_fused.cu, k_shard_p2p):
+// rank `rank` owns [k0, k1) of the compressed arena; it reads that range of
+// every rank's binary16 gradient over NVLink, sums in rank order, runs Adam
+// and writes the binary16 weights into every rank's theta16c arena.
+constexpr int kMaxP2PRanks = 8;
+struct P2PArgs {
+  const uint16_t* g16[kMaxP2PRanks];  // per-rank compressed binary16 gradients
+  uint16_t* c16[kMaxP2PRanks];        // per-rank theta16c arenas
+  int G;
+  int rank;
+  float* theta;
+  float* m;
+  float* v;
+  uint64_t k0, k1;                    // k0 a multiple of 8
+  float scale;                        // (1/loss_scale) * (1/G)
+  SamoAdamParams prm;
+  const SamoStepState* st;
+  const float* flag_slot;             // global skip indicator (already reduced)
+  float* norm_partials;
+  double* norm2_out;
+  uint32_t* done;
+};
+int launch_shard_p2p(const P2PArgs& a, cudaStream_t s);
+
 // Sharded data-parallel step pieces.
 struct ShardArgs {
   const float* g;              // reduce-scattered gradient (this rank's shard in place)

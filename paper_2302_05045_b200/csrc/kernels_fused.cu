@@ -529,6 +529,134 @@ __global__ void __launch_bounds__(kThreads) k_adam_shard(ShardArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused peer-to-peer exchange + shard update.  Every rank's K1 has written
+// its compressed binary16 gradient (raw grad16) into its own arena; the
+// skip-flag allreduce before this kernel is the cross-rank barrier.  For the
+// owned range, each thread loads 8 consecutive halves from every rank over
+// NVLink (16-byte peer loads), sums fl32(h * scale) in rank order — the
+// oracle's rank-ascending fp32 sum, so the result is bit-exact for any G —
+// runs Adam on its own fp32 state and stores the 8 new binary16 weights into
+// every rank's theta16c (16-byte peer stores).  Link bytes per rank:
+// 2n(G-1)/G in (gradients) + 2n(G-1)/G out (weights).
+
+__device__ __forceinline__ uint4 ld_peer_v4(const uint16_t* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ uint16_t half_lane(const uint4& v, int e) {
+  const uint32_t w = e < 2 ? v.x : e < 4 ? v.y : e < 6 ? v.z : v.w;
+  return static_cast<uint16_t>((e & 1) ? (w >> 16) : (w & 0xFFFFu));
+}
+
+template <int G>
+__global__ void __launch_bounds__(kThreads) k_shard_p2p(P2PArgs a) {
+  __shared__ float red[kThreads / 32];
+  __shared__ int last_cta;
+  const bool skip = *reinterpret_cast<const volatile float*>(a.flag_slot) != 0.0f;
+  const float b1p = __fmul_rn(a.st->beta1_pow, a.prm.beta1);
+  const float b2p = __fmul_rn(a.st->beta2_pow, a.prm.beta2);
+  const float bias1 = __fsub_rn(1.0f, b1p), bias2 = __fsub_rn(1.0f, b2p);
+  const float omb1 = __fsub_rn(1.0f, a.prm.beta1), omb2 = __fsub_rn(1.0f, a.prm.beta2);
+  const float lrwd = __fmul_rn(a.prm.lr, a.prm.wd);
+  const SamoAdamParams prm = a.prm;
+  const float scale = pin_f32(a.scale);
+  float nacc = 0.0f;
+  const uint64_t n = a.k1 - a.k0;
+  const uint64_t nv = (n + 7) / 8;  // 8-element vectors (the last one may be partial)
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kThreads;
+  for (uint64_t q = blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x; q < nv; q += stride) {
+    const uint64_t k = a.k0 + 8 * q;
+    const uint64_t left = a.k1 - k;
+    const int cnt = left < 8 ? static_cast<int>(left) : 8;
+    uint4 h[G];
+#pragma unroll
+    for (int r = 0; r < G; ++r) h[r] = ld_peer_v4(a.g16[r] + k);  // arenas are padded
+    float th[8], mm[8], vv[8];
+    if (cnt == 8) {
+      const float4 t0 = *reinterpret_cast<const float4*>(a.theta + k);
+      const float4 t1 = *reinterpret_cast<const float4*>(a.theta + k + 4);
+      const float4 m0 = *reinterpret_cast<const float4*>(a.m + k);
+      const float4 m1 = *reinterpret_cast<const float4*>(a.m + k + 4);
+      const float4 v0 = *reinterpret_cast<const float4*>(a.v + k);
+      const float4 v1 = *reinterpret_cast<const float4*>(a.v + k + 4);
+      th[0] = t0.x; th[1] = t0.y; th[2] = t0.z; th[3] = t0.w;
+      th[4] = t1.x; th[5] = t1.y; th[6] = t1.z; th[7] = t1.w;
+      mm[0] = m0.x; mm[1] = m0.y; mm[2] = m0.z; mm[3] = m0.w;
+      mm[4] = m1.x; mm[5] = m1.y; mm[6] = m1.z; mm[7] = m1.w;
+      vv[0] = v0.x; vv[1] = v0.y; vv[2] = v0.z; vv[3] = v0.w;
+      vv[4] = v1.x; vv[5] = v1.y; vv[6] = v1.z; vv[7] = v1.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        th[e] = e < cnt ? a.theta[k + e] : 0.0f;
+        mm[e] = e < cnt ? a.m[k + e] : 0.0f;
+        vv[e] = e < cnt ? a.v[k + e] : 0.0f;
+      }
+    }
+    uint32_t packed[4];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      float g = 0.0f;  // rank-ascending fp32 sum, as the oracle's dp_sum
+#pragma unroll
+      for (int r = 0; r < G; ++r) g = __fadd_rn(g, mul_x86(f16_bits_to_f32(half_lane(h[r], e)), scale));
+      if (e < cnt) nacc = __fadd_rn(nacc, __fmul_rn(g, g));
+      float t = th[e];
+      if (!skip && e < cnt) t = adam_one(g, mm[e], vv[e], t, prm, omb1, omb2, bias1, bias2, lrwd);
+      th[e] = t;
+      const uint32_t hb = f32_to_f16_bits(t);
+      packed[e >> 1] = (e & 1) ? (packed[e >> 1] | (hb << 16)) : hb;
+    }
+    if (!skip) {
+      if (cnt == 8) {
+        *reinterpret_cast<float4*>(a.theta + k) = make_float4(th[0], th[1], th[2], th[3]);
+        *reinterpret_cast<float4*>(a.theta + k + 4) = make_float4(th[4], th[5], th[6], th[7]);
+        *reinterpret_cast<float4*>(a.m + k) = make_float4(mm[0], mm[1], mm[2], mm[3]);
+        *reinterpret_cast<float4*>(a.m + k + 4) = make_float4(mm[4], mm[5], mm[6], mm[7]);
+        *reinterpret_cast<float4*>(a.v + k) = make_float4(vv[0], vv[1], vv[2], vv[3]);
+        *reinterpret_cast<float4*>(a.v + k + 4) = make_float4(vv[4], vv[5], vv[6], vv[7]);
+      } else {
+        for (int e = 0; e < cnt; ++e) {
+          a.theta[k + e] = th[e];
+          a.m[k + e] = mm[e];
+          a.v[k + e] = vv[e];
+        }
+      }
+    }
+    const uint4 pv = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+#pragma unroll
+    for (int r = 0; r < G; ++r) *reinterpret_cast<uint4*>(a.c16[r] + k) = pv;  // arenas are padded
+  }
+  // Make the peer stores visible system-wide before the kernel retires.
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  float x = nacc;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = __fadd_rn(x, __shfl_xor_sync(0xFFFFFFFFu, x, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int w = 0; w < kThreads / 32; ++w) s = __fadd_rn(s, red[w]);
+    a.norm_partials[blockIdx.x] = s;
+    __threadfence();
+    last_cta = atomicAdd(a.done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last_cta && threadIdx.x == 0) {
+    __threadfence();
+    double acc = 0.0;
+    const volatile float* np = a.norm_partials;
+    for (uint32_t b = 0; b < gridDim.x; ++b) acc += static_cast<double>(np[b]);
+    *a.norm2_out = acc;
+    *a.done = 0u;
+    __threadfence();
+  }
+}
+
 // One thread: the step's scalars once the global grad norm^2 and skip flag
 // are known (AdamScalars::advance, train.hpp:325-329; skip, 632-639).
 __global__ void k_step_finalize(SamoStepState* st, const double* norm2, int nslots, float* flag,
@@ -655,6 +783,24 @@ int launch_update(const StepArgs& a, bool g_f32, int grid, cudaStream_t s) {
     return launch_persistent(fn, a, sm, grid, s, kThreads + 32, "k23_update");
   };
   return g_f32 ? with_k23<false>(a.tile_elems, go) : with_k23<true>(a.tile_elems, go);
+}
+
+int launch_shard_p2p(const P2PArgs& a, cudaStream_t s) {
+  const uint64_t nv = (a.k1 > a.k0) ? (a.k1 - a.k0 + 7) / 8 : 0;
+  const int grid = static_cast<int>(
+      std::max<uint64_t>(1, std::min<uint64_t>(static_cast<uint64_t>(num_sms()) * 8, (nv + kThreads - 1) / kThreads)));
+  switch (a.G) {
+    case 2: k_shard_p2p<2><<<grid, kThreads, 0, s>>>(a); break;
+    case 3: k_shard_p2p<3><<<grid, kThreads, 0, s>>>(a); break;
+    case 4: k_shard_p2p<4><<<grid, kThreads, 0, s>>>(a); break;
+    case 5: k_shard_p2p<5><<<grid, kThreads, 0, s>>>(a); break;
+    case 6: k_shard_p2p<6><<<grid, kThreads, 0, s>>>(a); break;
+    case 7: k_shard_p2p<7><<<grid, kThreads, 0, s>>>(a); break;
+    case 8: k_shard_p2p<8><<<grid, kThreads, 0, s>>>(a); break;
+    default: return fail(SAMO_E_PARAMETER, "peer-to-peer exchange supports 2..8 ranks");
+  }
+  SAMO_LAUNCH_CHECK("k_shard_p2p");
+  return SAMO_OK;
 }
 
 int launch_adam_shard(const ShardArgs& a, int grid, cudaStream_t s) {

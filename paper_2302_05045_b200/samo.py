@@ -321,11 +321,13 @@ class SamoModel:
     def attach_comm(self, comm: Communicator | None) -> None:
         _abi.call("samo_model_attach_comm", self._h, comm.handle if comm else C.c_void_p())
 
-    EXCHANGE_NONE, EXCHANGE_ALLREDUCE, EXCHANGE_SHARDED = 0, 1, 2
+    EXCHANGE_NONE, EXCHANGE_ALLREDUCE, EXCHANGE_SHARDED, EXCHANGE_P2P = 0, 1, 2, 3
 
     def set_exchange(self, mode: int) -> None:
-        """EXCHANGE_ALLREDUCE (replicated state) or EXCHANGE_SHARDED (ZeRO-1 on
-        the compressed state); -1 restores the default."""
+        """EXCHANGE_ALLREDUCE (replicated state), EXCHANGE_SHARDED (ZeRO-1 on
+        the compressed state, NCCL reduce-scatter / all-gather) or EXCHANGE_P2P
+        (ZeRO-1 with the exchange fused into the shard kernel over NVLink peer
+        memory); -1 restores the default."""
         _abi.call("samo_model_set_exchange", self._h, int(mode))
 
     def exchange_mode(self) -> int:

@@ -58,7 +58,8 @@ def main() -> None:
     comm = sdist.make_communicator()
     model.attach_comm(comm)
     mode = os.environ.get("SAMO_DP_MODE", "sharded")
-    model.set_exchange(model.EXCHANGE_SHARDED if mode == "sharded" else model.EXCHANGE_ALLREDUCE)
+    model.set_exchange({"sharded": model.EXCHANGE_SHARDED, "p2p": model.EXCHANGE_P2P,
+                        "allreduce": model.EXCHANGE_ALLREDUCE}[mode])
     for s in range(STEPS):
         g = [torch.from_numpy(grads[(rank, s, l)].view(np.int16)).cuda() for l in range(len(DENSE_LEN))]
         model.set_grads(g)

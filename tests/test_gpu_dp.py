@@ -60,22 +60,22 @@ def _expected(oracle, world):
     return theta, m, v, t16, t, skipped
 
 
-@pytest.mark.parametrize("mode", ["sharded", "sharded-graph", "overlap", "staged", "graph"])
-def test_dp_two_gpus_bit_exact(tmp_path, oracle, mode):
-    if torch.cuda.device_count() < 2:
-        pytest.skip("needs 2 GPUs")
+def _run(tmp_path, mode, world):
     env = dict(os.environ)
-    env["SAMO_DP_MODE"] = "sharded" if mode.startswith("sharded") else "allreduce"
+    env["SAMO_DP_MODE"] = mode.split("-")[0] if mode.split("-")[0] in ("sharded", "p2p") else "allreduce"
     env["SAMO_OVERLAP"] = "0" if mode == "staged" else "1"
     env["SAMO_DP_GRAPH"] = "1" if mode.endswith("graph") else "0"
     env["SAMO_BUCKETS"] = "5"
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            str(HERE / "dp_worker.py"), str(tmp_path)]
     res = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
-    r = [dict(np.load(tmp_path / f"dp_rank{i}.npz")) for i in range(2)]
-    theta, m, v, t16, t, skipped = _expected(oracle, 2)
+    return [dict(np.load(tmp_path / f"dp_rank{i}.npz")) for i in range(world)]
+
+
+def _check(r, oracle, world, mode):
+    theta, m, v, t16, t, skipped = _expected(oracle, world)
     covered = 0
     for rr in r:
         assert int(rr["t"][0]) == t and int(rr["skipped"][0]) == skipped == 1
@@ -94,4 +94,19 @@ def test_dp_two_gpus_bit_exact(tmp_path, oracle, mode):
                     got = rr[f"{name}{l}"][lo:hi].view(np.uint32)
                     assert np.array_equal(got, want[l][lo:hi].view(np.uint32)), (name, l)
     n = sum(len(x) for x in theta)
-    assert covered == (n if mode.startswith("sharded") else 2 * n)
+    assert covered == (n if mode.split("-")[0] in ("sharded", "p2p") else world * n)
+
+
+@pytest.mark.parametrize("mode", ["p2p", "p2p-graph", "sharded", "sharded-graph", "overlap",
+                                  "staged", "graph"])
+def test_dp_two_gpus_bit_exact(tmp_path, oracle, mode):
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    _check(_run(tmp_path, mode, 2), oracle, 2, mode)
+
+
+def test_dp_four_gpus_p2p_bit_exact(tmp_path, oracle):
+    """The fused exchange sums in rank order: bit-exact for G = 4 too."""
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    _check(_run(tmp_path, "p2p", 4), oracle, 4, "p2p")
