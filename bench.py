@@ -6,11 +6,14 @@
     python bench.py --impl reference ...      (the reference's CPU implementation)
 
 One step = one pass of the SAMO per-step parameter-state path over one batch of
-synthetic dense gradients: K1 gather+unscale+cast -> (NCCL allreduce of the
-compressed fp32 gradient when N > 1) -> K23 Adam + downcast + expand.  Every
-rank holds the full replicated compressed state (data parallelism), so the
-per-GPU work is fixed as N grows ("scaling": "weak") and `value` is
-N * phi / t_step (dense parameters stepped per second, whole job).
+synthetic dense gradients.  N = 1: K1 gather (+unscale/cast) -> K23 Adam +
+downcast + expand.  N > 1 (data parallel, each rank its own gradient batch):
+the default exchange is fused over NVLink peer memory — K1 ->
+shard update (every rank's binary16 grads summed in rank order, Adam on the
+rank's 1/N shard, binary16 weights stored to every rank) -> expand; NCCL
+carries only two tiny allreduces that double as barriers.  The per-GPU
+workload (the full GPT set) is fixed as N grows ("scaling": "weak") and
+`value` is N * phi / t_step (dense parameters stepped per second, whole job).
 
 Rank 0 prints ONE JSON line.  All timing is CUDA events on the launching
 stream; multi-GPU times are the max over ranks.
@@ -397,35 +400,65 @@ def run_samo(args) -> None:
     value = world * phi / (ms_step * 1e-3)
 
     pk = peaks()
-    # Algorithmic bytes per launch: dense grad read 2phi + off16
-    # 2n + compressed grad write (fp32 4n when exchanged, binary16 2n
-    # otherwise); K23: grad read + off16 2n + theta/m/v read+write 24n + dense
-    # theta16 write 2phi.
-    gb = 4 if world > 1 else 2
-    bytes_k1 = 2 * phi + 2 * nnz + gb * nnz
-    bytes_k23 = 2 * phi + 2 * nnz + gb * nnz + 24 * nnz
+    p2p = world > 1 and model.exchange_mode() == model.EXCHANGE_P2P and phases
     k1_ms = statistics.mean(k1)
     k23_ms = statistics.mean(k23)
     ar_ms = statistics.mean(ar)
-    kern = {
-        "K1_gather_unscale": {"ms": k1_ms, "bytes": bytes_k1,
-                              "GBps": bytes_k1 / (k1_ms * 1e-3) / 1e9},
-        "K23_adam_downcast_expand": {"ms": k23_ms, "bytes": bytes_k23,
-                                     "GBps": bytes_k23 / (k23_ms * 1e-3) / 1e9},
-    }
+    if not p2p:
+        # Algorithmic bytes per launch: dense grad read 2phi +
+        # off16 2n + compressed grad write (fp32 4n when exchanged, binary16 2n
+        # otherwise); K23: grad read + off16 2n + theta/m/v read+write 24n +
+        # dense theta16 write 2phi.
+        gb = 4 if world > 1 else 2
+        bytes_k1 = 2 * phi + 2 * nnz + gb * nnz
+        bytes_k23 = 2 * phi + 2 * nnz + gb * nnz + 24 * nnz
+        kern = {
+            "K1_gather_unscale": {"ms": k1_ms, "bytes": bytes_k1,
+                                  "GBps": bytes_k1 / (k1_ms * 1e-3) / 1e9},
+            "K23_adam_downcast_expand": {"ms": k23_ms, "bytes": bytes_k23,
+                                         "GBps": bytes_k23 / (k23_ms * 1e-3) / 1e9},
+        }
+        hbm_kernels = list(kern)
+    else:
+        # Production data-parallel step (fused P2P exchange), per rank
+        # (DESIGN.md §7): K1 2phi + 2n off16 + 2n grad16; shard update: own
+        # theta/m/v r+w 24n/G + every rank reading this rank's grad16 (2n) +
+        # every owner storing binary16 weights here (2n); over NVLink per
+        # direction 2n(G-1)/G loads + 2n(G-1)/G stores; expand 2n theta16c +
+        # 2n off16 + 2phi.
+        G = world
+        ph = list(phases.values())
+        sh_ms, ex_ms = ph[2], ph[4]
+        k1_ms = ph[0]
+        b_k1 = 2 * phi + 4 * nnz
+        b_sh = 24 * nnz // G + 4 * nnz
+        b_nv = 4 * nnz * (G - 1) // G
+        b_ex = 2 * phi + 4 * nnz
+        kern = {
+            "K1_gather": {"ms": k1_ms, "bytes": b_k1, "GBps": b_k1 / (k1_ms * 1e-3) / 1e9},
+            "shard_update_p2p": {"ms": sh_ms, "bytes": b_sh, "GBps": b_sh / (sh_ms * 1e-3) / 1e9,
+                                 "nvlink_bytes_per_direction": b_nv,
+                                 "nvlink_GBps_per_direction": b_nv / (sh_ms * 1e-3) / 1e9,
+                                 "nvlink_frac_of_900": b_nv / (sh_ms * 1e-3) / 900e9},
+            "expand": {"ms": ex_ms, "bytes": b_ex, "GBps": b_ex / (ex_ms * 1e-3) / 1e9},
+        }
+        hbm_kernels = ["K1_gather", "expand"]
+        bytes_k1, bytes_k23 = b_k1, b_sh + b_ex
+        k23_ms = sh_ms + ex_ms
     for v in kern.values():
         v["frac"] = v["GBps"] / pk["hbm_gbs"]
     if world > 1:
         msg = 4 * (nnz + 1)
-        kern["allreduce"] = {"ms": ar_ms, "bytes": msg, "algbw_GBps": msg / (ar_ms * 1e-3) / 1e9,
-                             "note": "standalone (not overlapped) allreduce of the whole compressed "
-                                     "fp32 arena, from the stage-breakdown pass",
-                             "busbw_GBps": msg * 2 * (world - 1) / world / (ar_ms * 1e-3) / 1e9,
-                             "busbw_frac_of_900": msg * 2 * (world - 1) / world / (ar_ms * 1e-3) / 900e9}
-    dom = "K23_adam_downcast_expand" if k23_ms >= k1_ms else "K1_gather_unscale"
+        kern["nccl_allreduce_reference"] = {
+            "ms": ar_ms, "bytes": msg, "algbw_GBps": msg / (ar_ms * 1e-3) / 1e9,
+            "note": "standalone NCCL allreduce of the whole compressed fp32 arena (the "
+                    "replicated-exchange alternative), for context",
+            "busbw_GBps": msg * 2 * (world - 1) / world / (ar_ms * 1e-3) / 1e9,
+            "busbw_frac_of_900": msg * 2 * (world - 1) / world / (ar_ms * 1e-3) / 900e9}
+    dom = max(hbm_kernels, key=lambda k: kern[k]["ms"])
     traffic = None
     tp = ROOT / "profiles" / "traffic.json"
-    if tp.exists():
+    if tp.exists() and not p2p:
         try:
             traffic = json.loads(tp.read_text()).get(wl.name, {}).get(dom)
         except (ValueError, AttributeError):
