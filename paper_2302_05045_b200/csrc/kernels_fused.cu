@@ -50,6 +50,23 @@ __device__ __forceinline__ void st_na_f32(float* p, float v) {
 __device__ __forceinline__ void st_na_u16(uint16_t* p, uint16_t v) {
   asm volatile("st.global.L1::no_allocate.u16 [%0], %1;" ::"l"(p), "h"(v) : "memory");
 }
+__device__ __forceinline__ void st_na_v4f(float* p, float a, float b, float c, float d) {
+  asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b),
+               "f"(c), "f"(d)
+               : "memory");
+}
+__device__ __forceinline__ void st_na_v4u(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b),
+               "r"(c), "r"(d)
+               : "memory");
+}
+__device__ __forceinline__ uint4 ld_stream_v4(const uint16_t* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
 
 // ---------------------------------------------------------------------------
 // off16 construction (once, at finalize).
@@ -109,28 +126,57 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
     const uint16_t* sg = reinterpret_cast<const uint16_t*>(smem + static_cast<size_t>(s) * T * 2);
     mbar_wait(&full[s], (it / NS) & 1u);
 
-#pragma unroll 1
-    for (uint64_t kb = td.k_begin + tid; kb < td.k_end; kb += kU * kThreads) {
-      uint16_t off[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const uint64_t k = kb + static_cast<uint64_t>(u) * kThreads;
-        off[u] = k < td.k_end ? ld_stream_u16(a.off16 + k) : 0;
+    // Kept elements: 8-wide vectors on the 16-byte aligned middle of the
+    // tile's k range (one 16-byte off16 load and one 16/32-byte store per 8),
+    // scalar head and tail.
+    const uint64_t kb0 = td.k_begin, ke = td.k_end;
+    const uint64_t ka_up = (kb0 + 7) & ~7ull;
+    const uint64_t ka = ka_up < ke ? ka_up : ke;
+    const uint64_t ke8 = ka + ((ke - ka) & ~7ull);
+    auto gather_one = [&](uint64_t k) {
+      const uint16_t off = a.off16[k];
+      const uint16_t h = off < staged ? sg[off] : gsrc[off];
+      if constexpr (OUT_F32) {
+        const float gk = mul_x86(f16_bits_to_f32(h), a.inv_scale);
+        bad |= !finite_f32(gk);
+        st_na_f32(reinterpret_cast<float*>(a.g) + k, gk);
+      } else {
+        bad |= (h & 0x7C00u) == 0x7C00u;  // |h * 2^-s| is finite iff h is
+        st_na_u16(reinterpret_cast<uint16_t*>(a.g) + k, h);
       }
+    };
+    if (tid < ka - kb0) gather_one(kb0 + tid);
+    if (tid < ke - ke8) gather_one(ke8 + tid);
+    const uint32_t nv = static_cast<uint32_t>((ke8 - ka) >> 3);
+#pragma unroll 2
+    for (uint32_t q = tid; q < nv; q += kThreads) {
+      const uint64_t k = ka + 8ull * q;
+      const uint4 o = ld_stream_v4(a.off16 + k);
+      const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+      uint32_t hw[4];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const uint64_t k = kb + static_cast<uint64_t>(u) * kThreads;
-        if (k < td.k_end) {
-          const uint16_t h = off[u] < staged ? sg[off[u]] : gsrc[off[u]];
-          if constexpr (OUT_F32) {
-            const float gk = mul_x86(f16_bits_to_f32(h), a.inv_scale);
-            bad |= !finite_f32(gk);
-            st_na_f32(reinterpret_cast<float*>(a.g) + k, gk);
-          } else {
-            bad |= (h & 0x7C00u) == 0x7C00u;  // |h * 2^-s| is finite iff h is
-            st_na_u16(reinterpret_cast<uint16_t*>(a.g) + k, h);
-          }
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t o0 = ow[e] & 0xFFFFu, o1 = ow[e] >> 16;
+        const uint32_t h0 = o0 < staged ? sg[o0] : gsrc[o0];
+        const uint32_t h1 = o1 < staged ? sg[o1] : gsrc[o1];
+        hw[e] = h0 | (h1 << 16);
+      }
+      if constexpr (OUT_F32) {
+        float f[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const uint16_t h = static_cast<uint16_t>((e & 1) ? (hw[e >> 1] >> 16) : (hw[e >> 1] & 0xFFFFu));
+          f[e] = mul_x86(f16_bits_to_f32(h), a.inv_scale);
+          bad |= !finite_f32(f[e]);
         }
+        float* dst = reinterpret_cast<float*>(a.g) + k;
+        st_na_v4f(dst, f[0], f[1], f[2], f[3]);
+        st_na_v4f(dst + 4, f[4], f[5], f[6], f[7]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          bad |= ((hw[e] & 0x7C00u) == 0x7C00u) | ((hw[e] & 0x7C000000u) == 0x7C000000u);
+        st_na_v4u(reinterpret_cast<uint16_t*>(a.g) + k, hw[0], hw[1], hw[2], hw[3]);
       }
     }
     __syncthreads();  // every thread is done reading stage s
