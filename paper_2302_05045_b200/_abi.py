@@ -150,7 +150,7 @@ def load(path: os.PathLike | str | None = None) -> C.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("SAMO_LIB", LIB_PATH))
     if not p.exists():
         raise ImportError(
             f"{p} is missing: build it with `python -m paper_2302_05045_b200.build` "

@@ -39,6 +39,12 @@ namespace samo_dev {
 namespace {
 
 constexpr int kU = 4;         // independent elements per thread and pass (ILP)
+#ifndef SAMO_P2P_MINB
+#define SAMO_P2P_MINB 1  // min resident CTAs/SM hint for k_shard_p2p (tuning)
+#endif
+#ifndef SAMO_P2P_GRID
+#define SAMO_P2P_GRID 8  // CTAs per SM launched for k_shard_p2p (tuning)
+#endif
 
 __device__ __forceinline__ bool finite_f32(float x) {
   return (__float_as_uint(x) & 0x7F800000u) != 0x7F800000u;
@@ -600,7 +606,7 @@ __device__ __forceinline__ uint16_t half_lane(const uint4& v, int e) {
 }
 
 template <int G>
-__global__ void __launch_bounds__(kThreads) k_shard_p2p(P2PArgs a) {
+__global__ void __launch_bounds__(kThreads, SAMO_P2P_MINB) k_shard_p2p(P2PArgs a) {
   __shared__ float red[kThreads / 32];
   __shared__ int last_cta;
   const bool skip = *reinterpret_cast<const volatile float*>(a.flag_slot) != 0.0f;
@@ -834,7 +840,7 @@ int launch_update(const StepArgs& a, bool g_f32, int grid, cudaStream_t s) {
 int launch_shard_p2p(const P2PArgs& a, cudaStream_t s) {
   const uint64_t nv = (a.k1 > a.k0) ? (a.k1 - a.k0 + 7) / 8 : 0;
   const int grid = static_cast<int>(
-      std::max<uint64_t>(1, std::min<uint64_t>(static_cast<uint64_t>(num_sms()) * 8, (nv + kThreads - 1) / kThreads)));
+      std::max<uint64_t>(1, std::min<uint64_t>(static_cast<uint64_t>(num_sms()) * SAMO_P2P_GRID, (nv + kThreads - 1) / kThreads)));
   switch (a.G) {
     case 2: k_shard_p2p<2><<<grid, kThreads, 0, s>>>(a); break;
     case 3: k_shard_p2p<3><<<grid, kThreads, 0, s>>>(a); break;
