@@ -359,7 +359,7 @@ def run_samo(args) -> None:
             time.sleep(0.35)
     launches = samo.kernel_launch_count() - launches0
     total_ms = t0.elapsed_time(t1)
-    phases = None
+    phases = pipeline = None
     if world == 1 and args.graph:  # per-kernel breakdown from a staged pass
         for s in range(K):
             e = evs[s]
@@ -378,21 +378,38 @@ def run_samo(args) -> None:
         # Phase breakdown of the production step (events inside the driver;
         # sharded exchange only) — not the headline.
         phases = None
-        if model.exchange_mode() in (model.EXCHANGE_SHARDED, model.EXCHANGE_P2P):
+        pipeline = None
+
+        def phase_pass():
             _abi.call("samo_model_enable_phase_timing", model.handle, 1)
             for _ in range(3):
                 model.step()
             buf = (C.c_float * 16)()
             cnt = _abi.load().samo_model_phase_times(model.handle, buf, 16)
             _abi.call("samo_model_enable_phase_timing", model.handle, 0)
-            names = (["K1_gather", "skip-flag allreduce (barrier)",
-                      "shard update: fused NVLink exchange + Adam", "norm allreduce (barrier)",
-                      "expand", "finalize"]
-                     if model.exchange_mode() == model.EXCHANGE_P2P else
-                     ["K1_gather (reduce-scatter overlapped)",
-                      "skip flag + shard Adam + first all-gather bucket",
-                      "expand (all-gather overlapped)", "norm allreduce + finalize"])
-            phases = {names[i]: round(buf[i], 4) for i in range(max(0, cnt))}
+            return [round(buf[i], 4) for i in range(max(0, cnt))]
+
+        if model.exchange_mode() == model.EXCHANGE_P2P:
+            ph = phase_pass()
+            if len(ph) == 4:  # pipelined step (SAMO_P2P_BUCKETS > 1)
+                pipeline = dict(zip(["K1_gather", "skip-flag exchange (peer signals)",
+                                     "shard update || expand (pipelined over k-buckets)",
+                                     "finalize"], ph))
+                # per-kernel breakdown from the serial schedule of the same kernels
+                old_b = os.environ.get("SAMO_P2P_BUCKETS")
+                os.environ["SAMO_P2P_BUCKETS"] = "1"
+                ph = phase_pass()
+                if old_b is None:
+                    del os.environ["SAMO_P2P_BUCKETS"]
+                else:
+                    os.environ["SAMO_P2P_BUCKETS"] = old_b
+            phases = dict(zip(["K1_gather", "skip-flag allreduce (barrier)",
+                               "shard update: fused NVLink exchange + Adam", "norm allreduce (barrier)",
+                               "expand", "finalize"], ph))
+        elif model.exchange_mode() == model.EXCHANGE_SHARDED:
+            phases = dict(zip(["K1_gather (reduce-scatter overlapped)",
+                               "skip flag + shard Adam + first all-gather bucket",
+                               "expand (all-gather overlapped)", "norm allreduce + finalize"], phase_pass()))
         # Stage breakdown (not the headline): the same three stages run back
         # to back, the exchange as one allreduce of the whole arena.
         KB = min(K, 10)
@@ -577,15 +594,17 @@ def run_samo(args) -> None:
                        "gpu": gpu_name},
             "gpu_launches": int(launches),
             "step_mode": "K1 | K23 (no exchange)" if world == 1 else
-                         ("p2p (ZeRO-1, exchange fused over NVLink): K1 | shard kernel loads every "
-                          "rank's binary16 grads, rank-ordered fp32 sum, Adam, stores binary16 "
-                          "weights to every rank | expand"
+                         ("p2p (ZeRO-1, exchange fused over NVLink, no NCCL): K1 | peer-signalled "
+                          "flag exchange | per k-bucket: shard kernel loads every rank's binary16 "
+                          "grads, rank-ordered fp32 sum, Adam, stores binary16 weights to every "
+                          "rank, signals the bucket || expand of the signalled buckets"
                           if model.exchange_mode() == model.EXCHANGE_P2P else
                           "sharded (ZeRO-1), k-bucketed: K1 || NCCL reduce-scatter, shard Adam, "
                           "NCCL all-gather of binary16 weights || expand"
                           if model.exchange_mode() == model.EXCHANGE_SHARDED
                           else "allreduce: bucketed NCCL allreduce overlapped with K1/K23"),
             "phases_ms": phases,
+            "pipeline_phases_ms": pipeline,
             "roofline": roofline,
             "kernels": kern,
             "e2e": e2e,

@@ -319,6 +319,31 @@ int samo_copy_async(void* dst, const void* src, uint64_t bytes, samo_stream_t st
 int samo_stream_synchronize(samo_stream_t stream);
 
 /* ------------------------------------------------------------------------ */
+/* State formats.  Binary checkpoint with the fields of the reference's JSON  */
+/* checkpoint (serialize.hpp:120-190: per-layer indices, theta32, adam_m,     */
+/* adam_v; theta16 rebuilt by downcast+expand on load; gradients not saved)   */
+/* plus the device Adam scalars.  Load errors -> SAMO_E_CONFIG, as the        */
+/* reference's checkpoint_from_json.  Synchronise the stream.                 */
+int samo_model_save(samo_model* model, const char* path, samo_stream_t stream);
+int samo_model_load(const char* path, uint32_t tile_elems, samo_model** out,
+                    samo_stream_t stream);
+
+/* Memory accounting of a model (store.hpp:129-147 measured_bytes beside the
+ * real device footprint). */
+typedef struct samo_memory_report {
+  uint64_t dense_params;           /* phi */
+  uint64_t kept;                   /* n */
+  uint64_t theta16_bytes;          /* dense binary16 weights */
+  uint64_t compressed_state_bytes; /* theta32, m, v, grad arenas */
+  uint64_t index_bytes;            /* u32 index sets + off16 */
+  uint64_t table_bytes;            /* tile table */
+  uint64_t device_bytes;           /* everything the model allocated */
+  uint64_t reference_steady_bytes; /* measured_bytes(steady_state) = 2phi + 22n */
+  uint64_t reference_peak_bytes;   /* measured_bytes(peak) = 2phi + 24n */
+} samo_memory_report;
+int samo_model_memory(const samo_model* model, samo_memory_report* out);
+
+/* ------------------------------------------------------------------------ */
 /* Synthetic data (bench/test inputs; not part of the reference API).        */
 /* Counter-based: element i of stream s under seed gets                      */
 /*   u = mix64(seed, s, i); c = (u >> 40) * 2^-24;                           */

@@ -83,6 +83,12 @@ class StepRecord(C.Structure):
                 ("beta2_pow", C.c_float), ("grad_norm", C.c_float), ("last_skipped", C.c_uint32)]
 
 
+class MemoryReport(C.Structure):
+    _fields_ = [(k, C.c_uint64) for k in (
+        "dense_params", "kept", "theta16_bytes", "compressed_state_bytes", "index_bytes",
+        "table_bytes", "device_bytes", "reference_steady_bytes", "reference_peak_bytes")]
+
+
 _SIGS = {
     "samo_abi_version": (C.c_int, []),
     "samo_status_string": (C.c_char_p, [C.c_int]),
@@ -133,6 +139,9 @@ _SIGS = {
     "samo_model_step_record_async": (C.c_int, [vp, vp, vp]),
     "samo_model_set_step_record": (C.c_int, [vp, C.POINTER(StepRecord), vp]),
     "samo_model_check_invariants": (C.c_int, [vp, vp]),
+    "samo_model_save": (C.c_int, [vp, C.c_char_p, vp]),
+    "samo_model_load": (C.c_int, [C.c_char_p, C.c_uint32, C.POINTER(vp), vp]),
+    "samo_model_memory": (C.c_int, [vp, C.POINTER(MemoryReport)]),
     "samo_copy_async": (C.c_int, [vp, vp, C.c_uint64, vp]),
     "samo_stream_synchronize": (C.c_int, [vp]),
     "samo_synth_uniform_f32": (C.c_int, [vp, C.c_uint64, C.c_uint64, C.c_uint64, C.c_float, vp]),

@@ -483,6 +483,8 @@ struct samo_model {
   cudaEvent_t ev_fork = nullptr, ev_flag = nullptr;
   int reserve_sms = 16;                 // SMs left to NCCL while our kernels run
   ShardPlan shard_plan;
+  ShardPlan p2p_plan;                   // pipelined peer-to-peer step
+  SamoPeerSlots* slots = nullptr;       // this rank's signal area (in the block)
   // Peer mappings of the other ranks' model blocks (CUDA IPC) for the fused
   // peer-to-peer exchange; p2p_ok is agreed by every rank.
   void* peer_base[kMaxP2PRanks] = {};
@@ -677,6 +679,7 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   // relative placement measured best.
   const uint64_t o_c16 = carve((n_al + kArenaSlack) * 2);
   const uint64_t o_n2 = carve(256);  // 16 norm^2 slots + arrival counter
+  const uint64_t o_slots = carve(sizeof(SamoPeerSlots));
   md->block_bytes = off;
   cudaError_t e = cudaMalloc(&md->block, off);
   if (e != cudaSuccess) {
@@ -693,6 +696,7 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   md->c16 = reinterpret_cast<uint16_t*>(b + o_c16);
   md->norm2 = reinterpret_cast<double*>(b + o_n2);
   md->done = reinterpret_cast<uint32_t*>(b + o_n2 + 16 * sizeof(double));
+  md->slots = reinterpret_cast<SamoPeerSlots*>(b + o_slots);
   md->theta16 = reinterpret_cast<uint16_t*>(b + o_t16);
   md->tiles = reinterpret_cast<SamoTile*>(b + o_tiles);
   md->layers_dev = reinterpret_cast<SamoLayerDev*>(b + o_layers);
@@ -802,7 +806,7 @@ int samo_model_set_indices(samo_model* md, int l, const uint32_t* idx, uint64_t 
   if (n && !idx) return fail(SAMO_E_PARAMETER, "null index pointer");
   cudaStream_t s = as_stream(stream);
   uint32_t* dst = md->idx + md->k_off[l];
-  if (n) {
+  if (n && idx != dst) {  // idx == dst: validate in place (checkpoint load)
     SAMO_CUDA_TRY(cudaMemcpyAsync(dst, idx, n * 4,
                                   src_on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
   }
@@ -1066,8 +1070,12 @@ static int exchange_mode(const samo_model* md) {
 //                                       stores of the binary16 weights]
 //   -> allreduce(norm^2)               [NCCL, 8 bytes: also the barrier]
 //   -> expand every tile from theta16c -> scalars.
+static int p2p_buckets();
+static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B);
+
 static int step_p2p(samo_model* md, cudaStream_t S) {
   const int G = md->comm->nranks, r = md->comm->rank;
+  if (p2p_buckets() > 1) return step_p2p_pipelined(md, S, p2p_buckets());
   const uint64_t c = align_up((md->n_tot + G - 1) / G, 8);
   if (static_cast<uint64_t>(G) * c + 8 > md->n_al + kFlagOff)
     return fail(SAMO_E_PARAMETER, "too many ranks for the arena padding");
@@ -1100,6 +1108,7 @@ static int step_p2p(samo_model* md, cudaStream_t S) {
   pa.norm_partials = md->norm_partials;
   pa.norm2_out = md->norm2;
   pa.done = md->done;
+  pa.bucket = -1;
   if (pa.k1 > pa.k0) {
     SAMO_TRY(launch_shard_p2p(pa, S));
   } else {
@@ -1119,12 +1128,8 @@ static int step_p2p(samo_model* md, cudaStream_t S) {
   return SAMO_OK;
 }
 
-// Shard of the compressed arena owned by this rank in the sharded exchange:
-// [rank * cnt, min((rank + 1) * cnt, n)), cnt a multiple of 8.
-static uint64_t shard_count(const samo_model* md) {
-  const uint64_t G = comm_size(md);
-  return align_up((md->n_tot + G - 1) / G, 8);
-}
+static int shard_buckets() { return std::max(1, std::min(env_int("SAMO_SHARD_BUCKETS", 4), 16)); }
+static int p2p_buckets() { return std::max(1, std::min(env_int("SAMO_P2P_BUCKETS", 8), kMaxP2PBuckets)); }
 
 // One data-parallel step, ZeRO-1 style on the compressed state, pipelined
 // over B k-buckets (bucket b = arena range [b*C, (b+1)*C), C = G*c, rank r
@@ -1139,10 +1144,8 @@ static uint64_t shard_count(const samo_model* md) {
 // lies in bucket b (so it only waits for AG[0..b]).  The reduce-scatter hides
 // behind the gather kernels and the all-gather behind the expand kernels.
 // Link bytes per rank 6n(G-1)/G instead of 8n(G-1)/G; Adam HBM traffic / G.
-static int plan_shards(samo_model* md, ShardPlan& p) {
+static int plan_shards(samo_model* md, ShardPlan& p, int B) {
   const int G = comm_size(md);
-  int B = env_int("SAMO_SHARD_BUCKETS", 4);
-  B = std::max(1, std::min(B, 16));
   if (p.G == G && p.B == B) return SAMO_OK;
   p.G = G;
   p.B = B;
@@ -1178,7 +1181,7 @@ static int plan_shards(samo_model* md, ShardPlan& p) {
 static int step_sharded(samo_model* md, cudaStream_t S) {
   SAMO_TRY(plan_buckets(md));  // side streams + events
   ShardPlan& p = md->shard_plan;
-  SAMO_TRY(plan_shards(md, p));
+  SAMO_TRY(plan_shards(md, p, shard_buckets()));
   const int r = md->comm->rank, B = p.B;
   if (static_cast<int>(md->ev_sh.size()) < 2 * B) {
     for (int i = static_cast<int>(md->ev_sh.size()); i < 2 * B; ++i) {
@@ -1268,6 +1271,94 @@ static int step_sharded(samo_model* md, cudaStream_t S) {
   return SAMO_OK;
 }
 
+// The fused peer-to-peer step, pipelined over B k-buckets with no NCCL on
+// it at all: the barriers are release/acquire signals in the ranks' peer-
+// mapped SamoPeerSlots (bucket b = arena range [b*C, (b+1)*C), rank r owns
+// [b*C + r*c, b*C + (r+1)*c)).
+//
+//   S:   K1 -> flag exchange -> shard[0] -> shard[1] -> ... shard[B-1]   | join -> finalize
+//   E:                      wait[0] expand[0] -> wait[1] expand[1] -> ...
+//
+// shard[b] (NVLink-bound: peer loads of every rank's grad16, peer stores of
+// the binary16 weights) publishes bucket b's completion + norm^2 to every
+// rank; expand[b] (HBM-bound) covers the tiles whose last kept element lies
+// in bucket b, once every rank has published bucket b.  The global skip flag
+// forces every K1 to finish before any shard update, so K1 stays serial.
+// Grids: SAMO_P2P_SHARD_CTAS / SAMO_P2P_EXPAND_CTAS per SM (tuning).
+static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B) {
+  const int G = md->comm->nranks, r = md->comm->rank;
+  SAMO_TRY(plan_buckets(md));  // side streams + events
+  ShardPlan& p = md->p2p_plan;
+  SAMO_TRY(plan_shards(md, p, B));
+  if (static_cast<int>(md->ev_sh.size()) < 2 * B) {
+    for (int i = static_cast<int>(md->ev_sh.size()); i < 2 * B; ++i) {
+      cudaEvent_t e;
+      SAMO_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      md->ev_sh.push_back(e);
+    }
+  }
+  cudaStream_t E = md->s_comm;
+  float* flag = flag_ptr(md);
+  const char* base = static_cast<const char*>(md->block);
+  const size_t g_off = reinterpret_cast<const char*>(md->g) - base;
+  const size_t c_off = reinterpret_cast<const char*>(md->c16) - base;
+  const size_t s_off = reinterpret_cast<const char*>(md->slots) - base;
+  P2PArgs pa{};
+  for (int q = 0; q < G; ++q) {
+    char* pb = static_cast<char*>(md->peer_base[q]);
+    pa.g16[q] = reinterpret_cast<const uint16_t*>(pb + g_off);
+    pa.c16[q] = reinterpret_cast<uint16_t*>(pb + c_off);
+    pa.slots[q] = reinterpret_cast<SamoPeerSlots*>(pb + s_off);
+  }
+  pa.G = G;
+  pa.rank = r;
+  pa.theta = md->theta;
+  pa.m = md->m;
+  pa.v = md->v;
+  pa.scale = (1.0f / md->cfg.loss_scale) * (1.0f / static_cast<float>(G));
+  pa.prm = adam_params(&md->cfg);
+  pa.st = md->st;
+  pa.flag_slot = flag;
+  pa.norm_partials = md->norm_partials;
+  pa.norm2_out = md->norm2;  // scratch: the bucket totals travel in the slots
+  pa.done = md->done;
+  const int sms = num_sms();
+  pa.grid = sms * std::max(1, env_int("SAMO_P2P_SHARD_CTAS", 2));
+  const int ge = std::min(md->grid_expand, sms * std::max(1, env_int("SAMO_P2P_EXPAND_CTAS", 2)));
+
+  SAMO_TRY(phase_mark(md, 0, S));
+  SAMO_TRY(launch_gather(step_args(md), false, md->grid_gather16, S));
+  SAMO_TRY(phase_mark(md, 1, S));
+  SAMO_TRY(launch_p2p_flag(pa.slots, G, r, flag, S));
+  SAMO_TRY(phase_mark(md, 2, S));
+  SAMO_CUDA_TRY(cudaEventRecord(md->ev_fork, S));
+  SAMO_CUDA_TRY(cudaStreamWaitEvent(E, md->ev_fork, 0));
+  for (int b = 0; b < B; ++b) {
+    pa.k0 = std::min<uint64_t>(b * p.C + r * p.c, md->n_tot);
+    pa.k1 = std::min<uint64_t>(b * p.C + (r + 1) * p.c, md->n_tot);
+    pa.bucket = b;
+    SAMO_TRY(launch_shard_p2p(pa, S));  // also when empty: it signals
+  }
+  const StepArgs sbase = step_args(md);
+  for (int b = 0; b < B; ++b) {
+    SAMO_TRY(launch_p2p_wait(md->slots, G, b, E));
+    StepArgs a = sbase;
+    a.g = md->c16;
+    a.tiles = md->tiles + p.ex_t[b];
+    a.ntiles = p.ex_t[b + 1] - p.ex_t[b];
+    if (a.ntiles) SAMO_TRY(launch_expand_c16(a, std::min<int>(ge, a.ntiles), E));
+  }
+  SAMO_CUDA_TRY(cudaEventRecord(md->ev_flag, E));
+  SAMO_CUDA_TRY(cudaStreamWaitEvent(S, md->ev_flag, 0));
+  SAMO_TRY(phase_mark(md, 3, S));
+  SAMO_TRY(launch_step_finalize(md->st, md->slots->norm, B * kMaxP2PRanks, flag, md->cfg.beta1,
+                                md->cfg.beta2, S));
+  SAMO_TRY(launch_p2p_epoch(md->slots, S));
+  SAMO_TRY(phase_mark(md, 4, S));
+  md->phase_count = 4;
+  return SAMO_OK;
+}
+
 extern "C" {
 
 int samo_model_set_exchange(samo_model* md, int mode) {
@@ -1312,6 +1403,15 @@ int samo_model_shard_layout(samo_model* md, uint64_t* chunk, uint64_t* stride, i
     *rank = 0;
     return clear_ok();
   }
+  if (exchange_mode(md) == SAMO_EXCHANGE_P2P && p2p_buckets() > 1) {
+    if (!md->finalized) return fail(SAMO_E_STATE, "model not finalized");
+    SAMO_TRY(plan_shards(md, md->p2p_plan, p2p_buckets()));
+    *chunk = md->p2p_plan.c;
+    *stride = md->p2p_plan.C;
+    *buckets = md->p2p_plan.B;
+    *rank = md->comm->rank;
+    return clear_ok();
+  }
   if (exchange_mode(md) == SAMO_EXCHANGE_P2P) {
     const uint64_t G = comm_size(md);
     *chunk = align_up((md->n_tot + G - 1) / G, 8);
@@ -1321,7 +1421,7 @@ int samo_model_shard_layout(samo_model* md, uint64_t* chunk, uint64_t* stride, i
     return clear_ok();
   }
   if (!md->finalized) return fail(SAMO_E_STATE, "model not finalized");
-  SAMO_TRY(plan_shards(md, md->shard_plan));
+  SAMO_TRY(plan_shards(md, md->shard_plan, shard_buckets()));
   *chunk = md->shard_plan.c;
   *stride = md->shard_plan.C;
   *buckets = md->shard_plan.B;
@@ -1476,6 +1576,165 @@ int samo_model_check_invariants(samo_model* md, samo_stream_t stream) {
   SAMO_CUDA_TRY(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, s));
   SAMO_CUDA_TRY(cudaStreamSynchronize(s));
   if (hbad) return fail(SAMO_E_STATE, "theta16 disagrees with expand(half(theta32))");
+  return clear_ok();
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// State formats: binary checkpoint of the arenas (serialize.hpp:120-190
+// equivalent: indices, theta32, adam_m, adam_v per layer; theta16 rebuilt by
+// downcast+expand on load, gradients not saved) plus the Adam scalars, and
+// the memory report (store.hpp:129-147 measured_bytes).
+
+namespace {
+
+constexpr char kCkptMagic[8] = {'S', 'A', 'M', 'O', 'C', 'K', 'P', 'T'};
+constexpr uint32_t kCkptVersion = 1;
+
+struct CkptHeader {
+  char magic[8];
+  uint32_t version;
+  uint32_t nlayers;
+  uint32_t tile_elems;
+  uint32_t reserved;
+  samo_step_record rec;
+};
+
+// Streams `bytes` between a device buffer and a FILE through a pinned
+// staging buffer (64 MiB chunks).
+int stream_file(FILE* f, void* dev, uint64_t bytes, bool to_file, cudaStream_t s) {
+  constexpr uint64_t kChunk = 64ull << 20;
+  if (bytes == 0) return SAMO_OK;
+  void* host = nullptr;
+  SAMO_CUDA_TRY(cudaMallocHost(&host, std::min(bytes, kChunk)));
+  int rc = SAMO_OK;
+  for (uint64_t off = 0; off < bytes && rc == SAMO_OK; off += kChunk) {
+    const uint64_t n = std::min(kChunk, bytes - off);
+    char* d = static_cast<char*>(dev) + off;
+    if (to_file) {
+      cudaError_t e = cudaMemcpyAsync(host, d, n, cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) rc = cuda_fail(e, "checkpoint D2H");
+      else if (fwrite(host, 1, n, f) != n) rc = fail(SAMO_E_CONFIG, "checkpoint write failed");
+    } else {
+      if (fread(host, 1, n, f) != n) {
+        rc = fail(SAMO_E_CONFIG, "checkpoint truncated");
+        break;
+      }
+      cudaError_t e = cudaMemcpyAsync(d, host, n, cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) rc = cuda_fail(e, "checkpoint H2D");
+    }
+  }
+  cudaFreeHost(host);
+  return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int samo_model_save(samo_model* md, const char* path, samo_stream_t stream) {
+  SAMO_TRY(step_ready(md));
+  if (!path) return fail(SAMO_E_PARAMETER, "null path");
+  if (comm_size(md) > 1 && exchange_mode(md) != SAMO_EXCHANGE_ALLREDUCE)
+    return fail(SAMO_E_STATE, "sharded state: theta32/m/v are only authoritative on each rank's shard");
+  cudaStream_t s = as_stream(stream);
+  CkptHeader h{};
+  std::memcpy(h.magic, kCkptMagic, 8);
+  h.version = kCkptVersion;
+  h.nlayers = static_cast<uint32_t>(md->nlayers);
+  h.tile_elems = md->tile_elems;
+  SAMO_TRY(samo_model_step_record(md, &h.rec, stream));
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return fail(SAMO_E_CONFIG, "cannot open %s for writing", path);
+  int rc = SAMO_OK;
+  if (fwrite(&h, sizeof(h), 1, f) != 1) rc = fail(SAMO_E_CONFIG, "checkpoint write failed");
+  for (int l = 0; l < md->nlayers && rc == SAMO_OK; ++l) {
+    const uint64_t d[2] = {md->dense_len[l], md->nnz[l]};
+    if (fwrite(d, sizeof(d), 1, f) != 1) rc = fail(SAMO_E_CONFIG, "checkpoint write failed");
+  }
+  const uint64_t n = md->n_tot;
+  if (rc == SAMO_OK) rc = stream_file(f, md->idx, n * 4, true, s);
+  if (rc == SAMO_OK) rc = stream_file(f, md->theta, n * 4, true, s);
+  if (rc == SAMO_OK) rc = stream_file(f, md->m, n * 4, true, s);
+  if (rc == SAMO_OK) rc = stream_file(f, md->v, n * 4, true, s);
+  if (std::fclose(f) != 0 && rc == SAMO_OK) rc = fail(SAMO_E_CONFIG, "checkpoint close failed");
+  return rc == SAMO_OK ? clear_ok() : rc;
+}
+
+int samo_model_load(const char* path, uint32_t tile_elems, samo_model** out, samo_stream_t stream) {
+  if (!path || !out) return fail(SAMO_E_PARAMETER, "null argument");
+  SAMO_TRY(device_ok());
+  FILE* f = std::fopen(path, "rb");
+  if (!f) return fail(SAMO_E_CONFIG, "cannot open %s", path);
+  CkptHeader h{};
+  std::vector<samo_layer_desc> descs;
+  int rc = SAMO_OK;
+  if (fread(&h, sizeof(h), 1, f) != 1 || std::memcmp(h.magic, kCkptMagic, 8) != 0 ||
+      h.version != kCkptVersion) {
+    rc = fail(SAMO_E_CONFIG, "%s is not a SAMO checkpoint", path);
+  }
+  for (uint32_t l = 0; l < h.nlayers && rc == SAMO_OK; ++l) {
+    uint64_t d[2];
+    if (fread(d, sizeof(d), 1, f) != 1) rc = fail(SAMO_E_CONFIG, "checkpoint truncated");
+    else descs.push_back({d[0], d[1]});
+  }
+  samo_model* md = nullptr;
+  if (rc == SAMO_OK) {
+    rc = samo_model_create(descs.data(), static_cast<int>(descs.size()),
+                           tile_elems ? tile_elems : h.tile_elems, &md);
+    if (rc == SAMO_E_DIMENSION) rc = fail(SAMO_E_CONFIG, "checkpoint layer table: %s", samo_last_error());
+  }
+  cudaStream_t s = as_stream(stream);
+  if (rc == SAMO_OK) rc = stream_file(f, md->idx, md->n_tot * 4, false, s);
+  if (rc == SAMO_OK) {
+    // serialize.hpp:156-163: indices strictly ascending and in range -> ConfigError
+    for (int l = 0; l < md->nlayers && rc == SAMO_OK; ++l) {
+      const int r2 = samo_model_set_indices(md, l, md->idx + md->k_off[l], md->nnz[l], 0, stream);
+      if (r2 == SAMO_E_INDEX) rc = fail(SAMO_E_CONFIG, "checkpoint indices must be strictly ascending and in range (layer %d)", l);
+      else rc = r2;
+    }
+  }
+  if (rc == SAMO_OK) rc = samo_model_finalize(md, stream);
+  if (rc == SAMO_OK) rc = stream_file(f, md->theta, md->n_tot * 4, false, s);
+  if (rc == SAMO_OK) rc = stream_file(f, md->m, md->n_tot * 4, false, s);
+  if (rc == SAMO_OK) rc = stream_file(f, md->v, md->n_tot * 4, false, s);
+  std::fclose(f);
+  if (rc == SAMO_OK) {  // theta16 = expand(half(theta32)) for every tile (serialize.hpp:184-186)
+    ExpandArgs a{};
+    a.tiles = md->tiles;
+    a.ntiles = md->ntiles;
+    a.tile_elems = md->tile_elems;
+    a.out_base = md->theta16;
+    a.idx = md->idx;
+    a.theta = md->theta;
+    a.use_bulk = 1;
+    rc = launch_expand<kModeDowncast, uint16_t>(a, 0, s);
+  }
+  if (rc == SAMO_OK) rc = samo_model_set_step_record(md, &h.rec, stream);
+  if (rc != SAMO_OK) {
+    samo_model_destroy(md);
+    return rc;
+  }
+  *out = md;
+  return clear_ok();
+}
+
+int samo_model_memory(const samo_model* md, samo_memory_report* out) {
+  if (!md || !out) return fail(SAMO_E_PARAMETER, "null argument");
+  const uint64_t phi = md->phi, n = md->n_tot;
+  out->dense_params = phi;
+  out->kept = n;
+  out->theta16_bytes = md->d_tot * 2;
+  out->compressed_state_bytes = 4 * md->n_al * 4;          // theta32, m, v, grad
+  out->index_bytes = md->n_al * (4 + 2);                    // u32 index set + off16
+  out->table_bytes = static_cast<uint64_t>(md->ntiles) * sizeof(SamoTile);
+  out->device_bytes = md->block_bytes;
+  // store.hpp:129-147 (per layer 2*dense + (2+4+4+8+4)*nnz [+ 2*nnz peak])
+  out->reference_steady_bytes = 2 * phi + 22 * n;
+  out->reference_peak_bytes = 2 * phi + 24 * n;
   return clear_ok();
 }
 

@@ -65,6 +65,19 @@ int step_grid(int which, bool wide, uint32_t tile_elems);
 // every rank's binary16 gradient over NVLink, sums in rank order, runs Adam
 // and writes the binary16 weights into every rank's theta16c arena.
 constexpr int kMaxP2PRanks = 8;
+constexpr int kMaxP2PBuckets = 32;
+// Signal area of the pipelined peer-to-peer step, one per rank inside its
+// IPC-mapped model block.  Rank q writes only the [q] columns of its peers'
+// areas (release stores at system scope); each rank spins only on its own.
+// `epoch` (local) counts completed pipelined steps; every signal of step s
+// carries epoch + 1 = s + 1, so no slot is ever reset.
+struct SamoPeerSlots {
+  uint64_t epoch;
+  uint64_t flag_epoch[kMaxP2PRanks];
+  float flag_val[kMaxP2PRanks];
+  uint64_t bucket_epoch[kMaxP2PBuckets * kMaxP2PRanks];  // [bucket * 8 + rank]
+  double norm[kMaxP2PBuckets * kMaxP2PRanks];             // [bucket * 8 + rank]
+};
 struct P2PArgs {
   const uint16_t* g16[kMaxP2PRanks];  // per-rank compressed binary16 gradients
   uint16_t* c16[kMaxP2PRanks];        // per-rank theta16c arenas
@@ -81,8 +94,21 @@ struct P2PArgs {
   float* norm_partials;
   double* norm2_out;
   uint32_t* done;
+  // Pipelined step only (bucket >= 0): every rank's signal area; the last CTA
+  // publishes this bucket's norm^2 and its completion to all of them.
+  SamoPeerSlots* slots[kMaxP2PRanks];
+  int bucket;
+  int grid;                           // 0 = default
 };
 int launch_shard_p2p(const P2PArgs& a, cudaStream_t s);
+// Skip-flag exchange over peer memory (one warp): publishes this rank's
+// non-finite count to every peer, waits for all of theirs and writes the
+// rank-ordered sum to *flag.  Also the step's first cross-rank barrier.
+int launch_p2p_flag(SamoPeerSlots* const* slots, int G, int rank, float* flag, cudaStream_t s);
+// Waits (one warp) until every rank has published bucket `bucket`.
+int launch_p2p_wait(const SamoPeerSlots* mine, int G, int bucket, cudaStream_t s);
+// Advances the local epoch (after the step's last read of the slots).
+int launch_p2p_epoch(SamoPeerSlots* mine, cudaStream_t s);
 
 // Sharded data-parallel step pieces.
 struct ShardArgs {

@@ -706,8 +706,61 @@ __global__ void __launch_bounds__(kThreads, SAMO_P2P_MINB) k_shard_p2p(P2PArgs a
     *a.norm2_out = acc;
     *a.done = 0u;
     __threadfence();
+    if (a.bucket >= 0) {  // pipelined step: publish norm^2 + completion to every rank
+      const uint64_t e = a.slots[a.rank]->epoch + 1;
+      const int slot = a.bucket * kMaxP2PRanks + a.rank;
+#pragma unroll
+      for (int r = 0; r < G; ++r) a.slots[r]->norm[slot] = acc;
+      asm volatile("fence.sc.sys;" ::: "memory");
+#pragma unroll
+      for (int r = 0; r < G; ++r) st_release_sys(&a.slots[r]->bucket_epoch[slot], e);
+    }
   }
 }
+
+// Spin on a local signal word written by a peer (acquire, system scope).  A
+// peer that never arrives is a dead job: trap after ~30 s rather than hang.
+__device__ void spin_until(const uint64_t* p, uint64_t target) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  uint32_t ns = 32;
+  while (ld_acquire_sys(p) < target) {
+    __nanosleep(ns);
+    ns = ns < 1024 ? ns * 2 : ns;
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 30ull * 1000000000ull) __trap();
+  }
+}
+
+__global__ void k_p2p_flag(P2PArgs a, float* flag) {
+  SamoPeerSlots* mine = a.slots[a.rank];
+  const uint64_t e = mine->epoch + 1;
+  const int q = threadIdx.x;
+  if (q < a.G) {
+    a.slots[q]->flag_val[a.rank] = *flag;
+    asm volatile("fence.sc.sys;" ::: "memory");  // K1's grad16 + the value before the signal
+    st_release_sys(&a.slots[q]->flag_epoch[a.rank], e);
+    spin_until(&mine->flag_epoch[q], e);
+  }
+  __syncwarp();
+  if (q == 0) {
+    float f = 0.0f;  // rank order: every rank computes the same value
+    const volatile float* fv = mine->flag_val;
+    for (int r = 0; r < a.G; ++r) f = __fadd_rn(f, fv[r]);
+    *flag = f;
+    __threadfence();
+  }
+}
+
+__global__ void k_p2p_wait(const SamoPeerSlots* mine, int G, int bucket) {
+  const int q = threadIdx.x;
+  if (q < G) spin_until(&mine->bucket_epoch[bucket * kMaxP2PRanks + q], mine->epoch + 1);
+  __syncwarp();
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+
+__global__ void k_p2p_epoch(SamoPeerSlots* mine) { mine->epoch += 1; }
 
 // One thread: the step's scalars once the global grad norm^2 and skip flag
 // are known (AdamScalars::advance, train.hpp:325-329; skip, 632-639).
@@ -839,8 +892,9 @@ int launch_update(const StepArgs& a, bool g_f32, int grid, cudaStream_t s) {
 
 int launch_shard_p2p(const P2PArgs& a, cudaStream_t s) {
   const uint64_t nv = (a.k1 > a.k0) ? (a.k1 - a.k0 + 7) / 8 : 0;
+  const uint64_t cap = a.grid > 0 ? a.grid : static_cast<uint64_t>(num_sms()) * SAMO_P2P_GRID;
   const int grid = static_cast<int>(
-      std::max<uint64_t>(1, std::min<uint64_t>(static_cast<uint64_t>(num_sms()) * SAMO_P2P_GRID, (nv + kThreads - 1) / kThreads)));
+      std::max<uint64_t>(1, std::min<uint64_t>(cap, (nv + kThreads - 1) / kThreads)));
   switch (a.G) {
     case 2: k_shard_p2p<2><<<grid, kThreads, 0, s>>>(a); break;
     case 3: k_shard_p2p<3><<<grid, kThreads, 0, s>>>(a); break;
@@ -852,6 +906,29 @@ int launch_shard_p2p(const P2PArgs& a, cudaStream_t s) {
     default: return fail(SAMO_E_PARAMETER, "peer-to-peer exchange supports 2..8 ranks");
   }
   SAMO_LAUNCH_CHECK("k_shard_p2p");
+  return SAMO_OK;
+}
+
+int launch_p2p_flag(SamoPeerSlots* const* slots, int G, int rank, float* flag, cudaStream_t s) {
+  if (G < 2 || G > kMaxP2PRanks) return fail(SAMO_E_PARAMETER, "peer-to-peer exchange supports 2..8 ranks");
+  P2PArgs a{};
+  for (int q = 0; q < G; ++q) a.slots[q] = slots[q];
+  a.G = G;
+  a.rank = rank;
+  k_p2p_flag<<<1, 32, 0, s>>>(a, flag);
+  SAMO_LAUNCH_CHECK("k_p2p_flag");
+  return SAMO_OK;
+}
+
+int launch_p2p_wait(const SamoPeerSlots* mine, int G, int bucket, cudaStream_t s) {
+  k_p2p_wait<<<1, 32, 0, s>>>(mine, G, bucket);
+  SAMO_LAUNCH_CHECK("k_p2p_wait");
+  return SAMO_OK;
+}
+
+int launch_p2p_epoch(SamoPeerSlots* mine, cudaStream_t s) {
+  k_p2p_epoch<<<1, 1, 0, s>>>(mine);
+  SAMO_LAUNCH_CHECK("k_p2p_epoch");
   return SAMO_OK;
 }
 

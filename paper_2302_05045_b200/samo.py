@@ -401,6 +401,37 @@ class SamoModel:
     def device_bytes(self) -> int:
         return int(_abi.load().samo_model_device_bytes(self._h))
 
+    def memory(self) -> dict:
+        """Device footprint beside the reference's measured_bytes (store.hpp:129-147)."""
+        r = _abi.MemoryReport()
+        _abi.call("samo_model_memory", self._h, C.byref(r))
+        return {k: int(getattr(r, k)) for k, _ in r._fields_}
+
+    def save(self, path: str) -> None:
+        """Binary checkpoint: indices, theta32, adam_m, adam_v per layer + Adam
+        scalars (the fields of serialize.hpp:120-190)."""
+        _abi.call("samo_model_save", self._h, str(path).encode(), _stream())
+
+    @classmethod
+    def load(cls, path: str, layers: Sequence[LayerSpec] | None = None,
+             tile_elems: int = 0) -> "SamoModel":
+        """Rebuilds a model from samo_model_save output; theta16 is rebuilt by
+        downcast+expand (serialize.hpp:184-186)."""
+        h = C.c_void_p()
+        _abi.call("samo_model_load", str(path).encode(), int(tile_elems), C.byref(h), _stream())
+        model = cls.__new__(cls)
+        model._h = h
+        model._grads_keepalive = []
+        n = int(_abi.load().samo_model_num_layers(h))
+        if layers is None:
+            layers = []
+            for l in range(n):
+                v = _abi.LayerView()
+                _abi.call("samo_model_layer_view", h, l, C.byref(v))
+                layers.append(LayerSpec(f"l{l}", (int(v.dense_len),), int(v.nnz)))
+        model.layers = list(layers)
+        return model
+
     _FIELDS = {"theta16": (torch.float16, "dense"), "theta32": (torch.float32, "nnz"),
                "adam_m": (torch.float32, "nnz"), "adam_v": (torch.float32, "nnz"),
                "grad32": (torch.float32, "nnz"), "indices": (torch.int32, "nnz")}
