@@ -1109,6 +1109,7 @@ static int step_p2p(samo_model* md, cudaStream_t S) {
   pa.norm2_out = md->norm2;
   pa.done = md->done;
   pa.bucket = -1;
+  pa.tma = env_int("SAMO_P2P_TMA", 0);
   if (pa.k1 > pa.k0) {
     SAMO_TRY(launch_shard_p2p(pa, S));
   } else {
@@ -1323,7 +1324,8 @@ static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B) {
   pa.norm2_out = md->norm2;  // scratch: the bucket totals travel in the slots
   pa.done = md->done;
   const int sms = num_sms();
-  pa.grid = sms * std::max(1, env_int("SAMO_P2P_SHARD_CTAS", 2));
+  pa.tma = env_int("SAMO_P2P_TMA", 0);
+  pa.grid = sms * std::max(1, env_int("SAMO_P2P_SHARD_CTAS", pa.tma ? 1 : 2));
   const int ge = std::min(md->grid_expand, sms * std::max(1, env_int("SAMO_P2P_EXPAND_CTAS", 2)));
 
   SAMO_TRY(phase_mark(md, 0, S));

@@ -99,6 +99,7 @@ struct P2PArgs {
   SamoPeerSlots* slots[kMaxP2PRanks];
   int bucket;
   int grid;                           // 0 = default
+  int tma;                            // 1: k_shard_p2p_tma (TMA ring), 0: register loads
 };
 int launch_shard_p2p(const P2PArgs& a, cudaStream_t s);
 // Skip-flag exchange over peer memory (one warp): publishes this rank's
