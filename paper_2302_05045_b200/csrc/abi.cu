@@ -1070,12 +1070,12 @@ static int exchange_mode(const samo_model* md) {
 //                                       stores of the binary16 weights]
 //   -> allreduce(norm^2)               [NCCL, 8 bytes: also the barrier]
 //   -> expand every tile from theta16c -> scalars.
-static int p2p_buckets();
+static int p2p_buckets(int G);
 static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B);
 
 static int step_p2p(samo_model* md, cudaStream_t S) {
   const int G = md->comm->nranks, r = md->comm->rank;
-  if (p2p_buckets() > 1) return step_p2p_pipelined(md, S, p2p_buckets());
+  if (p2p_buckets(G) > 1) return step_p2p_pipelined(md, S, p2p_buckets(G));
   const uint64_t c = align_up((md->n_tot + G - 1) / G, 8);
   if (static_cast<uint64_t>(G) * c + 8 > md->n_al + kFlagOff)
     return fail(SAMO_E_PARAMETER, "too many ranks for the arena padding");
@@ -1130,7 +1130,11 @@ static int step_p2p(samo_model* md, cudaStream_t S) {
 }
 
 static int shard_buckets() { return std::max(1, std::min(env_int("SAMO_SHARD_BUCKETS", 4), 16)); }
-static int p2p_buckets() { return std::max(1, std::min(env_int("SAMO_P2P_BUCKETS", 8), kMaxP2PBuckets)); }
+// Pipelining pays once the shard update is NVLink-bound (G >= 4);
+// at G = 2 its HBM traffic (12n of theta/m/v) already matches the expand's.
+static int p2p_buckets(int G) {
+  return std::max(1, std::min(env_int("SAMO_P2P_BUCKETS", G >= 4 ? 8 : 1), kMaxP2PBuckets));
+}
 
 // One data-parallel step, ZeRO-1 style on the compressed state, pipelined
 // over B k-buckets (bucket b = arena range [b*C, (b+1)*C), C = G*c, rank r
@@ -1405,9 +1409,9 @@ int samo_model_shard_layout(samo_model* md, uint64_t* chunk, uint64_t* stride, i
     *rank = 0;
     return clear_ok();
   }
-  if (exchange_mode(md) == SAMO_EXCHANGE_P2P && p2p_buckets() > 1) {
+  if (exchange_mode(md) == SAMO_EXCHANGE_P2P && p2p_buckets(comm_size(md)) > 1) {
     if (!md->finalized) return fail(SAMO_E_STATE, "model not finalized");
-    SAMO_TRY(plan_shards(md, md->p2p_plan, p2p_buckets()));
+    SAMO_TRY(plan_shards(md, md->p2p_plan, p2p_buckets(comm_size(md))));
     *chunk = md->p2p_plan.c;
     *stride = md->p2p_plan.C;
     *buckets = md->p2p_plan.B;
