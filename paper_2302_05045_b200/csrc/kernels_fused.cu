@@ -224,6 +224,26 @@ __device__ __forceinline__ TileRegs load_tile(const SamoTile* p) {
   return r;
 }
 
+// Sum of n per-CTA float partials in double by all NT threads of the last
+// CTA: thread i takes partials i, i + NT, ... in order, then a fixed
+// shuffle/warp tree.  Deterministic for a given grid, and n/NT round trips to
+// L2 instead of n.  `red` holds NT/32 doubles; the result is valid in thread 0.
+template <int NT>
+__device__ __forceinline__ double sum_partials(const float* p, uint32_t n, double* red) {
+  const uint32_t tid = threadIdx.x;
+  double acc = 0.0;
+  const volatile float* vp = p;
+  for (uint32_t i = tid; i < n; i += NT) acc += static_cast<double>(vp[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+  if ((tid & 31) == 0) red[tid >> 5] = acc;
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+  double s = 0.0;
+  if (tid == 0)
+    for (int w = 0; w < NT / 32; ++w) s += red[w];
+  return s;
+}
+
 template <bool G16, int CH, bool EXPAND = false>
 struct K23Layout {
   // expand-only stages carry just the 16-bit values and off16 (compact, so
@@ -464,13 +484,17 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
     last_cta = (ticket == gridDim.x - 1);
   }
   asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
-  if (last_cta && tid == 0) {
+  if (!last_cta) return;
+  __shared__ double dred[kConsumerWarps];
+  double acc = 0.0;
+  if (a.finalize) {
+    if (tid == 0) __threadfence();
+    asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+    acc = sum_partials<kThreads>(a.norm_all, a.norm_count, dred);
+  }
+  if (tid == 0) {
     SamoStepState* stt = a.st;
     if (a.finalize) {  // the step's last update launch
-      __threadfence();
-      double acc = 0.0;
-      const volatile float* np = a.norm_all;
-      for (uint32_t b = 0; b < a.norm_count; ++b) acc += static_cast<double>(np[b]);
       stt->grad_norm = static_cast<float>(sqrt(acc));
       if (skip) {  // train.hpp:632-639
         stt->skipped_steps += 1;
@@ -570,11 +594,12 @@ __global__ void __launch_bounds__(kThreads) k_adam_shard(ShardArgs a) {
     last_cta = atomicAdd(a.done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last_cta && threadIdx.x == 0) {
-    __threadfence();
-    double acc = 0.0;
-    const volatile float* np = a.norm_partials;
-    for (uint32_t b = 0; b < gridDim.x; ++b) acc += static_cast<double>(np[b]);
+  if (!last_cta) return;
+  __shared__ double dred[kThreads / 32];
+  if (threadIdx.x == 0) __threadfence();
+  __syncthreads();
+  const double acc = sum_partials<kThreads>(a.norm_partials, gridDim.x, dred);
+  if (threadIdx.x == 0) {
     *a.norm2_out = acc;
     *a.done = 0u;
     __threadfence();
@@ -625,11 +650,12 @@ __device__ __forceinline__ void shard_finish(const P2PArgs& a, float nacc, float
     *last_cta = atomicAdd(a.done, 1u) == gridDim.x - 1;
   }
   asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
-  if (*last_cta && threadIdx.x == 0) {
-    __threadfence();
-    double acc = 0.0;
-    const volatile float* np = a.norm_partials;
-    for (uint32_t b = 0; b < gridDim.x; ++b) acc += static_cast<double>(np[b]);
+  if (!*last_cta) return;
+  __shared__ double dred[NT / 32];
+  if (threadIdx.x == 0) __threadfence();
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+  const double acc = sum_partials<NT>(a.norm_partials, gridDim.x, dred);
+  if (threadIdx.x == 0) {
     *a.norm2_out = acc;
     *a.done = 0u;
     __threadfence();
