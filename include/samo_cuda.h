@@ -187,6 +187,8 @@ typedef struct samo_layer_view { /* all device pointers */
   uint64_t dense_len;
   uint64_t nnz;
   uint64_t k_offset;  /* offset of this layer in the compressed arenas */
+  uint16_t* grad16;   /* nnz; the same arena viewed as binary16 (grad16 of the
+                         single-GPU and peer-to-peer steps) */
 } samo_layer_view;
 
 typedef struct samo_step_record { /* train.hpp:538-544 StepRecord + trainer counters */
@@ -284,6 +286,33 @@ int samo_model_set_grads(samo_model* model, const uint16_t* const* ptrs,
 /* Stage K1 alone — backward-sink gather (train.hpp:598-611) fused with the
  * unscale/cast/finite check of optimizer_step (train.hpp:619-629). */
 int samo_model_gather(samo_model* model, samo_stream_t stream);
+/* Backward sinks (the trainer's per-layer gradient sink, train.hpp:596-611):
+ * each writes one layer's compressed binary16 gradient (grad16) and raises
+ * the skip flag on a non-finite kept element, the moment the layer's
+ * gradient is produced.  Single-GPU models only (the data-parallel exchanges
+ * gather inside their fused step); follow the layers' sinks with
+ * samo_model_update.
+ *
+ * samo_model_sink_dense: K1 on one layer's tiles from its dense binary16
+ * gradient (dense_len elements, 16-byte aligned).
+ *
+ * samo_model_sink_dw: the layer's weight gradient dW = X^T . dY
+ * (mlp_backward, train.hpp:304-305; X [batch x in], dY [batch x out],
+ * binary16 row-major, 16-byte aligned, in and out multiples of 8,
+ * in * out == dense_len) computed on the tensor cores with the gather fused
+ * into the GEMM epilogue: the dense gradient never reaches HBM.  The result
+ * is bit-identical to samo_dw_gemm_f16 followed by samo_model_sink_dense. */
+int samo_model_sink_dense(samo_model* model, int layer, const uint16_t* dense_grad,
+                          samo_stream_t stream);
+int samo_model_sink_dw(samo_model* model, int layer, const uint16_t* x, const uint16_t* dy,
+                       uint64_t batch, uint64_t in, uint64_t out, samo_stream_t stream);
+
+/* Dense weight gradient dW[in x out] = X^T . dY as binary16 (tcgen05 tensor
+ * cores, fp32 accumulation, one rounding; matmul(transpose(x), dy) of
+ * tensor.hpp:88-105 up to the fp32 summation order). */
+int samo_dw_gemm_f16(const uint16_t* x, const uint16_t* dy, uint64_t batch, uint64_t in,
+                     uint64_t out, uint16_t* dw, samo_stream_t stream);
+
 /* Stage exchange alone (no-op without a communicator of size > 1). */
 int samo_model_exchange(samo_model* model, samo_stream_t stream);
 /* Stage K23 alone — skip decision, AdamScalars::advance, adam_update and

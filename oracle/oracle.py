@@ -91,6 +91,7 @@ class Oracle:
         lib.or_mt64_next.argtypes = [C.POINTER(MT64)]
         lib.or_mt64_uniform.argtypes = [C.POINTER(MT64), vp, u64, C.c_float]
         lib.or_dp_sum.argtypes = [vp, C.c_int, u64, vp, vp]
+        lib.or_dw_matmul.argtypes = [vp, vp, u64, u64, u64, vp]
 
     # half.hpp
     def f2h(self, x) -> np.ndarray:
@@ -193,6 +194,14 @@ class Oracle:
         self.lib.or_dp_sum(_ptr_array(bufs), len(bufs), n, _p(out), _p(a))
         return out, a
 
+    def dw_matmul(self, x: np.ndarray, dy: np.ndarray) -> np.ndarray:
+        """binary16 bits of matmul(transpose(x), dy) (tensor.hpp:88-105)."""
+        x = np.ascontiguousarray(x, dtype=np.uint16)
+        dy = np.ascontiguousarray(dy, dtype=np.uint16)
+        out = np.empty((x.shape[1], dy.shape[1]), dtype=np.uint16)
+        self.lib.or_dw_matmul(_p(x), _p(dy), x.shape[0], x.shape[1], dy.shape[1], _p(out))
+        return out
+
 
 class RefLib:
     """The reference itself (unmodified headers) behind extern "C"."""
@@ -227,6 +236,7 @@ class RefLib:
         lib.ref_session_check_invariants.argtypes = [vp]
         lib.ref_session_measured_bytes.restype = u64
         lib.ref_session_measured_bytes.argtypes = [vp, C.c_int]
+        lib.ref_dw_matmul.argtypes = [vp, vp, u64, u64, u64, vp]
 
     def f2h(self, x):
         x = np.ascontiguousarray(x, dtype=np.float32)
@@ -256,6 +266,13 @@ class RefLib:
         fn = self.lib.ref_expand_u16 if values.itemsize == 2 else self.lib.ref_expand_f32
         rc = fn(_p(values), values.size, _p(idx), idx.size,
                 numel if ind_dense_len is None else ind_dense_len, numel, _p(out))
+        return rc, out
+
+    def dw_matmul(self, x, dy):
+        x = np.ascontiguousarray(x, dtype=np.uint16)
+        dy = np.ascontiguousarray(dy, dtype=np.uint16)
+        out = np.empty((x.shape[1], dy.shape[1]), dtype=np.uint16)
+        rc = self.lib.ref_dw_matmul(_p(x), _p(dy), x.shape[0], x.shape[1], dy.shape[1], _p(out))
         return rc, out
 
     def adam_update(self, theta, m, v, g, cfg: Cfg, bias1, bias2):

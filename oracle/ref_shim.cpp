@@ -306,3 +306,23 @@ EXPORT uint64_t ref_session_measured_bytes(void* h, int peak) {
   return samo::measured_bytes(static_cast<RefSession*>(h)->trainer->state(),
                               peak ? samo::Accounting::peak : samo::Accounting::steady_state);
 }
+
+// mlp_backward's weight gradient (train.hpp:304): matmul(transpose(x), dy).
+EXPORT int ref_dw_matmul(const uint16_t* x, const uint16_t* dy, uint64_t batch, uint64_t in,
+                         uint64_t out, uint16_t* dw) {
+  try {
+    std::vector<samo::Half> xv(batch * in), dv(batch * out);
+    for (uint64_t i = 0; i < batch * in; ++i) xv[i] = samo::Half::from_bits(x[i]);
+    for (uint64_t i = 0; i < batch * out; ++i) dv[i] = samo::Half::from_bits(dy[i]);
+    const samo::Tensor<samo::Half> tx({static_cast<std::size_t>(batch), static_cast<std::size_t>(in)},
+                                      std::move(xv));
+    const samo::Tensor<samo::Half> td({static_cast<std::size_t>(batch), static_cast<std::size_t>(out)},
+                                      std::move(dv));
+    const auto w = samo::matmul(samo::transpose(tx), td);
+    const auto f = w.flat();
+    for (uint64_t i = 0; i < in * out; ++i) dw[i] = f[i].bits();
+    return 0;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}

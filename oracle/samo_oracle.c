@@ -364,3 +364,18 @@ EXPORT void or_dp_sum(const float* const* bufs, int G, uint64_t n, float* out, d
     if (abs_sum) abs_sum[i] = a;
   }
 }
+
+/* dW = matmul(transpose(x), dy) (train.hpp:304, tensor.hpp:88-105): exact
+ * half x half products, serial fp32 adds in ascending batch order, one
+ * rounding to binary16.  x [batch x in], dy [batch x out], dw [in x out]. */
+EXPORT void or_dw_matmul(const uint16_t* x, const uint16_t* dy, uint64_t batch, uint64_t in,
+                         uint64_t out, uint16_t* dw) {
+  for (uint64_t i = 0; i < in; ++i) {
+    for (uint64_t j = 0; j < out; ++j) {
+      float acc = 0.0f;
+      for (uint64_t b = 0; b < batch; ++b)
+        acc += or_half_to_float(x[b * in + i]) * or_half_to_float(dy[b * out + j]);
+      dw[i * out + j] = or_float_to_half(acc);
+    }
+  }
+}

@@ -75,7 +75,7 @@ class LayerDesc(C.Structure):
 class LayerView(C.Structure):
     _fields_ = [("theta16", vp), ("theta32", vp), ("adam_m", vp), ("adam_v", vp),
                 ("grad32", vp), ("indices", vp), ("dense_len", C.c_uint64),
-                ("nnz", C.c_uint64), ("k_offset", C.c_uint64)]
+                ("nnz", C.c_uint64), ("k_offset", C.c_uint64), ("grad16", vp)]
 
 
 class StepRecord(C.Structure):
@@ -131,6 +131,9 @@ _SIGS = {
     "samo_model_phase_times": (C.c_int, [vp, C.POINTER(C.c_float), C.c_int]),
     "samo_model_set_grads": (C.c_int, [vp, C.POINTER(vp), vp]),
     "samo_model_gather": (C.c_int, [vp, vp]),
+    "samo_model_sink_dense": (C.c_int, [vp, C.c_int, vp, vp]),
+    "samo_model_sink_dw": (C.c_int, [vp, C.c_int, vp, vp, C.c_uint64, C.c_uint64, C.c_uint64, vp]),
+    "samo_dw_gemm_f16": (C.c_int, [vp, vp, C.c_uint64, C.c_uint64, C.c_uint64, vp, vp]),
     "samo_model_exchange": (C.c_int, [vp, vp]),
     "samo_model_update": (C.c_int, [vp, vp]),
     "samo_model_step": (C.c_int, [vp, vp]),

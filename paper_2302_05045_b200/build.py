@@ -19,7 +19,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libsamo_cuda.so"
-SOURCES = ["abi.cu", "kernels_step.cu", "kernels_fused.cu", "kernels_prune.cu"]
+SOURCES = ["abi.cu", "kernels_step.cu", "kernels_fused.cu", "kernels_prune.cu", "kernels_gemm.cu"]
 HEADERS = ["common.cuh", "kernels.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -72,12 +72,6 @@ int num_sms() {
 
 using namespace samo_dev;
 
-#define SAMO_TRY(expr)             \
-  do {                             \
-    int rc_ = (expr);              \
-    if (rc_ != SAMO_OK) return rc_; \
-  } while (0)
-
 static int clear_ok() {
   g_last_error.clear();
   return SAMO_OK;
@@ -485,6 +479,11 @@ struct samo_model {
   ShardPlan shard_plan;
   ShardPlan p2p_plan;                   // pipelined peer-to-peer step
   SamoPeerSlots* slots = nullptr;       // this rank's signal area (in the block)
+  // Backward sinks: first tile of every layer; per-layer row/column-block k
+  // tables of the fused dW sink (built on first use).
+  std::vector<uint32_t> layer_t;
+  std::vector<uint32_t*> dw_kb;
+  std::vector<uint64_t> dw_kb_in;
   // Peer mappings of the other ranks' model blocks (CUDA IPC) for the fused
   // peer-to-peer exchange; p2p_ok is agreed by every rank.
   void* peer_base[kMaxP2PRanks] = {};
@@ -764,6 +763,8 @@ int samo_model_destroy(samo_model* md) {
   for (auto e : md->ev_sh) cudaEventDestroy(e);
   for (auto e : md->phase_ev)
     if (e) cudaEventDestroy(e);
+  for (auto p : md->dw_kb)
+    if (p) cudaFree(p);
   if (md->block) cudaFree(md->block);
   delete md;
   return clear_ok();
@@ -780,6 +781,7 @@ int samo_model_layer_view(const samo_model* md, int l, samo_layer_view* out) {
   out->adam_m = md->m + k;
   out->adam_v = md->v + k;
   out->grad32 = md->g + k;
+  out->grad16 = reinterpret_cast<uint16_t*>(md->g) + k;
   out->indices = md->idx + k;
   out->dense_len = md->dense_len[l];
   out->nnz = md->nnz[l];
@@ -1451,6 +1453,82 @@ int samo_model_exchange(samo_model* md, samo_stream_t stream) {
     // (the zero padding in between is noise-free and < 1024 elements).
     SAMO_TRY(samo_allreduce_sum_f32(md->comm, md->g, md->n_al + kFlagOff + 1, stream));
   }
+  return clear_ok();
+}
+
+static int sink_ready(samo_model* md, int l) {
+  SAMO_TRY(step_ready(md));
+  if (l < 0 || l >= md->nlayers) return fail(SAMO_E_INDEX, "layer %d out of range", l);
+  if (comm_size(md) > 1)
+    return fail(SAMO_E_STATE, "backward sinks need a single-GPU model (the exchanges gather in their step)");
+  if (md->layer_t.empty()) {
+    md->layer_t.assign(md->nlayers + 1, md->ntiles);
+    for (uint32_t t = md->ntiles; t-- > 0;) md->layer_t[md->tiles_host[t].layer] = t;
+    for (int q = md->nlayers - 1; q >= 0; --q)  // layers without tiles
+      md->layer_t[q] = std::min(md->layer_t[q], md->layer_t[q + 1]);
+  }
+  return SAMO_OK;
+}
+
+int samo_model_sink_dense(samo_model* md, int l, const uint16_t* grad, samo_stream_t stream) {
+  SAMO_TRY(sink_ready(md, l));
+  if (!grad) return fail(SAMO_E_PARAMETER, "layer %d: null gradient pointer", l);
+  if (reinterpret_cast<uintptr_t>(grad) % 16)
+    return fail(SAMO_E_PARAMETER, "layer %d: gradient pointer must be 16-byte aligned", l);
+  md->layers_host[l].grad = grad;
+  SAMO_CUDA_TRY(cudaMemcpyAsync(md->layers_dev + l, &md->layers_host[l], sizeof(SamoLayerDev),
+                                cudaMemcpyHostToDevice, as_stream(stream)));
+  StepArgs a = step_args(md);
+  a.tiles = md->tiles + md->layer_t[l];
+  a.ntiles = md->layer_t[l + 1] - md->layer_t[l];
+  if (a.ntiles) SAMO_TRY(launch_gather(a, false, std::min<int>(md->grid_gather16, a.ntiles), as_stream(stream)));
+  return clear_ok();
+}
+
+int samo_model_sink_dw(samo_model* md, int l, const uint16_t* x, const uint16_t* dy, uint64_t batch,
+                       uint64_t in, uint64_t out, samo_stream_t stream) {
+  SAMO_TRY(sink_ready(md, l));
+  SAMO_TRY(dw_check(batch, in, out, x, dy));
+  if (in * out != md->dense_len[l])
+    return fail(SAMO_E_DIMENSION, "layer %d: in x out = %llu, dense_len = %llu", l,
+                static_cast<unsigned long long>(in * out), static_cast<unsigned long long>(md->dense_len[l]));
+  cudaStream_t s = as_stream(stream);
+  if (md->dw_kb.empty()) {
+    md->dw_kb.assign(md->nlayers, nullptr);
+    md->dw_kb_in.assign(md->nlayers, 0);
+  }
+  if (!md->dw_kb[l] || md->dw_kb_in[l] != in) {
+    if (md->dw_kb[l]) cudaFree(md->dw_kb[l]);
+    md->dw_kb[l] = nullptr;
+    const uint64_t entries = (dw_col_blocks(out) + 1ull) * in;
+    SAMO_CUDA_TRY(cudaMalloc(&md->dw_kb[l], entries * sizeof(uint32_t)));
+    md->dw_kb_in[l] = in;
+    SAMO_TRY(launch_build_rowblocks(md->idx + md->k_off[l], md->nnz[l], in, out, md->dw_kb[l], s));
+  }
+  DwArgs a{};
+  a.M = in;
+  a.N = out;
+  a.K = batch;
+  a.idx = md->idx + md->k_off[l];
+  a.kb = md->dw_kb[l];
+  a.g16 = reinterpret_cast<uint16_t*>(md->g) + md->k_off[l];
+  a.flag = flag_ptr(md);
+  SAMO_TRY(launch_dw_gemm(x, dy, a, 1, s));
+  return clear_ok();
+}
+
+int samo_dw_gemm_f16(const uint16_t* x, const uint16_t* dy, uint64_t batch, uint64_t in, uint64_t out,
+                     uint16_t* dw, samo_stream_t stream) {
+  SAMO_TRY(device_ok());
+  SAMO_TRY(dw_check(batch, in, out, x, dy));
+  if (!dw) return fail(SAMO_E_PARAMETER, "dW GEMM: null output");
+  if (reinterpret_cast<uintptr_t>(dw) % 16) return fail(SAMO_E_PARAMETER, "dW GEMM: output must be 16-byte aligned");
+  DwArgs a{};
+  a.M = in;
+  a.N = out;
+  a.K = batch;
+  a.dw = dw;
+  SAMO_TRY(launch_dw_gemm(x, dy, a, 0, as_stream(stream)));
   return clear_ok();
 }
 

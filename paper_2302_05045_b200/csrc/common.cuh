@@ -29,6 +29,12 @@ int device_ok();  // SAMO_OK when a CUDA device is usable, else SAMO_E_CUDA
     if (e_ != cudaSuccess) return ::samo_dev::cuda_fail(e_, #expr); \
   } while (0)
 
+#define SAMO_TRY(expr)              \
+  do {                              \
+    int rc_ = (expr);               \
+    if (rc_ != SAMO_OK) return rc_; \
+  } while (0)
+
 #define SAMO_LAUNCH_CHECK(what)                                       \
   do {                                                                \
     cudaError_t e_ = cudaGetLastError();                              \

@@ -135,6 +135,23 @@ int expand_grid(uint32_t tile_elems);
 int launch_build_off16(const SamoTile* tiles, uint32_t ntiles, const uint32_t* idx,
                        uint16_t* off16, cudaStream_t s);
 
+// Weight-gradient GEMM dW[M x N] = X^T . dY, X [K x M], dY [K x N] binary16
+// row-major (kernels_gemm.cu).  epi 0: dense binary16 dW; epi 1: gather of
+// the kept elements into g16 (layer-local k) + skip flag.
+struct DwArgs {
+  uint64_t M, N, K;      // in, out, batch
+  uint16_t* dw;          // epi 0
+  const uint32_t* idx;   // epi 1: layer's ascending kept indices
+  const uint32_t* kb;    // epi 1: [(col blocks + 1) x M] row/column-block k starts
+  uint16_t* g16;         // epi 1: layer's compressed binary16 gradient
+  float* flag;           // epi 1: skip indicator
+};
+int dw_check(uint64_t batch, uint64_t in, uint64_t out, const void* x, const void* dy);
+uint32_t dw_col_blocks(uint64_t out);
+int launch_build_rowblocks(const uint32_t* idx, uint64_t n, uint64_t in, uint64_t out, uint32_t* kb,
+                           cudaStream_t s);
+int launch_dw_gemm(const uint16_t* x, const uint16_t* dy, const DwArgs& a, int epi, cudaStream_t s);
+
 template <int MODE, typename OutT>
 int launch_expand(const ExpandArgs& a, int grid, cudaStream_t s);
 template <int MODE, typename OutT>

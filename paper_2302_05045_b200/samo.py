@@ -134,6 +134,18 @@ def compress(dense: torch.Tensor, ind: PrunedIndexSet) -> torch.Tensor:
     return out
 
 
+def dw_gemm(x: torch.Tensor, dy: torch.Tensor) -> torch.Tensor:
+    """Dense weight gradient x^T . dy as binary16 (tcgen05, fp32 accumulate):
+    matmul(transpose(x), dy) of tensor.hpp:88-105 up to summation order."""
+    _require_cuda(x, dy)
+    if x.dim() != 2 or dy.dim() != 2 or x.shape[0] != dy.shape[0]:
+        raise DimensionError("dw_gemm expects x [batch, in] and dy [batch, out]")
+    x, dy = _bits16(x).contiguous(), _bits16(dy).contiguous()
+    out = torch.empty((x.shape[1], dy.shape[1]), dtype=x.dtype, device=x.device)
+    _abi.call("samo_dw_gemm_f16", _vp(x), _vp(dy), x.shape[0], x.shape[1], dy.shape[1], _vp(out), _stream())
+    return out
+
+
 def expand(values: torch.Tensor, ind: PrunedIndexSet, shape: Sequence[int]) -> torch.Tensor:
     """expand<T> (store.hpp:72-87): zeros except out.flat[ind.indices[k]] = values[k]."""
     _require_cuda(values, ind.indices)
@@ -270,6 +282,7 @@ class SamoModel:
         _abi.call("samo_model_create", descs, len(self.layers), int(tile_elems), C.byref(h))
         self._h = h
         self._grads_keepalive: list[torch.Tensor] = []
+        self._sink_keepalive: list[torch.Tensor] = []
 
     # -- construction ------------------------------------------------------
     @classmethod
@@ -365,11 +378,34 @@ class SamoModel:
     def gather(self) -> None:
         _abi.call("samo_model_gather", self._h, _stream())
 
+    def sink_dense(self, layer: int, grad: torch.Tensor) -> None:
+        """Backward sink (train.hpp:596-611) of one layer's dense binary16
+        gradient: K1 on that layer only.  Single-GPU models."""
+        _require_cuda(grad)
+        _bits16(grad)
+        if grad.numel() != self.layers[layer].dense_len:
+            raise DimensionError(f"{self.layers[layer].layer_id}: gradient length does not match layer")
+        _abi.call("samo_model_sink_dense", self._h, layer, _vp(grad), _stream())
+        self._sink_keepalive.append(grad)
+
+    def sink_dw(self, layer: int, x: torch.Tensor, dy: torch.Tensor) -> None:
+        """Fused backward sink: dW = x^T . dy (mlp_backward, train.hpp:304-305)
+        on the tensor cores with the gather in the GEMM epilogue; x [batch, in],
+        dy [batch, out] binary16."""
+        _require_cuda(x, dy)
+        if x.dim() != 2 or dy.dim() != 2 or x.shape[0] != dy.shape[0]:
+            raise DimensionError("sink_dw expects x [batch, in] and dy [batch, out]")
+        x, dy = _bits16(x).contiguous(), _bits16(dy).contiguous()
+        _abi.call("samo_model_sink_dw", self._h, layer, _vp(x), _vp(dy), x.shape[0], x.shape[1],
+                  dy.shape[1], _stream())
+        self._sink_keepalive.extend((x, dy))
+
     def exchange(self) -> None:
         _abi.call("samo_model_exchange", self._h, _stream())
 
     def update(self) -> None:
         _abi.call("samo_model_update", self._h, _stream())
+        self._sink_keepalive = []  # stream-ordered: later allocations reuse safely
 
     def step(self, graph: bool = False) -> None:
         """gather + exchange + Adam/downcast/expand; device-resident, async."""
@@ -422,6 +458,7 @@ class SamoModel:
         model = cls.__new__(cls)
         model._h = h
         model._grads_keepalive = []
+        model._sink_keepalive = []
         n = int(_abi.load().samo_model_num_layers(h))
         if layers is None:
             layers = []
@@ -434,7 +471,8 @@ class SamoModel:
 
     _FIELDS = {"theta16": (torch.float16, "dense"), "theta32": (torch.float32, "nnz"),
                "adam_m": (torch.float32, "nnz"), "adam_v": (torch.float32, "nnz"),
-               "grad32": (torch.float32, "nnz"), "indices": (torch.int32, "nnz")}
+               "grad32": (torch.float32, "nnz"), "indices": (torch.int32, "nnz"),
+               "grad16": (torch.float16, "nnz")}
 
     def read(self, layer: int, name: str) -> torch.Tensor:
         """Copy of one per-layer buffer (device tensor)."""

@@ -202,3 +202,18 @@ def test_dp_sum_order(oracle):
     s, absum = oracle.dp_sum([a, b])
     assert s.tolist() == [np.float32(1e8) + np.float32(1.0), np.float32(1.0) + np.float32(1e8), 0.0]
     assert absum.tolist() == [1e8 + 1, 1e8 + 1, 2.0]
+
+
+@pytest.mark.parametrize("batch,n_in,n_out", [(1, 8, 8), (64, 24, 40), (576, 16, 32), (7, 3, 5)])
+def test_dw_matmul_matches_reference(oracle, batch, n_in, n_out):
+    """The oracle's restatement of matmul(transpose(x), dy) (train.hpp:304,
+    tensor.hpp:88-105) equals the reference library bit for bit."""
+    from oracle.oracle import REF_SO, RefLib
+    if not REF_SO.exists():
+        pytest.skip("reference library not built")
+    rng = np.random.default_rng(batch + n_in)
+    x = oracle.f2h(rng.uniform(-1, 1, batch * n_in).astype(np.float32)).reshape(batch, n_in)
+    dy = oracle.f2h((rng.uniform(-1, 1, batch * n_out) * 1024 / batch).astype(np.float32)).reshape(batch, n_out)
+    rc, want = RefLib().dw_matmul(x, dy)
+    assert rc == 0
+    assert np.array_equal(oracle.dw_matmul(x, dy), want)
