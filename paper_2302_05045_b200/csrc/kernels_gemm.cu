@@ -15,12 +15,13 @@
 // EPI 1 is bit-identical to EPI 0 followed by the K1 gather.
 //
 // Operands: X [batch x in] and dY [batch x out], row-major binary16, so both
-// are MN-major for a contraction over the batch.  Tile 128 x BN x 64, NS-stage
-// TMA ring (128-byte swizzle, two or more 64-element boxes per operand),
-// one CTA per output tile:
+// are MN-major for a contraction over the batch.  Tile 128 x 256 x 64, 3-stage
+// TMA ring (128-byte swizzle, 64-element boxes), persistent CTAs with the
+// accumulator double-buffered in TMEM:
 //   warp 0      TMA producer (one lane)
 //   warp 1      TMEM allocation + MMA issue (one lane), tcgen05.commit
-//   warps 2..5  epilogue: tcgen05.ld (32 lanes x 32 columns per load)
+//   warps 2..5  epilogue: tcgen05.ld (32 lanes x 32 columns per load), in two
+//               128-column halves staged through shared memory
 #include "kernels.cuh"
 
 #include <cuda.h>
@@ -112,38 +113,69 @@ __device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity
   }
 }
 
+// OR over the 128 epilogue threads (named barrier 1); also orders the
+// staging buffer's reads before the next pass overwrites it.
+__device__ __forceinline__ int __syncthreads_or_named(uint32_t pred) {
+  uint32_t out;
+  asm volatile(
+      "{\n.reg .pred p, q;\nsetp.ne.u32 p, %1, 0;\nbar.red.or.pred q, 1, 128, p;\nselp.u32 %0, 1, 0, q;\n}\n"
+      : "=r"(out)
+      : "r"(pred)
+      : "memory");
+  return static_cast<int>(out);
+}
+
+// Shared memory: the epilogue staging half-tile (128 rows x 128 columns,
+// padded rows) first, then the NS-stage operand ring (1024-byte aligned for
+// the 128-byte swizzle atoms).
 template <int BN, int NS>
 struct GemmSmem {
   static constexpr uint32_t kA = kBM * kBK * 2;    // two 64(M) x 64(K) boxes
   static constexpr uint32_t kB = BN * kBK * 2;     // BN/64 boxes
   static constexpr uint32_t kStage = kA + kB;
-  static constexpr uint32_t kTileLd = BN + 8;      // epilogue tile row (halves), padded
+  static constexpr uint32_t kHalf = 128;           // epilogue columns per pass (= kb table granularity)
+  static constexpr uint32_t kTileLd = kHalf + 8;   // halves per staging row (16-byte multiple)
   static constexpr uint32_t kTile = kBM * kTileLd * 2;
-  static constexpr uint32_t kBytes = 1024 /* alignment slack */ + NS * kStage + kTile;
+  static_assert(kTile % 1024 == 0, "stages must stay 1024-byte aligned");
+  static constexpr uint32_t kBytes = kTile + NS * kStage;
 };
 
+// Persistent: CTA b takes output tiles b, b + grid, ... (M-block fastest, so
+// concurrent CTAs share dY column blocks in L2).  The accumulator is double
+// buffered in TMEM (2 x BN columns): the epilogue of tile i overlaps the
+// mainloop of tile i + 1.
 template <int EPI, int BN, int NS>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_dw_gemm(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tdy, DwArgs a) {
   using L = GemmSmem<BN, NS>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[NS];
   __shared__ __align__(8) uint64_t empty[NS];
-  __shared__ __align__(8) uint64_t accf;
+  __shared__ __align__(8) uint64_t accf[2];
+  __shared__ __align__(8) uint64_t acce[2];
   __shared__ uint32_t tmem_slot;
+  __shared__ uint32_t s_off[kBM + 1];  // epilogue: exclusive scan of kept counts per row
+  __shared__ uint32_t s_ks[kBM];       // epilogue: first k of each row in the column half
+  __shared__ uint32_t s_wsum[4];
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t m0 = blockIdx.x * kBM, n0 = blockIdx.y * BN;
   const uint32_t nk = static_cast<uint32_t>((a.K + kBK - 1) / kBK);
-  constexpr uint32_t kCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  const uint32_t mt = static_cast<uint32_t>((a.M + kBM - 1) / kBM);
+  const uint32_t ntiles = mt * static_cast<uint32_t>((a.N + BN - 1) / BN);
+  constexpr uint32_t kCols = 2 * BN;  // two accumulator buffers
+  static_assert(kCols == 256 || kCols == 512, "TMEM allocation must be a power of two");
+  uint8_t* ring = smem + L::kTile;
+  if (threadIdx.x == 0 && (smem_addr(ring) & 1023u)) __trap();  // swizzle atoms need 1024-byte alignment
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(&accf, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&accf[b], 1);
+      mbar_init(&acce[b], 4);  // one arrive per epilogue warp
+    }
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -160,92 +192,154 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer
-      for (uint32_t kb = 0; kb < nk; ++kb) {
-        const uint32_t s = kb % NS;
-        if (kb >= static_cast<uint32_t>(NS)) mbar_wait_bounded(&empty[s], ((kb / NS) - 1) & 1u);
-        uint8_t* st = smem + s * L::kStage;
-        mbar_arrive_expect_tx(&full[s], L::kStage);  // out-of-bounds box parts are zero-filled and counted
-        const int kc = static_cast<int>(kb * kBK);
-        tma_load_2d(st, &tx, static_cast<int>(m0), kc, &full[s]);
-        tma_load_2d(st + 8192, &tx, static_cast<int>(m0 + 64), kc, &full[s]);
+      uint32_t g = 0;
+      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int m0 = static_cast<int>((t % mt) * kBM), n0 = static_cast<int>((t / mt) * BN);
+        for (uint32_t kb = 0; kb < nk; ++kb, ++g) {
+          const uint32_t s = g % NS;
+          if (g >= static_cast<uint32_t>(NS)) mbar_wait_bounded(&empty[s], ((g / NS) - 1) & 1u);
+          uint8_t* st = ring + s * L::kStage;
+          mbar_arrive_expect_tx(&full[s], L::kStage);  // out-of-bounds box parts are zero-filled and counted
+          const int kc = static_cast<int>(kb * kBK);
+          tma_load_2d(st, &tx, m0, kc, &full[s]);
+          tma_load_2d(st + 8192, &tx, m0 + 64, kc, &full[s]);
 #pragma unroll
-        for (int c = 0; c < BN / 64; ++c)
-          tma_load_2d(st + L::kA + c * 8192, &tdy, static_cast<int>(n0 + 64 * c), kc, &full[s]);
+          for (int c = 0; c < BN / 64; ++c) tma_load_2d(st + L::kA + c * 8192, &tdy, n0 + 64 * c, kc, &full[s]);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issue
       constexpr uint32_t idesc = umma_idesc<BN>();
-      for (uint32_t kb = 0; kb < nk; ++kb) {
-        const uint32_t s = kb % NS;
-        mbar_wait_bounded(&full[s], (kb / NS) & 1u);
+      uint32_t g = 0, i = 0;
+      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        const uint32_t buf = i & 1u;
+        if (i >= 2) mbar_wait_bounded(&acce[buf], ((i >> 1) - 1) & 1u);  // epilogue drained this buffer
         tc_fence_after();
-        const uint32_t sa = smem_addr(smem + s * L::kStage), sb = sa + L::kA;
+        const uint32_t acc = tmem + buf * BN;
+        for (uint32_t kb = 0; kb < nk; ++kb, ++g) {
+          const uint32_t s = g % NS;
+          mbar_wait_bounded(&full[s], (g / NS) & 1u);
+          tc_fence_after();
+          const uint32_t sa = smem_addr(ring + s * L::kStage), sb = sa + L::kA;
 #pragma unroll
-        for (uint32_t j = 0; j < kBK / 16; ++j) {  // UMMA_K = 16: 16 K-rows of 128 bytes
-          const uint64_t da = umma_desc_mn_sw128(sa + j * 2048, 8192, 1024);
-          const uint64_t db = umma_desc_mn_sw128(sb + j * 2048, 8192, 1024);
-          umma_f16(tmem, da, db, idesc, (kb | j) != 0u);
+          for (uint32_t j = 0; j < kBK / 16; ++j) {  // UMMA_K = 16: 16 K-rows of 128 bytes
+            const uint64_t da = umma_desc_mn_sw128(sa + j * 2048, 8192, 1024);
+            const uint64_t db = umma_desc_mn_sw128(sb + j * 2048, 8192, 1024);
+            umma_f16(acc, da, db, idesc, (kb | j) != 0u);
+          }
+          umma_commit(&empty[s]);  // frees the stage once these MMAs have read it
         }
-        umma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+        umma_commit(&accf[buf]);   // accumulator of this tile complete
       }
-      umma_commit(&accf);        // accumulator complete
     }
   } else {
-    // ---- epilogue: warp w reads TMEM lanes 32*(w % 4) .. +31 (= tile rows)
+    // ---- epilogue (warps 2..5): warp w reads TMEM lanes 32*(w % 4) .. +31
     const uint32_t q = warp & 3u;
     const uint32_t r = q * 32 + lane;  // tile row of this thread
-    const uint64_t i = m0 + r;         // dW row
-    mbar_wait_bounded(&accf, 0);
-    tc_fence_after();
-    uint16_t* tile = reinterpret_cast<uint16_t*>(smem + NS * L::kStage);
+    const uint32_t tid = threadIdx.x - 64;
+    uint16_t* tile = reinterpret_cast<uint16_t*>(smem);
+    uint32_t i = 0;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      const uint32_t buf = i & 1u;
+      const uint64_t m0 = static_cast<uint64_t>(t % mt) * kBM;
+      const uint32_t nb = t / mt;
+      const uint64_t row = m0 + r;
+      mbar_wait_bounded(&accf[buf], (i >> 1) & 1u);
+      tc_fence_after();
 #pragma unroll 1
-    for (uint32_t c = 0; c < static_cast<uint32_t>(BN); c += 32) {
-      uint32_t v[32];
-      tmem_ld32(tmem + ((q * 32u) << 16) + c, v);
-      uint32_t h[16];
-#pragma unroll
-      for (int e = 0; e < 16; ++e)
-        h[e] = f32_to_f16_bits(__uint_as_float(v[2 * e])) |
-               (f32_to_f16_bits(__uint_as_float(v[2 * e + 1])) << 16);
-      if constexpr (EPI == 0) {
-        const uint64_t n = n0 + c;
-        if (i < a.M && n < a.N) {
-          uint16_t* dst = a.dw + i * a.N + n;
-          if (n + 32 <= a.N) {
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              reinterpret_cast<uint4*>(dst)[e] = make_uint4(h[4 * e], h[4 * e + 1], h[4 * e + 2], h[4 * e + 3]);
-          } else {
-            for (uint32_t e = 0; e < a.N - n; ++e) dst[e] = static_cast<uint16_t>(h[e >> 1] >> ((e & 1) * 16));
+      for (uint32_t h = 0; h < BN / L::kHalf; ++h) {
+        const uint64_t nh = static_cast<uint64_t>(nb) * BN + h * L::kHalf;  // first column of this half
+        uint32_t ks = 0, cnt = 0;
+        if constexpr (EPI == 1) {  // this row's kept range in the column half (kb: 128-column blocks)
+          if (row < a.M && nh < a.N) {
+            const uint64_t cb = nh / L::kHalf;
+            ks = a.kb[cb * a.M + row];
+            cnt = a.kb[(cb + 1) * a.M + row] - ks;
           }
         }
-      } else {
-        uint4* dst = reinterpret_cast<uint4*>(tile + r * L::kTileLd + c);
+        // accumulator half -> binary16 -> staging row r
+#pragma unroll 1
+        for (uint32_t c = 0; c < L::kHalf; c += 32) {
+          uint32_t v[32];
+          tmem_ld32(tmem + ((q * 32u) << 16) + buf * BN + h * L::kHalf + c, v);
+          uint4* dst = reinterpret_cast<uint4*>(tile + r * L::kTileLd + c);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) dst[e] = make_uint4(h[4 * e], h[4 * e + 1], h[4 * e + 2], h[4 * e + 3]);
-      }
-    }
-    if constexpr (EPI == 1) {
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      // Gather: warp e handles tile rows e, e + 4, ...; the row's kept
-      // elements in this column block are the contiguous arena range
-      // [kb[y][i], kb[y+1][i]) (indices ascending).
-      const uint32_t e = warp - 2;
-      uint32_t bad = 0;
-      for (uint32_t rr = e; rr < kBM; rr += 4) {
-        const uint64_t row = m0 + rr;
-        if (row >= a.M) break;
-        const uint32_t ks = a.kb[static_cast<uint64_t>(blockIdx.y) * a.M + row];
-        const uint32_t ke = a.kb[static_cast<uint64_t>(blockIdx.y + 1) * a.M + row];
-        const uint32_t base = static_cast<uint32_t>(row * a.N) + n0;
-        for (uint32_t k = ks + lane; k < ke; k += 32) {
-          const uint16_t hv = tile[rr * L::kTileLd + (a.idx[k] - base)];
-          a.g16[k] = hv;
-          bad |= (hv & 0x7C00u) == 0x7C00u;
+          for (int e = 0; e < 4; ++e) {
+            uint32_t w[4];
+#pragma unroll
+            for (int z = 0; z < 4; ++z)
+              w[z] = f32_to_f16_bits(__uint_as_float(v[8 * e + 2 * z])) |
+                     (static_cast<uint32_t>(f32_to_f16_bits(__uint_as_float(v[8 * e + 2 * z + 1]))) << 16);
+            dst[e] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+        }
+        if (h + 1 == BN / L::kHalf) {  // TMEM buffer drained: the MMA warp may reuse it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&acce[buf]);
+        }
+        if constexpr (EPI == 1) {
+          // exclusive scan of the per-row counts over the 128 rows
+          uint32_t x = cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (lane >= static_cast<uint32_t>(o)) x += y;
+          }
+          if (lane == 31) s_wsum[q] = x;
+          s_ks[r] = ks;
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          uint32_t base = 0;
+          for (uint32_t w = 0; w < q; ++w) base += s_wsum[w];
+          s_off[r] = base + x - cnt;
+          if (r == kBM - 1) s_off[kBM] = base + x;
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          const uint32_t total = s_off[kBM];
+          const uint32_t colbase = static_cast<uint32_t>(nh);
+          uint32_t bad = 0;
+          for (uint32_t f0 = 0; f0 < total; f0 += 4 * 128) {
+            uint32_t kk[4], rr[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const uint32_t f = f0 + u * 128 + tid;
+              uint32_t lo = 0, hi = kBM;  // last row with s_off[row] <= f
+              while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (s_off[mid] <= f) lo = mid; else hi = mid;
+              }
+              rr[u] = lo;
+              kk[u] = f < total ? s_ks[lo] + (f - s_off[lo]) : 0xFFFFFFFFu;
+            }
+            uint32_t ix[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) ix[u] = kk[u] != 0xFFFFFFFFu ? __ldg(a.idx + kk[u]) : 0u;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (kk[u] == 0xFFFFFFFFu) continue;
+              const uint32_t col = ix[u] - static_cast<uint32_t>((m0 + rr[u]) * a.N) - colbase;
+              const uint16_t hv = tile[rr[u] * L::kTileLd + col];
+              a.g16[kk[u]] = hv;
+              bad |= (hv & 0x7C00u) == 0x7C00u;
+            }
+          }
+          if (__syncthreads_or_named(bad)) {
+            if (tid == 0) atomicAdd(a.flag, 1.0f);
+          }
+        } else {
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          // coalesced copy-out of the staged half: warp q writes rows q, q + 4, ...
+          for (uint32_t rr = q; rr < kBM; rr += 4) {
+            const uint64_t grow = m0 + rr;
+            const uint64_t col = nh + lane * 4;
+            if (grow < a.M && col < a.N) {
+              const uint2 v = *reinterpret_cast<const uint2*>(tile + rr * L::kTileLd + lane * 4);
+              *reinterpret_cast<uint2*>(a.dw + grow * a.N + col) = v;
+            }
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
         }
       }
-      if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicAdd(a.flag, 1.0f);
     }
   }
   __syncwarp();
@@ -299,8 +393,9 @@ int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) {
   return SAMO_OK;
 }
 
-constexpr int kGemmBN = 128;
-constexpr int kGemmNS = 4;
+constexpr int kGemmBN = 256;
+constexpr int kGemmNS = 3;
+constexpr uint32_t kKbCols = 128;  // column granularity of the row/column-block k table
 
 }  // namespace
 
@@ -317,14 +412,14 @@ int dw_check(uint64_t batch, uint64_t in, uint64_t out, const void* x, const voi
   return SAMO_OK;
 }
 
-uint32_t dw_col_blocks(uint64_t out) { return static_cast<uint32_t>((out + kGemmBN - 1) / kGemmBN); }
+uint32_t dw_col_blocks(uint64_t out) { return static_cast<uint32_t>((out + kKbCols - 1) / kKbCols); }
 
 int launch_build_rowblocks(const uint32_t* idx, uint64_t n, uint64_t in, uint64_t out, uint32_t* kb,
                            cudaStream_t s) {
   const uint32_t nb = dw_col_blocks(out);
   const uint64_t total = (nb + 1ull) * in;
   const int grid = static_cast<int>((total + 255) / 256);
-  k_build_rowblocks<<<grid, 256, 0, s>>>(idx, n, in, out, kGemmBN, nb, kb);
+  k_build_rowblocks<<<grid, 256, 0, s>>>(idx, n, in, out, kKbCols, nb, kb);
   SAMO_LAUNCH_CHECK("k_build_rowblocks");
   return SAMO_OK;
 }
@@ -333,8 +428,8 @@ int launch_dw_gemm(const uint16_t* x, const uint16_t* dy, const DwArgs& a, int e
   CUtensorMap tx, tdy;
   SAMO_TRY(make_map(&tx, x, a.K, a.M));
   SAMO_TRY(make_map(&tdy, dy, a.K, a.N));
-  const dim3 grid(static_cast<unsigned>((a.M + kBM - 1) / kBM), dw_col_blocks(a.N));
-  if (grid.y > 65535) return fail(SAMO_E_DIMENSION, "dW GEMM: too many column blocks");
+  const uint64_t tiles = ((a.M + kBM - 1) / kBM) * ((a.N + kGemmBN - 1) / kGemmBN);
+  const int grid = static_cast<int>(std::min<uint64_t>(tiles, static_cast<uint64_t>(num_sms())));
   constexpr uint32_t smem = GemmSmem<kGemmBN, kGemmNS>::kBytes;
   if (epi == 0) {
     auto fn = k_dw_gemm<0, kGemmBN, kGemmNS>;

@@ -1,0 +1,81 @@
+"""Weight-gradient GEMM + backward sink timings (1 GPU), one JSON line per shape.
+
+    python tools/bench_dw.py [--p 0.9] [--reps 20]
+
+For each (batch, in, out): our tcgen05 dW GEMM (dense binary16 out), cuBLAS
+via torch.matmul(x.T, dy) for reference, the unfused sink (dense dW GEMM ->
+K1 on the layer) and the fused sink (GEMM with the gather in its epilogue).
+CUDA events, inputs resident in HBM, median of --reps after 3 warm-ups.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import statistics
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_2302_05045_b200 import samo  # noqa: E402
+
+SHAPES = [  # (batch tokens, in, out)
+    (576, 4096, 4096),      # config 2's largest FC layer at batch 576
+    (4096, 2560, 10240),    # GPT-2.7B MLP up
+    (4096, 10240, 2560),    # GPT-2.7B MLP down
+    (4096, 2560, 7680),     # GPT-2.7B attention qkv
+    (4096, 2560, 2560),     # GPT-2.7B attention out
+    (8192, 2560, 10240),
+]
+
+
+def timed(fn, reps):
+    for _ in range(3):
+        fn()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--p", type=float, default=0.9)
+    ap.add_argument("--reps", type=int, default=20)
+    args = ap.parse_args()
+    torch.manual_seed(0)
+    for batch, n_in, n_out in SHAPES:
+        x = (torch.rand(batch, n_in, device="cuda") * 2 - 1).half()
+        dy = ((torch.rand(batch, n_out, device="cuda") * 2 - 1) * 4).half()
+        n = n_in * n_out
+        keep = int(round((1 - args.p) * n))
+        idx = torch.randperm(n, device="cuda")[:keep].sort().values.to(torch.int32)
+        m = samo.SamoModel.from_index_sets([samo.PrunedIndexSet("fc.weight", n, idx)], [(n_in, n_out)], 0)
+        m.init_layer(0, torch.zeros(n, device="cuda"))
+        flops = 2.0 * batch * n_in * n_out
+        t_ours = timed(lambda: samo.dw_gemm(x, dy), args.reps)
+        t_cublas = timed(lambda: torch.matmul(x.t(), dy), args.reps)
+        dense = samo.dw_gemm(x, dy).reshape(-1)
+        t_k1 = timed(lambda: m.sink_dense(0, dense), args.reps)
+        t_unfused = timed(lambda: (m.sink_dense(0, samo.dw_gemm(x, dy).reshape(-1))), args.reps)
+        t_fused = timed(lambda: m.sink_dw(0, x, dy), args.reps)
+        m._sink_keepalive.clear()
+        print(json.dumps({
+            "batch": batch, "in": n_in, "out": n_out, "p": args.p,
+            "dw_gemm_ms": round(t_ours, 4), "dw_gemm_tflops": round(flops / t_ours / 1e9, 1),
+            "cublas_ms": round(t_cublas, 4), "cublas_tflops": round(flops / t_cublas / 1e9, 1),
+            "k1_layer_ms": round(t_k1, 4),
+            "unfused_sink_ms": round(t_unfused, 4), "fused_sink_ms": round(t_fused, 4),
+            "fused_saving": round(1 - t_fused / t_unfused, 3),
+        }), flush=True)
+        del m
+
+
+if __name__ == "__main__":
+    main()
