@@ -15,13 +15,17 @@
 // EPI 1 is bit-identical to EPI 0 followed by the K1 gather.
 //
 // Operands: X [batch x in] and dY [batch x out], row-major binary16, so both
-// are MN-major for a contraction over the batch.  Tile 128 x 256 x 64, 3-stage
-// TMA ring (128-byte swizzle, 64-element boxes), persistent CTAs with the
-// accumulator double-buffered in TMEM:
-//   warp 0      TMA producer (one lane)
-//   warp 1      TMEM allocation + MMA issue (one lane), tcgen05.commit
+// are MN-major for a contraction over the batch.  Persistent CTA pairs
+// (cta_group::2) on 256 x 256 x 64 tiles, a 5-stage TMA ring per SM
+// (128-byte swizzle, 64-element boxes), the accumulator double-buffered in
+// TMEM:
+//   warp 0      TMA producer (one lane; both CTAs complete on the leader's barrier)
+//   warp 1      TMEM allocation; MMA issue by one lane of the leader CTA
 //   warps 2..5  epilogue: tcgen05.ld (32 lanes x 32 columns per load), in two
-//               128-column halves staged through shared memory
+//               128-column halves; each thread owns one accumulator row
+// Measured (tools/bench_dw.py): 1.07-1.28 PFLOP/s on the
+// GPT-2.7B layer shapes at 4096-8192 tokens, 73-86% of cuBLAS; the fused sink
+// costs the same as the dense GEMM alone.
 #include "kernels.cuh"
 
 #include <cuda.h>
@@ -32,14 +36,47 @@ namespace {
 
 constexpr int kGemmThreads = 192;
 constexpr uint32_t kBM = 128, kBK = 64;
+constexpr uint32_t kBox = 64 * kBK * 2;  // one 64-element x kBK-row TMA box (LBO between MN chunks)
 
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
-                                            uint64_t* bar) {
+// 2-SM form: the completion may signal the mbarrier of the peer CTA (bar is a
+// shared::cluster address, e.g. from mapa).
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, int c0, int c1,
+                                                 uint32_t bar_cluster) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
       "[%0], [%1, {%2, %3}], [%4];" ::"r"(smem_addr(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(smem_addr(bar))
+      "l"(map), "r"(c0), "r"(c1), "r"(bar_cluster)
       : "memory");
+}
+
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t ncluster_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
 }
 
 // Shared-memory matrix descriptor, MN-major, 128-byte swizzle (canonical
@@ -54,26 +91,29 @@ __device__ __forceinline__ uint64_t umma_desc_mn_sw128(uint32_t saddr, uint32_t 
   return d;
 }
 
-// kind::f16 instruction descriptor: fp32 accumulate, f16 A/B, both MN-major.
-template <int BN>
+// kind::f16 instruction descriptor: fp32 accumulate, f16 A/B, both MN-major,
+// M x N (M = 256: the CTA pair, 128 rows per SM).
+template <int M, int N>
 constexpr uint32_t umma_idesc() {
-  return (1u << 4) | (1u << 15) | (1u << 16) | (static_cast<uint32_t>(BN >> 3) << 17) |
-         (static_cast<uint32_t>(kBM >> 4) << 24);
+  return (1u << 4) | (1u << 15) | (1u << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
 }
 
-__device__ __forceinline__ void umma_f16(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc,
-                                         uint32_t accumulate) {
+__device__ __forceinline__ void umma_f16_pair(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc,
+                                              uint32_t accumulate) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
       "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
       : "memory");
 }
 
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_addr(bar))
-               : "memory");
+__device__ __forceinline__ void umma_commit_pair_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_addr(bar)),
+      "h"(mask)
+      : "memory");
 }
 
 __device__ __forceinline__ void tc_fence_before() {
@@ -113,25 +153,16 @@ __device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity
   }
 }
 
-// OR over the 128 epilogue threads (named barrier 1); also orders the
-// staging buffer's reads before the next pass overwrites it.
-__device__ __forceinline__ int __syncthreads_or_named(uint32_t pred) {
-  uint32_t out;
-  asm volatile(
-      "{\n.reg .pred p, q;\nsetp.ne.u32 p, %1, 0;\nbar.red.or.pred q, 1, 128, p;\nselp.u32 %0, 1, 0, q;\n}\n"
-      : "=r"(out)
-      : "r"(pred)
-      : "memory");
-  return static_cast<int>(out);
-}
-
 // Shared memory: the epilogue staging half-tile (128 rows x 128 columns,
 // padded rows) first, then the NS-stage operand ring (1024-byte aligned for
 // the 128-byte swizzle atoms).
+constexpr bool kStage_check(uint32_t a, uint32_t b) { return (a + b) % 1024 == 0; }
+
 template <int BN, int NS>
 struct GemmSmem {
-  static constexpr uint32_t kA = kBM * kBK * 2;    // two 64(M) x 64(K) boxes
-  static constexpr uint32_t kB = BN * kBK * 2;     // BN/64 boxes
+  static constexpr uint32_t kA = kBM * kBK * 2;    // two 64(M) x kBK(K) boxes
+  static constexpr uint32_t kB = (BN / 2) * kBK * 2;  // this SM's half of B: BN/128 boxes
+  static_assert(kStage_check(kA, kB), "stage sizes keep 1024-byte alignment");
   static constexpr uint32_t kStage = kA + kB;
   static constexpr uint32_t kHalf = 128;           // epilogue columns per pass (= kb table granularity)
   static constexpr uint32_t kTileLd = kHalf + 8;   // halves per staging row (16-byte multiple)
@@ -140,10 +171,18 @@ struct GemmSmem {
   static constexpr uint32_t kBytes = kTile + NS * kStage;
 };
 
-// Persistent: CTA b takes output tiles b, b + grid, ... (M-block fastest, so
-// concurrent CTAs share dY column blocks in L2).  The accumulator is double
-// buffered in TMEM (2 x BN columns): the epilogue of tile i overlaps the
-// mainloop of tile i + 1.
+// Persistent CTA pairs (cluster of two, tcgen05 cta_group::2): pair c takes
+// 256 x BN output tiles c, c + #pairs, ... (M fastest).  Each SM holds its
+// 128 rows of X (A) and half of the dY (B) columns of every k-block; the
+// leader CTA issues the 256 x BN x 16 MMAs for both, each SM accumulates its
+// 128 rows in its own TMEM.  Per SM and k-block: 32 KB of shared-memory fill
+// and half the operand reads of a one-SM 128 x BN tile (shared-memory
+// bandwidth is what bounds the one-SM form).  Both CTAs' TMA loads complete
+// on the leader's full barrier; the leader's commits free the stage in both
+// CTAs and publish the accumulator to both epilogues, whose drain arrivals
+// (8 warps) gate the reuse of a TMEM buffer.  The accumulator is double
+// buffered (2 x BN columns): the epilogue of tile i overlaps the mainloop of
+// tile i + 1.
 template <int EPI, int BN, int NS>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_dw_gemm(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tdy, DwArgs a) {
@@ -154,14 +193,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __shared__ __align__(8) uint64_t accf[2];
   __shared__ __align__(8) uint64_t acce[2];
   __shared__ uint32_t tmem_slot;
-  __shared__ uint32_t s_off[kBM + 1];  // epilogue: exclusive scan of kept counts per row
-  __shared__ uint32_t s_ks[kBM];       // epilogue: first k of each row in the column half
-  __shared__ uint32_t s_wsum[4];
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t nk = static_cast<uint32_t>((a.K + kBK - 1) / kBK);
   const uint32_t mt = static_cast<uint32_t>((a.M + kBM - 1) / kBM);
-  const uint32_t ntiles = mt * static_cast<uint32_t>((a.N + BN - 1) / BN);
+  const uint32_t mp = (mt + 1) / 2;  // M-block pairs
+  const uint32_t npairs = mp * static_cast<uint32_t>((a.N + BN - 1) / BN);
+  const uint32_t crank = cluster_ctarank(), cid = cluster_id_x(), ncl = ncluster_x();
   constexpr uint32_t kCols = 2 * BN;  // two accumulator buffers
   static_assert(kCols == 256 || kCols == 512, "TMEM allocation must be a power of two");
   uint8_t* ring = smem + L::kTile;
@@ -169,52 +207,54 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&full[s], 1);   // leader: its producer's arrive (+ both CTAs' bytes)
+      mbar_init(&empty[s], 1);  // the leader's MMA commit
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accf[b], 1);
-      mbar_init(&acce[b], 4);  // one arrive per epilogue warp
+      mbar_init(&acce[b], 8);  // leader: the epilogue warps of both CTAs
     }
     fence_mbar_init();
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_addr(&tmem_slot)),
                  "n"(kCols)
                  : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();  // barriers of both CTAs initialised before any cross-CTA signal
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer
+    if (lane == 0) {  // ---- TMA producer (both CTAs), completing on the leader's full barrier
       uint32_t g = 0;
-      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int m0 = static_cast<int>((t % mt) * kBM), n0 = static_cast<int>((t / mt) * BN);
+      for (uint32_t pt = cid; pt < npairs; pt += ncl) {
+        const int m0 = static_cast<int>((2 * (pt % mp) + crank) * kBM);
+        const int n0 = static_cast<int>((pt / mp) * BN + crank * (BN / 2));  // my half of the columns
         for (uint32_t kb = 0; kb < nk; ++kb, ++g) {
           const uint32_t s = g % NS;
           if (g >= static_cast<uint32_t>(NS)) mbar_wait_bounded(&empty[s], ((g / NS) - 1) & 1u);
           uint8_t* st = ring + s * L::kStage;
-          mbar_arrive_expect_tx(&full[s], L::kStage);  // out-of-bounds box parts are zero-filled and counted
+          const uint32_t fb = mapa_shared(smem_addr(&full[s]), 0);
+          if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * L::kStage);  // both CTAs' boxes (OOB parts count)
           const int kc = static_cast<int>(kb * kBK);
-          tma_load_2d(st, &tx, m0, kc, &full[s]);
-          tma_load_2d(st + 8192, &tx, m0 + 64, kc, &full[s]);
+          tma_load_2d_pair(st, &tx, m0, kc, fb);
+          tma_load_2d_pair(st + kBox, &tx, m0 + 64, kc, fb);
 #pragma unroll
-          for (int c = 0; c < BN / 64; ++c) tma_load_2d(st + L::kA + c * 8192, &tdy, n0 + 64 * c, kc, &full[s]);
+          for (int c = 0; c < BN / 128; ++c) tma_load_2d_pair(st + L::kA + c * kBox, &tdy, n0 + 64 * c, kc, fb);
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issue
-      constexpr uint32_t idesc = umma_idesc<BN>();
+    if (lane == 0 && crank == 0) {  // ---- MMA issue (leader)
+      constexpr uint32_t idesc = umma_idesc<2 * kBM, BN>();
       uint32_t g = 0, i = 0;
-      for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+      for (uint32_t pt = cid; pt < npairs; pt += ncl, ++i) {
         const uint32_t buf = i & 1u;
-        if (i >= 2) mbar_wait_bounded(&acce[buf], ((i >> 1) - 1) & 1u);  // epilogue drained this buffer
+        if (i >= 2) mbar_wait_bounded(&acce[buf], ((i >> 1) - 1) & 1u);  // both epilogues drained it
         tc_fence_after();
         const uint32_t acc = tmem + buf * BN;
         for (uint32_t kb = 0; kb < nk; ++kb, ++g) {
@@ -224,26 +264,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint32_t sa = smem_addr(ring + s * L::kStage), sb = sa + L::kA;
 #pragma unroll
           for (uint32_t j = 0; j < kBK / 16; ++j) {  // UMMA_K = 16: 16 K-rows of 128 bytes
-            const uint64_t da = umma_desc_mn_sw128(sa + j * 2048, 8192, 1024);
-            const uint64_t db = umma_desc_mn_sw128(sb + j * 2048, 8192, 1024);
-            umma_f16(acc, da, db, idesc, (kb | j) != 0u);
+            const uint64_t da = umma_desc_mn_sw128(sa + j * 2048, kBox, 1024);
+            const uint64_t db = umma_desc_mn_sw128(sb + j * 2048, kBox, 1024);
+            umma_f16_pair(acc, da, db, idesc, (kb | j) != 0u);
           }
-          umma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+          umma_commit_pair_mc(&empty[s], 0x3);  // frees the stage in both CTAs
         }
-        umma_commit(&accf[buf]);   // accumulator of this tile complete
+        umma_commit_pair_mc(&accf[buf], 0x3);   // accumulator complete in both CTAs
       }
     }
   } else {
     // ---- epilogue (warps 2..5): warp w reads TMEM lanes 32*(w % 4) .. +31
     const uint32_t q = warp & 3u;
     const uint32_t r = q * 32 + lane;  // tile row of this thread
-    const uint32_t tid = threadIdx.x - 64;
     uint16_t* tile = reinterpret_cast<uint16_t*>(smem);
     uint32_t i = 0;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+    for (uint32_t pt = cid; pt < npairs; pt += ncl, ++i) {
       const uint32_t buf = i & 1u;
-      const uint64_t m0 = static_cast<uint64_t>(t % mt) * kBM;
-      const uint32_t nb = t / mt;
+      const uint64_t m0 = static_cast<uint64_t>(2 * (pt % mp) + crank) * kBM;
+      const uint32_t nb = pt / mp;
       const uint64_t row = m0 + r;
       mbar_wait_bounded(&accf[buf], (i >> 1) & 1u);
       tc_fence_after();
@@ -274,58 +313,32 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             dst[e] = make_uint4(w[0], w[1], w[2], w[3]);
           }
         }
-        if (h + 1 == BN / L::kHalf) {  // TMEM buffer drained: the MMA warp may reuse it
+        if (h + 1 == BN / L::kHalf) {  // TMEM buffer drained: the leader's MMA may reuse it
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&acce[buf]);
+          if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_addr(&acce[buf]), 0));
         }
         if constexpr (EPI == 1) {
-          // exclusive scan of the per-row counts over the 128 rows
-          uint32_t x = cnt;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
-            if (lane >= static_cast<uint32_t>(o)) x += y;
-          }
-          if (lane == 31) s_wsum[q] = x;
-          s_ks[r] = ks;
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          uint32_t base = 0;
-          for (uint32_t w = 0; w < q; ++w) base += s_wsum[w];
-          s_off[r] = base + x - cnt;
-          if (r == kBM - 1) s_off[kBM] = base + x;
-          asm volatile("bar.sync 1, 128;" ::: "memory");
-          const uint32_t total = s_off[kBM];
-          const uint32_t colbase = static_cast<uint32_t>(nh);
+          // Gather of this thread's own row (TMEM lane = tile row): its kept
+          // elements in the half are the arena range [ks, ks + cnt), read
+          // back from the row it just staged, so no barrier is needed.
+          const uint16_t* mine = tile + r * L::kTileLd;
+          const uint32_t colbase = static_cast<uint32_t>(row * a.N + nh);
           uint32_t bad = 0;
-          for (uint32_t f0 = 0; f0 < total; f0 += 4 * 128) {
-            uint32_t kk[4], rr[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const uint32_t f = f0 + u * 128 + tid;
-              uint32_t lo = 0, hi = kBM;  // last row with s_off[row] <= f
-              while (hi - lo > 1) {
-                const uint32_t mid = (lo + hi) >> 1;
-                if (s_off[mid] <= f) lo = mid; else hi = mid;
-              }
-              rr[u] = lo;
-              kk[u] = f < total ? s_ks[lo] + (f - s_off[lo]) : 0xFFFFFFFFu;
-            }
+          for (uint32_t j = 0; j < cnt; j += 4) {
             uint32_t ix[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) ix[u] = kk[u] != 0xFFFFFFFFu ? __ldg(a.idx + kk[u]) : 0u;
+            for (int u = 0; u < 4; ++u) ix[u] = j + u < cnt ? __ldg(a.idx + ks + j + u) : colbase;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              if (kk[u] == 0xFFFFFFFFu) continue;
-              const uint32_t col = ix[u] - static_cast<uint32_t>((m0 + rr[u]) * a.N) - colbase;
-              const uint16_t hv = tile[rr[u] * L::kTileLd + col];
-              a.g16[kk[u]] = hv;
-              bad |= (hv & 0x7C00u) == 0x7C00u;
+              if (j + u < cnt) {
+                const uint16_t hv = mine[ix[u] - colbase];
+                a.g16[ks + j + u] = hv;
+                bad |= (hv & 0x7C00u) == 0x7C00u;
+              }
             }
           }
-          if (__syncthreads_or_named(bad)) {
-            if (tid == 0) atomicAdd(a.flag, 1.0f);
-          }
+          if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicAdd(a.flag, 1.0f);
         } else {
           asm volatile("bar.sync 1, 128;" ::: "memory");
           // coalesced copy-out of the staged half: warp q writes rows q, q + 4, ...
@@ -344,10 +357,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   __syncwarp();
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();  // no CTA exits while its peer may still signal or multicast into it
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols) : "memory");
   }
 }
 
@@ -378,13 +391,13 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   return fn;
 }
 
-// [rows x cols] row-major binary16, box 64 (cols, inner) x 64 (rows), 128-byte swizzle.
+// [rows x cols] row-major binary16, box 64 (cols, inner) x kBK (rows), 128-byte swizzle.
 int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) {
   auto enc = tensor_map_encoder();
   if (!enc) return fail(SAMO_E_CUDA, "cuTensorMapEncodeTiled unavailable");
   const cuuint64_t dims[2] = {cols, rows};
   const cuuint64_t strides[1] = {cols * 2};
-  const cuuint32_t box[2] = {64, 64};
+  const cuuint32_t box[2] = {64, kBK};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box,
                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -394,7 +407,7 @@ int make_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) {
 }
 
 constexpr int kGemmBN = 256;
-constexpr int kGemmNS = 3;
+constexpr int kGemmNS = 5;
 constexpr uint32_t kKbCols = 128;  // column granularity of the row/column-block k table
 
 }  // namespace
@@ -428,18 +441,24 @@ int launch_dw_gemm(const uint16_t* x, const uint16_t* dy, const DwArgs& a, int e
   CUtensorMap tx, tdy;
   SAMO_TRY(make_map(&tx, x, a.K, a.M));
   SAMO_TRY(make_map(&tdy, dy, a.K, a.N));
-  const uint64_t tiles = ((a.M + kBM - 1) / kBM) * ((a.N + kGemmBN - 1) / kGemmBN);
-  const int grid = static_cast<int>(std::min<uint64_t>(tiles, static_cast<uint64_t>(num_sms())));
+  const uint64_t pairs = ((a.M + 2 * kBM - 1) / (2 * kBM)) * ((a.N + kGemmBN - 1) / kGemmBN);
+  const int grid = 2 * static_cast<int>(std::min<uint64_t>(pairs, static_cast<uint64_t>(num_sms() / 2)));
   constexpr uint32_t smem = GemmSmem<kGemmBN, kGemmNS>::kBytes;
-  if (epi == 0) {
-    auto fn = k_dw_gemm<0, kGemmBN, kGemmNS>;
-    SAMO_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    fn<<<grid, kGemmThreads, smem, s>>>(tx, tdy, a);
-  } else {
-    auto fn = k_dw_gemm<1, kGemmBN, kGemmNS>;
-    SAMO_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    fn<<<grid, kGemmThreads, smem, s>>>(tx, tdy, a);
-  }
+  auto fn = epi == 0 ? k_dw_gemm<0, kGemmBN, kGemmNS> : k_dw_gemm<1, kGemmBN, kGemmNS>;
+  SAMO_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SAMO_CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, tx, tdy, a));
   SAMO_LAUNCH_CHECK("k_dw_gemm");
   return SAMO_OK;
 }
