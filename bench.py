@@ -50,6 +50,7 @@ def parse_args():
     ap.add_argument("--seed", type=int, default=1234)
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = min(steps, 10)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-fused", action="store_true", help="skip the fused dW-GEMM sink probe")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-blocks", type=int, default=0, help="GPT blocks in the CPU sample")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/CPU legs)")
@@ -66,8 +67,9 @@ def peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return {"hbm_gbs": float(d["hbm_gbs"]), "src": "measured"}
-    return {"hbm_gbs": 6650.0, "src": "fallback"}
+        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d.get("bf16_tflops", 0)) or None,
+                "src": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 2250.0, "src": "fallback"}
 
 
 class ClockSampler:
@@ -235,6 +237,51 @@ def run_reference(args) -> None:
 
 # ---------------------------------------------------------------------------
 # SAMO arm
+
+def fused_sink_probe(reps: int = 10) -> dict:
+    """SURVEY §8(f)-1 (not the headline): one GPT-2.7B MLP layer (4096 tokens,
+    2560 x 10240, p = 0.9) — the weight-gradient GEMM with the gather fused
+    into its epilogue (samo_model_sink_dw) vs the dense GEMM + K1 on the layer,
+    and cuBLAS for the GEMM alone.  CUDA events, median of `reps`."""
+    batch, n_in, n_out, p = 4096, 2560, 10240, 0.9
+    g = torch.Generator(device="cuda").manual_seed(1)
+    x = (torch.rand(batch, n_in, device="cuda", generator=g) * 2 - 1).half()
+    dy = ((torch.rand(batch, n_out, device="cuda", generator=g) * 2 - 1) * 4).half()
+    n = n_in * n_out
+    idx = torch.randperm(n, device="cuda", generator=g)[: int(round((1 - p) * n))].sort().values.to(torch.int32)
+    m = samo.SamoModel.from_index_sets([samo.PrunedIndexSet("mlp.fc_in.weight", n, idx)], [(n_in, n_out)], 0)
+    m.init_layer(0, torch.zeros(n, device="cuda"))
+
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    flops = 2.0 * batch * n_in * n_out
+    t_gemm = timed(lambda: samo.dw_gemm(x, dy))
+    t_cublas = timed(lambda: torch.matmul(x.t(), dy))
+    t_unfused = timed(lambda: m.sink_dense(0, samo.dw_gemm(x, dy).reshape(-1)))
+    t_fused = timed(lambda: m.sink_dw(0, x, dy))
+    m._sink_keepalive.clear()
+    m.close()
+    pk = peaks()
+    return {"shape": {"batch": batch, "in": n_in, "out": n_out, "sparsity": p},
+            "dw_gemm_ms": t_gemm, "dw_gemm_tflops": flops / t_gemm / 1e9,
+            "roofline": {"bound": "tensor", "achieved": flops / t_gemm / 1e9, "peak": pk.get("bf16_tflops"),
+                         "unit": "TFLOP/s",
+                         "frac": (flops / t_gemm / 1e9) / pk["bf16_tflops"] if pk.get("bf16_tflops") else None},
+            "cublas_ms": t_cublas, "cublas_tflops": flops / t_cublas / 1e9,
+            "unfused_sink_ms": t_unfused, "fused_sink_ms": t_fused,
+            "fused_saving": 1 - t_fused / t_unfused}
+
 
 def run_samo(args) -> None:
     import numpy as np
@@ -577,6 +624,13 @@ def run_samo(args) -> None:
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                    "sample": f"failed: {ex}"}
 
+    fused = None
+    if world == 1 and not (args.profile or args.no_fused):
+        try:
+            fused = fused_sink_probe()
+        except Exception as ex:  # a probe failure must not drop the headline line
+            fused = {"error": str(ex)}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
@@ -609,6 +663,7 @@ def run_samo(args) -> None:
             "kernels": kern,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "fused_dw_sink": fused,
             "clocks": clk.summary(),
             "step_record": {"t": int(rec.t), "skipped": int(rec.skipped_steps),
                             "grad_norm": float(rec.grad_norm)},

@@ -196,6 +196,9 @@ class Tensor {
   }
   const std::vector<std::size_t>& shape() const { return shape_; }
   std::size_t size() const { return data_.size(); }
+  std::size_t rank() const { return shape_.size(); }
+  std::size_t rows() const { return shape_.at(0); }  // 2-D accessors (tensor.hpp:55-56)
+  std::size_t cols() const { return shape_.at(1); }
   std::span<const T> flat() const { return data_; }
   std::span<T> flat() { return data_; }
   T operator[](std::size_t i) const { return data_[i]; }
@@ -369,6 +372,22 @@ inline void adam_update(std::span<float> theta, std::span<float> m, std::span<fl
   vv.download(v.data(), n);
 }
 
+// matmul(transpose(x), dy) (train.hpp:304, tensor.hpp:88-105) on the tensor
+// cores: x [batch x in], dy [batch x out] -> [in x out] binary16.  Host
+// containers in, host tensor out (the reference's value semantics).
+inline Tensor<Half> dw_matmul(const Tensor<Half>& x, const Tensor<Half>& dy) {
+  if (x.rank() != 2 || dy.rank() != 2 || x.rows() != dy.rows())
+    throw DimensionError("matmul expects MxK and KxN operands");
+  const std::uint64_t batch = x.rows(), in = x.cols(), out = dy.cols();
+  DeviceBuffer<std::uint16_t> dx(reinterpret_cast<const std::uint16_t*>(x.flat().data()), x.size());
+  DeviceBuffer<std::uint16_t> dd(reinterpret_cast<const std::uint16_t*>(dy.flat().data()), dy.size());
+  DeviceBuffer<std::uint16_t> dw(in * out);
+  check(samo_dw_gemm_f16(dx.get(), dd.get(), batch, in, out, dw.get(), nullptr));
+  std::vector<Half> h(in * out);
+  dw.download(reinterpret_cast<std::uint16_t*>(h.data()), in * out);
+  return Tensor<Half>({static_cast<std::size_t>(in), static_cast<std::size_t>(out)}, std::move(h));
+}
+
 // ---------------------------------------------------------------------------
 // Device-resident model state + step driver (ModelState / SamoTrainer).
 
@@ -410,6 +429,19 @@ class Model {
   void set_grads(const std::vector<const std::uint16_t*>& dev_ptrs, cudaStream_t s = nullptr) {
     check(samo_model_set_grads(h_.get(), dev_ptrs.data(), s));
   }
+  // The trainer's backward sink (train.hpp:596-611), one layer at a time, as
+  // each dense gradient is produced (single-GPU models; then update()).
+  void sink_dense(int l, const std::uint16_t* dev_grad, cudaStream_t s = nullptr) {
+    check(samo_model_sink_dense(h_.get(), l, dev_grad, s));
+  }
+  // Fused sink: dW = X^T . dY (mlp_backward, train.hpp:304-305) on the tensor
+  // cores with the gather in the GEMM epilogue; x [batch x in], dy [batch x out].
+  void sink_dw(int l, const std::uint16_t* x, const std::uint16_t* dy, std::uint64_t batch, std::uint64_t in,
+               std::uint64_t out, cudaStream_t s = nullptr) {
+    check(samo_model_sink_dw(h_.get(), l, x, dy, batch, in, out, s));
+  }
+  // Skip decision, AdamScalars::advance, Adam, downcast + expand after the sinks.
+  void update(cudaStream_t s = nullptr) { check(samo_model_update(h_.get(), s)); }
   // SamoTrainer::optimizer_step (train.hpp:617-656) without host sync.
   void step(cudaStream_t s = nullptr, bool graph = false) {
     check(graph ? samo_model_step_graph(h_.get(), s) : samo_model_step(h_.get(), s));

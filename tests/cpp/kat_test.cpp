@@ -286,6 +286,52 @@ int main() {
     CHECK(throws<ParameterError>([&] { model.set_config(bad); }));
   });
 
+  run("Matmul.TransposeTimes (train.hpp:304, tensor.hpp:88-105) on the tensor cores", [] {
+    // small integers: every product and partial sum is exact in fp32 and fp16
+    const std::size_t batch = 3, in = 8, out = 16;
+    std::vector<Half> xv, dv;
+    for (std::size_t i = 0; i < batch * in; ++i) xv.push_back(Half(static_cast<float>(static_cast<int>(i % 7) - 3)));
+    for (std::size_t i = 0; i < batch * out; ++i) dv.push_back(Half(static_cast<float>(static_cast<int>(i % 5) - 2)));
+    const Tensor<Half> x({batch, in}, xv), dy({batch, out}, dv);
+    const auto w = dw_matmul(x, dy);
+    CHECK(w.shape() == std::vector<std::size_t>({in, out}));
+    bool ok = true;
+    for (std::size_t i = 0; i < in; ++i)
+      for (std::size_t j = 0; j < out; ++j) {
+        float acc = 0.0f;
+        for (std::size_t b = 0; b < batch; ++b) acc += float(xv[b * in + i]) * float(dv[b * out + j]);
+        ok = ok && float(w[i * out + j]) == acc;
+      }
+    CHECK(ok);
+    CHECK(throws<DimensionError>([&] { dw_matmul(x, Tensor<Half>({2, out})); }));
+  });
+  run("Sink.FusedDwEqualsDenseSink (train.hpp:596-611)", [] {
+    const std::size_t batch = 5, in = 16, out = 24;
+    std::vector<std::uint32_t> keep;
+    for (std::uint32_t k = 0; k < in * out; k += 7) keep.push_back(k);
+    std::vector<Half> xv, dv;
+    for (std::size_t i = 0; i < batch * in; ++i) xv.push_back(Half(0.25f * static_cast<float>(static_cast<int>(i % 9) - 4)));
+    for (std::size_t i = 0; i < batch * out; ++i) dv.push_back(Half(8.0f * static_cast<float>(static_cast<int>(i % 5) - 2)));
+    const Tensor<Half> x({batch, in}, xv), dy({batch, out}, dv);
+    const auto w = dw_matmul(x, dy);
+    auto make = [&] {
+      Model m({*make_ind(in * out, keep)});
+      m.init_layer(0, Tensor<float>({in, out}, std::vector<float>(in * out, 0.1f)));
+      return m;
+    };
+    Model fused = make(), dense = make();
+    DeviceBuffer<std::uint16_t> dx(reinterpret_cast<const std::uint16_t*>(xv.data()), xv.size());
+    DeviceBuffer<std::uint16_t> dd(reinterpret_cast<const std::uint16_t*>(dv.data()), dv.size());
+    DeviceBuffer<std::uint16_t> dw(reinterpret_cast<const std::uint16_t*>(w.flat().data()), w.size());
+    fused.sink_dw(0, dx.get(), dd.get(), batch, in, out);
+    fused.update();
+    dense.set_grads({dw.get()});
+    dense.step();
+    CHECK(fused.theta32(0) == dense.theta32(0));
+    CHECK(fused.record().t == 1);
+    CHECK(throws<DimensionError>([&] { fused.sink_dw(0, dx.get(), dd.get(), batch, in, out - 8); }));
+  });
+
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail ? 1 : 0;
 }
