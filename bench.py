@@ -243,6 +243,8 @@ def fused_sink_probe(reps: int = 10) -> dict:
     2560 x 10240, p = 0.9) — the weight-gradient GEMM with the gather fused
     into its epilogue (samo_model_sink_dw) vs the dense GEMM + K1 on the layer,
     and cuBLAS for the GEMM alone.  CUDA events, median of `reps`."""
+    import torch
+    from paper_2302_05045_b200 import samo
     batch, n_in, n_out, p = 4096, 2560, 10240, 0.9
     g = torch.Generator(device="cuda").manual_seed(1)
     x = (torch.rand(batch, n_in, device="cuda", generator=g) * 2 - 1).half()
