@@ -442,6 +442,8 @@ class Model {
   }
   // Skip decision, AdamScalars::advance, Adam, downcast + expand after the sinks.
   void update(cudaStream_t s = nullptr) { check(samo_model_update(h_.get(), s)); }
+  // After the sinks on a data-parallel model: exchange + update.
+  void step_sunk(cudaStream_t s = nullptr) { check(samo_model_step_sunk(h_.get(), s)); }
   // SamoTrainer::optimizer_step (train.hpp:617-656) without host sync.
   void step(cudaStream_t s = nullptr, bool graph = false) {
     check(graph ? samo_model_step_graph(h_.get(), s) : samo_model_step(h_.get(), s));

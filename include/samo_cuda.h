@@ -289,9 +289,9 @@ int samo_model_gather(samo_model* model, samo_stream_t stream);
 /* Backward sinks (the trainer's per-layer gradient sink, train.hpp:596-611):
  * each writes one layer's compressed binary16 gradient (grad16) and raises
  * the skip flag on a non-finite kept element, the moment the layer's
- * gradient is produced.  Single-GPU models only (the data-parallel exchanges
- * gather inside their fused step); follow the layers' sinks with
- * samo_model_update.
+ * gradient is produced.  Single-GPU models or the peer-to-peer exchange (the
+ * NCCL exchanges gather fp32 inside their step); follow the layers' sinks
+ * with samo_model_step_sunk (= samo_model_update on one GPU).
  *
  * samo_model_sink_dense: K1 on one layer's tiles from its dense binary16
  * gradient (dense_len elements, 16-byte aligned).
@@ -301,11 +301,19 @@ int samo_model_gather(samo_model* model, samo_stream_t stream);
  * binary16 row-major, 16-byte aligned, in and out multiples of 8,
  * in * out == dense_len) computed on the tensor cores with the gather fused
  * into the GEMM epilogue: the dense gradient never reaches HBM.  The result
- * is bit-identical to samo_dw_gemm_f16 followed by samo_model_sink_dense. */
+ * is bit-identical to samo_dw_gemm_f16 followed by samo_model_sink_dense.
+ *
+ * Data-parallel models (peer-to-peer exchange only): each rank sinks its own
+ * gradients, then samo_model_step_sunk runs the exchange and the update. */
 int samo_model_sink_dense(samo_model* model, int layer, const uint16_t* dense_grad,
                           samo_stream_t stream);
 int samo_model_sink_dw(samo_model* model, int layer, const uint16_t* x, const uint16_t* dy,
                        uint64_t batch, uint64_t in, uint64_t out, samo_stream_t stream);
+
+/* The step after the backward sinks: exchange (peer-to-peer) + update — the
+ * same as samo_model_step without its gather.  Single-GPU models: the same as
+ * samo_model_update. */
+int samo_model_step_sunk(samo_model* model, samo_stream_t stream);
 
 /* Dense weight gradient dW[in x out] = X^T . dY as binary16 (tcgen05 tensor
  * cores, fp32 accumulation, one rounding; matmul(transpose(x), dy) of

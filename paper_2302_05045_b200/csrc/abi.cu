@@ -1073,17 +1073,19 @@ static int exchange_mode(const samo_model* md) {
 //   -> allreduce(norm^2)               [NCCL, 8 bytes: also the barrier]
 //   -> expand every tile from theta16c -> scalars.
 static int p2p_buckets(int G);
-static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B);
+static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather);
 
-static int step_p2p(samo_model* md, cudaStream_t S) {
+// gather = false: the backward sinks have already written grad16 (and the
+// local skip count) — the step starts at the exchange.
+static int step_p2p(samo_model* md, cudaStream_t S, bool gather = true) {
   const int G = md->comm->nranks, r = md->comm->rank;
-  if (p2p_buckets(G) > 1) return step_p2p_pipelined(md, S, p2p_buckets(G));
+  if (p2p_buckets(G) > 1) return step_p2p_pipelined(md, S, p2p_buckets(G), gather);
   const uint64_t c = align_up((md->n_tot + G - 1) / G, 8);
   if (static_cast<uint64_t>(G) * c + 8 > md->n_al + kFlagOff)
     return fail(SAMO_E_PARAMETER, "too many ranks for the arena padding");
   float* flag = flag_ptr(md);
   SAMO_TRY(phase_mark(md, 0, S));
-  SAMO_TRY(launch_gather(step_args(md), false, md->grid_gather16, S));
+  if (gather) SAMO_TRY(launch_gather(step_args(md), false, md->grid_gather16, S));
   SAMO_TRY(phase_mark(md, 1, S));
   ncclResult_t rr = ncclAllReduce(flag, flag, 1, ncclFloat32, ncclSum, md->comm->flag, S);
   if (rr != ncclSuccess) return nccl_fail(rr, "ncclAllReduce(flag)");
@@ -1292,7 +1294,7 @@ static int step_sharded(samo_model* md, cudaStream_t S) {
 // in bucket b, once every rank has published bucket b.  The global skip flag
 // forces every K1 to finish before any shard update, so K1 stays serial.
 // Grids: SAMO_P2P_SHARD_CTAS / SAMO_P2P_EXPAND_CTAS per SM (tuning).
-static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B) {
+static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather) {
   const int G = md->comm->nranks, r = md->comm->rank;
   SAMO_TRY(plan_buckets(md));  // side streams + events
   ShardPlan& p = md->p2p_plan;
@@ -1335,7 +1337,7 @@ static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B) {
   const int ge = std::min(md->grid_expand, sms * std::max(1, env_int("SAMO_P2P_EXPAND_CTAS", 2)));
 
   SAMO_TRY(phase_mark(md, 0, S));
-  SAMO_TRY(launch_gather(step_args(md), false, md->grid_gather16, S));
+  if (gather) SAMO_TRY(launch_gather(step_args(md), false, md->grid_gather16, S));
   SAMO_TRY(phase_mark(md, 1, S));
   SAMO_TRY(launch_p2p_flag(pa.slots, G, r, flag, S));
   SAMO_TRY(phase_mark(md, 2, S));
@@ -1459,8 +1461,9 @@ int samo_model_exchange(samo_model* md, samo_stream_t stream) {
 static int sink_ready(samo_model* md, int l) {
   SAMO_TRY(step_ready(md));
   if (l < 0 || l >= md->nlayers) return fail(SAMO_E_INDEX, "layer %d out of range", l);
-  if (comm_size(md) > 1)
-    return fail(SAMO_E_STATE, "backward sinks need a single-GPU model (the exchanges gather in their step)");
+  if (comm_size(md) > 1 && (exchange_mode(md) != SAMO_EXCHANGE_P2P || !md->p2p_ok))
+    return fail(SAMO_E_STATE,
+                "backward sinks need a single-GPU model or the peer-to-peer exchange (binary16 gradient arena)");
   if (md->layer_t.empty()) {
     md->layer_t.assign(md->nlayers + 1, md->ntiles);
     for (uint32_t t = md->ntiles; t-- > 0;) md->layer_t[md->tiles_host[t].layer] = t;
@@ -1539,6 +1542,18 @@ int samo_model_update(samo_model* md, samo_stream_t stream) {
   const int grid = std::min<int>(wide ? md->grid_update32 : md->grid_update16, md->ntiles);
   a.norm_count = static_cast<uint32_t>(grid);
   SAMO_TRY(launch_update(a, wide, grid, as_stream(stream)));
+  return clear_ok();
+}
+
+int samo_model_step_sunk(samo_model* md, samo_stream_t stream) {
+  SAMO_TRY(step_ready(md));
+  if (comm_size(md) > 1) {
+    if (exchange_mode(md) != SAMO_EXCHANGE_P2P || !md->p2p_ok)
+      return fail(SAMO_E_STATE, "step after backward sinks needs the peer-to-peer exchange");
+    SAMO_TRY(step_p2p(md, as_stream(stream), false));
+    return clear_ok();
+  }
+  SAMO_TRY(samo_model_update(md, stream));
   return clear_ok();
 }
 

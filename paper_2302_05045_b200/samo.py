@@ -403,6 +403,11 @@ class SamoModel:
     def exchange(self) -> None:
         _abi.call("samo_model_exchange", self._h, _stream())
 
+    def step_sunk(self) -> None:
+        """The step after the backward sinks: exchange (peer-to-peer) + update."""
+        _abi.call("samo_model_step_sunk", self._h, _stream())
+        self._sink_keepalive = []
+
     def update(self) -> None:
         _abi.call("samo_model_update", self._h, _stream())
         self._sink_keepalive = []  # stream-ordered: later allocations reuse safely

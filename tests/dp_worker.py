@@ -60,10 +60,16 @@ def main() -> None:
     mode = os.environ.get("SAMO_DP_MODE", "sharded")
     model.set_exchange({"sharded": model.EXCHANGE_SHARDED, "p2p": model.EXCHANGE_P2P,
                         "allreduce": model.EXCHANGE_ALLREDUCE}[mode])
+    sink = os.environ.get("SAMO_DP_SINK") == "1"
     for s in range(STEPS):
         g = [torch.from_numpy(grads[(rank, s, l)].view(np.int16)).cuda() for l in range(len(DENSE_LEN))]
-        model.set_grads(g)
-        model.step(graph=os.environ.get("SAMO_DP_GRAPH") == "1")
+        if sink:  # per-layer backward sinks (last layer first), then exchange + update
+            for l in reversed(range(len(DENSE_LEN))):
+                model.sink_dense(l, g[l])
+            model.step_sunk()
+        else:
+            model.set_grads(g)
+            model.step(graph=os.environ.get("SAMO_DP_GRAPH") == "1")
     torch.cuda.synchronize()
     rec = model.step_record()
     ranges = np.array(model.shard_ranges(), np.uint64).reshape(-1, 2)

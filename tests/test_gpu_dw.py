@@ -147,3 +147,19 @@ def test_sink_errors(S):
         m.sink_dw(0, x, torch.zeros((8, 136), dtype=torch.float16, device="cuda"))  # 256 x 136 != 256 x 384
     with pytest.raises(S.SamoIndexError):
         m.sink_dw(7, x, torch.zeros((8, 384), dtype=torch.float16, device="cuda"))
+
+
+@pytest.mark.parametrize("shapes,p", [([(8, 8), (24, 16)], 0.0),        # every element kept
+                                      ([(16, 8), (8, 264)], 0.9999),    # one kept element per layer
+                                      ([(136, 72)], 0.5)])
+def test_sink_dw_density_edges(S, shapes, p):
+    rng = np.random.default_rng(17)
+    batch = 33
+    fused, unfused = _model(S, shapes, p, 8), _model(S, shapes, p, 8)
+    for l, (i, o) in enumerate(shapes):
+        x, dy = _half(rng, (batch, i), 1.0), _half(rng, (batch, o), 2.0)
+        fused.sink_dw(l, x, dy)
+        unfused.sink_dense(l, S.dw_gemm(x, dy).reshape(-1))
+    torch.cuda.synchronize()
+    for l in range(len(shapes)):
+        assert np.array_equal(_bits(fused.read(l, "grad16")), _bits(unfused.read(l, "grad16"))), l
