@@ -23,6 +23,8 @@
 
 #include "common.cuh"
 
+#include <cub/block/block_scan.cuh>
+
 namespace samo_dev {
 namespace {
 
@@ -169,38 +171,62 @@ k_prune_count(const PChunk* __restrict__ chunks, const PSeg* __restrict__ segs,
   }
 }
 
-// Ordered scan over all chunks (one thread; loads are independent so the
-// loop pipelines).  eq ranks restart per problem, output offsets per layer.
-__global__ void k_prune_scan(const PChunk* __restrict__ chunks, const PSeg* __restrict__ segs,
-                             const PProblem* __restrict__ probs, uint32_t nchunks,
-                             const uint32_t* __restrict__ gt_cnt, const uint32_t* __restrict__ eq_cnt,
-                             uint64_t* __restrict__ eq_before, uint64_t* __restrict__ out_pos,
-                             uint64_t* __restrict__ seg_count) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  uint32_t cur_seg = 0xFFFFFFFFu, cur_prob = 0xFFFFFFFFu;
-  uint64_t eqb = 0, pos = 0, need = 0;
-  for (uint32_t c = 0; c < nchunks; ++c) {
-    const uint32_t s = chunks[c].seg;
-    if (s != cur_seg) {
-      if (cur_seg != 0xFFFFFFFFu) seg_count[cur_seg] = pos;
-      cur_seg = s;
-      pos = 0;
-      const uint32_t p = segs[s].problem;
-      if (p != cur_prob) {
-        cur_prob = p;
-        eqb = 0;
-        need = probs[p].need_eq;
-      }
+// Ordered scan over all chunks, one block of kScanT threads walking windows
+// of kScanT chunks: two exclusive prefix sums with carries — the key==T
+// counts (eq ranks restart per problem: subtract the prefix at the problem's
+// first chunk) and the kept counts gt + take (output offsets restart per
+// layer: subtract the prefix at the segment's first chunk).
+constexpr int kScanT = 1024;
+__global__ void __launch_bounds__(kScanT)
+k_prune_scan(const PChunk* __restrict__ chunks, const PSeg* __restrict__ segs,
+             const PProblem* __restrict__ probs, uint32_t nchunks,
+             const uint32_t* __restrict__ gt_cnt, const uint32_t* __restrict__ eq_cnt,
+             const uint32_t* __restrict__ seg_first, const uint32_t* __restrict__ prob_first,
+             uint64_t* __restrict__ pre_e, uint64_t* __restrict__ pre_w,
+             uint64_t* __restrict__ eq_before, uint64_t* __restrict__ out_pos,
+             uint64_t* __restrict__ seg_count) {
+  using Scan = cub::BlockScan<uint64_t, kScanT>;
+  __shared__ typename Scan::TempStorage tmp;
+  uint64_t carry_e = 0, carry_w = 0;
+  for (uint32_t base = 0; base < nchunks; base += kScanT) {
+    const uint32_t c = base + threadIdx.x;
+    const bool on = c < nchunks;
+    uint32_t sg = 0, pb = 0;
+    uint64_t e = 0, gt = 0;
+    if (on) {
+      sg = chunks[c].seg;
+      pb = segs[sg].problem;
+      e = eq_cnt[c];
+      gt = gt_cnt[c];
     }
-    const uint64_t e = eq_cnt[c];
-    const uint64_t rest = (need > eqb) ? need - eqb : 0;
-    const uint64_t take = rest < e ? rest : e;
-    eq_before[c] = eqb;
-    out_pos[c] = pos;
-    eqb += e;
-    pos += gt_cnt[c] + take;
+    uint64_t ex, agg;
+    Scan(tmp).ExclusiveSum(e, ex, agg);
+    ex += carry_e;
+    carry_e += agg;
+    if (on) pre_e[c] = ex;
+    __syncthreads();
+    uint64_t w = 0;
+    if (on) {
+      const uint64_t eqb = ex - pre_e[prob_first[pb]];
+      const uint64_t need = probs[pb].need_eq;
+      const uint64_t rest = need > eqb ? need - eqb : 0;
+      eq_before[c] = eqb;
+      w = gt + (rest < e ? rest : e);
+    }
+    __syncthreads();  // tmp reuse
+    uint64_t wx;
+    Scan(tmp).ExclusiveSum(w, wx, agg);
+    wx += carry_w;
+    carry_w += agg;
+    if (on) pre_w[c] = wx;
+    __syncthreads();
+    if (on) {
+      const uint64_t pos = wx - pre_w[seg_first[sg]];
+      out_pos[c] = pos;
+      if (c + 1 == nchunks || chunks[c + 1].seg != sg) seg_count[sg] = pos + w;
+    }
+    __syncthreads();
   }
-  if (cur_seg != 0xFFFFFFFFu) seg_count[cur_seg] = pos;
 }
 
 __global__ void __launch_bounds__(kPT)
@@ -369,6 +395,8 @@ int samo_magnitude_prune(const float* const* values, const uint64_t* lens, const
   const size_t o_gt = carve(nchunks * 4ull), o_eq = carve(nchunks * 4ull);
   const size_t o_eqb = carve(nchunks * 8ull), o_pos = carve(nchunks * 8ull);
   const size_t o_cnt = carve(nsegs * 8ull);
+  const size_t o_pe = carve(nchunks * 8ull), o_pw = carve(nchunks * 8ull);
+  const size_t o_sf = carve(nsegs * 4ull), o_pf = carve(nprobs * 4ull);
   void* block = nullptr;
   SAMO_CUDA_TRY(cudaMallocAsync(&block, off, s));
   char* b = static_cast<char*>(block);
@@ -381,6 +409,23 @@ int samo_magnitude_prune(const float* const* values, const uint64_t* lens, const
   auto* d_eqb = reinterpret_cast<uint64_t*>(b + o_eqb);
   auto* d_pos = reinterpret_cast<uint64_t*>(b + o_pos);
   auto* d_cnt = reinterpret_cast<uint64_t*>(b + o_cnt);
+  auto* d_pe = reinterpret_cast<uint64_t*>(b + o_pe);
+  auto* d_pw = reinterpret_cast<uint64_t*>(b + o_pw);
+  auto* d_sf = reinterpret_cast<uint32_t*>(b + o_sf);
+  auto* d_pf = reinterpret_cast<uint32_t*>(b + o_pf);
+  // first chunk of every segment and of every problem (segments are ordered by problem)
+  std::vector<uint32_t> seg_first(nsegs, 0), prob_first(nprobs, 0);
+  {
+    std::vector<uint8_t> seen_p(nprobs, 0);
+    for (uint32_t c = nchunks; c-- > 0;) seg_first[chunks[c].seg] = c;
+    for (uint32_t si = 0; si < nsegs; ++si) {
+      const uint32_t pb = segs_o[si].problem;
+      if (!seen_p[pb]) {
+        seen_p[pb] = 1;
+        prob_first[pb] = seg_first[si];
+      }
+    }
+  }
   int rc = SAMO_OK;
   std::vector<uint64_t> seg_counts(nsegs);
   do {
@@ -388,6 +433,9 @@ int samo_magnitude_prune(const float* const* values, const uint64_t* lens, const
     if ((e = cudaMemcpyAsync(d_chunks, chunks.data(), nchunks * sizeof(PChunk), cudaMemcpyHostToDevice, s)) ||
         (e = cudaMemcpyAsync(d_segs, segs_o.data(), nsegs * sizeof(PSeg), cudaMemcpyHostToDevice, s)) ||
         (e = cudaMemcpyAsync(d_probs, probs.data(), nprobs * sizeof(PProblem), cudaMemcpyHostToDevice, s)) ||
+        (e = cudaMemcpyAsync(d_sf, seg_first.data(), nsegs * 4ull, cudaMemcpyHostToDevice, s)) ||
+        (e = cudaMemcpyAsync(d_pf, prob_first.data(), nprobs * 4ull, cudaMemcpyHostToDevice, s)) ||
+        (e = cudaMemsetAsync(d_cnt, 0, nsegs * 8ull, s)) ||
         (e = cudaMemsetAsync(d_hist, 0, 3ull * nprobs * kBins * 4, s))) {
       rc = cuda_fail(e, "prune setup");
       break;
@@ -404,7 +452,8 @@ int samo_magnitude_prune(const float* const* values, const uint64_t* lens, const
     if (rc != SAMO_OK) break;
     k_prune_count<<<nchunks, kPT, 0, s>>>(d_chunks, d_segs, d_probs, d_gt, d_eq);
     if ((e = cudaGetLastError())) { rc = cuda_fail(e, "k_prune_count"); break; }
-    k_prune_scan<<<1, 32, 0, s>>>(d_chunks, d_segs, d_probs, nchunks, d_gt, d_eq, d_eqb, d_pos, d_cnt);
+    k_prune_scan<<<1, kScanT, 0, s>>>(d_chunks, d_segs, d_probs, nchunks, d_gt, d_eq, d_sf, d_pf, d_pe, d_pw,
+                                      d_eqb, d_pos, d_cnt);
     if ((e = cudaGetLastError())) { rc = cuda_fail(e, "k_prune_scan"); break; }
     k_prune_write<<<nchunks, kPT, 0, s>>>(d_chunks, d_segs, d_probs, d_eqb, d_pos);
     if ((e = cudaGetLastError())) { rc = cuda_fail(e, "k_prune_write"); break; }

@@ -116,3 +116,12 @@ def test_dp_four_gpus_p2p_bit_exact(tmp_path, oracle, mode):
     if torch.cuda.device_count() < 4:
         pytest.skip("needs 4 GPUs")
     _check(_run(tmp_path, mode, 4), oracle, 4, mode)
+
+
+def test_dp_three_gpus_p2p_bit_exact(tmp_path, oracle):
+    """Non-power-of-two G: 1/G is inexact, but the kernel applies the same
+    fp32 scale (1/loss_scale * 1/G) per rank before the rank-ordered sum as
+    the oracle, so replicas still match it bit for bit."""
+    if torch.cuda.device_count() < 3:
+        pytest.skip("needs 3 GPUs")
+    _check(_run(tmp_path, "p2p", 3), oracle, 3, "p2p")
