@@ -477,7 +477,12 @@ struct samo_model {
   cudaEvent_t ev_fork = nullptr, ev_flag = nullptr;
   int reserve_sms = 16;                 // SMs left to NCCL while our kernels run
   ShardPlan shard_plan;
-  ShardPlan p2p_plan;                   // pipelined peer-to-peer step
+  ShardPlan p2p_plan;                   // peer-to-peer step (serial: 1 bucket)
+  // K1 tile table of the push-mode P2P step: tiles split at owner boundaries,
+  // pad_ = owner rank, pad2_ = receive-buffer element of k_begin.
+  SamoTile* push_tiles = nullptr;
+  uint32_t push_ntiles = 0;
+  int push_G = 0, push_B = 0;
   SamoPeerSlots* slots = nullptr;       // this rank's signal area (in the block)
   // Backward sinks: first tile of every layer; per-layer row/column-block k
   // tables of the fused dW sink (built on first use).
@@ -765,6 +770,7 @@ int samo_model_destroy(samo_model* md) {
     if (e) cudaEventDestroy(e);
   for (auto p : md->dw_kb)
     if (p) cudaFree(p);
+  if (md->push_tiles) cudaFree(md->push_tiles);
   if (md->block) cudaFree(md->block);
   delete md;
   return clear_ok();
@@ -1073,6 +1079,10 @@ static int exchange_mode(const samo_model* md) {
 //   -> allreduce(norm^2)               [NCCL, 8 bytes: also the barrier]
 //   -> expand every tile from theta16c -> scalars.
 static int p2p_buckets(int G);
+static bool p2p_push();
+static int plan_shards(samo_model* md, ShardPlan& p, int B);
+static int build_push_tiles(samo_model* md, const ShardPlan& p);
+static int launch_gather_push(samo_model* md, cudaStream_t S);
 static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather);
 
 // gather = false: the backward sinks have already written grad16 (and the
@@ -1084,8 +1094,18 @@ static int step_p2p(samo_model* md, cudaStream_t S, bool gather = true) {
   if (static_cast<uint64_t>(G) * c + 8 > md->n_al + kFlagOff)
     return fail(SAMO_E_PARAMETER, "too many ranks for the arena padding");
   float* flag = flag_ptr(md);
+  const bool push = gather && p2p_push();
+  if (push) {
+    SAMO_TRY(plan_shards(md, md->p2p_plan, 1));
+    if (md->p2p_plan.c != c) return fail(SAMO_E_STATE, "P2P plan mismatch");
+    SAMO_TRY(build_push_tiles(md, md->p2p_plan));
+  }
   SAMO_TRY(phase_mark(md, 0, S));
-  if (gather) SAMO_TRY(launch_gather(step_args(md), false, md->grid_gather16, S));
+  if (push) {
+    SAMO_TRY(launch_gather_push(md, S));
+  } else if (gather) {
+    SAMO_TRY(launch_gather(step_args(md), false, md->grid_gather16, S));
+  }
   SAMO_TRY(phase_mark(md, 1, S));
   ncclResult_t rr = ncclAllReduce(flag, flag, 1, ncclFloat32, ncclSum, md->comm->flag, S);
   if (rr != ncclSuccess) return nccl_fail(rr, "ncclAllReduce(flag)");
@@ -1114,6 +1134,10 @@ static int step_p2p(samo_model* md, cudaStream_t S, bool gather = true) {
   pa.done = md->done;
   pa.bucket = -1;
   pa.tma = env_int("SAMO_P2P_TMA", 0);
+  pa.push = push ? 1 : 0;
+  pa.recv = reinterpret_cast<const uint16_t*>(md->g);
+  pa.rstride = c;  // one bucket: [G][c]
+  pa.i0 = 0;
   if (pa.k1 > pa.k0) {
     SAMO_TRY(launch_shard_p2p(pa, S));
   } else {
@@ -1134,10 +1158,11 @@ static int step_p2p(samo_model* md, cudaStream_t S, bool gather = true) {
 }
 
 static int shard_buckets() { return std::max(1, std::min(env_int("SAMO_SHARD_BUCKETS", 4), 16)); }
-// Pipelining pays once the shard update is NVLink-bound (G >= 4);
-// at G = 2 its HBM traffic (12n of theta/m/v) already matches the expand's.
+// Buckets of the P2P step (DESIGN §7 sweeps): 8 from G = 3 — the pipelined
+// schedule's peer-signalled flag exchange also avoids the NCCL barrier that
+// stalls behind K1's NVLink pushes; at G = 2 one bucket is as fast.
 static int p2p_buckets(int G) {
-  return std::max(1, std::min(env_int("SAMO_P2P_BUCKETS", G >= 4 ? 8 : 1), kMaxP2PBuckets));
+  return std::max(1, std::min(env_int("SAMO_P2P_BUCKETS", G >= 3 ? 8 : 1), kMaxP2PBuckets));
 }
 
 // One data-parallel step, ZeRO-1 style on the compressed state, pipelined
@@ -1280,6 +1305,63 @@ static int step_sharded(samo_model* md, cudaStream_t S) {
   return SAMO_OK;
 }
 
+// Push mode of the P2P step (SAMO_P2P_PUSH, default on): K1 writes every
+// kept gradient straight into its owner's receive buffer over NVLink, so the
+// reduce-scatter traffic rides under K1's HBM-bound gather and the shard
+// update reads all G contributions locally.  Receive buffer of rank r = its
+// gradient arena as binary16, [G][B * c]: source q's element k (bucket b,
+// owner r) at q * B * c + b * c + (k - b * C - r * c).
+static bool p2p_push() { return env_int("SAMO_P2P_PUSH", 1) != 0; }
+
+static int build_push_tiles(samo_model* md, const ShardPlan& p) {
+  if (md->push_tiles && md->push_G == p.G && md->push_B == p.B) return SAMO_OK;
+  const uint64_t q = static_cast<uint64_t>(md->comm->rank);
+  std::vector<SamoTile> out;
+  out.reserve(md->ntiles + 2ull * p.G * p.B);
+  for (uint32_t t = 0; t < md->ntiles; ++t) {
+    SamoTile td = md->tiles_host[t];
+    if (td.k_end <= td.k_begin) {
+      td.pad_ = 0;
+      td.pad2_ = 0;
+      out.push_back(td);
+      continue;
+    }
+    for (uint64_t cur = td.k_begin; cur < td.k_end;) {
+      const uint64_t b = std::min<uint64_t>(cur / p.C, p.B - 1);
+      const uint64_t r = (cur - b * p.C) / p.c;
+      const uint64_t end = std::min<uint64_t>(td.k_end, b * p.C + (r + 1) * p.c);
+      SamoTile piece = td;
+      piece.k_begin = cur;
+      piece.k_end = end;
+      piece.pad_ = static_cast<uint32_t>(r);
+      piece.pad2_ = q * p.B * p.c + b * p.c + (cur - b * p.C - r * p.c);
+      out.push_back(piece);
+      cur = end;
+    }
+  }
+  if (md->push_tiles) cudaFree(md->push_tiles);
+  md->push_tiles = nullptr;
+  SAMO_CUDA_TRY(cudaMalloc(&md->push_tiles, out.size() * sizeof(SamoTile)));
+  SAMO_CUDA_TRY(cudaMemcpy(md->push_tiles, out.data(), out.size() * sizeof(SamoTile), cudaMemcpyHostToDevice));
+  md->push_ntiles = static_cast<uint32_t>(out.size());
+  md->push_G = p.G;
+  md->push_B = p.B;
+  return SAMO_OK;
+}
+
+// K1 of the P2P step in push mode.
+static int launch_gather_push(samo_model* md, cudaStream_t S) {
+  StepArgs a = step_args(md);
+  a.tiles = md->push_tiles;
+  a.ntiles = md->push_ntiles;
+  a.push = 1;
+  const char* base = static_cast<const char*>(md->block);
+  const size_t g_off = reinterpret_cast<const char*>(md->g) - base;
+  for (int q = 0; q < md->comm->nranks; ++q)
+    a.push16[q] = reinterpret_cast<uint16_t*>(static_cast<char*>(md->peer_base[q]) + g_off);
+  return launch_gather(a, false, std::min<int>(md->grid_gather16, std::max<uint32_t>(1, a.ntiles)), S);
+}
+
 // The fused peer-to-peer step, pipelined over B k-buckets with no NCCL on
 // it at all: the barriers are release/acquire signals in the ranks' peer-
 // mapped SamoPeerSlots (bucket b = arena range [b*C, (b+1)*C), rank r owns
@@ -1308,6 +1390,8 @@ static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather
   }
   cudaStream_t E = md->s_comm;
   float* flag = flag_ptr(md);
+  const bool push = gather && p2p_push();
+  if (push) SAMO_TRY(build_push_tiles(md, p));
   const char* base = static_cast<const char*>(md->block);
   const size_t g_off = reinterpret_cast<const char*>(md->g) - base;
   const size_t c_off = reinterpret_cast<const char*>(md->c16) - base;
@@ -1336,8 +1420,15 @@ static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather
   pa.grid = sms * std::max(1, env_int("SAMO_P2P_SHARD_CTAS", pa.tma ? 1 : 2));
   const int ge = std::min(md->grid_expand, sms * std::max(1, env_int("SAMO_P2P_EXPAND_CTAS", 2)));
 
+  pa.push = push ? 1 : 0;
+  pa.recv = reinterpret_cast<const uint16_t*>(md->g);
+  pa.rstride = static_cast<uint64_t>(B) * p.c;
   SAMO_TRY(phase_mark(md, 0, S));
-  if (gather) SAMO_TRY(launch_gather(step_args(md), false, md->grid_gather16, S));
+  if (push) {
+    SAMO_TRY(launch_gather_push(md, S));
+  } else if (gather) {
+    SAMO_TRY(launch_gather(step_args(md), false, md->grid_gather16, S));
+  }
   SAMO_TRY(phase_mark(md, 1, S));
   SAMO_TRY(launch_p2p_flag(pa.slots, G, r, flag, S));
   SAMO_TRY(phase_mark(md, 2, S));
@@ -1346,6 +1437,7 @@ static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather
   for (int b = 0; b < B; ++b) {
     pa.k0 = std::min<uint64_t>(b * p.C + r * p.c, md->n_tot);
     pa.k1 = std::min<uint64_t>(b * p.C + (r + 1) * p.c, md->n_tot);
+    pa.i0 = static_cast<uint64_t>(b) * p.c;
     pa.bucket = b;
     SAMO_TRY(launch_shard_p2p(pa, S));  // also when empty: it signals
   }
@@ -1592,6 +1684,11 @@ int samo_model_step_graph(samo_model* md, samo_stream_t stream) {
     // captured); the instantiated graph is then launched on the caller's.
     if (!md->capture_stream)
       SAMO_CUDA_TRY(cudaStreamCreateWithFlags(&md->capture_stream, cudaStreamNonBlocking));
+    // Host-side planning (allocations, synchronous uploads) before capture.
+    if (comm_size(md) > 1 && exchange_mode(md) == SAMO_EXCHANGE_P2P && md->p2p_ok && p2p_push()) {
+      SAMO_TRY(plan_shards(md, md->p2p_plan, p2p_buckets(comm_size(md))));
+      SAMO_TRY(build_push_tiles(md, md->p2p_plan));
+    }
     const uint64_t before = samo_kernel_launch_count();
     SAMO_CUDA_TRY(cudaStreamBeginCapture(md->capture_stream, cudaStreamCaptureModeThreadLocal));
     int rc = samo_model_step(md, md->capture_stream);

@@ -32,6 +32,8 @@ struct ExpandArgs {
 int launch_tiles_fill(SamoTile* tiles, uint32_t ntiles, const uint64_t* k_off,
                       const uint32_t* idx, cudaStream_t s);
 
+constexpr int kMaxP2PRanks = 8;
+
 // Arguments of the two per-step kernels (kernels_fused.cu).
 struct StepArgs {
   const SamoTile* tiles;
@@ -52,6 +54,11 @@ struct StepArgs {
   const float* norm_all;       // every partial of the step (read when finalize)
   uint32_t norm_count;
   uint32_t finalize;           // 1 on the step's last update launch
+  // K1 push mode (peer-to-peer step): tile t's kept elements go to rank
+  // tiles[t].pad_'s receive buffer push16[pad_] at element pad2_ + (k - k_begin)
+  // instead of g + k (binary16 output only).
+  uint32_t push;
+  uint16_t* push16[kMaxP2PRanks];
 };
 
 // K1 gather: out_f32 -> unscaled fp32 for the exchange, else raw binary16.
@@ -64,7 +71,6 @@ int step_grid(int which, bool wide, uint32_t tile_elems);
 // rank `rank` owns [k0, k1) of the compressed arena; it reads that range of
 // every rank's binary16 gradient over NVLink, sums in rank order, runs Adam
 // and writes the binary16 weights into every rank's theta16c arena.
-constexpr int kMaxP2PRanks = 8;
 constexpr int kMaxP2PBuckets = 32;
 // Signal area of the pipelined peer-to-peer step, one per rank inside its
 // IPC-mapped model block.  Rank q writes only the [q] columns of its peers'
@@ -100,6 +106,11 @@ struct P2PArgs {
   int bucket;
   int grid;                           // 0 = default
   int tma;                            // 1: k_shard_p2p_tma (TMA ring), 0: register loads
+  // Push mode: every rank's K1 already wrote its contribution for [k0, k1)
+  // into this rank's receive buffer: rank q's at recv[q * rstride + i0 + (k - k0)].
+  int push;
+  const uint16_t* recv;
+  uint64_t rstride, i0;
 };
 int launch_shard_p2p(const P2PArgs& a, cudaStream_t s);
 // Skip-flag exchange over peer memory (one warp): publishes this rank's

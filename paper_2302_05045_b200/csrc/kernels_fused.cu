@@ -127,6 +127,12 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
   for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++it) {
     const int s = static_cast<int>(it % NS);
     const SamoTile td = a.tiles[t];
+    // binary16 destination of element k: the local arena, or (push) the
+    // owner's receive buffer over NVLink (tile-constant shift, same k % 8)
+    uint16_t* g16 = reinterpret_cast<uint16_t*>(a.g);
+    if (!OUT_F32 && a.push)
+      g16 = reinterpret_cast<uint16_t*>(reinterpret_cast<uintptr_t>(a.push16[td.pad_]) +
+                                        2 * (td.pad2_ - td.k_begin));
     const uint16_t* gsrc = a.layers[td.layer].grad + td.dense_begin;
     const uint32_t staged = ((td.dense_count * 2u) & ~15u) >> 1;
     const uint16_t* sg = reinterpret_cast<const uint16_t*>(smem + static_cast<size_t>(s) * T * 2);
@@ -148,7 +154,7 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
         st_na_f32(reinterpret_cast<float*>(a.g) + k, gk);
       } else {
         bad |= (h & 0x7C00u) == 0x7C00u;  // |h * 2^-s| is finite iff h is
-        st_na_u16(reinterpret_cast<uint16_t*>(a.g) + k, h);
+        st_na_u16(g16 + k, h);
       }
     };
     if (tid < ka - kb0) gather_one(kb0 + tid);
@@ -182,7 +188,7 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
 #pragma unroll
         for (int e = 0; e < 4; ++e)
           bad |= ((hw[e] & 0x7C00u) == 0x7C00u) | ((hw[e] & 0x7C000000u) == 0x7C000000u);
-        st_na_v4u(reinterpret_cast<uint16_t*>(a.g) + k, hw[0], hw[1], hw[2], hw[3]);
+        st_na_v4u(g16 + k, hw[0], hw[1], hw[2], hw[3]);
       }
     }
     __syncthreads();  // every thread is done reading stage s
@@ -194,6 +200,7 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
       }
     }
   }
+  if (!OUT_F32 && a.push) asm volatile("fence.acq_rel.sys;" ::: "memory");  // peer stores visible system-wide
   if (__syncthreads_or(bad) && tid == 0) atomicAdd(a.flag_slot, 1.0f);
 }
 
@@ -671,7 +678,7 @@ __device__ __forceinline__ void shard_finish(const P2PArgs& a, float nacc, float
   }
 }
 
-template <int G>
+template <int G, bool PUSH>
 __global__ void __launch_bounds__(kThreads, SAMO_P2P_MINB) k_shard_p2p(P2PArgs a) {
   __shared__ float red[kThreads / 32];
   __shared__ int last_cta;
@@ -692,8 +699,14 @@ __global__ void __launch_bounds__(kThreads, SAMO_P2P_MINB) k_shard_p2p(P2PArgs a
     const uint64_t left = a.k1 - k;
     const int cnt = left < 8 ? static_cast<int>(left) : 8;
     uint4 h[G];
+    if constexpr (PUSH) {  // every rank's contribution is already in the local receive buffer
+      const uint16_t* src = a.recv + a.i0 + (k - a.k0);
 #pragma unroll
-    for (int r = 0; r < G; ++r) h[r] = ld_peer_v4(a.g16[r] + k);  // arenas are padded
+      for (int r = 0; r < G; ++r) h[r] = ld_stream_v4(src + r * a.rstride);
+    } else {
+#pragma unroll
+      for (int r = 0; r < G; ++r) h[r] = ld_peer_v4(a.g16[r] + k);  // arenas are padded
+    }
     float th[8], mm[8], vv[8];
     if (cnt == 8) {
       const float4 t0 = *reinterpret_cast<const float4*>(a.theta + k);
@@ -1083,7 +1096,7 @@ static int launch_shard_tma(const P2PArgs& a, cudaStream_t s) {
 
 int launch_shard_p2p(const P2PArgs& a, cudaStream_t s) {
   if (a.G < 2 || a.G > kMaxP2PRanks) return fail(SAMO_E_PARAMETER, "peer-to-peer exchange supports 2..8 ranks");
-  if (a.tma) {
+  if (a.tma && !a.push) {
     switch (a.G) {
       case 2: return launch_shard_tma<2>(a, s);
       case 3: return launch_shard_tma<3>(a, s);
@@ -1098,15 +1111,22 @@ int launch_shard_p2p(const P2PArgs& a, cudaStream_t s) {
   const uint64_t cap = a.grid > 0 ? a.grid : static_cast<uint64_t>(num_sms()) * SAMO_P2P_GRID;
   const int grid = static_cast<int>(
       std::max<uint64_t>(1, std::min<uint64_t>(cap, (nv + kThreads - 1) / kThreads)));
+#define SAMO_SHARD_CASE(GG)                                                   \
+  case GG:                                                                    \
+    if (a.push) k_shard_p2p<GG, true><<<grid, kThreads, 0, s>>>(a);           \
+    else k_shard_p2p<GG, false><<<grid, kThreads, 0, s>>>(a);                 \
+    break;
   switch (a.G) {
-    case 2: k_shard_p2p<2><<<grid, kThreads, 0, s>>>(a); break;
-    case 3: k_shard_p2p<3><<<grid, kThreads, 0, s>>>(a); break;
-    case 4: k_shard_p2p<4><<<grid, kThreads, 0, s>>>(a); break;
-    case 5: k_shard_p2p<5><<<grid, kThreads, 0, s>>>(a); break;
-    case 6: k_shard_p2p<6><<<grid, kThreads, 0, s>>>(a); break;
-    case 7: k_shard_p2p<7><<<grid, kThreads, 0, s>>>(a); break;
-    default: k_shard_p2p<8><<<grid, kThreads, 0, s>>>(a); break;
+    SAMO_SHARD_CASE(2)
+    SAMO_SHARD_CASE(3)
+    SAMO_SHARD_CASE(4)
+    SAMO_SHARD_CASE(5)
+    SAMO_SHARD_CASE(6)
+    SAMO_SHARD_CASE(7)
+    SAMO_SHARD_CASE(8)
+    default: return fail(SAMO_E_PARAMETER, "peer-to-peer exchange supports 2..8 ranks");
   }
+#undef SAMO_SHARD_CASE
   SAMO_LAUNCH_CHECK("k_shard_p2p");
   return SAMO_OK;
 }
