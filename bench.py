@@ -504,21 +504,26 @@ def run_samo(args) -> None:
         hbm_kernels = list(kern)
     else:
         # Production data-parallel step (fused P2P exchange), per rank
-        # (DESIGN.md §7): K1 2phi + 2n off16 + 2n grad16; shard update: own
-        # theta/m/v r+w 24n/G + every rank reading this rank's grad16 (2n) +
-        # every owner storing binary16 weights here (2n); over NVLink per
-        # direction 2n(G-1)/G loads + 2n(G-1)/G stores; expand 2n theta16c +
-        # 2n off16 + 2phi.
+        # (DESIGN.md §7), push mode (default): K1 2phi + 2n off16 + 2n grad16,
+        # the grad16 of other owners' shards going out over NVLink
+        # (2n(G-1)/G per direction); shard update: the G contributions to the
+        # own shard from the local receive buffer (2n) + own theta/m/v r+w
+        # 24n/G + every owner storing binary16 weights here (2n), binary16
+        # weights out over NVLink 2n(G-1)/G per direction; expand 2n
+        # theta16c + 2n off16 + 2phi.  Pull mode (SAMO_P2P_PUSH=0): the shard
+        # kernel also loads the other ranks' grad16 over NVLink.
         G = world
+        push = os.environ.get("SAMO_P2P_PUSH", "1") != "0"
         ph = list(phases.values())
         sh_ms, ex_ms = ph[2], ph[4]
         k1_ms = ph[0]
         b_k1 = 2 * phi + 4 * nnz
         b_sh = 24 * nnz // G + 4 * nnz
-        b_nv = 4 * nnz * (G - 1) // G
+        b_nv = (2 if push else 4) * nnz * (G - 1) // G
         b_ex = 2 * phi + 4 * nnz
         kern = {
-            "K1_gather": {"ms": k1_ms, "bytes": b_k1, "GBps": b_k1 / (k1_ms * 1e-3) / 1e9},
+            "K1_gather": {"ms": k1_ms, "bytes": b_k1, "GBps": b_k1 / (k1_ms * 1e-3) / 1e9,
+                          "nvlink_bytes_per_direction": (2 * nnz * (G - 1) // G) if push else 0},
             "shard_update_p2p": {"ms": sh_ms, "bytes": b_sh, "GBps": b_sh / (sh_ms * 1e-3) / 1e9,
                                  "nvlink_bytes_per_direction": b_nv,
                                  "nvlink_GBps_per_direction": b_nv / (sh_ms * 1e-3) / 1e9,
@@ -650,10 +655,11 @@ def run_samo(args) -> None:
                        "gpu": gpu_name},
             "gpu_launches": int(launches),
             "step_mode": "K1 | K23 (no exchange)" if world == 1 else
-                         ("p2p (ZeRO-1, exchange fused over NVLink, no NCCL): K1 | peer-signalled "
-                          "flag exchange | per k-bucket: shard kernel loads every rank's binary16 "
-                          "grads, rank-ordered fp32 sum, Adam, stores binary16 weights to every "
-                          "rank, signals the bucket || expand of the signalled buckets"
+                         ("p2p (ZeRO-1, exchange fused over NVLink, no NCCL): K1 pushes each kept "
+                          "binary16 grad into its owner's receive buffer | peer-signalled flag "
+                          "exchange | per k-bucket: shard kernel sums the G local contributions "
+                          "in rank order, Adam, stores binary16 weights to every rank, signals "
+                          "the bucket || expand of the signalled buckets"
                           if model.exchange_mode() == model.EXCHANGE_P2P else
                           "sharded (ZeRO-1), k-bucketed: K1 || NCCL reduce-scatter, shard Adam, "
                           "NCCL all-gather of binary16 weights || expand"
