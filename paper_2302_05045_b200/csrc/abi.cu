@@ -1080,6 +1080,8 @@ static int exchange_mode(const samo_model* md) {
 //   -> expand every tile from theta16c -> scalars.
 static int p2p_buckets(int G);
 static bool p2p_push();
+static bool p2p_pull();
+static void set_pull_args(samo_model* md, const ShardPlan& p, StepArgs& a);
 static int plan_shards(samo_model* md, ShardPlan& p, int B);
 static int build_push_tiles(samo_model* md, const ShardPlan& p);
 static int launch_gather_push(samo_model* md, cudaStream_t S);
@@ -1095,11 +1097,10 @@ static int step_p2p(samo_model* md, cudaStream_t S, bool gather = true) {
     return fail(SAMO_E_PARAMETER, "too many ranks for the arena padding");
   float* flag = flag_ptr(md);
   const bool push = gather && p2p_push();
-  if (push) {
-    SAMO_TRY(plan_shards(md, md->p2p_plan, 1));
-    if (md->p2p_plan.c != c) return fail(SAMO_E_STATE, "P2P plan mismatch");
-    SAMO_TRY(build_push_tiles(md, md->p2p_plan));
-  }
+  const bool pull = p2p_pull();
+  SAMO_TRY(plan_shards(md, md->p2p_plan, 1));
+  if (md->p2p_plan.c != c) return fail(SAMO_E_STATE, "P2P plan mismatch");
+  if (push) SAMO_TRY(build_push_tiles(md, md->p2p_plan));
   SAMO_TRY(phase_mark(md, 0, S));
   if (push) {
     SAMO_TRY(launch_gather_push(md, S));
@@ -1138,6 +1139,7 @@ static int step_p2p(samo_model* md, cudaStream_t S, bool gather = true) {
   pa.recv = reinterpret_cast<const uint16_t*>(md->g);
   pa.rstride = c;  // one bucket: [G][c]
   pa.i0 = 0;
+  pa.local_c16 = pull ? 1 : 0;
   if (pa.k1 > pa.k0) {
     SAMO_TRY(launch_shard_p2p(pa, S));
   } else {
@@ -1149,6 +1151,7 @@ static int step_p2p(samo_model* md, cudaStream_t S, bool gather = true) {
   SAMO_TRY(phase_mark(md, 4, S));
   StepArgs a = step_args(md);
   a.g = md->c16;
+  if (pull) set_pull_args(md, md->p2p_plan, a);
   SAMO_TRY(launch_expand_c16(a, std::min<int>(md->grid_expand, md->ntiles), S));
   SAMO_TRY(phase_mark(md, 5, S));
   SAMO_TRY(launch_step_finalize(md->st, md->norm2, 1, flag, md->cfg.beta1, md->cfg.beta2, S));
@@ -1312,6 +1315,23 @@ static int step_sharded(samo_model* md, cudaStream_t S) {
 // gradient arena as binary16, [G][B * c]: source q's element k (bucket b,
 // owner r) at q * B * c + b * c + (k - b * C - r * c).
 static bool p2p_push() { return env_int("SAMO_P2P_PUSH", 1) != 0; }
+// Pull mode of the expand (SAMO_P2P_PULL=1, off by default): each owner keeps
+// its binary16 weights in its own theta16c arena and every rank's expand
+// pulls them over NVLink with its TMA loads.  Measured: the shard
+// update drops 0.62 -> 0.46 ms at G = 4 but the expand rises 1.03 -> 1.29 ms
+// (any ring depth), so pushing the weights stays the default.
+static bool p2p_pull() { return env_int("SAMO_P2P_PULL", 0) != 0; }
+
+static void set_pull_args(samo_model* md, const ShardPlan& p, StepArgs& a) {
+  a.pull = 1;
+  a.pB = static_cast<uint32_t>(p.B);
+  a.pc = p.c;
+  a.pC = p.C;
+  const char* base = static_cast<const char*>(md->block);
+  const size_t c_off = reinterpret_cast<const char*>(md->c16) - base;
+  for (int q = 0; q < md->comm->nranks; ++q)
+    a.peer16c[q] = reinterpret_cast<const uint16_t*>(static_cast<const char*>(md->peer_base[q]) + c_off);
+}
 
 static int build_push_tiles(samo_model* md, const ShardPlan& p) {
   if (md->push_tiles && md->push_G == p.G && md->push_B == p.B) return SAMO_OK;
@@ -1391,6 +1411,7 @@ static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather
   cudaStream_t E = md->s_comm;
   float* flag = flag_ptr(md);
   const bool push = gather && p2p_push();
+  const bool pull = p2p_pull();
   if (push) SAMO_TRY(build_push_tiles(md, p));
   const char* base = static_cast<const char*>(md->block);
   const size_t g_off = reinterpret_cast<const char*>(md->g) - base;
@@ -1423,6 +1444,7 @@ static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather
   pa.push = push ? 1 : 0;
   pa.recv = reinterpret_cast<const uint16_t*>(md->g);
   pa.rstride = static_cast<uint64_t>(B) * p.c;
+  pa.local_c16 = pull ? 1 : 0;
   SAMO_TRY(phase_mark(md, 0, S));
   if (push) {
     SAMO_TRY(launch_gather_push(md, S));
@@ -1441,7 +1463,8 @@ static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather
     pa.bucket = b;
     SAMO_TRY(launch_shard_p2p(pa, S));  // also when empty: it signals
   }
-  const StepArgs sbase = step_args(md);
+  StepArgs sbase = step_args(md);
+  if (pull) set_pull_args(md, p, sbase);
   for (int b = 0; b < B; ++b) {
     SAMO_TRY(launch_p2p_wait(md->slots, G, b, E));
     StepArgs a = sbase;

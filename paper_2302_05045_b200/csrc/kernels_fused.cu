@@ -326,7 +326,23 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
                                  : static_cast<const void*>(reinterpret_cast<const float*>(a.g) + f0);
           if constexpr (EXPAND) {  // theta/m/v slots unused; hb > 0 here
             mbar_arrive_expect_tx(&full[s], 2 * hb);
-            bulk_g2s(st + 3 * L::kF32, gsrc, hb, &full[s], policy);
+            if (a.pull) {
+              // pull each owner's part of [h0, h0 + hb/2) over NVLink; owner
+              // boundaries are multiples of 8 elements, so pieces stay 16-byte aligned
+              const uint64_t h1 = h0 + hb / 2;
+              for (uint64_t cur = h0; cur < h1;) {
+                uint64_t b = cur / a.pC;
+                if (b >= a.pB) b = a.pB - 1;
+                const uint64_t r = (cur - b * a.pC) / a.pc;
+                uint64_t end = b * a.pC + (r + 1) * a.pc;
+                if (end > h1) end = h1;
+                bulk_g2s_peer(st + 3 * L::kF32 + (cur - h0) * 2, a.peer16c[r] + cur,
+                              static_cast<uint32_t>((end - cur) * 2), &full[s]);
+                cur = end;
+              }
+            } else {
+              bulk_g2s(st + 3 * L::kF32, gsrc, hb, &full[s], policy);
+            }
             bulk_g2s(st + 3 * L::kF32 + L::kG, a.off16 + h0, hb, &full[s], policy);
           } else {
             // kc1 > kc0, so every range rounded out to 16 bytes is non-empty.
@@ -760,7 +776,8 @@ __global__ void __launch_bounds__(kThreads, SAMO_P2P_MINB) k_shard_p2p(P2PArgs a
     }
     const uint4 pv = make_uint4(packed[0], packed[1], packed[2], packed[3]);
 #pragma unroll
-    for (int r = 0; r < G; ++r) *reinterpret_cast<uint4*>(a.c16[r] + k) = pv;  // arenas are padded
+    for (int r = 0; r < G; ++r)
+      if (!a.local_c16 || r == a.rank) *reinterpret_cast<uint4*>(a.c16[r] + k) = pv;  // arenas are padded
   }
   shard_finish<G, kThreads>(a, nacc, red, &last_cta);
 }
@@ -900,7 +917,8 @@ __global__ void __launch_bounds__(32 * (kShardConsumers + 1)) k_shard_p2p_tma(P2
       }
       const uint4 pv = make_uint4(packed[0], packed[1], packed[2], packed[3]);
 #pragma unroll
-      for (int r = 0; r < G; ++r) *reinterpret_cast<uint4*>(a.c16[r] + kk) = pv;  // arenas are padded
+      for (int r = 0; r < G; ++r)
+        if (!a.local_c16 || r == a.rank) *reinterpret_cast<uint4*>(a.c16[r] + kk) = pv;  // arenas are padded
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -1168,6 +1186,11 @@ int launch_step_finalize(SamoStepState* st, const double* norm2, int nslots, flo
   return SAMO_OK;
 }
 
+static int env_ns() {
+  const char* e = getenv("SAMO_EXPAND_PULL_NS");
+  return (e && *e) ? atoi(e) : 6;
+}
+
 int expand_grid(uint32_t tile_elems) {
   return grid_for(k23_update<true, 1024, 3, true>, k23_smem<true, 1024, 3, true>(tile_elems),
                   kThreads + 32);
@@ -1176,6 +1199,14 @@ int expand_grid(uint32_t tile_elems) {
 int launch_expand_c16(const StepArgs& a, int grid, cudaStream_t s) {
   if (a.ntiles == 0) return SAMO_OK;
   if (grid <= 0) grid = expand_grid(a.tile_elems);
+  // Pulled weights (NVLink latency) get a deeper ring (SAMO_EXPAND_PULL_NS).
+  const int ns = a.pull ? env_ns() : 3;
+  if (ns >= 8)
+    return launch_persistent(k23_update<true, 1024, 8, true>, a, k23_smem<true, 1024, 8, true>(a.tile_elems),
+                             grid, s, kThreads + 32, "k23_expand");
+  if (ns >= 6)
+    return launch_persistent(k23_update<true, 1024, 6, true>, a, k23_smem<true, 1024, 6, true>(a.tile_elems),
+                             grid, s, kThreads + 32, "k23_expand");
   return launch_persistent(k23_update<true, 1024, 3, true>, a, k23_smem<true, 1024, 3, true>(a.tile_elems),
                            grid, s, kThreads + 32, "k23_expand");
 }
