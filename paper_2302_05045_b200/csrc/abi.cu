@@ -1,8 +1,10 @@
 // abi.cu — the C ABI (include/samo_cuda.h): argument checks with the
 // reference's error taxonomy, the plain API-parity entry points, the model
-// state (flat device arenas + tile table + device scalars), the step driver
-// (gather -> NCCL exchange -> update, optionally as one CUDA graph) and the
-// NCCL communicator.
+// state (flat device arenas + tile table + device scalars), the step drivers
+// (single GPU: K1 -> K23; data parallel: the peer-to-peer step over CUDA-IPC
+// peer memory — push-mode K1, peer-signalled barriers, bucketed shard update
+// || expand — or the NCCL sharded / allreduce steps; any of them as one CUDA
+// graph), the backward sinks, checkpoints and the NCCL communicator.
 #include <nccl.h>
 
 #include <algorithm>

@@ -1,8 +1,8 @@
-// kernels_fused.cu — the two per-step kernels of the SAMO path (sm_100a).
+// kernels_fused.cu — the per-step kernels of the SAMO path (sm_100a).
 //
 // Data layout (per rank, HBM):
 //   dense side : per-layer binary16 gradients (inputs) and theta16 (outputs),
-//                cut into tiles of T dense elements (T = tile_elems, 8192 by
+//                cut into tiles of T dense elements (T = tile_elems, 16384 by
 //                default, <= 65536).
 //   compressed : flat arenas theta32 / adam_m / adam_v / grad and the tile-
 //                local index arena off16 (layer segments concatenated in layer
@@ -15,21 +15,30 @@
 //
 // K1 gather (train.hpp:598-611 sink + 619-629 unscale/finite):
 //   TMA ring of dense gradient tiles (cp.async.bulk + mbarrier complete_tx);
-//   kept elements gathered out of shared memory through off16, written with
-//   coalesced stores — unscaled fp32 when the gradient is exchanged between
-//   ranks, the raw compressed binary16 (the reference's grad16) otherwise.
-//   Non-finite gradients raise the step's skip flag.
+//   kept elements gathered out of shared memory through off16, 8 per thread,
+//   written with 16/32-byte stores — unscaled fp32 for the NCCL exchanges,
+//   the raw compressed binary16 (the reference's grad16) otherwise, or, in
+//   the peer-to-peer step's push mode, straight into the owner rank's receive
+//   buffer over NVLink.  Non-finite gradients raise the step's skip flag.
 //
 // K23 update (train.hpp:632-654, adam_update 332-347, expand store.hpp:72-87):
-//   TMA ring over chunks of <= kChunk kept elements; a stage holds the
-//   16-byte aligned superset of theta32/m/v/grad/off16 of the chunk.  Per tile
-//   the dense theta16 tile is built in shared memory (zero fill + scatter of
-//   half_rn(theta) at off16) and written back with one bulk store,
-//   double-buffered against the next tile.  theta/m/v are written straight
-//   from registers with coalesced stores.  The last CTA reduces the per-CTA
-//   grad-norm partials in CTA order and advances the device Adam scalars.
+//   warp-specialised: one producer warp streams the 16-byte aligned supersets
+//   of theta32/m/v/grad/off16 per <= 1024-element chunk through a TMA ring
+//   (full/empty mbarriers); eight consumer warps run the IEEE Adam from
+//   shared memory, write theta/m/v from registers, scatter half_rn(theta)
+//   into a dense tile in shared memory and copy it out with 128-bit stores
+//   that also clear it (one named barrier per tile).  The last CTA reduces
+//   the per-CTA grad-norm partials (fixed order) and advances the device
+//   Adam scalars.  EXPAND = true is the expand-only pass of the data-
+//   parallel steps (binary16 weights in, no Adam).
 //
-// Both kernels are persistent (grid = resident CTAs x SMs) and HBM-bound.
+// Data-parallel pieces: k_adam_shard (NCCL sharded exchange), k_shard_p2p /
+// k_shard_p2p_tma (fused peer-to-peer exchange: rank-ordered sum of the G
+// contributions, Adam, binary16 weights stored to every rank, bucket
+// signals), the peer-signal kernels (flag exchange, bucket wait, epoch) and
+// k_step_finalize.
+//
+// The step kernels are persistent (grid = resident CTAs x SMs) and HBM-bound.
 #include <cstdio>
 #include <cstdlib>
 
