@@ -244,13 +244,18 @@ int samo_model_attach_comm(samo_model* model, samo_comm* comm);
  *    authoritative only on the rank's shard (samo_model_shard_layout);
  *    theta16 everywhere.  The exchange is pipelined over k-buckets
  *    (SAMO_SHARD_BUCKETS, default 4) behind the gather and expand kernels.
- *  SAMO_EXCHANGE_P2P — the sharded update with the exchange fused into it:
- *    every rank's shard kernel loads its shard of all ranks' binary16
- *    gradients over NVLink (CUDA IPC peer mappings made by
- *    samo_model_attach_comm, which is then collective), sums them in rank
- *    order in fp32 (deterministic, bit-exact with a rank-ordered sum for any
- *    G), runs Adam and stores the binary16 weights into every rank.  NCCL
- *    only carries two 4/8-byte allreduces that double as barriers.
+ *  SAMO_EXCHANGE_P2P — the sharded update with the exchange fused into our
+ *    own kernels over NVLink peer memory (CUDA IPC mappings made by
+ *    samo_model_attach_comm, which is then collective).  Push mode (default):
+ *    K1 writes every kept binary16 gradient straight into its owner rank's
+ *    receive buffer; the shard kernel sums its shard's G contributions in
+ *    rank order in fp32 (deterministic, bit-exact with a rank-ordered sum
+ *    for any G), runs Adam and stores the binary16 weights into every rank.
+ *    From G = 3 the step is pipelined over k-buckets (shard update || expand)
+ *    with release/acquire signals in peer memory as its only barriers — no
+ *    NCCL call at all; at G = 2 two 4/8-byte NCCL allreduces are the
+ *    barriers.  Tuning: SAMO_P2P_BUCKETS, SAMO_P2P_PUSH, SAMO_P2P_PULL,
+ *    SAMO_P2P_TMA.
  * The default is P2P when the peer mappings succeeded on every rank, else
  * SHARDED (environment SAMO_EXCHANGE=allreduce|sharded overrides); mode -1
  * restores the default. */
@@ -271,9 +276,12 @@ int samo_model_shard_layout(samo_model* model, uint64_t* chunk, uint64_t* stride
 
 /* Phase timing of the data-parallel step (CUDA events between its stages;
  * off by default).  samo_model_phase_times writes the durations (ms) of the
- * last step's phases and returns their count (sharded exchange: gather, skip
- * flag allreduce, reduce-scatter, shard Adam, all-gather, norm allreduce,
- * expand, finalize); it synchronises on the last phase. */
+ * last step's phases and returns their count; it synchronises on the last
+ * phase.  Phases: P2P serial — gather, flag allreduce, shard update, norm
+ * allreduce, expand, finalize; P2P pipelined — gather, flag exchange,
+ * shard update || expand, finalize; sharded — gather (+ reduce-scatter),
+ * flag + shard Adam + first all-gather, expand (+ all-gathers), norm +
+ * finalize. */
 int samo_model_enable_phase_timing(samo_model* model, int on);
 int samo_model_phase_times(samo_model* model, float* ms, int cap);
 
