@@ -22,7 +22,7 @@ from paper_2302_05045_b200 import samo  # noqa: E402
 
 DENSE_LEN = [40000, 3000, 100003, 512]
 PRUNABLE = [True, True, True, False]
-STEPS = 4
+STEPS = int(os.environ.get("SAMO_DP_STEPS", "4"))  # the stress variant runs 40
 INF_STEP, INF_RANK = 2, 1
 
 

@@ -28,9 +28,12 @@ def _port() -> int:
         return s.getsockname()[1]
 
 
-def _expected(oracle, world):
+def _expected(oracle, world, steps=4):
     sys.path.insert(0, str(HERE))
+    os.environ["SAMO_DP_STEPS"] = str(steps)
+    import importlib
     import dp_worker as W
+    W = importlib.reload(W)
     from oracle.oracle import Cfg
     vals, sets, grads = W.inputs(oracle, world)
     L = len(W.DENSE_LEN)
@@ -60,8 +63,9 @@ def _expected(oracle, world):
     return theta, m, v, t16, t, skipped
 
 
-def _run(tmp_path, mode, world):
+def _run(tmp_path, mode, world, steps=4):
     env = dict(os.environ)
+    env["SAMO_DP_STEPS"] = str(steps)
     env["SAMO_DP_MODE"] = mode.split("-")[0] if mode.split("-")[0] in ("sharded", "p2p") else "allreduce"
     env["SAMO_OVERLAP"] = "0" if mode == "staged" else "1"
     env["SAMO_DP_GRAPH"] = "1" if mode.endswith("graph") else "0"
@@ -80,8 +84,8 @@ def _run(tmp_path, mode, world):
     return [dict(np.load(tmp_path / f"dp_rank{i}.npz")) for i in range(world)]
 
 
-def _check(r, oracle, world, mode):
-    theta, m, v, t16, t, skipped = _expected(oracle, world)
+def _check(r, oracle, world, mode, steps=4):
+    theta, m, v, t16, t, skipped = _expected(oracle, world, steps)
     covered = 0
     for rr in r:
         assert int(rr["t"][0]) == t and int(rr["skipped"][0]) == skipped == 1
@@ -126,3 +130,11 @@ def test_dp_three_gpus_p2p_bit_exact(tmp_path, oracle):
     if torch.cuda.device_count() < 3:
         pytest.skip("needs 3 GPUs")
     _check(_run(tmp_path, "p2p", 3), oracle, 3, "p2p")
+
+
+def test_dp_four_gpus_p2p_stress(tmp_path, oracle):
+    """40 pipelined push-mode steps: the peer-signal epochs wrap through many
+    steps and every replica must still equal the oracle bit for bit."""
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    _check(_run(tmp_path, "p2p", 4, steps=40), oracle, 4, "p2p", steps=40)
