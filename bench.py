@@ -667,6 +667,7 @@ def run_samo(args) -> None:
                           else "allreduce: bucketed NCCL allreduce overlapped with K1/K23"),
             "phases_ms": phases,
             "pipeline_phases_ms": pipeline,
+            "p2p_features": model.p2p_features() if world > 1 else None,
             "roofline": roofline,
             "kernels": kern,
             "e2e": e2e,

@@ -268,6 +268,17 @@ enum samo_exchange_mode {
 int samo_model_set_exchange(samo_model* model, int mode);
 /* SAMO_EXCHANGE_NONE without a communicator of size > 1. */
 int samo_model_exchange_mode(const samo_model* model);
+/* Which peer-to-peer mechanisms this model's step uses (bitmask): peer
+ * mappings made, K1 push, expand pull, NVLS multicast of the binary16
+ * weights (SAMO_P2P_NVLS=0 disables; set up at attach time, agreed by every
+ * rank, otherwise the weights are stored to each peer). */
+enum samo_p2p_feature {
+  SAMO_P2P_MAPPED = 1,
+  SAMO_P2P_PUSH = 2,
+  SAMO_P2P_PULL = 4,
+  SAMO_P2P_NVLS = 8
+};
+int samo_model_p2p_features(const samo_model* model);
 /* Compressed-arena elements this rank updates: for b in [0, buckets) the
  * range [b*stride + rank*chunk, b*stride + (rank+1)*chunk) clipped to the
  * arena (chunk = stride = nnz, buckets = 1, rank = 0 unless sharded). */

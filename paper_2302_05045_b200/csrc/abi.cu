@@ -5,7 +5,12 @@
 // peer memory — push-mode K1, peer-signalled barriers, bucketed shard update
 // || expand — or the NCCL sharded / allreduce steps; any of them as one CUDA
 // graph), the backward sinks, checkpoints and the NCCL communicator.
+#include <cuda.h>
 #include <nccl.h>
+#include <poll.h>
+#include <sys/socket.h>
+#include <sys/un.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -357,6 +362,8 @@ struct samo_comm {
   ncclComm_t flag = nullptr;  // the skip indicator, concurrently with the buckets
   int nranks = 1;
   int rank = 0;
+  uint8_t uid[SAMO_UNIQUE_ID_BYTES] = {};  // names the local rendezvous socket of the NVLS setup
+  int nvls_seq = 0;                        // one multicast object per attached model
 };
 
 static int nccl_fail(ncclResult_t r, const char* what) {
@@ -384,6 +391,7 @@ int samo_comm_create(const uint8_t id[SAMO_UNIQUE_ID_BYTES], int nranks, int ran
   auto* c = new samo_comm();
   c->nranks = nranks;
   c->rank = rank;
+  std::memcpy(c->uid, id, SAMO_UNIQUE_ID_BYTES);
   ncclResult_t r = ncclCommInitRank(&c->comm, nranks, uid, rank);
   if (r != ncclSuccess) {
     delete c;
@@ -495,6 +503,13 @@ struct samo_model {
   // peer-to-peer exchange; p2p_ok is agreed by every rank.
   void* peer_base[kMaxP2PRanks] = {};
   bool p2p_ok = false;
+  // NVLS multicast of the binary16 weights (P2P step): every rank's theta16c
+  // lives in VMM memory bound to one multicast object; the shard kernel
+  // stores each vector once through mc_c16 and the switch replicates it.
+  uint16_t* mc_c16 = nullptr;        // multicast mapping
+  uint16_t* uc_c16 = nullptr;        // this rank's unicast mapping of the bound memory
+  uint64_t nvls_bytes = 0;
+  CUmemGenericAllocationHandle nvls_mem = 0, nvls_mc = 0;
   std::vector<cudaEvent_t> ev_sh;       // sharded pipeline: K1 and all-gather events
   int grid_expand = 0;
   // Phase timing of the data-parallel step.
@@ -519,12 +534,262 @@ static int phase_mark(samo_model* md, int i, cudaStream_t s) {
 
 static uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 
+static void close_nvls(samo_model* md);
+
 static void close_peers(samo_model* md) {
+  close_nvls(md);
   for (int q = 0; q < kMaxP2PRanks; ++q) {
     if (md->peer_base[q] && md->peer_base[q] != md->block) cudaIpcCloseMemHandle(md->peer_base[q]);
     md->peer_base[q] = nullptr;
   }
   md->p2p_ok = false;
+}
+
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return (e && *e) ? atoi(e) : dflt;
+}
+
+// ---------------------------------------------------------------------------
+// NVLS multicast for the P2P weight push (SAMO_P2P_NVLS, default on).  Driver
+// API through cudaGetDriverEntryPoint (the runtime is linked statically).
+
+struct NvlsApi {
+  decltype(&cuMulticastCreate) mc_create = nullptr;
+  decltype(&cuMulticastAddDevice) mc_add = nullptr;
+  decltype(&cuMulticastBindMem) mc_bind = nullptr;
+  decltype(&cuMulticastUnbind) mc_unbind = nullptr;
+  decltype(&cuMulticastGetGranularity) mc_gran = nullptr;
+  decltype(&cuMemCreate) mem_create = nullptr;
+  decltype(&cuMemRelease) mem_release = nullptr;
+  decltype(&cuMemAddressReserve) va_reserve = nullptr;
+  decltype(&cuMemAddressFree) va_free = nullptr;
+  decltype(&cuMemMap) mem_map = nullptr;
+  decltype(&cuMemUnmap) mem_unmap = nullptr;
+  decltype(&cuMemSetAccess) set_access = nullptr;
+  decltype(&cuMemExportToShareableHandle) export_h = nullptr;
+  decltype(&cuMemImportFromShareableHandle) import_h = nullptr;
+  decltype(&cuMemGetAllocationGranularity) mem_gran = nullptr;
+  decltype(&cuCtxGetDevice) ctx_device = nullptr;
+  bool ok = false;
+};
+
+static const NvlsApi& nvls_api() {
+  static NvlsApi api;
+  static bool init = false;
+  if (init) return api;
+  init = true;
+  auto get = [](const char* name, auto& fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+      return false;
+    fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(p);
+    return true;
+  };
+  api.ok = get("cuMulticastCreate", api.mc_create) && get("cuMulticastAddDevice", api.mc_add) &&
+           get("cuMulticastBindMem", api.mc_bind) && get("cuMulticastUnbind", api.mc_unbind) &&
+           get("cuMulticastGetGranularity", api.mc_gran) && get("cuMemCreate", api.mem_create) &&
+           get("cuMemRelease", api.mem_release) && get("cuMemAddressReserve", api.va_reserve) &&
+           get("cuMemAddressFree", api.va_free) && get("cuMemMap", api.mem_map) &&
+           get("cuMemUnmap", api.mem_unmap) && get("cuMemSetAccess", api.set_access) &&
+           get("cuMemExportToShareableHandle", api.export_h) &&
+           get("cuMemImportFromShareableHandle", api.import_h) &&
+           get("cuMemGetAllocationGranularity", api.mem_gran) && get("cuCtxGetDevice", api.ctx_device);
+  cudaGetLastError();
+  return api;
+}
+
+// min over ranks of `ok` (a barrier as well).
+static int agree(samo_comm* c, int* ok) {
+  int* d = nullptr;
+  cudaStream_t s = nullptr;
+  SAMO_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  int rc = SAMO_OK;
+  cudaError_t e = cudaMalloc(&d, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d, ok, sizeof(int), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) {
+    const ncclResult_t nr = ncclAllReduce(d, d, 1, ncclInt32, ncclMin, c->comm, s);
+    if (nr != ncclSuccess) rc = nccl_fail(nr, "ncclAllReduce(agree)");
+  }
+  if (rc == SAMO_OK && e == cudaSuccess) e = cudaMemcpyAsync(ok, d, sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (rc == SAMO_OK && e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (rc == SAMO_OK && e != cudaSuccess) rc = cuda_fail(e, "agree");
+  if (d) cudaFree(d);
+  cudaStreamDestroy(s);
+  return rc;
+}
+
+// Rank 0 hands the multicast object's file descriptor to the other ranks of
+// this node over an abstract Unix socket named after the communicator id.
+static void nvls_sock_name(const samo_comm* c, int seq, sockaddr_un* a, socklen_t* len) {
+  std::memset(a, 0, sizeof(*a));
+  a->sun_family = AF_UNIX;
+  char name[96];
+  int n = std::snprintf(name, sizeof(name), "samo-nvls-");
+  for (int i = 0; i < 12; ++i) n += std::snprintf(name + n, sizeof(name) - n, "%02x", c->uid[i]);
+  n += std::snprintf(name + n, sizeof(name) - n, "-%d", seq);
+  std::memcpy(a->sun_path + 1, name, n);  // leading NUL: abstract namespace
+  *len = static_cast<socklen_t>(offsetof(sockaddr_un, sun_path) + 1 + n);
+}
+
+static bool send_fd(int sock, int fd) {
+  char byte = 0;
+  iovec iov{&byte, 1};
+  char ctl[CMSG_SPACE(sizeof(int))] = {};
+  msghdr msg{};
+  msg.msg_iov = &iov;
+  msg.msg_iovlen = 1;
+  msg.msg_control = ctl;
+  msg.msg_controllen = sizeof(ctl);
+  cmsghdr* cm = CMSG_FIRSTHDR(&msg);
+  cm->cmsg_level = SOL_SOCKET;
+  cm->cmsg_type = SCM_RIGHTS;
+  cm->cmsg_len = CMSG_LEN(sizeof(int));
+  std::memcpy(CMSG_DATA(cm), &fd, sizeof(int));
+  return sendmsg(sock, &msg, 0) == 1;
+}
+
+static int recv_fd(int sock) {
+  char byte = 0;
+  iovec iov{&byte, 1};
+  char ctl[CMSG_SPACE(sizeof(int))] = {};
+  msghdr msg{};
+  msg.msg_iov = &iov;
+  msg.msg_iovlen = 1;
+  msg.msg_control = ctl;
+  msg.msg_controllen = sizeof(ctl);
+  if (recvmsg(sock, &msg, 0) != 1) return -1;
+  cmsghdr* cm = CMSG_FIRSTHDR(&msg);
+  if (!cm || cm->cmsg_type != SCM_RIGHTS) return -1;
+  int fd = -1;
+  std::memcpy(&fd, CMSG_DATA(cm), sizeof(int));
+  return fd;
+}
+
+static void close_nvls(samo_model* md) {
+  const NvlsApi& api = nvls_api();
+  if (!api.ok) return;
+  if (md->mc_c16) {
+    api.mem_unmap(reinterpret_cast<CUdeviceptr>(md->mc_c16), md->nvls_bytes);
+    api.va_free(reinterpret_cast<CUdeviceptr>(md->mc_c16), md->nvls_bytes);
+  }
+  if (md->uc_c16) {
+    api.mem_unmap(reinterpret_cast<CUdeviceptr>(md->uc_c16), md->nvls_bytes);
+    api.va_free(reinterpret_cast<CUdeviceptr>(md->uc_c16), md->nvls_bytes);
+  }
+  if (md->nvls_mem) api.mem_release(md->nvls_mem);
+  if (md->nvls_mc) api.mem_release(md->nvls_mc);
+  md->mc_c16 = md->uc_c16 = nullptr;
+  md->nvls_mem = md->nvls_mc = 0;
+  md->nvls_bytes = 0;
+}
+
+// Collective (after open_peers succeeded).  Any failure on any rank leaves
+// every rank on the peer-store path.
+static int open_nvls(samo_model* md) {
+  samo_comm* c = md->comm;
+  const int G = c->nranks, r = c->rank;
+  const NvlsApi& api = nvls_api();
+  const bool dbg = env_int("SAMO_NVLS_DEBUG", 0) != 0;
+  auto chk = [&](const char* what, CUresult e) {
+    if (e != CUDA_SUCCESS && dbg) std::fprintf(stderr, "[samo nvls] rank %d: %s failed (%d)\n", r, what, int(e));
+    return e == CUDA_SUCCESS;
+  };
+  if (dbg && !api.ok) std::fprintf(stderr, "[samo nvls] rank %d: driver entry points missing\n", r);
+  int ok = (api.ok && env_int("SAMO_P2P_NVLS", 1) != 0) ? 1 : 0;
+  SAMO_TRY(agree(c, &ok));
+  if (!ok) return SAMO_OK;
+  const int seq = c->nvls_seq++;
+  CUdevice dev = 0;
+  CUmulticastObjectProp mp{};
+  CUmemAllocationProp ap{};
+  size_t gran = 0, g2 = 0;
+  int fd = -1;
+  ok = chk("cuCtxGetDevice", api.ctx_device(&dev));
+  if (ok) {
+    ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    ap.location.id = static_cast<int>(dev);
+    ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;  // bindable to the multicast object
+    mp.numDevices = static_cast<unsigned>(G);
+    mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    mp.size = 2 * (md->n_al + kArenaSlack) * sizeof(uint16_t);
+    ok = chk("cuMulticastGetGranularity", api.mc_gran(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED)) &&
+         chk("cuMemGetAllocationGranularity", api.mem_gran(&g2, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+    gran = std::max(gran, g2);
+    if (ok) mp.size = (mp.size + gran - 1) / gran * gran;
+  }
+  if (ok && r == 0) {
+    ok = chk("cuMulticastCreate", api.mc_create(&md->nvls_mc, &mp)) &&
+         chk("cuMemExportToShareableHandle", api.export_h(&fd, md->nvls_mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+  }
+  SAMO_TRY(agree(c, &ok));
+  // file descriptor hand-over (rank 0 serves G - 1 connections)
+  if (ok) {
+    sockaddr_un addr;
+    socklen_t alen;
+    nvls_sock_name(c, seq, &addr, &alen);
+    if (r == 0) {
+      const int ls = socket(AF_UNIX, SOCK_STREAM, 0);
+      ok = ls >= 0 && bind(ls, reinterpret_cast<sockaddr*>(&addr), alen) == 0 && listen(ls, G) == 0;
+      for (int i = 1; ok && i < G; ++i) {
+        pollfd pf{ls, POLLIN, 0};
+        if (poll(&pf, 1, 30000) != 1) { ok = 0; break; }
+        const int cs = accept(ls, nullptr, nullptr);
+        ok = cs >= 0 && send_fd(cs, fd);
+        if (cs >= 0) close(cs);
+      }
+      if (ls >= 0) close(ls);
+    } else {
+      int got = -1;
+      for (int attempt = 0; attempt < 3000 && got < 0; ++attempt) {  // up to ~30 s for rank 0 to listen
+        const int cs = socket(AF_UNIX, SOCK_STREAM, 0);
+        if (cs < 0) break;
+        if (connect(cs, reinterpret_cast<sockaddr*>(&addr), alen) == 0) got = recv_fd(cs);
+        close(cs);
+        if (got < 0) usleep(10000);
+      }
+      if (got < 0 && dbg) std::fprintf(stderr, "[samo nvls] rank %d: no file descriptor from rank 0\n", r);
+      ok = got >= 0 && chk("cuMemImportFromShareableHandle",
+                           api.import_h(&md->nvls_mc, reinterpret_cast<void*>(static_cast<intptr_t>(got)),
+                                        CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR));
+      if (got >= 0) close(got);
+    }
+  }
+  if (fd >= 0) close(fd);
+  SAMO_TRY(agree(c, &ok));
+  if (ok) ok = chk("cuMulticastAddDevice", api.mc_add(md->nvls_mc, dev));
+  SAMO_TRY(agree(c, &ok));  // every device added before any bind
+  if (ok) {
+    md->nvls_bytes = mp.size;
+    CUdeviceptr uc = 0, mc = 0;
+    CUmemAccessDesc acc{};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = static_cast<int>(dev);
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    ok = chk("cuMemCreate", api.mem_create(&md->nvls_mem, mp.size, &ap, 0)) &&
+         chk("cuMulticastBindMem", api.mc_bind(md->nvls_mc, 0, md->nvls_mem, 0, mp.size, 0)) &&
+         chk("cuMemAddressReserve", api.va_reserve(&uc, mp.size, gran, 0, 0));
+    if (ok) {
+      ok = chk("cuMemMap(uc)", api.mem_map(uc, mp.size, 0, md->nvls_mem, 0)) &&
+           chk("cuMemSetAccess(uc)", api.set_access(uc, mp.size, &acc, 1));
+      if (ok) md->uc_c16 = reinterpret_cast<uint16_t*>(uc);
+      else api.va_free(uc, mp.size);
+    }
+    if (ok) ok = api.va_reserve(&mc, mp.size, gran, 0, 0) == CUDA_SUCCESS;
+    if (ok) {
+      ok = chk("cuMemMap(mc)", api.mem_map(mc, mp.size, 0, md->nvls_mc, 0)) &&
+           chk("cuMemSetAccess(mc)", api.set_access(mc, mp.size, &acc, 1));
+      if (ok) md->mc_c16 = reinterpret_cast<uint16_t*>(mc);
+      else api.va_free(mc, mp.size);
+    }
+  }
+  cudaGetLastError();
+  SAMO_TRY(agree(c, &ok));
+  if (!ok) close_nvls(md);
+  if (dbg) std::fprintf(stderr, "[samo nvls] rank %d: multicast %s\n", r, ok ? "on" : "off");
+  return SAMO_OK;
 }
 
 // Collective over the attached communicator: exchanges the CUDA IPC handles
@@ -597,7 +862,7 @@ static int open_peers(samo_model* md) {
     return rc;
   }
   md->p2p_ok = true;
-  return SAMO_OK;
+  return open_nvls(md);
 }
 
 extern "C" {
@@ -969,11 +1234,6 @@ static StepArgs step_args(samo_model* md) {
   return a;
 }
 
-static int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return (e && *e) ? atoi(e) : dflt;
-}
-
 // Splits the tiles into contiguous buckets of about equal kept-element count.
 static int plan_buckets(samo_model* md) {
   if (md->nbuckets > 0) return SAMO_OK;
@@ -1142,6 +1402,8 @@ static int step_p2p(samo_model* md, cudaStream_t S, bool gather = true) {
   pa.rstride = c;  // one bucket: [G][c]
   pa.i0 = 0;
   pa.local_c16 = pull ? 1 : 0;
+  const bool nvls = md->mc_c16 && !pull;
+  pa.mc16 = nvls ? md->mc_c16 : nullptr;
   if (pa.k1 > pa.k0) {
     SAMO_TRY(launch_shard_p2p(pa, S));
   } else {
@@ -1152,7 +1414,7 @@ static int step_p2p(samo_model* md, cudaStream_t S, bool gather = true) {
   if (rr != ncclSuccess) return nccl_fail(rr, "ncclAllReduce(norm)");
   SAMO_TRY(phase_mark(md, 4, S));
   StepArgs a = step_args(md);
-  a.g = md->c16;
+  a.g = nvls ? md->uc_c16 : md->c16;
   if (pull) set_pull_args(md, md->p2p_plan, a);
   SAMO_TRY(launch_expand_c16(a, std::min<int>(md->grid_expand, md->ntiles), S));
   SAMO_TRY(phase_mark(md, 5, S));
@@ -1447,6 +1709,8 @@ static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather
   pa.recv = reinterpret_cast<const uint16_t*>(md->g);
   pa.rstride = static_cast<uint64_t>(B) * p.c;
   pa.local_c16 = pull ? 1 : 0;
+  const bool nvls = md->mc_c16 && !pull;
+  pa.mc16 = nvls ? md->mc_c16 : nullptr;
   SAMO_TRY(phase_mark(md, 0, S));
   if (push) {
     SAMO_TRY(launch_gather_push(md, S));
@@ -1470,7 +1734,7 @@ static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather
   for (int b = 0; b < B; ++b) {
     SAMO_TRY(launch_p2p_wait(md->slots, G, b, E));
     StepArgs a = sbase;
-    a.g = md->c16;
+    a.g = nvls ? md->uc_c16 : md->c16;
     a.tiles = md->tiles + p.ex_t[b];
     a.ntiles = p.ex_t[b + 1] - p.ex_t[b];
     if (a.ntiles) SAMO_TRY(launch_expand_c16(a, std::min<int>(ge, a.ntiles), E));
@@ -1515,6 +1779,16 @@ int samo_model_phase_times(samo_model* md, float* ms, int cap) {
   if (cudaEventSynchronize(md->phase_ev[n]) != cudaSuccess) return -fail(SAMO_E_CUDA, "event sync");
   for (int i = 0; i < n; ++i) cudaEventElapsedTime(&ms[i], md->phase_ev[i], md->phase_ev[i + 1]);
   return n;
+}
+
+int samo_model_p2p_features(const samo_model* md) {
+  if (!md || comm_size(md) <= 1) return 0;
+  int f = 0;
+  if (md->p2p_ok) f |= SAMO_P2P_MAPPED;
+  if (md->p2p_ok && p2p_push()) f |= SAMO_P2P_PUSH;
+  if (md->p2p_ok && p2p_pull()) f |= SAMO_P2P_PULL;
+  if (md->mc_c16 && !p2p_pull()) f |= SAMO_P2P_NVLS;
+  return f;
 }
 
 int samo_model_exchange_mode(const samo_model* md) {

@@ -119,6 +119,7 @@ struct P2PArgs {
   const uint16_t* recv;
   uint64_t rstride, i0;
   int local_c16;                      // store the binary16 weights only locally (pulled by the expand)
+  uint16_t* mc16;                     // NVLS: store each weight vector once through this multicast mapping
 };
 int launch_shard_p2p(const P2PArgs& a, cudaStream_t s);
 // Skip-flag exchange over peer memory (one warp): publishes this rank's

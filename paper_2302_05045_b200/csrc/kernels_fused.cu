@@ -667,7 +667,9 @@ __device__ __forceinline__ uint16_t half_lane(const uint4& v, int e) {
 // pipelined step, publishes bucket completion + norm^2 to every rank.
 template <int G, int NT>
 __device__ __forceinline__ void shard_finish(const P2PArgs& a, float nacc, float* red, int* last_cta) {
-  // Make the peer stores visible system-wide before the kernel retires.
+  // Make the peer (or multicast) stores visible system-wide before the
+  // kernel retires and before the completion signals below.
+  if (a.mc16) asm volatile("fence.proxy.alias;" ::: "memory");
   asm volatile("fence.acq_rel.sys;" ::: "memory");
   float x = nacc;
 #pragma unroll
@@ -784,9 +786,13 @@ __global__ void __launch_bounds__(kThreads, SAMO_P2P_MINB) k_shard_p2p(P2PArgs a
       }
     }
     const uint4 pv = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+    if (a.mc16) {
+      multimem_st_v4(a.mc16 + k, pv);
+    } else {
 #pragma unroll
-    for (int r = 0; r < G; ++r)
-      if (!a.local_c16 || r == a.rank) *reinterpret_cast<uint4*>(a.c16[r] + k) = pv;  // arenas are padded
+      for (int r = 0; r < G; ++r)
+        if (!a.local_c16 || r == a.rank) *reinterpret_cast<uint4*>(a.c16[r] + k) = pv;  // arenas are padded
+    }
   }
   shard_finish<G, kThreads>(a, nacc, red, &last_cta);
 }
@@ -925,9 +931,12 @@ __global__ void __launch_bounds__(32 * (kShardConsumers + 1)) k_shard_p2p_tma(P2
         }
       }
       const uint4 pv = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-#pragma unroll
-      for (int r = 0; r < G; ++r)
-        if (!a.local_c16 || r == a.rank) *reinterpret_cast<uint4*>(a.c16[r] + kk) = pv;  // arenas are padded
+      if (a.mc16) {
+        multimem_st_v4(a.mc16 + kk, pv);
+      } else {
+        for (int r = 0; r < G; ++r)
+          if (!a.local_c16 || r == a.rank) *reinterpret_cast<uint4*>(a.c16[r] + kk) = pv;  // arenas are padded
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);

@@ -403,6 +403,11 @@ class SamoModel:
     def exchange(self) -> None:
         _abi.call("samo_model_exchange", self._h, _stream())
 
+    def p2p_features(self) -> dict:
+        """Peer-to-peer mechanisms in use: mapped, push, pull, nvls."""
+        f = int(_abi.load().samo_model_p2p_features(self._h))
+        return {"mapped": bool(f & 1), "push": bool(f & 2), "pull": bool(f & 4), "nvls": bool(f & 8)}
+
     def step_sunk(self) -> None:
         """The step after the backward sinks: exchange (peer-to-peer) + update."""
         _abi.call("samo_model_step_sunk", self._h, _stream())
