@@ -270,8 +270,9 @@ int samo_model_set_exchange(samo_model* model, int mode);
 int samo_model_exchange_mode(const samo_model* model);
 /* Which peer-to-peer mechanisms this model's step uses (bitmask): peer
  * mappings made, K1 push, expand pull, NVLS multicast of the binary16
- * weights (SAMO_P2P_NVLS=0 disables; set up at attach time, agreed by every
- * rank, otherwise the weights are stored to each peer). */
+ * weights (opt-in with SAMO_P2P_NVLS=1 before samo_model_attach_comm; set
+ * up at attach time, agreed by every rank, otherwise the weights are stored
+ * to each peer). */
 enum samo_p2p_feature {
   SAMO_P2P_MAPPED = 1,
   SAMO_P2P_PUSH = 2,

@@ -133,7 +133,9 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // NVLS multicast store: one 16-byte store through a multicast mapping lands
 // in every GPU bound to the multicast object (replicated by the NVSwitch).
 __device__ __forceinline__ void multimem_st_v4(void* mc, const uint4& v) {
-  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc),
+  // weak: ordered for the readers by the fence.proxy.alias + fence.acq_rel.sys
+  // + release signal that follow the kernel's stores
+  asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc),
                "f"(__uint_as_float(v.x)), "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)),
                "f"(__uint_as_float(v.w))
                : "memory");

@@ -76,6 +76,7 @@ def _run(tmp_path, mode, world, steps=4):
     env["SAMO_P2P_TMA"] = "1" if mode == "p2p-tma" else "0"  # TMA-fed shard kernel
     env["SAMO_DP_SINK"] = "1" if mode == "p2p-sink" else "0"  # per-layer sinks + step_sunk
     env["SAMO_P2P_PULL"] = "1" if mode == "p2p-pull" else "0"  # expand pulls the weights
+    env["SAMO_P2P_NVLS"] = "1" if mode == "p2p-nvls" else "0"  # multicast weight stores
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            str(HERE / "dp_worker.py"), str(tmp_path)]
@@ -107,7 +108,8 @@ def _check(r, oracle, world, mode, steps=4):
     assert covered == (n if mode.split("-")[0] in ("sharded", "p2p") else world * n)
 
 
-@pytest.mark.parametrize("mode", ["p2p", "p2p-serial", "p2p-graph", "p2p-tma", "p2p-sink", "p2p-pull", "sharded", "sharded-graph", "overlap",
+@pytest.mark.parametrize("mode", ["p2p", "p2p-serial", "p2p-graph", "p2p-tma", "p2p-sink", "p2p-pull",
+                                  "p2p-nvls", "sharded", "sharded-graph", "overlap",
                                   "staged", "graph"])
 def test_dp_two_gpus_bit_exact(tmp_path, oracle, mode):
     if torch.cuda.device_count() < 2:
@@ -115,7 +117,8 @@ def test_dp_two_gpus_bit_exact(tmp_path, oracle, mode):
     _check(_run(tmp_path, mode, 2), oracle, 2, mode)
 
 
-@pytest.mark.parametrize("mode", ["p2p", "p2p-serial", "p2p-graph", "p2p-tma", "p2p-sink", "p2p-pull"])
+@pytest.mark.parametrize("mode", ["p2p", "p2p-serial", "p2p-graph", "p2p-tma", "p2p-sink", "p2p-pull",
+                                  "p2p-nvls"])
 def test_dp_four_gpus_p2p_bit_exact(tmp_path, oracle, mode):
     """The fused exchange sums in rank order: bit-exact for G = 4 too."""
     if torch.cuda.device_count() < 4:
