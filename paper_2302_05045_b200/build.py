@@ -19,8 +19,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libsamo_cuda.so"
-SOURCES = ["abi.cu", "kernels_step.cu", "kernels_fused.cu", "kernels_prune.cu", "kernels_gemm.cu"]
-HEADERS = ["common.cuh", "kernels.cuh"]
+SOURCES = ["abi.cu", "model.cu", "dp.cu", "kernels_step.cu", "kernels_fused.cu", "kernels_prune.cu", "kernels_gemm.cu"]
+HEADERS = ["common.cuh", "kernels.cuh", "host.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [

@@ -18,9 +18,11 @@ namespace samo_dev {
 // Host-side status plumbing.
 
 void set_error(const char* fmt, ...);
+void clear_error();
 int fail(int status, const char* fmt, ...);
 int cuda_fail(cudaError_t err, const char* what);
 void note_launch(uint64_t n = 1);
+void unnote_launch(uint64_t n);  // captured into a graph, not launched
 int device_ok();  // SAMO_OK when a CUDA device is usable, else SAMO_E_CUDA
 
 #define SAMO_CUDA_TRY(expr)                                   \
