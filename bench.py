@@ -50,7 +50,8 @@ def parse_args():
     ap.add_argument("--seed", type=int, default=1234)
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = min(steps, 10)")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-fused", action="store_true", help="skip the fused dW-GEMM sink probe")
+    ap.add_argument("--no-fused", action="store_true",
+                    help="skip the side probes (fused dW-GEMM sink, FC-layer sweep of config 2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-blocks", type=int, default=0, help="GPT blocks in the CPU sample")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/CPU legs)")
@@ -283,6 +284,57 @@ def fused_sink_probe(reps: int = 10) -> dict:
             "cublas_ms": t_cublas, "cublas_tflops": flops / t_cublas / 1e9,
             "unfused_sink_ms": t_unfused, "fused_sink_ms": t_fused,
             "fused_saving": 1 - t_fused / t_unfused}
+
+
+def fc_sweep_probe(reps: int = 200, cpu: bool = True) -> list:
+    """BASELINE config 2 (config 1 = its 4096 row): one [n, n]
+    FC layer, 90% magnitude mask (K0), loss-scaled binary16 gradients.  The
+    device step as a CUDA graph — L2-resident, so this is latency, reported
+    per step — next to the reference's own step (oracle/_ref: sink gather +
+    SamoTrainer::optimizer_step, single thread as shipped) on the same data."""
+    import numpy as np
+    import torch
+
+    from paper_2302_05045_b200 import samo, workloads
+    ref_reps = {128: 1000, 256: 300, 512: 100, 1024: 30, 2048: 10, 4096: 3}
+    out = []
+    for n in (128, 256, 512, 1024, 2048, 4096):
+        wl = workloads.fc(n, 0.9)
+        t = wl.tensors[0]
+        w = samo.synth_uniform_f32(t.numel, 7, 0, t.init_bound)
+        sets = samo.magnitude_prune([samo.LayerParams(t.name, w, True)], 0.9)
+        m = samo.SamoModel.from_index_sets(sets, [t.shape])
+        m.init_layer(0, w)
+        m.set_config(samo.OptimizerConfig())
+        theta0 = m.read(0, "theta32").cpu().numpy()
+        g = samo.synth_uniform_f16(t.numel, 8, 1, 2.0**-7, 1024.0)
+        m.set_grads([g])
+        for _ in range(10):
+            m.step(graph=True)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            m.step(graph=True)
+        b.record()
+        b.synchronize()
+        us = a.elapsed_time(b) * 1000.0 / reps
+        entry = {"workload": wl.name, "params": t.numel, "kept": int(sets[0].count()),
+                 "step_us": us, "params_per_s": t.numel / (us * 1e-6)}
+        if cpu:
+            try:
+                idx = sets[0].indices.cpu().numpy().view(np.uint32)
+                gh = g.cpu().numpy().view(np.uint16)
+                dt, _ = cpu_reference_sample([t.numel], [idx], [theta0], [gh],
+                                             (1e-3, 0.9, 0.999, 1e-8, 1024.0, 0.0), reps=ref_reps[n])
+                entry["reference_cpu_us"] = dt * 1e6
+                entry["speedup_vs_reference"] = dt * 1e6 / us
+            except Exception as ex:  # no oracle/_ref on this host
+                entry["reference_cpu_us"] = None
+                entry["reference_error"] = str(ex)
+        m.close()
+        out.append(entry)
+    return out
 
 
 def run_samo(args) -> None:
@@ -630,12 +682,16 @@ def run_samo(args) -> None:
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                    "sample": f"failed: {ex}"}
 
-    fused = None
+    fused = fc_sweep = None
     if world == 1 and not (args.profile or args.no_fused):
         try:
             fused = fused_sink_probe()
         except Exception as ex:  # a probe failure must not drop the headline line
             fused = {"error": str(ex)}
+        try:
+            fc_sweep = fc_sweep_probe(cpu=not args.no_cpu_baseline)
+        except Exception as ex:
+            fc_sweep = [{"error": str(ex)}]
 
     if rank == 0:
         line = {
@@ -672,6 +728,7 @@ def run_samo(args) -> None:
             "e2e": e2e,
             "cpu_baseline": cpu,
             "fused_dw_sink": fused,
+            "fc_sweep": fc_sweep,
             "clocks": clk.summary(),
             "step_record": {"t": int(rec.t), "skipped": int(rec.skipped_steps),
                             "grad_norm": float(rec.grad_norm)},
