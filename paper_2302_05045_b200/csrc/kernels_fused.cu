@@ -112,6 +112,8 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
     fence_mbar_init();
   }
   __syncthreads();
+  // a PDL-launched K23 may begin its own setup now (no effect otherwise)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   auto issue = [&](uint32_t t, int s) {
     const SamoTile td = a.tiles[t];
@@ -302,6 +304,9 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
     fence_mbar_init();
   }
   __syncthreads();  // the only CTA-wide barrier
+  // PDL: everything above is local setup; K1's gradients and skip flag are
+  // read only after the previous grid has completed (no-op without PDL).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == kConsumerWarps) {
     // ---- producer warp: one elected lane walks the CTA's chunks and keeps
@@ -1089,11 +1094,28 @@ int step_grid(int which, bool wide, uint32_t tile_elems) {
 
 template <typename F>
 static int launch_persistent(F fn, const StepArgs& a, size_t sm, int grid, cudaStream_t s, int threads,
-                             const char* what) {
+                             const char* what, bool pdl = false) {
   SAMO_CUDA_TRY(
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
   if (static_cast<uint32_t>(grid) > a.ntiles) grid = static_cast<int>(a.ntiles);
-  fn<<<grid, threads, sm, s>>>(a);
+  if (pdl) {
+    // Programmatic dependent launch: the kernel may start (set up its
+    // barriers and shared memory) while the previous one drains; it waits
+    // with griddepcontrol.wait before reading that kernel's results.
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SAMO_CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, a));
+  } else {
+    fn<<<grid, threads, sm, s>>>(a);
+  }
   SAMO_LAUNCH_CHECK(what);
   return SAMO_OK;
 }
@@ -1110,8 +1132,10 @@ int launch_gather(const StepArgs& a, bool out_f32, int grid, cudaStream_t s) {
 int launch_update(const StepArgs& a, bool g_f32, int grid, cudaStream_t s) {
   if (a.ntiles == 0) return SAMO_OK;
   if (grid <= 0) grid = step_grid(1, g_f32, a.tile_elems);
+  const char* e = getenv("SAMO_PDL");
+  const bool pdl = !(e && *e && atoi(e) == 0);
   auto go = [&](auto fn, size_t sm) {
-    return launch_persistent(fn, a, sm, grid, s, kThreads + 32, "k23_update");
+    return launch_persistent(fn, a, sm, grid, s, kThreads + 32, "k23_update", pdl);
   };
   return g_f32 ? with_k23<false>(a.tile_elems, go) : with_k23<true>(a.tile_elems, go);
 }
