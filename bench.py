@@ -243,7 +243,8 @@ def fused_sink_probe(reps: int = 10) -> dict:
     """SURVEY §8(f)-1 (not the headline): one GPT-2.7B MLP layer (4096 tokens,
     2560 x 10240, p = 0.9) — the weight-gradient GEMM with the gather fused
     into its epilogue (samo_model_sink_dw) vs the dense GEMM + K1 on the layer,
-    and cuBLAS for the GEMM alone.  CUDA events, median of `reps`."""
+    and cuBLAS for the GEMM alone.  CUDA events around `reps` back-to-back
+    calls, best of 3."""
     import torch
     from paper_2302_05045_b200 import samo
     batch, n_in, n_out, p = 4096, 2560, 10240, 0.9
@@ -255,18 +256,19 @@ def fused_sink_probe(reps: int = 10) -> dict:
     m = samo.SamoModel.from_index_sets([samo.PrunedIndexSet("mlp.fc_in.weight", n, idx)], [(n_in, n_out)], 0)
     m.init_layer(0, torch.zeros(n, device="cuda"))
 
-    def timed(fn):
+    def timed(fn):  # back-to-back calls between two events, best of 3
         for _ in range(3):
             fn()
-        ts = []
-        for _ in range(reps):
+        best = float("inf")
+        for _ in range(3):
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            fn()
+            for _ in range(reps):
+                fn()
             b.record()
             b.synchronize()
-            ts.append(a.elapsed_time(b))
-        return statistics.median(ts)
+            best = min(best, a.elapsed_time(b) / reps)
+        return best
 
     flops = 2.0 * batch * n_in * n_out
     t_gemm = timed(lambda: samo.dw_gemm(x, dy))

@@ -23,9 +23,9 @@
 //   warp 1      TMEM allocation; MMA issue by one lane of the leader CTA
 //   warps 2..5  epilogue: tcgen05.ld (32 lanes x 32 columns per load), in two
 //               128-column halves; each thread owns one accumulator row
-// Measured (tools/bench_dw.py): 1.07-1.28 PFLOP/s on the
-// GPT-2.7B layer shapes at 4096-8192 tokens, 73-86% of cuBLAS; the fused sink
-// costs the same as the dense GEMM alone.
+// Measured (tools/bench_dw.py): 1.0-1.28 PFLOP/s on the
+// GPT-2.7B layer shapes at 4096-8192 tokens, 72-88% of cuBLAS; the fused sink
+// is within +-7% of the dense GEMM followed by the K1 gather.
 #include "kernels.cuh"
 
 #include <cuda.h>
@@ -437,15 +437,41 @@ int launch_build_rowblocks(const uint32_t* idx, uint64_t n, uint64_t in, uint64_
   return SAMO_OK;
 }
 
+// Tensor maps are encoded on the host (cuTensorMapEncodeTiled, ~µs each);
+// a small cache keyed by (base, rows, cols) keeps repeated launches on the
+// same operands — every training step — free of that host work.
+static int cached_map(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols) {
+  struct Entry {
+    const void* base;
+    uint64_t rows, cols;
+    CUtensorMap map;
+  };
+  static thread_local Entry cache[16];
+  static thread_local unsigned next = 0;
+  for (const Entry& e : cache)
+    if (e.base == base && e.rows == rows && e.cols == cols && base) {
+      *m = e.map;
+      return SAMO_OK;
+    }
+  SAMO_TRY(make_map(m, base, rows, cols));
+  cache[next % 16] = Entry{base, rows, cols, *m};
+  ++next;
+  return SAMO_OK;
+}
+
 int launch_dw_gemm(const uint16_t* x, const uint16_t* dy, const DwArgs& a, int epi, cudaStream_t s) {
   CUtensorMap tx, tdy;
-  SAMO_TRY(make_map(&tx, x, a.K, a.M));
-  SAMO_TRY(make_map(&tdy, dy, a.K, a.N));
+  SAMO_TRY(cached_map(&tx, x, a.K, a.M));
+  SAMO_TRY(cached_map(&tdy, dy, a.K, a.N));
   const uint64_t pairs = ((a.M + 2 * kBM - 1) / (2 * kBM)) * ((a.N + kGemmBN - 1) / kGemmBN);
   const int grid = 2 * static_cast<int>(std::min<uint64_t>(pairs, static_cast<uint64_t>(num_sms() / 2)));
   constexpr uint32_t smem = GemmSmem<kGemmBN, kGemmNS>::kBytes;
   auto fn = epi == 0 ? k_dw_gemm<0, kGemmBN, kGemmNS> : k_dw_gemm<1, kGemmBN, kGemmNS>;
-  SAMO_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[epi != 0]) {
+    SAMO_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set[epi != 0] = true;
+  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kGemmThreads);

@@ -5,7 +5,7 @@
 For each (batch, in, out): our tcgen05 dW GEMM (dense binary16 out), cuBLAS
 via torch.matmul(x.T, dy) for reference, the unfused sink (dense dW GEMM ->
 K1 on the layer) and the fused sink (GEMM with the gather in its epilogue).
-CUDA events, inputs resident in HBM, median of --reps after 3 warm-ups.
+CUDA events around --reps back-to-back calls (best of 3), inputs resident in HBM.
 """
 from __future__ import annotations
 
@@ -31,17 +31,20 @@ SHAPES = [  # (batch tokens, in, out)
 
 
 def timed(fn, reps):
+    """Device time per call: `reps` calls queued back to back between two
+    events (host launch overhead overlaps the previous call), best of 3."""
     for _ in range(3):
         fn()
-    ts = []
-    for _ in range(reps):
+    best = float("inf")
+    for _ in range(3):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        fn()
+        for _ in range(reps):
+            fn()
         b.record()
         b.synchronize()
-        ts.append(a.elapsed_time(b))
-    return statistics.median(ts)
+        best = min(best, a.elapsed_time(b) / reps)
+    return best
 
 
 def main():
@@ -59,13 +62,19 @@ def main():
         m = samo.SamoModel.from_index_sets([samo.PrunedIndexSet("fc.weight", n, idx)], [(n_in, n_out)], 0)
         m.init_layer(0, torch.zeros(n, device="cuda"))
         flops = 2.0 * batch * n_in * n_out
-        t_ours = timed(lambda: samo.dw_gemm(x, dy), args.reps)
-        t_cublas = timed(lambda: torch.matmul(x.t(), dy), args.reps)
         dense = samo.dw_gemm(x, dy).reshape(-1)
         t_k1 = timed(lambda: m.sink_dense(0, dense), args.reps)
-        t_unfused = timed(lambda: (m.sink_dense(0, samo.dw_gemm(x, dy).reshape(-1))), args.reps)
-        t_fused = timed(lambda: m.sink_dw(0, x, dy), args.reps)
-        m._sink_keepalive.clear()
+        # the four contenders round-robin (best of 5 rounds each), so that
+        # power-capped clocks under sustained tensor load hit all alike
+        fns = {"gemm": lambda: samo.dw_gemm(x, dy), "cublas": lambda: torch.matmul(x.t(), dy),
+               "unfused": lambda: m.sink_dense(0, samo.dw_gemm(x, dy).reshape(-1)),
+               "fused": lambda: m.sink_dw(0, x, dy)}
+        best = {k: float("inf") for k in fns}
+        for _ in range(5):
+            for k, fn in fns.items():
+                best[k] = min(best[k], timed(fn, args.reps))
+            m._sink_keepalive.clear()
+        t_ours, t_cublas, t_unfused, t_fused = best["gemm"], best["cublas"], best["unfused"], best["fused"]
         print(json.dumps({
             "batch": batch, "in": n_in, "out": n_out, "p": args.p,
             "dw_gemm_ms": round(t_ours, 4), "dw_gemm_tflops": round(flops / t_ours / 1e9, 1),
