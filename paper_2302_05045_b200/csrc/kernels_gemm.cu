@@ -123,8 +123,11 @@ __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
-// 32 lanes x 32 consecutive fp32 columns of the accumulator.
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+// 32 lanes x 32 consecutive fp32 columns of the accumulator, without the
+// wait, so several loads are in flight at once;
+// tmem_wait32 then waits and ties the registers to the wait ("+r"), so no use
+// of them can be scheduled before it.
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
       "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
@@ -135,7 +138,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
         "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_wait32(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
+                 "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]),
+                 "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]),
+                 "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]),
+                 "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
 }
 
 // Bounded mbarrier wait for the GEMM pipeline: a protocol bug traps (an
@@ -297,20 +309,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             cnt = a.kb[(cb + 1) * a.M + row] - ks;
           }
         }
-        // accumulator half -> binary16 -> staging row r
-#pragma unroll 1
-        for (uint32_t c = 0; c < L::kHalf; c += 32) {
-          uint32_t v[32];
-          tmem_ld32(tmem + ((q * 32u) << 16) + buf * BN + h * L::kHalf + c, v);
-          uint4* dst = reinterpret_cast<uint4*>(tile + r * L::kTileLd + c);
+        // accumulator half -> binary16 -> staging row r: the four 32-column
+        // loads of the half are in flight together, one wait
+        {
+          uint32_t v[L::kHalf / 32][32];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            uint32_t w[4];
+          for (uint32_t cc = 0; cc < L::kHalf / 32; ++cc)
+            tmem_ld32_nowait(tmem + ((q * 32u) << 16) + buf * BN + h * L::kHalf + cc * 32, v[cc]);
 #pragma unroll
-            for (int z = 0; z < 4; ++z)
-              w[z] = f32_to_f16_bits(__uint_as_float(v[8 * e + 2 * z])) |
-                     (static_cast<uint32_t>(f32_to_f16_bits(__uint_as_float(v[8 * e + 2 * z + 1]))) << 16);
-            dst[e] = make_uint4(w[0], w[1], w[2], w[3]);
+          for (uint32_t cc = 0; cc < L::kHalf / 32; ++cc) {
+            tmem_wait32(v[cc]);
+            uint4* dst = reinterpret_cast<uint4*>(tile + r * L::kTileLd + cc * 32);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              uint32_t w[4];
+#pragma unroll
+              for (int z = 0; z < 4; ++z)
+                w[z] = f32_to_f16_bits(__uint_as_float(v[cc][8 * e + 2 * z])) |
+                       (static_cast<uint32_t>(f32_to_f16_bits(__uint_as_float(v[cc][8 * e + 2 * z + 1]))) << 16);
+              dst[e] = make_uint4(w[0], w[1], w[2], w[3]);
+            }
           }
         }
         if (h + 1 == BN / L::kHalf) {  // TMEM buffer drained: the leader's MMA may reuse it
