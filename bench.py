@@ -613,9 +613,23 @@ def run_samo(args) -> None:
 
     # -- e2e: public API with HOST buffers (pinned), copies inside the region --
     e2e = None
-    if not (args.no_e2e or args.profile):
+    e2e_ok = not (args.no_e2e or args.profile)
+    if e2e_ok:
+        # The pinned staging buffer (5.3 GB per rank) is the one allocation
+        # that can fail on a small host; every rank agrees before going on.
+        try:
+            host = torch.empty(off, dtype=torch.float16, pin_memory=True)
+        except Exception as ex:  # noqa: BLE001
+            host, e2e_err = None, str(ex)
+        ok = torch.tensor([1 if host is not None else 0], device=dev, dtype=torch.int32)
+        if world > 1:
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        e2e_ok = bool(ok.item())
+        if not e2e_ok:
+            e2e = {"value": None, "error": f"pinned host staging buffer unavailable: {e2e_err if host is None else 'on another rank'}"}
+            host = None
+    if e2e_ok:
         E = args.e2e_steps or min(K, 10)
-        host = torch.empty(off, dtype=torch.float16, pin_memory=True)
         host.copy_(grad_arena)  # this rank's synthetic gradients, staged on the host
         dbuf = [grad_arena, torch.empty_like(grad_arena)]
         dgrads = [[d[offs[i]:offs[i] + t.numel] for i, t in enumerate(wl.tensors)] for d in dbuf]
