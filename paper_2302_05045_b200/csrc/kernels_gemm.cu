@@ -34,7 +34,8 @@
 namespace samo_dev {
 namespace {
 
-constexpr int kGemmThreads = 192;
+// warps: producer, MMA, then EW groups of four epilogue warps
+constexpr int gemm_threads(int ew) { return 64 + 128 * ew; }
 constexpr uint32_t kBM = 128, kBK = 64;
 constexpr uint32_t kBox = 64 * kBK * 2;  // one 64-element x kBK-row TMA box (LBO between MN chunks)
 
@@ -170,7 +171,7 @@ __device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity
 // the 128-byte swizzle atoms).
 constexpr bool kStage_check(uint32_t a, uint32_t b) { return (a + b) % 1024 == 0; }
 
-template <int BN, int NS>
+template <int BN, int NS, int EW>
 struct GemmSmem {
   static constexpr uint32_t kA = kBM * kBK * 2;    // two 64(M) x kBK(K) boxes
   static constexpr uint32_t kB = (BN / 2) * kBK * 2;  // this SM's half of B: BN/128 boxes
@@ -180,7 +181,7 @@ struct GemmSmem {
   static constexpr uint32_t kTileLd = kHalf + 8;   // halves per staging row (16-byte multiple)
   static constexpr uint32_t kTile = kBM * kTileLd * 2;
   static_assert(kTile % 1024 == 0, "stages must stay 1024-byte aligned");
-  static constexpr uint32_t kBytes = kTile + NS * kStage;
+  static constexpr uint32_t kBytes = EW * kTile + NS * kStage;  // one staging half-tile per epilogue group
 };
 
 // Persistent CTA pairs (cluster of two, tcgen05 cta_group::2): pair c takes
@@ -192,13 +193,15 @@ struct GemmSmem {
 // bandwidth is what bounds the one-SM form).  Both CTAs' TMA loads complete
 // on the leader's full barrier; the leader's commits free the stage in both
 // CTAs and publish the accumulator to both epilogues, whose drain arrivals
-// (8 warps) gate the reuse of a TMEM buffer.  The accumulator is double
+// (4 * EW warps per CTA) gate the reuse of a TMEM buffer.  The accumulator is double
 // buffered (2 x BN columns): the epilogue of tile i overlaps the mainloop of
 // tile i + 1.
-template <int EPI, int BN, int NS>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+// EW = 2: two epilogue groups work on the two 128-column halves at once
+// (short-K problems, where the epilogue would pace the mainloop).
+template <int EPI, int BN, int NS, int EW>
+__global__ void __launch_bounds__(gemm_threads(EW), 1)
     k_dw_gemm(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tdy, DwArgs a) {
-  using L = GemmSmem<BN, NS>;
+  using L = GemmSmem<BN, NS, EW>;
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[NS];
   __shared__ __align__(8) uint64_t empty[NS];
@@ -214,7 +217,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t crank = cluster_ctarank(), cid = cluster_id_x(), ncl = ncluster_x();
   constexpr uint32_t kCols = 2 * BN;  // two accumulator buffers
   static_assert(kCols == 256 || kCols == 512, "TMEM allocation must be a power of two");
-  uint8_t* ring = smem + L::kTile;
+  uint8_t* ring = smem + EW * L::kTile;
   if (threadIdx.x == 0 && (smem_addr(ring) & 1023u)) __trap();  // swizzle atoms need 1024-byte alignment
 
   if (threadIdx.x == 0) {
@@ -224,7 +227,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&accf[b], 1);
-      mbar_init(&acce[b], 8);  // leader: the epilogue warps of both CTAs
+      mbar_init(&acce[b], 8 * EW);  // leader: the epilogue warps of both CTAs
     }
     fence_mbar_init();
   }
@@ -286,10 +289,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else {
-    // ---- epilogue (warps 2..5): warp w reads TMEM lanes 32*(w % 4) .. +31
+    // ---- epilogue (warps 2..): warp w reads TMEM lanes 32*(w % 4) .. +31;
+    // group gx = (w - 2) / 4 takes the halves gx, gx + EW, ...
     const uint32_t q = warp & 3u;
     const uint32_t r = q * 32 + lane;  // tile row of this thread
-    uint16_t* tile = reinterpret_cast<uint16_t*>(smem);
+    const uint32_t gx = (warp - 2) >> 2;
+    uint16_t* tile = reinterpret_cast<uint16_t*>(smem + gx * L::kTile);
     uint32_t i = 0;
     for (uint32_t pt = cid; pt < npairs; pt += ncl, ++i) {
       const uint32_t buf = i & 1u;
@@ -299,7 +304,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_wait_bounded(&accf[buf], (i >> 1) & 1u);
       tc_fence_after();
 #pragma unroll 1
-      for (uint32_t h = 0; h < BN / L::kHalf; ++h) {
+      for (uint32_t h = gx; h < BN / L::kHalf; h += EW) {
         const uint64_t nh = static_cast<uint64_t>(nb) * BN + h * L::kHalf;  // first column of this half
         uint32_t ks = 0, cnt = 0;
         if constexpr (EPI == 1) {  // this row's kept range in the column half (kb: 128-column blocks)
@@ -331,7 +336,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             }
           }
         }
-        if (h + 1 == BN / L::kHalf) {  // TMEM buffer drained: the leader's MMA may reuse it
+        if (h + EW >= BN / L::kHalf) {  // this group's last half: TMEM drained for it
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_addr(&acce[buf]), 0));
@@ -358,7 +363,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
           if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicAdd(a.flag, 1.0f);
         } else {
-          asm volatile("bar.sync 1, 128;" ::: "memory");
+          asm volatile("bar.sync %0, 128;" ::"r"(1 + gx) : "memory");
           // coalesced copy-out of the staged half: warp q writes rows q, q + 4, ...
           for (uint32_t rr = q; rr < kBM; rr += 4) {
             const uint64_t grow = m0 + rr;
@@ -368,7 +373,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               *reinterpret_cast<uint2*>(a.dw + grow * a.N + col) = v;
             }
           }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
+          asm volatile("bar.sync %0, 128;" ::"r"(1 + gx) : "memory");
         }
       }
     }
@@ -483,16 +488,31 @@ int launch_dw_gemm(const uint16_t* x, const uint16_t* dy, const DwArgs& a, int e
   SAMO_TRY(cached_map(&tdy, dy, a.K, a.N));
   const uint64_t pairs = ((a.M + 2 * kBM - 1) / (2 * kBM)) * ((a.N + kGemmBN - 1) / kGemmBN);
   const int grid = 2 * static_cast<int>(std::min<uint64_t>(pairs, static_cast<uint64_t>(num_sms() / 2)));
-  constexpr uint32_t smem = GemmSmem<kGemmBN, kGemmNS>::kBytes;
-  auto fn = epi == 0 ? k_dw_gemm<0, kGemmBN, kGemmNS> : k_dw_gemm<1, kGemmBN, kGemmNS>;
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[epi != 0]) {
+  // Short K (<= 16 k-blocks per tile): two epilogue groups (one stage less).
+  const char* ew = getenv("SAMO_DW_EW");  // tuning override: 1 or 2 epilogue groups
+  const bool short_k = (ew && *ew) ? atoi(ew) == 2 : a.K <= 16 * kBK;
+  using F = void (*)(CUtensorMap, CUtensorMap, DwArgs);
+  F fn;
+  uint32_t smem;
+  int threads;
+  if (short_k) {
+    fn = epi == 0 ? k_dw_gemm<0, kGemmBN, 4, 2> : k_dw_gemm<1, kGemmBN, 4, 2>;
+    smem = GemmSmem<kGemmBN, 4, 2>::kBytes;
+    threads = gemm_threads(2);
+  } else {
+    fn = epi == 0 ? k_dw_gemm<0, kGemmBN, kGemmNS, 1> : k_dw_gemm<1, kGemmBN, kGemmNS, 1>;
+    smem = GemmSmem<kGemmBN, kGemmNS, 1>::kBytes;
+    threads = gemm_threads(1);
+  }
+  static bool attr_set[4] = {false, false, false, false};
+  const int slot = (epi != 0) + 2 * short_k;
+  if (!attr_set[slot]) {
     SAMO_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr_set[epi != 0] = true;
+    attr_set[slot] = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kGemmThreads);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];

@@ -40,7 +40,9 @@ def _ulp16(h_bits):
     return 2.0 ** (e - 10)
 
 
-SHAPES = [(576, 128, 128), (64, 256, 384), (100, 136, 200), (1, 8, 8), (576, 1024, 512), (130, 8, 264)]
+# batch <= 1024 runs the two-epilogue-group variant, larger batches the other
+SHAPES = [(576, 128, 128), (64, 256, 384), (100, 136, 200), (1, 8, 8), (576, 1024, 512), (130, 8, 264),
+          (1100, 256, 384), (2048, 512, 264)]
 
 
 @pytest.mark.parametrize("batch,n_in,n_out", SHAPES)
@@ -90,9 +92,9 @@ def _model(S, shapes, p, seed):
 FC = [(256, 384), (384, 136), (136, 64)]
 
 
-def test_sink_dw_equals_unfused_gather(S):
+@pytest.mark.parametrize("batch", [200, 1500])
+def test_sink_dw_equals_unfused_gather(S, batch):
     rng = np.random.default_rng(5)
-    batch = 200
     fused, unfused = _model(S, FC, 0.9, 1), _model(S, FC, 0.9, 1)
     for l, (i, o) in enumerate(FC):
         x, dy = _half(rng, (batch, i), 1.0), _half(rng, (batch, o), 4.0)
