@@ -321,3 +321,45 @@ def test_synth_matches_oracle(S, oracle):
     assert np.array_equal(a, bits(oracle.synth_f32(0, 100_000, 3, 17, 0.25)))
     h = N(S.synth_uniform_f16(100_000, 3, 18, 2.0**-7, 1024.0), np.uint16)
     assert np.array_equal(h, oracle.synth_f16(0, 100_000, 3, 18, 2.0**-7, 1024.0))
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_model_step_empty_and_full_layers(S, oracle, graph):
+    """Layers with no kept element (p = 1: unpruned_count = 0), every element
+    kept (non-prunable / p = 0) and tiny odd sizes, stepped together through
+    K1 + K23 (empty tiles, tiles smaller than a chunk): bit-exact vs the
+    oracle's optimizer_step over two steps."""
+    from oracle.oracle import Cfg, StepState
+    dense_len = [5000, 7, 3 * 8192 + 3, 1, 40000]
+    rng = np.random.default_rng(21)
+    vals = [(rng.standard_normal(d) * 0.05).astype(np.float32) for d in dense_len]
+    idx = [np.zeros(0, np.uint32),                                   # nothing kept
+           np.arange(7, dtype=np.uint32),                            # everything kept
+           np.sort(rng.choice(dense_len[2], 2000, replace=False)).astype(np.uint32),
+           np.arange(1, dtype=np.uint32),
+           np.sort(rng.choice(dense_len[4], 1, replace=False)).astype(np.uint32)]
+    sets = [S.PrunedIndexSet(f"l{l}", d, T(i.view(np.int32))) for l, (d, i) in enumerate(zip(dense_len, idx))]
+    model = S.SamoModel.from_index_sets(sets, [(d,) for d in dense_len], 1024)
+    for l, v in enumerate(vals):
+        model.init_layer(l, T(v))
+    model.set_config(S.OptimizerConfig(learning_rate=1e-2))
+    idx_arena = np.concatenate(idx).astype(np.uint32)
+    theta = np.concatenate([oracle.compress(v, i) for v, i in zip(vals, idx)])
+    m, v, g32 = (np.zeros_like(theta) for _ in range(3))
+    t16 = [np.zeros(d, np.uint16) for d in dense_len]
+    st = StepState()
+    for s in range(2):
+        grads = [oracle.synth_f16(0, d, 9, 10 * s + l, 2.0**-7, 1024.0) for l, d in enumerate(dense_len)]
+        model.set_grads([T(g.view(np.int16)) for g in grads])
+        model.step(graph=graph)
+        oracle.optimizer_step(dense_len, [len(i) for i in idx], idx_arena, grads, theta, m, v, g32, t16,
+                              Cfg(lr=1e-2), st)
+    k0 = 0
+    for l, d in enumerate(dense_len):
+        n = len(idx[l])
+        assert np.array_equal(N(model.read(l, "theta32"), np.uint32), bits(theta[k0:k0 + n])), l
+        assert np.array_equal(N(model.read(l, "adam_v"), np.uint32), bits(v[k0:k0 + n])), l
+        assert np.array_equal(N(model.read(l, "theta16").reshape(-1), np.uint16), t16[l]), l
+        k0 += n
+    model.check_invariants()
+    assert model.step_record().t == 2
