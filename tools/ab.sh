@@ -1,4 +1,5 @@
-# A/B: ab_old (older build) vs the current tree, alternating, same box.
+# A/B: an older build vs the current tree, alternating on the same box.
+# Prepare: git worktree add ab_old <commit> && (cd ab_old && python -m paper_2302_05045_b200.build)
 mkdir -p gpurun_out
 for i in 1 2; do
   for d in ab_old .; do

@@ -1,4 +1,4 @@
-# A/B of ab_old vs the current tree at several sparsities (1 GPU).
+# A/B of an older build (git worktree at ab_old, built in place) vs the current tree at several sparsities (1 GPU).
 mkdir -p gpurun_out
 for p in ${PS:-0.9 0.5 0.8}; do
   for d in ab_old .; do
