@@ -42,7 +42,8 @@ def _ulp16(h_bits):
 
 # batch <= 1024 runs the two-epilogue-group variant, larger batches the other
 SHAPES = [(576, 128, 128), (64, 256, 384), (100, 136, 200), (1, 8, 8), (576, 1024, 512), (130, 8, 264),
-          (1100, 256, 384), (2048, 512, 264)]
+          (1100, 256, 384), (2048, 512, 264),
+          (130, 2560, 2560)]  # 100 pair tiles over 74 pairs: a partial second wave
 
 
 @pytest.mark.parametrize("batch,n_in,n_out", SHAPES)
@@ -165,3 +166,18 @@ def test_sink_dw_density_edges(S, shapes, p):
     torch.cuda.synchronize()
     for l in range(len(shapes)):
         assert np.array_equal(_bits(fused.read(l, "grad16")), _bits(unfused.read(l, "grad16"))), l
+
+
+def test_sink_dw_many_tiles_equals_unfused(S):
+    """2560 x 2560 (100 pair tiles over 74 pairs, a partial second wave): the
+    fused sink still equals dense dW -> K1."""
+    rng = np.random.default_rng(23)
+    shapes = [(2560, 2560)]
+    fused, unfused = _model(S, shapes, 0.9, 9), _model(S, shapes, 0.9, 9)
+    for batch in (300, 1500):  # both epilogue variants
+        x, dy = _half(rng, (batch, 2560), 1.0), _half(rng, (batch, 2560), 2.0)
+        fused.sink_dw(0, x, dy)
+        unfused.sink_dense(0, S.dw_gemm(x, dy).reshape(-1))
+        torch.cuda.synchronize()
+        assert np.array_equal(_bits(fused.read(0, "grad16")), _bits(unfused.read(0, "grad16"))), batch
+
