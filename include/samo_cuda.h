@@ -351,10 +351,10 @@ int samo_model_update(samo_model* model, samo_stream_t stream);
  * (no host synchronisation). */
 int samo_model_step(samo_model* model, samo_stream_t stream);
 /* Same step through a CUDA graph captured on first use.  The optimizer
- * scalars are baked into the captured kernels, so samo_model_set_config,
- * samo_model_set_exchange and a new communicator drop the graph and the next
- * call re-captures it: with a per-step learning-rate schedule prefer
- * samo_model_step (the graph pays off only for launch-bound small models). */
+ * scalars live in device memory and are refreshed on `stream` before the
+ * graph launch whenever samo_model_set_config changed them, so a per-step
+ * learning-rate schedule replays the same graph; samo_model_set_exchange and
+ * a new communicator drop the graph and the next call re-captures it. */
 int samo_model_step_graph(samo_model* model, samo_stream_t stream);
 
 /* Reads the device-resident step scalars (synchronises the stream). */

@@ -292,3 +292,15 @@ struct SamoStepState {
 struct SamoAdamParams {
   float lr, beta1, beta2, eps, wd;
 };
+
+// The optimizer scalars of a model step in device memory, written by a
+// one-thread kernel on the step's stream whenever samo_model_set_config
+// changed them — so a captured CUDA graph keeps working under a learning-rate
+// schedule.  Kernels read this when their `cfg` pointer is set, else their
+// by-value arguments.
+struct SamoStepConfig {
+  SamoAdamParams prm;
+  float inv_scale;   // K1 fp32 output / K23 binary16 input: 1/loss_scale (x 1/G for fp32 exchanges)
+  float p2p_scale;   // (1/loss_scale) * (1/G), the P2P shard kernels
+  float pad_;
+};

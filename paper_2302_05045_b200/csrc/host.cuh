@@ -110,6 +110,10 @@ struct samo_model {
   uint32_t push_ntiles = 0;
   int push_G = 0, push_B = 0;
   SamoPeerSlots* slots = nullptr;       // this rank's signal area (in the block)
+  // Device copy of the step scalars (SamoStepConfig), refreshed on the step's
+  // stream before the next step whenever set_config / attach_comm changed them.
+  SamoStepConfig* cfg_dev = nullptr;
+  bool cfg_dirty = true;
   // Backward sinks: first tile of every layer; per-layer row/column-block k
   // tables of the fused dW sink (built on first use).
   std::vector<uint32_t> layer_t;
@@ -168,6 +172,7 @@ inline int step_ready(samo_model* md) {
 // and the raw compressed binary16 gradient (the reference's grad16) otherwise.
 bool wide_grads(const samo_model* md);
 StepArgs step_args(samo_model* md);
+int flush_cfg(samo_model* md, cudaStream_t s);  // stream-ordered update of cfg_dev if dirty
 
 // dp.cu — data-parallel machinery
 int open_peers(samo_model* md);   // collective: CUDA IPC peer mappings (+ optional NVLS)

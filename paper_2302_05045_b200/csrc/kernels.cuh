@@ -54,6 +54,7 @@ struct StepArgs {
   const float* norm_all;       // every partial of the step (read when finalize)
   uint32_t norm_count;
   uint32_t finalize;           // 1 on the step's last update launch
+  const SamoStepConfig* cfg;   // device scalars (model steps); overrides prm / inv_scale
   // K1 push mode (peer-to-peer step): tile t's kept elements go to rank
   // tiles[t].pad_'s receive buffer push16[pad_] at element pad2_ + (k - k_begin)
   // instead of g + k (binary16 output only).
@@ -119,6 +120,7 @@ struct P2PArgs {
   const uint16_t* recv;
   uint64_t rstride, i0;
   int local_c16;                      // store the binary16 weights only locally (pulled by the expand)
+  const SamoStepConfig* cfg;          // device scalars: override prm / scale
   uint16_t* mc16;                     // NVLS: store each weight vector once through this multicast mapping
 };
 int launch_shard_p2p(const P2PArgs& a, cudaStream_t s);
@@ -145,10 +147,14 @@ struct ShardArgs {
   float* norm_partials;
   double* norm2_out;           // this rank's sum of g^2
   uint32_t* done;
+  const SamoStepConfig* cfg;   // device scalars: override prm
 };
 int launch_adam_shard(const ShardArgs& a, int grid, cudaStream_t s);
 int launch_step_finalize(SamoStepState* st, const double* norm2, int nslots, float* flag,
-                         float beta1, float beta2, cudaStream_t s);
+                         float beta1, float beta2, const SamoStepConfig* cfg, cudaStream_t s);
+// Writes `v` to `dst` (one thread) on `s`: the stream-ordered update of the
+// device step scalars.
+int launch_set_step_config(SamoStepConfig* dst, const SamoStepConfig& v, cudaStream_t s);
 // Expand-only tile pass: a.g holds theta16c.
 int launch_expand_c16(const StepArgs& a, int grid, cudaStream_t s);
 int expand_grid(uint32_t tile_elems);

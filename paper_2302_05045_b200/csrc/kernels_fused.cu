@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
   const uint32_t T = a.tile_elems;
   const uint32_t tid = threadIdx.x;
   const uint64_t policy = policy_evict_first();
+  const float inv_scale = a.cfg ? a.cfg->inv_scale : a.inv_scale;
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
       const uint16_t off = a.off16[k];
       const uint16_t h = off < staged ? sg[off] : gsrc[off];
       if constexpr (OUT_F32) {
-        const float gk = mul_x86(f16_bits_to_f32(h), a.inv_scale);
+        const float gk = mul_x86(f16_bits_to_f32(h), inv_scale);
         bad |= !finite_f32(gk);
         st_na_f32(reinterpret_cast<float*>(a.g) + k, gk);
       } else {
@@ -189,7 +190,7 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const uint16_t h = static_cast<uint16_t>((e & 1) ? (hw[e >> 1] >> 16) : (hw[e >> 1] & 0xFFFFu));
-          f[e] = mul_x86(f16_bits_to_f32(h), a.inv_scale);
+          f[e] = mul_x86(f16_bits_to_f32(h), inv_scale);
           bad |= !finite_f32(f[e]);
         }
         float* dst = reinterpret_cast<float*>(a.g) + k;
@@ -376,17 +377,18 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
   // ---- consumer warps ------------------------------------------------------
   // Step scalars (train.hpp:640-642), identical float ops in every CTA.
   const bool skip = !EXPAND && *reinterpret_cast<volatile float*>(a.flag_slot) != 0.0f;
-  const float b1p = __fmul_rn(a.st->beta1_pow, a.prm.beta1);
-  const float b2p = __fmul_rn(a.st->beta2_pow, a.prm.beta2);
+  const SamoAdamParams cprm = a.cfg ? a.cfg->prm : a.prm;
+  const float b1p = __fmul_rn(a.st->beta1_pow, cprm.beta1);
+  const float b2p = __fmul_rn(a.st->beta2_pow, cprm.beta2);
   const float bias1 = __fsub_rn(1.0f, b1p), bias2 = __fsub_rn(1.0f, b2p);
-  const float omb1 = __fsub_rn(1.0f, a.prm.beta1);  // train.hpp:335
-  const float omb2 = __fsub_rn(1.0f, a.prm.beta2);  // train.hpp:336
-  const float lrwd = __fmul_rn(a.prm.lr, a.prm.wd);
+  const float omb1 = __fsub_rn(1.0f, cprm.beta1);  // train.hpp:335
+  const float omb2 = __fsub_rn(1.0f, cprm.beta2);  // train.hpp:336
+  const float lrwd = __fmul_rn(cprm.lr, cprm.wd);
 
   // Hot-loop parameters in registers (see pin_f32).
-  const float p_beta1 = pin_f32(a.prm.beta1), p_beta2 = pin_f32(a.prm.beta2);
-  const float p_lr = pin_f32(a.prm.lr), p_eps = pin_f32(a.prm.eps), p_wd = pin_f32(a.prm.wd);
-  const float p_inv = pin_f32(a.inv_scale);
+  const float p_beta1 = pin_f32(cprm.beta1), p_beta2 = pin_f32(cprm.beta2);
+  const float p_lr = pin_f32(cprm.lr), p_eps = pin_f32(cprm.eps), p_wd = pin_f32(cprm.wd);
+  const float p_inv = pin_f32(a.cfg ? a.cfg->inv_scale : a.inv_scale);
   const uint32_t p_T = pin_u32(T);
   float* const p_theta = pin_ptr(a.theta);
   float* const p_m = pin_ptr(a.m);
@@ -571,11 +573,12 @@ __global__ void __launch_bounds__(kThreads) k_adam_shard(ShardArgs a) {
   __shared__ float red[kThreads / 32];
   __shared__ int last_cta;
   const bool skip = *reinterpret_cast<const volatile float*>(a.flag_slot) != 0.0f;
-  const float b1p = __fmul_rn(a.st->beta1_pow, a.prm.beta1);
-  const float b2p = __fmul_rn(a.st->beta2_pow, a.prm.beta2);
+  const SamoAdamParams prm = a.cfg ? a.cfg->prm : a.prm;
+  const float b1p = __fmul_rn(a.st->beta1_pow, prm.beta1);
+  const float b2p = __fmul_rn(a.st->beta2_pow, prm.beta2);
   const float bias1 = __fsub_rn(1.0f, b1p), bias2 = __fsub_rn(1.0f, b2p);
-  const float omb1 = __fsub_rn(1.0f, a.prm.beta1), omb2 = __fsub_rn(1.0f, a.prm.beta2);
-  const float lrwd = __fmul_rn(a.prm.lr, a.prm.wd);
+  const float omb1 = __fsub_rn(1.0f, prm.beta1), omb2 = __fsub_rn(1.0f, prm.beta2);
+  const float lrwd = __fmul_rn(prm.lr, prm.wd);
   float nacc = 0.0f;
   // k0 is a multiple of 8 (shard size), so 4-element vectors stay aligned.
   const uint64_t nv = (a.k1 - a.k0) / 4;
@@ -591,10 +594,10 @@ __global__ void __launch_bounds__(kThreads) k_adam_shard(ShardArgs a) {
     nacc = __fadd_rn(nacc, __fmul_rn(g.z, g.z));
     nacc = __fadd_rn(nacc, __fmul_rn(g.w, g.w));
     if (!skip) {
-      t.x = adam_one(g.x, m.x, v.x, t.x, a.prm, omb1, omb2, bias1, bias2, lrwd);
-      t.y = adam_one(g.y, m.y, v.y, t.y, a.prm, omb1, omb2, bias1, bias2, lrwd);
-      t.z = adam_one(g.z, m.z, v.z, t.z, a.prm, omb1, omb2, bias1, bias2, lrwd);
-      t.w = adam_one(g.w, m.w, v.w, t.w, a.prm, omb1, omb2, bias1, bias2, lrwd);
+      t.x = adam_one(g.x, m.x, v.x, t.x, prm, omb1, omb2, bias1, bias2, lrwd);
+      t.y = adam_one(g.y, m.y, v.y, t.y, prm, omb1, omb2, bias1, bias2, lrwd);
+      t.z = adam_one(g.z, m.z, v.z, t.z, prm, omb1, omb2, bias1, bias2, lrwd);
+      t.w = adam_one(g.w, m.w, v.w, t.w, prm, omb1, omb2, bias1, bias2, lrwd);
       *reinterpret_cast<float4*>(a.theta + k) = t;
       *reinterpret_cast<float4*>(a.m + k) = m;
       *reinterpret_cast<float4*>(a.v + k) = v;
@@ -611,7 +614,7 @@ __global__ void __launch_bounds__(kThreads) k_adam_shard(ShardArgs a) {
     float t = a.theta[k], m = a.m[k], v = a.v[k];
     nacc = __fadd_rn(nacc, __fmul_rn(g, g));
     if (!skip) {
-      t = adam_one(g, m, v, t, a.prm, omb1, omb2, bias1, bias2, lrwd);
+      t = adam_one(g, m, v, t, prm, omb1, omb2, bias1, bias2, lrwd);
       a.theta[k] = t;
       a.m[k] = m;
       a.v[k] = v;
@@ -715,13 +718,13 @@ __global__ void __launch_bounds__(kThreads, SAMO_P2P_MINB) k_shard_p2p(P2PArgs a
   __shared__ float red[kThreads / 32];
   __shared__ int last_cta;
   const bool skip = *reinterpret_cast<const volatile float*>(a.flag_slot) != 0.0f;
-  const float b1p = __fmul_rn(a.st->beta1_pow, a.prm.beta1);
-  const float b2p = __fmul_rn(a.st->beta2_pow, a.prm.beta2);
+  const SamoAdamParams prm = a.cfg ? a.cfg->prm : a.prm;
+  const float b1p = __fmul_rn(a.st->beta1_pow, prm.beta1);
+  const float b2p = __fmul_rn(a.st->beta2_pow, prm.beta2);
   const float bias1 = __fsub_rn(1.0f, b1p), bias2 = __fsub_rn(1.0f, b2p);
-  const float omb1 = __fsub_rn(1.0f, a.prm.beta1), omb2 = __fsub_rn(1.0f, a.prm.beta2);
-  const float lrwd = __fmul_rn(a.prm.lr, a.prm.wd);
-  const SamoAdamParams prm = a.prm;
-  const float scale = pin_f32(a.scale);
+  const float omb1 = __fsub_rn(1.0f, prm.beta1), omb2 = __fsub_rn(1.0f, prm.beta2);
+  const float lrwd = __fmul_rn(prm.lr, prm.wd);
+  const float scale = pin_f32(a.cfg ? a.cfg->p2p_scale : a.scale);
   float nacc = 0.0f;
   const uint64_t n = a.k1 - a.k0;
   const uint64_t nv = (n + 7) / 8;  // 8-element vectors (the last one may be partial)
@@ -867,13 +870,13 @@ __global__ void __launch_bounds__(32 * (kShardConsumers + 1)) k_shard_p2p_tma(P2
   }
 
   const bool skip = *reinterpret_cast<const volatile float*>(a.flag_slot) != 0.0f;
-  const float b1p = __fmul_rn(a.st->beta1_pow, a.prm.beta1);
-  const float b2p = __fmul_rn(a.st->beta2_pow, a.prm.beta2);
+  const SamoAdamParams prm = a.cfg ? a.cfg->prm : a.prm;
+  const float b1p = __fmul_rn(a.st->beta1_pow, prm.beta1);
+  const float b2p = __fmul_rn(a.st->beta2_pow, prm.beta2);
   const float bias1 = __fsub_rn(1.0f, b1p), bias2 = __fsub_rn(1.0f, b2p);
-  const float omb1 = __fsub_rn(1.0f, a.prm.beta1), omb2 = __fsub_rn(1.0f, a.prm.beta2);
-  const float lrwd = __fmul_rn(a.prm.lr, a.prm.wd);
-  const SamoAdamParams prm = a.prm;
-  const float scale = pin_f32(a.scale);
+  const float omb1 = __fsub_rn(1.0f, prm.beta1), omb2 = __fsub_rn(1.0f, prm.beta2);
+  const float lrwd = __fmul_rn(prm.lr, prm.wd);
+  const float scale = pin_f32(a.cfg ? a.cfg->p2p_scale : a.scale);
   float* const p_theta = pin_ptr(a.theta);
   float* const p_m = pin_ptr(a.m);
   float* const p_v = pin_ptr(a.v);
@@ -993,10 +996,16 @@ __global__ void k_p2p_wait(const SamoPeerSlots* mine, int G, int bucket) {
 
 __global__ void k_p2p_epoch(SamoPeerSlots* mine) { mine->epoch += 1; }
 
+__global__ void k_set_step_config(SamoStepConfig* dst, SamoStepConfig v) { *dst = v; }
+
 // One thread: the step's scalars once the global grad norm^2 and skip flag
 // are known (AdamScalars::advance, train.hpp:325-329; skip, 632-639).
 __global__ void k_step_finalize(SamoStepState* st, const double* norm2, int nslots, float* flag,
-                                float beta1, float beta2) {
+                                float beta1, float beta2, const SamoStepConfig* cfg) {
+  if (cfg) {
+    beta1 = cfg->prm.beta1;
+    beta2 = cfg->prm.beta2;
+  }
   const bool skip = *flag != 0.0f;
   double acc = 0.0;
   for (int i = 0; i < nslots; ++i) acc += norm2[i];  // fixed order: deterministic
@@ -1208,6 +1217,12 @@ int launch_p2p_wait(const SamoPeerSlots* mine, int G, int bucket, cudaStream_t s
   return SAMO_OK;
 }
 
+int launch_set_step_config(SamoStepConfig* dst, const SamoStepConfig& v, cudaStream_t s) {
+  k_set_step_config<<<1, 1, 0, s>>>(dst, v);
+  SAMO_LAUNCH_CHECK("k_set_step_config");
+  return SAMO_OK;
+}
+
 int launch_p2p_epoch(SamoPeerSlots* mine, cudaStream_t s) {
   k_p2p_epoch<<<1, 1, 0, s>>>(mine);
   SAMO_LAUNCH_CHECK("k_p2p_epoch");
@@ -1222,8 +1237,8 @@ int launch_adam_shard(const ShardArgs& a, int grid, cudaStream_t s) {
 }
 
 int launch_step_finalize(SamoStepState* st, const double* norm2, int nslots, float* flag,
-                         float beta1, float beta2, cudaStream_t s) {
-  k_step_finalize<<<1, 1, 0, s>>>(st, norm2, nslots, flag, beta1, beta2);
+                         float beta1, float beta2, const SamoStepConfig* cfg, cudaStream_t s) {
+  k_step_finalize<<<1, 1, 0, s>>>(st, norm2, nslots, flag, beta1, beta2, cfg);
   SAMO_LAUNCH_CHECK("k_step_finalize");
   return SAMO_OK;
 }

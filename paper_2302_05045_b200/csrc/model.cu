@@ -101,6 +101,7 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   const uint64_t o_c16 = carve((n_al + kArenaSlack) * 2);
   const uint64_t o_n2 = carve(256);  // 16 norm^2 slots + arrival counter
   const uint64_t o_slots = carve(sizeof(SamoPeerSlots));
+  const uint64_t o_cfg = carve(sizeof(SamoStepConfig));
   md->block_bytes = off;
   cudaError_t e = cudaMalloc(&md->block, off);
   if (e != cudaSuccess) {
@@ -118,6 +119,7 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   md->norm2 = reinterpret_cast<double*>(b + o_n2);
   md->done = reinterpret_cast<uint32_t*>(b + o_n2 + 16 * sizeof(double));
   md->slots = reinterpret_cast<SamoPeerSlots*>(b + o_slots);
+  md->cfg_dev = reinterpret_cast<SamoStepConfig*>(b + o_cfg);
   md->theta16 = reinterpret_cast<uint16_t*>(b + o_t16);
   md->tiles = reinterpret_cast<SamoTile*>(b + o_tiles);
   md->layers_dev = reinterpret_cast<SamoLayerDev*>(b + o_layers);
@@ -310,10 +312,7 @@ int samo_model_set_config(samo_model* md, const samo_optimizer_config* cfg) {
   if (!md) return fail(SAMO_E_PARAMETER, "null model");
   SAMO_TRY(samo_optimizer_config_validate(cfg));
   md->cfg = *cfg;
-  if (md->graph) {  // scalars are baked into the graph's kernel nodes
-    cudaGraphExecDestroy(md->graph);
-    md->graph = nullptr;
-  }
+  md->cfg_dirty = true;  // the step kernels read cfg_dev: a captured graph stays valid
   return clear_ok();
 }
 
@@ -321,6 +320,7 @@ int samo_model_attach_comm(samo_model* md, samo_comm* comm) {
   if (!md) return fail(SAMO_E_PARAMETER, "null model");
   close_peers(md);
   md->comm = comm;
+  md->cfg_dirty = true;  // the scales fold in 1/G
   if (comm && comm->nranks > 1) SAMO_TRY(open_peers(md));
   return clear_ok();
 }
@@ -375,6 +375,7 @@ StepArgs step_args(samo_model* md) {
   a.norm_all = md->norm_partials;
   a.norm_count = 0;
   a.finalize = 1;
+  a.cfg = md->cfg_dev;
   return a;
 }
 
@@ -458,8 +459,23 @@ int samo_dw_gemm_f16(const uint16_t* x, const uint16_t* dy, uint64_t batch, uint
   return clear_ok();
 }
 
+extern "C++" int flush_cfg(samo_model* md, cudaStream_t s) {
+  if (!md->cfg_dirty) return SAMO_OK;
+  SamoStepConfig v{};
+  v.prm = adam_params(&md->cfg);
+  const int G = comm_size(md);
+  float inv_scale = 1.0f / md->cfg.loss_scale;  // as step_args
+  if (G > 1) inv_scale = inv_scale * (1.0f / static_cast<float>(G));
+  v.inv_scale = inv_scale;
+  v.p2p_scale = (1.0f / md->cfg.loss_scale) * (1.0f / static_cast<float>(G));
+  SAMO_TRY(launch_set_step_config(md->cfg_dev, v, s));
+  md->cfg_dirty = false;
+  return SAMO_OK;
+}
+
 int samo_model_update(samo_model* md, samo_stream_t stream) {
   SAMO_TRY(step_ready(md));
+  SAMO_TRY(flush_cfg(md, as_stream(stream)));
   const bool wide = wide_grads(md);
   StepArgs a = step_args(md);
   const int grid = std::min<int>(wide ? md->grid_update32 : md->grid_update16, md->ntiles);
@@ -470,6 +486,7 @@ int samo_model_update(samo_model* md, samo_stream_t stream) {
 
 int samo_model_step_sunk(samo_model* md, samo_stream_t stream) {
   SAMO_TRY(step_ready(md));
+  SAMO_TRY(flush_cfg(md, as_stream(stream)));
   if (comm_size(md) > 1) {
     if (exchange_mode(md) != SAMO_EXCHANGE_P2P || !md->p2p_ok)
       return fail(SAMO_E_STATE, "step after backward sinks needs the peer-to-peer exchange");
@@ -483,6 +500,7 @@ int samo_model_step_sunk(samo_model* md, samo_stream_t stream) {
 int samo_model_step(samo_model* md, samo_stream_t stream) {
   SAMO_TRY(step_ready(md));
   if (!md->grads_set) return fail(SAMO_E_STATE, "optimizer_step requires backward (no gradients set)");
+  SAMO_TRY(flush_cfg(md, as_stream(stream)));  // (never inside a capture: step_graph flushes first)
   if (comm_size(md) > 1 && exchange_mode(md) == SAMO_EXCHANGE_P2P) {
     if (!md->p2p_ok) return fail(SAMO_E_STATE, "peer-to-peer exchange unavailable (IPC mapping failed)");
     SAMO_TRY(step_p2p(md, as_stream(stream)));
@@ -506,6 +524,7 @@ int samo_model_step_graph(samo_model* md, samo_stream_t stream) {
   SAMO_TRY(step_ready(md));
   if (!md->grads_set) return fail(SAMO_E_STATE, "optimizer_step requires backward (no gradients set)");
   cudaStream_t s = as_stream(stream);
+  SAMO_TRY(flush_cfg(md, s));  // outside the graph: new scalars without a re-capture
   if (md->graph && md->graph_comm != md->comm) {
     cudaGraphExecDestroy(md->graph);
     md->graph = nullptr;
