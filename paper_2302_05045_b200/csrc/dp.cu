@@ -495,7 +495,7 @@ int step_p2p(samo_model* md, cudaStream_t S, bool gather) {
   pa.k1 = std::min<uint64_t>((r + 1) * c, md->n_tot);
   pa.scale = (1.0f / md->cfg.loss_scale) * (1.0f / static_cast<float>(G));
   pa.prm = adam_params(&md->cfg);
-  pa.cfg = md->cfg_dev;
+  pa.cfg = md->capturing ? md->cfg_dev : nullptr;
   pa.st = md->st;
   pa.flag_slot = flag;
   pa.norm_partials = md->norm_partials;
@@ -524,7 +524,7 @@ int step_p2p(samo_model* md, cudaStream_t S, bool gather) {
   if (pull) set_pull_args(md, md->p2p_plan, a);
   SAMO_TRY(launch_expand_c16(a, std::min<int>(md->grid_expand, md->ntiles), S));
   SAMO_TRY(phase_mark(md, 5, S));
-  SAMO_TRY(launch_step_finalize(md->st, md->norm2, 1, flag, md->cfg.beta1, md->cfg.beta2, md->cfg_dev, S));
+  SAMO_TRY(launch_step_finalize(md->st, md->norm2, 1, flag, md->cfg.beta1, md->cfg.beta2, md->capturing ? md->cfg_dev : nullptr, S));
   SAMO_TRY(phase_mark(md, 6, S));
   md->phase_count = 6;
   return SAMO_OK;
@@ -640,7 +640,7 @@ int step_sharded(samo_model* md, cudaStream_t S) {
     sa.k0 = std::min<uint64_t>(b * p.C + r * p.c, md->n_tot);
     sa.k1 = std::min<uint64_t>(b * p.C + (r + 1) * p.c, md->n_tot);
     sa.prm = adam_params(&md->cfg);
-    sa.cfg = md->cfg_dev;
+    sa.cfg = md->capturing ? md->cfg_dev : nullptr;
     sa.st = md->st;
     sa.flag_slot = flag;
     sa.norm_partials = md->norm_partials;
@@ -673,7 +673,7 @@ int step_sharded(samo_model* md, cudaStream_t S) {
   }
   SAMO_TRY(phase_mark(md, 3, S));
   SAMO_CUDA_TRY(cudaStreamWaitEvent(S, md->ev_flag, 0));
-  SAMO_TRY(launch_step_finalize(md->st, md->norm2, B, flag, md->cfg.beta1, md->cfg.beta2, md->cfg_dev, S));
+  SAMO_TRY(launch_step_finalize(md->st, md->norm2, B, flag, md->cfg.beta1, md->cfg.beta2, md->capturing ? md->cfg_dev : nullptr, S));
   SAMO_TRY(phase_mark(md, 4, S));
   md->phase_count = 4;
   return SAMO_OK;
@@ -802,7 +802,7 @@ static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather
   pa.v = md->v;
   pa.scale = (1.0f / md->cfg.loss_scale) * (1.0f / static_cast<float>(G));
   pa.prm = adam_params(&md->cfg);
-  pa.cfg = md->cfg_dev;
+  pa.cfg = md->capturing ? md->cfg_dev : nullptr;
   pa.st = md->st;
   pa.flag_slot = flag;
   pa.norm_partials = md->norm_partials;
@@ -851,7 +851,7 @@ static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather
   SAMO_CUDA_TRY(cudaStreamWaitEvent(S, md->ev_flag, 0));
   SAMO_TRY(phase_mark(md, 3, S));
   SAMO_TRY(launch_step_finalize(md->st, md->slots->norm, B * kMaxP2PRanks, flag, md->cfg.beta1,
-                                md->cfg.beta2, md->cfg_dev, S));
+                                md->cfg.beta2, md->capturing ? md->cfg_dev : nullptr, S));
   SAMO_TRY(launch_p2p_epoch(md->slots, S));
   SAMO_TRY(phase_mark(md, 4, S));
   md->phase_count = 4;

@@ -114,6 +114,7 @@ struct samo_model {
   // stream before the next step whenever set_config / attach_comm changed them.
   SamoStepConfig* cfg_dev = nullptr;
   bool cfg_dirty = true;
+  bool capturing = false;  // only captured steps read cfg_dev (eager steps pass the scalars by value)
   // Backward sinks: first tile of every layer; per-layer row/column-block k
   // tables of the fused dW sink (built on first use).
   std::vector<uint32_t> layer_t;

@@ -83,6 +83,21 @@ __device__ __forceinline__ uint4 ld_stream_v4(const uint16_t* p) {
   return v;
 }
 
+// The step scalars: from the device copy when `cfg` is set, else the by-value
+// kernel arguments.  Field-wise, so no struct address is ever selected (that
+// forced a local-memory copy of the arguments and cost K23 3%).
+__device__ __forceinline__ SamoAdamParams step_prm(const SamoStepConfig* cfg, const SamoAdamParams& arg) {
+  SamoAdamParams p = arg;
+  if (cfg) {
+    p.lr = cfg->prm.lr;
+    p.beta1 = cfg->prm.beta1;
+    p.beta2 = cfg->prm.beta2;
+    p.eps = cfg->prm.eps;
+    p.wd = cfg->prm.wd;
+  }
+  return p;
+}
+
 // ---------------------------------------------------------------------------
 // off16 construction (once, at finalize).
 
@@ -276,7 +291,10 @@ struct K23Layout {
 // EXPAND = true: expand-only pass of the sharded data-parallel step — the
 // grad slot carries the all-gathered compressed binary16 weights (theta16c),
 // no Adam, no theta/m/v traffic.
-template <bool G16, int CH, int NS, bool EXPAND = false>
+// CFG: the optimizer scalars come from a.cfg (graph captures); the eager
+// instantiation keeps them kernel parameters — at 96 registers (the per-SMSP
+// cap at 2 CTAs/SM) values derived from a global load would spill (+3%).
+template <bool G16, int CH, int NS, bool EXPAND = false, bool CFG = false>
 __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
   static_assert(!EXPAND || G16, "expand-only reads 16-bit values");
   using L = K23Layout<G16, CH, EXPAND>;
@@ -377,7 +395,8 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
   // ---- consumer warps ------------------------------------------------------
   // Step scalars (train.hpp:640-642), identical float ops in every CTA.
   const bool skip = !EXPAND && *reinterpret_cast<volatile float*>(a.flag_slot) != 0.0f;
-  const SamoAdamParams cprm = a.cfg ? a.cfg->prm : a.prm;
+  SamoAdamParams cprm = a.prm;
+  if constexpr (CFG) cprm = step_prm(a.cfg, a.prm);
   const float b1p = __fmul_rn(a.st->beta1_pow, cprm.beta1);
   const float b2p = __fmul_rn(a.st->beta2_pow, cprm.beta2);
   const float bias1 = __fsub_rn(1.0f, b1p), bias2 = __fsub_rn(1.0f, b2p);
@@ -388,7 +407,9 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
   // Hot-loop parameters in registers (see pin_f32).
   const float p_beta1 = pin_f32(cprm.beta1), p_beta2 = pin_f32(cprm.beta2);
   const float p_lr = pin_f32(cprm.lr), p_eps = pin_f32(cprm.eps), p_wd = pin_f32(cprm.wd);
-  const float p_inv = pin_f32(a.cfg ? a.cfg->inv_scale : a.inv_scale);
+  float inv_scale = a.inv_scale;
+  if constexpr (CFG) inv_scale = a.cfg ? a.cfg->inv_scale : a.inv_scale;
+  const float p_inv = pin_f32(inv_scale);
   const uint32_t p_T = pin_u32(T);
   float* const p_theta = pin_ptr(a.theta);
   float* const p_m = pin_ptr(a.m);
@@ -573,7 +594,7 @@ __global__ void __launch_bounds__(kThreads) k_adam_shard(ShardArgs a) {
   __shared__ float red[kThreads / 32];
   __shared__ int last_cta;
   const bool skip = *reinterpret_cast<const volatile float*>(a.flag_slot) != 0.0f;
-  const SamoAdamParams prm = a.cfg ? a.cfg->prm : a.prm;
+  const SamoAdamParams prm = step_prm(a.cfg, a.prm);
   const float b1p = __fmul_rn(a.st->beta1_pow, prm.beta1);
   const float b2p = __fmul_rn(a.st->beta2_pow, prm.beta2);
   const float bias1 = __fsub_rn(1.0f, b1p), bias2 = __fsub_rn(1.0f, b2p);
@@ -718,7 +739,7 @@ __global__ void __launch_bounds__(kThreads, SAMO_P2P_MINB) k_shard_p2p(P2PArgs a
   __shared__ float red[kThreads / 32];
   __shared__ int last_cta;
   const bool skip = *reinterpret_cast<const volatile float*>(a.flag_slot) != 0.0f;
-  const SamoAdamParams prm = a.cfg ? a.cfg->prm : a.prm;
+  const SamoAdamParams prm = step_prm(a.cfg, a.prm);
   const float b1p = __fmul_rn(a.st->beta1_pow, prm.beta1);
   const float b2p = __fmul_rn(a.st->beta2_pow, prm.beta2);
   const float bias1 = __fsub_rn(1.0f, b1p), bias2 = __fsub_rn(1.0f, b2p);
@@ -870,7 +891,7 @@ __global__ void __launch_bounds__(32 * (kShardConsumers + 1)) k_shard_p2p_tma(P2
   }
 
   const bool skip = *reinterpret_cast<const volatile float*>(a.flag_slot) != 0.0f;
-  const SamoAdamParams prm = a.cfg ? a.cfg->prm : a.prm;
+  const SamoAdamParams prm = step_prm(a.cfg, a.prm);
   const float b1p = __fmul_rn(a.st->beta1_pow, prm.beta1);
   const float b2p = __fmul_rn(a.st->beta2_pow, prm.beta2);
   const float bias1 = __fsub_rn(1.0f, b1p), bias2 = __fsub_rn(1.0f, b2p);
@@ -1073,22 +1094,22 @@ static size_t k23_smem(uint32_t tile_elems) {
 }
 
 // Calls f(kernel, smem) for the selected variant.
-template <bool G16, typename F>
+template <bool G16, bool CFG, typename F>
 static int with_k23(uint32_t tile_elems, F f) {
   const char* env = getenv("SAMO_K23_VARIANT");
   if (!(env && *env)) {
     // Default: 1024-element chunks, three stages when two CTAs still fit per
     // SM (227 KB of shared memory), else two.
     if (k23_smem<G16, 1024, 3>(tile_elems) <= 113u * 1024u)
-      return f(k23_update<G16, 1024, 3>, k23_smem<G16, 1024, 3>(tile_elems));
-    return f(k23_update<G16, 1024, 2>, k23_smem<G16, 1024, 2>(tile_elems));
+      return f(k23_update<G16, 1024, 3, false, CFG>, k23_smem<G16, 1024, 3>(tile_elems));
+    return f(k23_update<G16, 1024, 2, false, CFG>, k23_smem<G16, 1024, 2>(tile_elems));
   }
   switch (k23_variant()) {
-    case 1: return f(k23_update<G16, 1024, 2>, k23_smem<G16, 1024, 2>(tile_elems));
-    case 2: return f(k23_update<G16, 512, 3>, k23_smem<G16, 512, 3>(tile_elems));
-    case 3: return f(k23_update<G16, 512, 4>, k23_smem<G16, 512, 4>(tile_elems));
-    case 4: return f(k23_update<G16, 2048, 2>, k23_smem<G16, 2048, 2>(tile_elems));
-    default: return f(k23_update<G16, 1024, 3>, k23_smem<G16, 1024, 3>(tile_elems));
+    case 1: return f(k23_update<G16, 1024, 2, false, CFG>, k23_smem<G16, 1024, 2>(tile_elems));
+    case 2: return f(k23_update<G16, 512, 3, false, CFG>, k23_smem<G16, 512, 3>(tile_elems));
+    case 3: return f(k23_update<G16, 512, 4, false, CFG>, k23_smem<G16, 512, 4>(tile_elems));
+    case 4: return f(k23_update<G16, 2048, 2, false, CFG>, k23_smem<G16, 2048, 2>(tile_elems));
+    default: return f(k23_update<G16, 1024, 3, false, CFG>, k23_smem<G16, 1024, 3>(tile_elems));
   }
 }
 
@@ -1098,7 +1119,7 @@ int step_grid(int which, bool wide, uint32_t tile_elems) {
     return wide ? with_k1<true>(tile_elems, g) : with_k1<false>(tile_elems, g);
   }
   auto g = [](auto fn, size_t sm) { return grid_for(fn, sm, kThreads + 32); };
-  return wide ? with_k23<false>(tile_elems, g) : with_k23<true>(tile_elems, g);
+  return wide ? with_k23<false, false>(tile_elems, g) : with_k23<true, false>(tile_elems, g);
 }
 
 template <typename F>
@@ -1146,7 +1167,8 @@ int launch_update(const StepArgs& a, bool g_f32, int grid, cudaStream_t s) {
   auto go = [&](auto fn, size_t sm) {
     return launch_persistent(fn, a, sm, grid, s, kThreads + 32, "k23_update", pdl);
   };
-  return g_f32 ? with_k23<false>(a.tile_elems, go) : with_k23<true>(a.tile_elems, go);
+  if (a.cfg) return g_f32 ? with_k23<false, true>(a.tile_elems, go) : with_k23<true, true>(a.tile_elems, go);
+  return g_f32 ? with_k23<false, false>(a.tile_elems, go) : with_k23<true, false>(a.tile_elems, go);
 }
 
 template <int G>

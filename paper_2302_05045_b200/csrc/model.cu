@@ -375,7 +375,7 @@ StepArgs step_args(samo_model* md) {
   a.norm_all = md->norm_partials;
   a.norm_count = 0;
   a.finalize = 1;
-  a.cfg = md->cfg_dev;
+  a.cfg = md->capturing ? md->cfg_dev : nullptr;
   return a;
 }
 
@@ -541,7 +541,9 @@ int samo_model_step_graph(samo_model* md, samo_stream_t stream) {
     }
     const uint64_t before = samo_kernel_launch_count();
     SAMO_CUDA_TRY(cudaStreamBeginCapture(md->capture_stream, cudaStreamCaptureModeThreadLocal));
+    md->capturing = true;
     int rc = samo_model_step(md, md->capture_stream);
+    md->capturing = false;
     cudaGraph_t graph = nullptr;
     cudaError_t e = cudaStreamEndCapture(md->capture_stream, &graph);
     if (rc != SAMO_OK) {
