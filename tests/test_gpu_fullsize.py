@@ -90,3 +90,50 @@ def test_gpt_2_7b_fullsize(cuda, oracle):
         assert np.array_equal(_bits32(model.read(i, "adam_v")), v.view(np.uint32)), name
         assert np.array_equal(model.read(i, "theta16").reshape(-1).cpu().numpy().view(np.uint16), t16[0]), name
     model.close()
+
+
+def test_max_layer_size(cuda, oracle):
+    """The largest layer the reference allows (dense_len < 2^32, prune.hpp:
+    106-109): 32-bit tile offsets, K0's histograms and the step kernels at
+    the edge.  K0 count and top-|v| property, two steps, whole-layer
+    invariants (theta16 == expand(half(theta32)), zeros elsewhere) and the
+    kept elements bit-exact vs the oracle's optimizer_step arithmetic."""
+    from paper_2302_05045_b200 import samo
+    from oracle.oracle import Cfg
+    n = 2**32 - 64
+    if torch.cuda.mem_get_info()[0] < 64e9:
+        pytest.skip("needs ~64 GB of free device memory")
+    p = 0.9999
+    w = samo.synth_uniform_f32(n, 5, 0, 0.05)
+    sets = samo.magnitude_prune([samo.LayerParams("big", w, True)], p)
+    keep = oracle.unpruned_count(p, n)
+    assert sets[0].count() == keep
+    idx_t = sets[0].indices.long() & 0xFFFFFFFF  # uint32 indices held in an int32 tensor
+    idx = sets[0].indices.cpu().numpy().view(np.uint32)
+    assert np.all(np.diff(idx.astype(np.int64)) > 0) and int(idx[-1]) < n
+    thr = w[idx_t].abs().min()
+    assert int((w.abs() > thr).sum()) <= keep  # nothing larger was dropped
+    model = samo.SamoModel.from_index_sets(sets, [(n,)], 0)
+    model.init_layer(0, w)
+    theta = w[idx_t].cpu().numpy()
+    del w
+    torch.cuda.empty_cache()
+    model.set_config(samo.OptimizerConfig(learning_rate=1e-2))
+    m, v = np.zeros_like(theta), np.zeros_like(theta)
+    cfg = Cfg(lr=1e-2)
+    b1p = b2p = np.float32(1.0)
+    for s in range(2):
+        g = samo.synth_uniform_f16(n, 6, s, 2.0**-7, 1024.0)
+        model.set_grads([g])
+        model.step()
+        gk = oracle.h2f(g[idx_t].cpu().numpy().view(np.uint16))
+        g32 = (gk * np.float32(1.0 / 1024.0)).astype(np.float32)  # train.hpp:619-624
+        b1p, b2p = np.float32(b1p * np.float32(0.9)), np.float32(b2p * np.float32(0.999))
+        oracle.adam_update(theta, m, v, g32, cfg, float(np.float32(1) - b1p), float(np.float32(1) - b2p))
+        del g
+    torch.cuda.synchronize()
+    model.check_invariants()
+    assert np.array_equal(model.read(0, "theta32").cpu().numpy().view(np.uint32), theta.view(np.uint32))
+    assert np.array_equal(model.read(0, "adam_v").cpu().numpy().view(np.uint32), v.view(np.uint32))
+    assert model.step_record().t == 2
+    model.close()
