@@ -284,7 +284,10 @@ int open_peers(samo_model* md) {
   cudaStream_t s = nullptr;
   SAMO_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   uint8_t* d = nullptr;
-  SAMO_CUDA_TRY(cudaMalloc(&d, G * sizeof(cudaIpcMemHandle_t) + 16));
+  if (const cudaError_t e = cudaMalloc(&d, G * sizeof(cudaIpcMemHandle_t) + 16)) {
+    cudaStreamDestroy(s);
+    return cuda_fail(e, "ipc handle buffer");
+  }
   int* dok = reinterpret_cast<int*>(d + G * sizeof(cudaIpcMemHandle_t));
   std::vector<cudaIpcMemHandle_t> all(G);
   int rc = SAMO_OK;
@@ -565,7 +568,6 @@ int plan_shards(samo_model* md, ShardPlan& p, int B) {
   p.ex_t.assign(B + 1, md->ntiles);
   p.k1_t[0] = p.ex_t[0] = 0;
   // first tile of each bucket (keys are non-decreasing in tile order)
-  std::vector<int> k1_first(B + 1, -1), ex_first(B + 1, -1);
   for (uint32_t t = 0; t < md->ntiles; ++t) {
     const SamoTile& td = md->tiles_host[t];
     const int b1 = bucket_of(td.k_begin);
@@ -575,8 +577,6 @@ int plan_shards(samo_model* md, ShardPlan& p, int B) {
     for (int b = 1; b <= be; ++b)
       if (p.ex_t[b] == md->ntiles) p.ex_t[b] = t;
   }
-  (void)k1_first;
-  (void)ex_first;
   for (int b = 1; b <= B; ++b) {  // monotone
     p.k1_t[b] = std::max(p.k1_t[b], p.k1_t[b - 1]);
     p.ex_t[b] = std::max(p.ex_t[b], p.ex_t[b - 1]);
