@@ -171,6 +171,7 @@ struct DwArgs {
   const uint32_t* kb;    // epi 1: [(col blocks + 1) x M] row/column-block k starts
   uint16_t* g16;         // epi 1: layer's compressed binary16 gradient
   float* flag;           // epi 1: skip indicator
+  uint32_t tail0;        // set by launch_dw_gemm: pair tiles >= tail0 run as two 256 x BN/2 halves
 };
 int dw_check(uint64_t batch, uint64_t in, uint64_t out, const void* x, const void* dy);
 uint32_t dw_col_blocks(uint64_t out);

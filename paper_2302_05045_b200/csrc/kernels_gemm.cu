@@ -23,9 +23,11 @@
 //   warp 1      TMEM allocation; MMA issue by one lane of the leader CTA
 //   warps 2..5  epilogue: tcgen05.ld (32 lanes x 32 columns per load), in two
 //               128-column halves; each thread owns one accumulator row
-// Measured (tools/bench_dw.py): 1.0-1.28 PFLOP/s on the
-// GPT-2.7B layer shapes at 4096-8192 tokens, 72-88% of cuBLAS; the fused sink
-// is within +-7% of the dense GEMM followed by the K1 gather.
+// Long K uses 512 x 256 pair tiles (MS = 2, both accumulators in TMEM) where
+// they fill the waves; see launch_dw_gemm.  Measured (tools/bench_dw.py,
+// DESIGN.md §7c): 1.0-1.41 PFLOP/s on the GPT-2.7B layer shapes at 4096-8192
+// tokens, 69-95% of cuBLAS; the fused sink is within +-10% of the dense GEMM
+// followed by the K1 gather.
 #include "kernels.cuh"
 
 #include <cuda.h>
@@ -166,14 +168,32 @@ __device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity
   }
 }
 
+// Work units of the persistent schedule: pair tiles [0, tail0) whole
+// (256 x BN), then every remaining tile as two 256 x BN/2 halves, so that a
+// last wave of r < #pairs / 2 tiles keeps 2r pairs busy for about half as
+// long instead of r pairs for a whole tile (launch_dw_gemm picks tail0).
+struct DwUnit {
+  uint32_t mpair, n0, width;  // M-block pair, first column, columns (BN or BN / 2)
+};
+template <int BN>
+__device__ __forceinline__ DwUnit dw_unit(uint32_t u, uint32_t tail0, uint32_t mp) {
+  uint32_t pt = u, n0 = 0, width = BN;
+  if (u >= tail0) {
+    pt = tail0 + (u - tail0) / 2;
+    n0 = ((u - tail0) & 1u) * (BN / 2);
+    width = BN / 2;
+  }
+  return DwUnit{pt % mp, (pt / mp) * BN + n0, width};
+}
+
 // Shared memory: the epilogue staging half-tile (128 rows x 128 columns,
 // padded rows) first, then the NS-stage operand ring (1024-byte aligned for
 // the 128-byte swizzle atoms).
 constexpr bool kStage_check(uint32_t a, uint32_t b) { return (a + b) % 1024 == 0; }
 
-template <int BN, int NS, int EW>
+template <int BN, int NS, int EW, int MS = 1>
 struct GemmSmem {
-  static constexpr uint32_t kA = kBM * kBK * 2;    // two 64(M) x kBK(K) boxes
+  static constexpr uint32_t kA = MS * kBM * kBK * 2;  // per M sub-tile two 64(M) x kBK(K) boxes
   static constexpr uint32_t kB = (BN / 2) * kBK * 2;  // this SM's half of B: BN/128 boxes
   static_assert(kStage_check(kA, kB), "stage sizes keep 1024-byte alignment");
   static constexpr uint32_t kStage = kA + kB;
@@ -198,10 +218,17 @@ struct GemmSmem {
 // tile i + 1.
 // EW = 2: two epilogue groups work on the two 128-column halves at once
 // (short-K problems, where the epilogue would pace the mainloop).
-template <int EPI, int BN, int NS, int EW>
+// MS = 2: a pair tile is 512 x BN — two 256-row M sub-tiles that share every
+// dY stage (per SM and k-block 48 KB of fill for twice the MMAs: 25% fewer
+// operand bytes per flop, the bound of the MS = 1 form at 256 x 256, DESIGN
+// §7c).  Both accumulators fill the 512 TMEM columns, so there is one
+// buffer and the epilogue does not overlap the next tile's mainloop.
+template <int EPI, int BN, int NS, int EW, int MS>
 __global__ void __launch_bounds__(gemm_threads(EW), 1)
     k_dw_gemm(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tdy, DwArgs a) {
-  using L = GemmSmem<BN, NS, EW>;
+  using L = GemmSmem<BN, NS, EW, MS>;
+  static_assert(MS == 1 || MS == 2, "one or two M sub-tiles");
+  constexpr uint32_t NBUF = MS == 1 ? 2 : 1;  // accumulator buffers
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[NS];
   __shared__ __align__(8) uint64_t empty[NS];
@@ -212,10 +239,12 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t nk = static_cast<uint32_t>((a.K + kBK - 1) / kBK);
   const uint32_t mt = static_cast<uint32_t>((a.M + kBM - 1) / kBM);
-  const uint32_t mp = (mt + 1) / 2;  // M-block pairs
-  const uint32_t npairs = mp * static_cast<uint32_t>((a.N + BN - 1) / BN);
+  const uint32_t mp = (mt + 2 * MS - 1) / (2 * MS);  // pair tiles along M
+  const uint32_t ntiles = mp * static_cast<uint32_t>((a.N + BN - 1) / BN);
+  const uint32_t tail0 = a.tail0 < ntiles ? a.tail0 : ntiles;
+  const uint32_t nunits = tail0 + 2 * (ntiles - tail0);
   const uint32_t crank = cluster_ctarank(), cid = cluster_id_x(), ncl = ncluster_x();
-  constexpr uint32_t kCols = 2 * BN;  // two accumulator buffers
+  constexpr uint32_t kCols = NBUF * MS * BN;
   static_assert(kCols == 256 || kCols == 512, "TMEM allocation must be a power of two");
   uint8_t* ring = smem + EW * L::kTile;
   if (threadIdx.x == 0 && (smem_addr(ring) & 1023u)) __trap();  // swizzle atoms need 1024-byte alignment
@@ -246,42 +275,50 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer (both CTAs), completing on the leader's full barrier
       uint32_t g = 0;
-      for (uint32_t pt = cid; pt < npairs; pt += ncl) {
-        const int m0 = static_cast<int>((2 * (pt % mp) + crank) * kBM);
-        const int n0 = static_cast<int>((pt / mp) * BN + crank * (BN / 2));  // my half of the columns
+      for (uint32_t u = cid; u < nunits; u += ncl) {
+        const DwUnit t = dw_unit<BN>(u, tail0, mp);
+        const int n0 = static_cast<int>(t.n0 + crank * (t.width / 2));  // my half of the columns
+        const uint32_t boxes = t.width / 128;                          // 64-column dY boxes per CTA
         for (uint32_t kb = 0; kb < nk; ++kb, ++g) {
           const uint32_t s = g % NS;
           if (g >= static_cast<uint32_t>(NS)) mbar_wait_bounded(&empty[s], ((g / NS) - 1) & 1u);
           uint8_t* st = ring + s * L::kStage;
           const uint32_t fb = mapa_shared(smem_addr(&full[s]), 0);
-          if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * L::kStage);  // both CTAs' boxes (OOB parts count)
+          if (crank == 0) mbar_arrive_expect_tx(&full[s], 2 * (L::kA + boxes * kBox));  // both CTAs (OOB parts count)
           const int kc = static_cast<int>(kb * kBK);
-          tma_load_2d_pair(st, &tx, m0, kc, fb);
-          tma_load_2d_pair(st + kBox, &tx, m0 + 64, kc, fb);
 #pragma unroll
-          for (int c = 0; c < BN / 128; ++c) tma_load_2d_pair(st + L::kA + c * kBox, &tdy, n0 + 64 * c, kc, fb);
+          for (int j = 0; j < MS; ++j) {  // my 128 rows of each M sub-tile
+            const int m0 = static_cast<int>((2 * (MS * t.mpair + j) + crank) * kBM);
+            tma_load_2d_pair(st + 2 * j * kBox, &tx, m0, kc, fb);
+            tma_load_2d_pair(st + (2 * j + 1) * kBox, &tx, m0 + 64, kc, fb);
+          }
+          for (uint32_t c = 0; c < boxes; ++c) tma_load_2d_pair(st + L::kA + c * kBox, &tdy, n0 + 64 * c, kc, fb);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && crank == 0) {  // ---- MMA issue (leader)
-      constexpr uint32_t idesc = umma_idesc<2 * kBM, BN>();
+      constexpr uint32_t idesc_full = umma_idesc<2 * kBM, BN>(), idesc_half = umma_idesc<2 * kBM, BN / 2>();
       uint32_t g = 0, i = 0;
-      for (uint32_t pt = cid; pt < npairs; pt += ncl, ++i) {
-        const uint32_t buf = i & 1u;
-        if (i >= 2) mbar_wait_bounded(&acce[buf], ((i >> 1) - 1) & 1u);  // both epilogues drained it
+      for (uint32_t u = cid; u < nunits; u += ncl, ++i) {
+        const uint32_t idesc = u < tail0 ? idesc_full : idesc_half;
+        const uint32_t buf = i % NBUF;
+        if (i >= NBUF) mbar_wait_bounded(&acce[buf], ((i / NBUF) - 1) & 1u);  // both epilogues drained it
         tc_fence_after();
-        const uint32_t acc = tmem + buf * BN;
+        const uint32_t acc = tmem + buf * MS * BN;
         for (uint32_t kb = 0; kb < nk; ++kb, ++g) {
           const uint32_t s = g % NS;
           mbar_wait_bounded(&full[s], (g / NS) & 1u);
           tc_fence_after();
           const uint32_t sa = smem_addr(ring + s * L::kStage), sb = sa + L::kA;
 #pragma unroll
-          for (uint32_t j = 0; j < kBK / 16; ++j) {  // UMMA_K = 16: 16 K-rows of 128 bytes
-            const uint64_t da = umma_desc_mn_sw128(sa + j * 2048, kBox, 1024);
-            const uint64_t db = umma_desc_mn_sw128(sb + j * 2048, kBox, 1024);
-            umma_f16_pair(acc, da, db, idesc, (kb | j) != 0u);
+          for (uint32_t kk = 0; kk < kBK / 16; ++kk) {  // UMMA_K = 16: 16 K-rows of 128 bytes
+            const uint64_t db = umma_desc_mn_sw128(sb + kk * 2048, kBox, 1024);
+#pragma unroll
+            for (uint32_t j = 0; j < static_cast<uint32_t>(MS); ++j) {
+              const uint64_t da = umma_desc_mn_sw128(sa + 2 * j * kBox + kk * 2048, kBox, 1024);
+              umma_f16_pair(acc + j * BN, da, db, idesc, (kb | kk) != 0u);
+            }
           }
           umma_commit_pair_mc(&empty[s], 0x3);  // frees the stage in both CTAs
         }
@@ -296,16 +333,25 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
     const uint32_t gx = (warp - 2) >> 2;
     uint16_t* tile = reinterpret_cast<uint16_t*>(smem + gx * L::kTile);
     uint32_t i = 0;
-    for (uint32_t pt = cid; pt < npairs; pt += ncl, ++i) {
-      const uint32_t buf = i & 1u;
-      const uint64_t m0 = static_cast<uint64_t>(2 * (pt % mp) + crank) * kBM;
-      const uint32_t nb = pt / mp;
-      const uint64_t row = m0 + r;
-      mbar_wait_bounded(&accf[buf], (i >> 1) & 1u);
+    for (uint32_t u = cid; u < nunits; u += ncl, ++i) {
+      const uint32_t buf = i % NBUF;
+      const DwUnit t = dw_unit<BN>(u, tail0, mp);
+      const uint32_t nhalves = t.width / L::kHalf;
+      mbar_wait_bounded(&accf[buf], (i / NBUF) & 1u);
       tc_fence_after();
+      if (gx >= nhalves) {  // nothing of this unit for this group: release the buffer at once
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_addr(&acce[buf]), 0));
+        continue;
+      }
 #pragma unroll 1
-      for (uint32_t h = gx; h < BN / L::kHalf; h += EW) {
-        const uint64_t nh = static_cast<uint64_t>(nb) * BN + h * L::kHalf;  // first column of this half
+      for (uint32_t sub = 0; sub < static_cast<uint32_t>(MS); ++sub) {
+      const uint64_t m0 = static_cast<uint64_t>(2 * (MS * t.mpair + sub) + crank) * kBM;
+      const uint64_t row = m0 + r;
+      const uint32_t tcol = (buf * MS + sub) * BN;  // this sub-tile's accumulator columns
+#pragma unroll 1
+      for (uint32_t h = gx; h < nhalves; h += EW) {
+        const uint64_t nh = static_cast<uint64_t>(t.n0) + h * L::kHalf;  // first column of this half
         uint32_t ks = 0, cnt = 0;
         if constexpr (EPI == 1) {  // this row's kept range in the column half (kb: 128-column blocks)
           if (row < a.M && nh < a.N) {
@@ -320,7 +366,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
           uint32_t v[L::kHalf / 32][32];
 #pragma unroll
           for (uint32_t cc = 0; cc < L::kHalf / 32; ++cc)
-            tmem_ld32_nowait(tmem + ((q * 32u) << 16) + buf * BN + h * L::kHalf + cc * 32, v[cc]);
+            tmem_ld32_nowait(tmem + ((q * 32u) << 16) + tcol + h * L::kHalf + cc * 32, v[cc]);
 #pragma unroll
           for (uint32_t cc = 0; cc < L::kHalf / 32; ++cc) {
             tmem_wait32(v[cc]);
@@ -336,7 +382,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
             }
           }
         }
-        if (h + EW >= BN / L::kHalf) {  // this group's last half: TMEM drained for it
+        if (sub + 1 == MS && h + EW >= nhalves) {  // this group's last half: TMEM drained for it
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_addr(&acce[buf]), 0));
@@ -376,6 +422,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
           asm volatile("bar.sync %0, 128;" ::"r"(1 + gx) : "memory");
         }
       }
+      }  // M sub-tiles
     }
   }
   __syncwarp();
@@ -486,26 +533,63 @@ int launch_dw_gemm(const uint16_t* x, const uint16_t* dy, const DwArgs& a, int e
   CUtensorMap tx, tdy;
   SAMO_TRY(cached_map(&tx, x, a.K, a.M));
   SAMO_TRY(cached_map(&tdy, dy, a.K, a.N));
-  const uint64_t pairs = ((a.M + 2 * kBM - 1) / (2 * kBM)) * ((a.N + kGemmBN - 1) / kGemmBN);
-  const int grid = 2 * static_cast<int>(std::min<uint64_t>(pairs, static_cast<uint64_t>(num_sms() / 2)));
-  // Short K (<= 16 k-blocks per tile): two epilogue groups (one stage less).
-  const char* ew = getenv("SAMO_DW_EW");  // tuning override: 1 or 2 epilogue groups
-  const bool short_k = (ew && *ew) ? atoi(ew) == 2 : a.K <= 16 * kBK;
+  // Variants: short K (<= 16 k-blocks per tile) -> two epilogue groups,
+  // 256 x 256 pair tiles (one stage less); long K -> 512 x 256 pair tiles
+  // (MS = 2, two epilogue groups, 3 stages of 48 KB; SAMO_DW_MS2_EW=1: one
+  // group, 4 stages, 0.6-7% slower) or 256 x 256 (MS = 1, 5 stages).
+  auto env_on = [](const char* name, int dflt) {
+    const char* e = getenv(name);
+    return (e && *e) ? atoi(e) : dflt;
+  };
+  const int ew = env_on("SAMO_DW_EW", 0);  // tuning override: 1 or 2 epilogue groups
+  const bool short_k = ew ? ew == 2 : a.K <= 16 * kBK;
+  // MS = 2 fills its waves worse (half as many tiles) and exposes its
+  // epilogue, so it is taken when its last wave is >= 85% full and K spans
+  // >= 48 k-blocks, or when it fits in one wave where MS = 1 needs two
+  // (measured on 10 shapes; SAMO_DW_MS=1/2 forces a form).
+  const uint64_t P = static_cast<uint64_t>(num_sms() / 2);
+  const uint64_t ncol = (a.N + kGemmBN - 1) / kGemmBN, nkb = (a.K + kBK - 1) / kBK;
+  const uint64_t t1 = ((a.M + 2 * kBM - 1) / (2 * kBM)) * ncol, t2 = ((a.M + 4 * kBM - 1) / (4 * kBM)) * ncol;
+  const double fill2 = static_cast<double>(t2) / static_cast<double>(((t2 + P - 1) / P) * P);
+  const bool auto2 = (fill2 >= 0.85 && nkb >= 48) || (t2 <= P && t1 > P);
+  const int ms_env = env_on("SAMO_DW_MS", 0);
+  const int ms = short_k ? 1 : (ms_env == 1 || ms_env == 2) ? ms_env : (auto2 ? 2 : 1);
+  // Tail split (MS = 1): a last partial wave of r tiles with 2r <= #pairs
+  // runs as 2r half tiles (SAMO_DW_TAIL=0 turns it off, for A/B).
+  const uint64_t tiles = ms == 2 ? t2 : t1;
+  const uint64_t r = tiles % P;
+  DwArgs args = a;
+  args.tail0 = static_cast<uint32_t>(tiles);
+  if (ms == 1 && r > 0 && 2 * r <= P && env_on("SAMO_DW_TAIL", 1) != 0) args.tail0 = static_cast<uint32_t>(tiles - r);
+  const uint64_t units = args.tail0 + 2 * (tiles - args.tail0);
+  const int grid = 2 * static_cast<int>(std::min<uint64_t>(units, P));
   using F = void (*)(CUtensorMap, CUtensorMap, DwArgs);
   F fn;
   uint32_t smem;
-  int threads;
+  int threads, variant;
   if (short_k) {
-    fn = epi == 0 ? k_dw_gemm<0, kGemmBN, 4, 2> : k_dw_gemm<1, kGemmBN, 4, 2>;
+    fn = epi == 0 ? k_dw_gemm<0, kGemmBN, 4, 2, 1> : k_dw_gemm<1, kGemmBN, 4, 2, 1>;
     smem = GemmSmem<kGemmBN, 4, 2>::kBytes;
     threads = gemm_threads(2);
-  } else {
-    fn = epi == 0 ? k_dw_gemm<0, kGemmBN, kGemmNS, 1> : k_dw_gemm<1, kGemmBN, kGemmNS, 1>;
+    variant = 0;
+  } else if (ms == 1) {
+    fn = epi == 0 ? k_dw_gemm<0, kGemmBN, kGemmNS, 1, 1> : k_dw_gemm<1, kGemmBN, kGemmNS, 1, 1>;
     smem = GemmSmem<kGemmBN, kGemmNS, 1>::kBytes;
     threads = gemm_threads(1);
+    variant = 1;
+  } else if (env_on("SAMO_DW_MS2_EW", 2) != 2) {
+    fn = epi == 0 ? k_dw_gemm<0, kGemmBN, 4, 1, 2> : k_dw_gemm<1, kGemmBN, 4, 1, 2>;
+    smem = GemmSmem<kGemmBN, 4, 1, 2>::kBytes;
+    threads = gemm_threads(1);
+    variant = 2;
+  } else {
+    fn = epi == 0 ? k_dw_gemm<0, kGemmBN, 3, 2, 2> : k_dw_gemm<1, kGemmBN, 3, 2, 2>;
+    smem = GemmSmem<kGemmBN, 3, 2, 2>::kBytes;
+    threads = gemm_threads(2);
+    variant = 3;
   }
-  static bool attr_set[4] = {false, false, false, false};
-  const int slot = (epi != 0) + 2 * short_k;
+  static bool attr_set[8] = {false, false, false, false, false, false, false, false};
+  const int slot = (epi != 0) + 2 * variant;
   if (!attr_set[slot]) {
     SAMO_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set[slot] = true;
@@ -522,7 +606,7 @@ int launch_dw_gemm(const uint16_t* x, const uint16_t* dy, const DwArgs& a, int e
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  SAMO_CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, tx, tdy, a));
+  SAMO_CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, tx, tdy, args));
   SAMO_LAUNCH_CHECK("k_dw_gemm");
   return SAMO_OK;
 }
