@@ -46,23 +46,63 @@ SHAPES = [(576, 128, 128), (64, 256, 384), (100, 136, 200), (1, 8, 8), (576, 102
           (130, 2560, 2560)]  # 100 pair tiles over 74 pairs: a partial second wave
 
 
+_REF = {}  # (batch, in, out) -> (x, dy, reference bits, tolerance): the oracle GEMM runs once per shape
+
+
+def _reference(oracle, batch, n_in, n_out):
+    key = (batch, n_in, n_out)
+    if key not in _REF:
+        rng = np.random.default_rng(batch * 7 + n_in)
+        x = _half(rng, (batch, n_in), 1.0)
+        dy = _half(rng, (batch, n_out), 1024.0 / batch)  # loss-scaled softmax grads (train.hpp:276)
+        xb, db = _bits(x), _bits(dy)
+        want = oracle.dw_matmul(xb, db)
+        absum = np.abs(xb.view(np.float16).astype(np.float64)).T @ np.abs(db.view(np.float16).astype(np.float64))
+        _REF[key] = (x, dy, want, _ulp16(want) + 2.0 * batch * 2.0 ** -24 * absum)
+    return _REF[key]
+
+
 @pytest.mark.parametrize("batch,n_in,n_out", SHAPES)
 def test_dw_gemm_vs_reference(S, oracle, batch, n_in, n_out):
-    rng = np.random.default_rng(batch * 7 + n_in)
-    x = _half(rng, (batch, n_in), 1.0)
-    dy = _half(rng, (batch, n_out), 1024.0 / batch)  # loss-scaled softmax grads (train.hpp:276)
+    x, dy, want, tol = _reference(oracle, batch, n_in, n_out)
     got = _bits(S.dw_gemm(x, dy))
-    xb, db = _bits(x), _bits(dy)
-    want = oracle.dw_matmul(xb, db)
-    xf = xb.view(np.float16).astype(np.float64)
-    df = db.view(np.float16).astype(np.float64)
-    absum = np.abs(xf).T @ np.abs(df)
     gf = got.view(np.float16).astype(np.float64)
     wf = want.view(np.float16).astype(np.float64)
-    tol = _ulp16(want) + 2.0 * batch * 2.0 ** -24 * absum
     bad = np.abs(gf - wf) > tol
     assert not bad.any(), (int(bad.sum()), np.argwhere(bad)[:5])
     assert np.mean(got == want) > 0.5
+
+
+# Long-K shapes under each launch form (the launcher reads the knobs on every
+# call): MS = 1 / 2 (256 x 256 or 512 x 256 pair tiles), with and without
+# the tail-wave split; ragged M (520: a partly out-of-range sub-tile) and N.
+FORMS = [{"SAMO_DW_MS": "1", "SAMO_DW_TAIL": "1"}, {"SAMO_DW_MS": "1", "SAMO_DW_TAIL": "0"},
+         {"SAMO_DW_MS": "2"}, {"SAMO_DW_MS": "2", "SAMO_DW_MS2_EW": "1"}]
+LONG_K = [(1100, 256, 384), (1100, 520, 1032), (1100, 2560, 2560), (3000, 136, 8)]
+
+
+@pytest.mark.parametrize("form", FORMS, ids=lambda f: "-".join(f"{k[8:]}{v}" for k, v in f.items()))
+@pytest.mark.parametrize("batch,n_in,n_out", LONG_K)
+def test_dw_gemm_forms_vs_reference(S, oracle, monkeypatch, form, batch, n_in, n_out):
+    for k, v in form.items():
+        monkeypatch.setenv(k, v)
+    test_dw_gemm_vs_reference(S, oracle, batch, n_in, n_out)
+
+
+@pytest.mark.parametrize("form", FORMS, ids=lambda f: "-".join(f"{k[8:]}{v}" for k, v in f.items()))
+def test_sink_dw_forms_equal_unfused(S, monkeypatch, form):
+    for k, v in form.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(29)
+    shapes = [(2560, 2560), (520, 1032)]
+    fused, unfused = _model(S, shapes, 0.9, 10), _model(S, shapes, 0.9, 10)
+    for l, (i, o) in enumerate(shapes):
+        x, dy = _half(rng, (1100, i), 1.0), _half(rng, (1100, o), 2.0)
+        fused.sink_dw(l, x, dy)
+        unfused.sink_dense(l, S.dw_gemm(x, dy).reshape(-1))
+    torch.cuda.synchronize()
+    for l in range(len(shapes)):
+        assert np.array_equal(_bits(fused.read(l, "grad16")), _bits(unfused.read(l, "grad16"))), l
 
 
 def test_dw_gemm_errors(S):
