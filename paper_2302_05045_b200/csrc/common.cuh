@@ -216,6 +216,16 @@ __device__ __forceinline__ uint16_t f32_to_f16_bits(float x) {
   return h;
 }
 
+// Two at once (one cvt.rn.f16x2.f32): lo -> bits 0-15, hi -> bits 16-31;
+// NaN inputs (rare) take the exact path above.
+__device__ __forceinline__ uint32_t f32x2_to_f16x2_bits(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  if ((__float_as_uint(lo) & 0x7FFFFFFFu) > 0x7F800000u || (__float_as_uint(hi) & 0x7FFFFFFFu) > 0x7F800000u)
+    r = static_cast<uint32_t>(f32_to_f16_bits(lo)) | (static_cast<uint32_t>(f32_to_f16_bits(hi)) << 16);
+  return r;
+}
+
 // half_bits_to_float (half.hpp:52-71): exact widening; NaNs keep their
 // payload (signalling NaNs stay signalling).
 __device__ __forceinline__ float f16_bits_to_f32(uint16_t h) {

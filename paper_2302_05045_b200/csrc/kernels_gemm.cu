@@ -26,7 +26,7 @@
 // Long K uses 512 x 256 pair tiles (MS = 2, both accumulators in TMEM) where
 // they fill the waves; see launch_dw_gemm.  Measured (tools/bench_dw.py,
 // DESIGN.md §7c): 1.0-1.41 PFLOP/s on the GPT-2.7B layer shapes at 4096-8192
-// tokens, 69-95% of cuBLAS; the fused sink is within +-10% of the dense GEMM
+// tokens, 70-95% of cuBLAS; the fused sink is within +-10% of the dense GEMM
 // followed by the K1 gather.
 #include "kernels.cuh"
 
@@ -376,8 +376,8 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
               uint32_t w[4];
 #pragma unroll
               for (int z = 0; z < 4; ++z)
-                w[z] = f32_to_f16_bits(__uint_as_float(v[cc][8 * e + 2 * z])) |
-                       (static_cast<uint32_t>(f32_to_f16_bits(__uint_as_float(v[cc][8 * e + 2 * z + 1]))) << 16);
+                w[z] = f32x2_to_f16x2_bits(__uint_as_float(v[cc][8 * e + 2 * z]),
+                                           __uint_as_float(v[cc][8 * e + 2 * z + 1]));
               dst[e] = make_uint4(w[0], w[1], w[2], w[3]);
             }
           }
