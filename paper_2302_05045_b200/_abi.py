@@ -169,6 +169,10 @@ def load(path: os.PathLike | str | None = None) -> C.CDLL:
         raise ImportError(
             f"{p} is missing: build it with `python -m paper_2302_05045_b200.build` "
             "(the SAMO path has no CPU fallback)")
+    try:  # torch first: its bundled libnccl.so.2 (newer than the system one) then
+        import torch  # noqa: F401  serves our NCCL dependency, and torch stays importable
+    except ImportError:
+        pass
     lib = C.CDLL(str(p))
     for name, (res, args) in _SIGS.items():
         fn = getattr(lib, name)

@@ -83,6 +83,12 @@ class PrunedIndexSet:
     def count(self) -> int:
         return int(self.indices.numel())
 
+    def as_int64(self) -> torch.Tensor:
+        """The indices widened for torch indexing: values >= 2^31 (layers up to
+        2^32 - 1 elements, prune.hpp:106-109) are held as negative int32, so a
+        plain .long() would sign-extend them."""
+        return self.indices.long() & 0xFFFFFFFF
+
 
 @dataclass
 class LayerParams:

@@ -86,3 +86,14 @@ def test_no_cpu_fallback(lib):
     d = (LayerDesc * 1)(LayerDesc(16, 4))
     assert lib.samo_model_create(d, 1, 0, C.byref(h)) == 6  # SAMO_E_CUDA
     assert b"no CPU fallback" in lib.samo_last_error()
+
+
+def test_index_set_widening():
+    """uint32 indices >= 2^31 live in int32 tensors as negative values;
+    as_int64 widens them without sign extension (dense_len < 2^32)."""
+    torch = pytest.importorskip("torch")
+    from paper_2302_05045_b200 import samo
+    raw = torch.tensor([0, 5, 2**31 - 1, 2**31, 2**32 - 2], dtype=torch.int64).to(torch.int32)
+    s = samo.PrunedIndexSet("big", 2**32 - 1, raw)
+    assert s.as_int64().tolist() == [0, 5, 2**31 - 1, 2**31, 2**32 - 2]
+    assert s.count() == 5

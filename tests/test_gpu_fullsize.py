@@ -108,7 +108,7 @@ def test_max_layer_size(cuda, oracle):
     sets = samo.magnitude_prune([samo.LayerParams("big", w, True)], p)
     keep = oracle.unpruned_count(p, n)
     assert sets[0].count() == keep
-    idx_t = sets[0].indices.long() & 0xFFFFFFFF  # uint32 indices held in an int32 tensor
+    idx_t = sets[0].as_int64()  # uint32 indices held in an int32 tensor
     idx = sets[0].indices.cpu().numpy().view(np.uint32)
     assert np.all(np.diff(idx.astype(np.int64)) > 0) and int(idx[-1]) < n
     thr = w[idx_t].abs().min()
