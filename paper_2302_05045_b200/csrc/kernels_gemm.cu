@@ -588,11 +588,14 @@ int launch_dw_gemm(const uint16_t* x, const uint16_t* dy, const DwArgs& a, int e
     threads = gemm_threads(2);
     variant = 3;
   }
-  static bool attr_set[8] = {false, false, false, false, false, false, false, false};
+  // The shared-memory opt-in is per device: remember it per (device, kernel).
+  static bool attr_set[64][8] = {};
+  int dev = 0;
+  SAMO_CUDA_TRY(cudaGetDevice(&dev));
   const int slot = (epi != 0) + 2 * variant;
-  if (!attr_set[slot]) {
+  if (dev < 0 || dev >= 64 || !attr_set[dev][slot]) {
     SAMO_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr_set[slot] = true;
+    if (dev >= 0 && dev < 64) attr_set[dev][slot] = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
