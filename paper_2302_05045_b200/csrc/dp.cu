@@ -17,8 +17,9 @@
 
 void close_peers(samo_model* md) {
   close_nvls(md);
+  const bool ipc = !(md->comm && md->comm->local_group);  // a local group maps its peers directly
   for (int q = 0; q < kMaxP2PRanks; ++q) {
-    if (md->peer_base[q] && md->peer_base[q] != md->block) cudaIpcCloseMemHandle(md->peer_base[q]);
+    if (ipc && md->peer_base[q] && md->peer_base[q] != md->block) cudaIpcCloseMemHandle(md->peer_base[q]);
     md->peer_base[q] = nullptr;
   }
   md->p2p_ok = false;
@@ -462,6 +463,8 @@ static void set_pull_args(samo_model* md, const ShardPlan& p, StepArgs& a);
 int step_p2p(samo_model* md, cudaStream_t S, bool gather) {
   const int G = md->comm->nranks, r = md->comm->rank;
   if (p2p_buckets(G) > 1) return step_p2p_pipelined(md, S, p2p_buckets(G), gather);
+  if (md->comm->local_group)
+    return fail(SAMO_E_STATE, "a local group has no NCCL: it needs the pipelined exchange (SAMO_P2P_BUCKETS >= 2)");
   const uint64_t c = align_up((md->n_tot + G - 1) / G, 8);
   if (static_cast<uint64_t>(G) * c + 8 > md->n_al + kFlagOff)
     return fail(SAMO_E_PARAMETER, "too many ranks for the arena padding");
@@ -767,7 +770,17 @@ static int launch_gather_push(samo_model* md, cudaStream_t S) {
 // in bucket b, once every rank has published bucket b.  The global skip flag
 // forces every K1 to finish before any shard update, so K1 stays serial.
 // Grids: SAMO_P2P_SHARD_CTAS / SAMO_P2P_EXPAND_CTAS per SM (tuning).
-static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather) {
+// The pipelined step in phases, so that a local group (one device, no
+// concurrency between its ranks' streams) can queue every rank's phase
+// before any rank's next one: then each wait below is already satisfied.
+struct P2PStep {
+  P2PArgs pa{};
+  StepArgs sbase{};
+  int B = 1, ge = 0;
+  bool push = false, gather = true, nvls = false, pull = false;
+};
+
+static int p2p_prepare(samo_model* md, int B, bool gather, P2PStep& sp) {
   const int G = md->comm->nranks, r = md->comm->rank;
   SAMO_TRY(plan_buckets(md));  // side streams + events
   ShardPlan& p = md->p2p_plan;
@@ -779,16 +792,17 @@ static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather
       md->ev_sh.push_back(e);
     }
   }
-  cudaStream_t E = md->s_comm;
-  float* flag = flag_ptr(md);
-  const bool push = gather && p2p_push();
-  const bool pull = p2p_pull();
-  if (push) SAMO_TRY(build_push_tiles(md, p));
+  sp.B = B;
+  sp.gather = gather;
+  sp.push = gather && p2p_push();
+  sp.pull = p2p_pull();
+  if (sp.push) SAMO_TRY(build_push_tiles(md, p));
   const char* base = static_cast<const char*>(md->block);
   const size_t g_off = reinterpret_cast<const char*>(md->g) - base;
   const size_t c_off = reinterpret_cast<const char*>(md->c16) - base;
   const size_t s_off = reinterpret_cast<const char*>(md->slots) - base;
-  P2PArgs pa{};
+  P2PArgs& pa = sp.pa;
+  pa = P2PArgs{};
   for (int q = 0; q < G; ++q) {
     char* pb = static_cast<char*>(md->peer_base[q]);
     pa.g16[q] = reinterpret_cast<const uint16_t*>(pb + g_off);
@@ -804,57 +818,108 @@ static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather
   pa.prm = adam_params(&md->cfg);
   pa.cfg = md->capturing ? md->cfg_dev : nullptr;
   pa.st = md->st;
-  pa.flag_slot = flag;
+  pa.flag_slot = flag_ptr(md);
   pa.norm_partials = md->norm_partials;
   pa.norm2_out = md->norm2;  // scratch: the bucket totals travel in the slots
   pa.done = md->done;
   const int sms = num_sms();
   pa.tma = env_int("SAMO_P2P_TMA", 0);
   pa.grid = sms * std::max(1, env_int("SAMO_P2P_SHARD_CTAS", pa.tma ? 1 : 2));
-  const int ge = std::min(md->grid_expand, sms * std::max(1, env_int("SAMO_P2P_EXPAND_CTAS", 2)));
-
-  pa.push = push ? 1 : 0;
+  sp.ge = std::min(md->grid_expand, sms * std::max(1, env_int("SAMO_P2P_EXPAND_CTAS", 2)));
+  pa.push = sp.push ? 1 : 0;
   pa.recv = reinterpret_cast<const uint16_t*>(md->g);
   pa.rstride = static_cast<uint64_t>(B) * p.c;
-  pa.local_c16 = pull ? 1 : 0;
-  const bool nvls = md->mc_c16 && !pull;
-  pa.mc16 = nvls ? md->mc_c16 : nullptr;
-  SAMO_TRY(phase_mark(md, 0, S));
-  if (push) {
-    SAMO_TRY(launch_gather_push(md, S));
-  } else if (gather) {
-    SAMO_TRY(launch_gather(step_args(md), false, md->grid_gather16, S));
+  pa.local_c16 = sp.pull ? 1 : 0;
+  sp.nvls = md->mc_c16 && !sp.pull;
+  pa.mc16 = sp.nvls ? md->mc_c16 : nullptr;
+  sp.sbase = step_args(md);
+  if (sp.pull) set_pull_args(md, p, sp.sbase);
+  return SAMO_OK;
+}
+
+static int p2p_gather(samo_model* md, const P2PStep& sp, cudaStream_t S) {
+  if (sp.push) return launch_gather_push(md, S);
+  if (sp.gather) return launch_gather(step_args(md), false, md->grid_gather16, S);
+  return SAMO_OK;
+}
+
+// phase 1: publish this rank's skip indicator; 2: wait for every rank's and
+// sum them in rank order; 3: both (one kernel).
+static int p2p_flag(samo_model* md, const P2PStep& sp, int phase, cudaStream_t S) {
+  return launch_p2p_flag(sp.pa.slots, sp.pa.G, sp.pa.rank, flag_ptr(md), phase, S);
+}
+
+static int p2p_shards(samo_model* md, P2PStep& sp, cudaStream_t S) {
+  const ShardPlan& p = md->p2p_plan;
+  const int r = md->comm->rank;
+  for (int b = 0; b < sp.B; ++b) {
+    sp.pa.k0 = std::min<uint64_t>(b * p.C + r * p.c, md->n_tot);
+    sp.pa.k1 = std::min<uint64_t>(b * p.C + (r + 1) * p.c, md->n_tot);
+    sp.pa.i0 = static_cast<uint64_t>(b) * p.c;
+    sp.pa.bucket = b;
+    SAMO_TRY(launch_shard_p2p(sp.pa, S));  // also when empty: it signals
   }
+  return SAMO_OK;
+}
+
+static int p2p_expand(samo_model* md, const P2PStep& sp, cudaStream_t E) {
+  const ShardPlan& p = md->p2p_plan;
+  for (int b = 0; b < sp.B; ++b) {
+    SAMO_TRY(launch_p2p_wait(md->slots, sp.pa.G, b, E));
+    StepArgs a = sp.sbase;
+    a.g = sp.nvls ? md->uc_c16 : md->c16;
+    a.tiles = md->tiles + p.ex_t[b];
+    a.ntiles = p.ex_t[b + 1] - p.ex_t[b];
+    if (a.ntiles) SAMO_TRY(launch_expand_c16(a, std::min<int>(sp.ge, a.ntiles), E));
+  }
+  return SAMO_OK;
+}
+
+static int p2p_finish(samo_model* md, const P2PStep& sp, cudaStream_t S) {
+  SAMO_TRY(launch_step_finalize(md->st, md->slots->norm, sp.B * kMaxP2PRanks, flag_ptr(md), md->cfg.beta1,
+                                md->cfg.beta2, md->capturing ? md->cfg_dev : nullptr, S));
+  return launch_p2p_epoch(md->slots, S);
+}
+
+static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather) {
+  P2PStep sp;
+  SAMO_TRY(p2p_prepare(md, B, gather, sp));
+  cudaStream_t E = md->s_comm;
+  SAMO_TRY(phase_mark(md, 0, S));
+  SAMO_TRY(p2p_gather(md, sp, S));
   SAMO_TRY(phase_mark(md, 1, S));
-  SAMO_TRY(launch_p2p_flag(pa.slots, G, r, flag, S));
+  SAMO_TRY(p2p_flag(md, sp, 3, S));
   SAMO_TRY(phase_mark(md, 2, S));
   SAMO_CUDA_TRY(cudaEventRecord(md->ev_fork, S));
   SAMO_CUDA_TRY(cudaStreamWaitEvent(E, md->ev_fork, 0));
-  for (int b = 0; b < B; ++b) {
-    pa.k0 = std::min<uint64_t>(b * p.C + r * p.c, md->n_tot);
-    pa.k1 = std::min<uint64_t>(b * p.C + (r + 1) * p.c, md->n_tot);
-    pa.i0 = static_cast<uint64_t>(b) * p.c;
-    pa.bucket = b;
-    SAMO_TRY(launch_shard_p2p(pa, S));  // also when empty: it signals
-  }
-  StepArgs sbase = step_args(md);
-  if (pull) set_pull_args(md, p, sbase);
-  for (int b = 0; b < B; ++b) {
-    SAMO_TRY(launch_p2p_wait(md->slots, G, b, E));
-    StepArgs a = sbase;
-    a.g = nvls ? md->uc_c16 : md->c16;
-    a.tiles = md->tiles + p.ex_t[b];
-    a.ntiles = p.ex_t[b + 1] - p.ex_t[b];
-    if (a.ntiles) SAMO_TRY(launch_expand_c16(a, std::min<int>(ge, a.ntiles), E));
-  }
+  SAMO_TRY(p2p_shards(md, sp, S));
+  SAMO_TRY(p2p_expand(md, sp, E));
   SAMO_CUDA_TRY(cudaEventRecord(md->ev_flag, E));
   SAMO_CUDA_TRY(cudaStreamWaitEvent(S, md->ev_flag, 0));
   SAMO_TRY(phase_mark(md, 3, S));
-  SAMO_TRY(launch_step_finalize(md->st, md->slots->norm, B * kMaxP2PRanks, flag, md->cfg.beta1,
-                                md->cfg.beta2, md->capturing ? md->cfg_dev : nullptr, S));
-  SAMO_TRY(launch_p2p_epoch(md->slots, S));
+  SAMO_TRY(p2p_finish(md, sp, S));
   SAMO_TRY(phase_mark(md, 4, S));
   md->phase_count = 4;
+  return SAMO_OK;
+}
+
+// One step of every rank of a local group, queued phase by phase on one
+// stream: each rank's waits (flag, buckets) find their signals already
+// written, so no kernel spins on another that is queued behind it.
+static int step_local_group(samo_model* const* models, int G, bool gather, cudaStream_t S) {
+  const int B = p2p_buckets(G);
+  if (B < 2) return fail(SAMO_E_STATE, "a local group needs the pipelined exchange (SAMO_P2P_BUCKETS >= 2)");
+  std::vector<P2PStep> sp(G);
+  for (int r = 0; r < G; ++r) {
+    SAMO_TRY(flush_cfg(models[r], S));
+    SAMO_TRY(p2p_prepare(models[r], B, gather, sp[r]));
+  }
+  for (int r = 0; r < G; ++r) SAMO_TRY(p2p_gather(models[r], sp[r], S));
+  for (int r = 0; r < G; ++r) SAMO_TRY(p2p_flag(models[r], sp[r], 1, S));
+  for (int r = 0; r < G; ++r) SAMO_TRY(p2p_flag(models[r], sp[r], 2, S));
+  for (int r = 0; r < G; ++r) SAMO_TRY(p2p_shards(models[r], sp[r], S));
+  for (int r = 0; r < G; ++r) SAMO_TRY(p2p_expand(models[r], sp[r], S));
+  for (int r = 0; r < G; ++r) SAMO_TRY(p2p_finish(models[r], sp[r], S));
   return SAMO_OK;
 }
 
@@ -870,6 +935,66 @@ int samo_model_set_exchange(samo_model* md, int mode) {
     cudaGraphExecDestroy(md->graph);
     md->graph = nullptr;
   }
+  return clear_ok();
+}
+
+// Test harness (samo_cuda.h): G models on this device become the ranks of
+// one data-parallel group with directly mapped peers.  Everything the
+// pipelined peer-to-peer step needs is planned here, before any rank's
+// kernels are queued, because those kernels wait for each other.
+int samo_model_attach_local_group(samo_model* const* models, int G) {
+  if (!models || G < 2 || G > kMaxP2PRanks)
+    return fail(SAMO_E_PARAMETER, "local group of %d models (2..%d)", G, kMaxP2PRanks);
+  int dev = -1;
+  SAMO_CUDA_TRY(cudaGetDevice(&dev));
+  for (int r = 0; r < G; ++r) {
+    samo_model* md = models[r];
+    if (!md) return fail(SAMO_E_PARAMETER, "null model %d", r);
+    SAMO_TRY(step_ready(md));
+    if (md->block_bytes != models[0]->block_bytes || md->n_tot != models[0]->n_tot ||
+        md->ntiles != models[0]->ntiles || md->nlayers != models[0]->nlayers)
+      return fail(SAMO_E_DIMENSION, "model %d: layout differs from model 0", r);
+    cudaPointerAttributes pa{};
+    SAMO_CUDA_TRY(cudaPointerGetAttributes(&pa, md->block));
+    if (pa.device != dev) return fail(SAMO_E_PARAMETER, "model %d is not on the current device", r);
+  }
+  for (int r = 0; r < G; ++r) {
+    samo_model* md = models[r];
+    close_peers(md);
+    delete md->own_comm;
+    md->own_comm = new samo_comm{};
+    md->own_comm->nranks = G;
+    md->own_comm->rank = r;
+    md->own_comm->local_group = true;
+    md->comm = md->own_comm;
+    md->cfg_dirty = true;
+    md->exchange = SAMO_EXCHANGE_P2P;
+    for (int q = 0; q < G; ++q) md->peer_base[q] = models[q]->block;
+    md->p2p_ok = true;
+    if (md->graph) {
+      cudaGraphExecDestroy(md->graph);
+      md->graph = nullptr;
+    }
+  }
+  const int B = p2p_buckets(G);
+  for (int r = 0; r < G && B > 1; ++r) {
+    SAMO_TRY(plan_shards(models[r], models[r]->p2p_plan, B));
+    if (p2p_push()) SAMO_TRY(build_push_tiles(models[r], models[r]->p2p_plan));
+  }
+  return clear_ok();
+}
+
+int samo_local_group_step(samo_model* const* models, int G, samo_stream_t stream) {
+  if (!models || G < 2 || G > kMaxP2PRanks) return fail(SAMO_E_PARAMETER, "local group of %d models", G);
+  for (int r = 0; r < G; ++r) {
+    samo_model* md = models[r];
+    SAMO_TRY(step_ready(md));
+    if (!md->comm || !md->comm->local_group || md->comm->nranks != G || md->comm->rank != r ||
+        md->peer_base[0] != models[0]->block)
+      return fail(SAMO_E_STATE, "model %d is not rank %d of this local group", r, r);
+    if (!md->grads_set) return fail(SAMO_E_STATE, "optimizer_step requires backward (no gradients set)");
+  }
+  SAMO_TRY(step_local_group(models, G, true, as_stream(stream)));
   return clear_ok();
 }
 

@@ -24,6 +24,7 @@ struct samo_comm {
   int rank = 0;
   uint8_t uid[SAMO_UNIQUE_ID_BYTES] = {};  // names the local rendezvous socket of the NVLS setup
   int nvls_seq = 0;                        // one multicast object per attached model
+  bool local_group = false;  // samo_model_attach_local_group: peers are models on this device, no NCCL
 };
 
 inline int nccl_fail(ncclResult_t r, const char* what) {
@@ -124,6 +125,7 @@ struct samo_model {
   // peer-to-peer exchange; p2p_ok is agreed by every rank.
   void* peer_base[kMaxP2PRanks] = {};
   bool p2p_ok = false;
+  samo_comm* own_comm = nullptr;  // the virtual communicator of a local group (owned)
   // NVLS multicast of the binary16 weights (P2P step): every rank's theta16c
   // lives in VMM memory bound to one multicast object; the shard kernel
   // stores each vector once through mc_c16 and the switch replicates it.

@@ -127,7 +127,7 @@ int launch_shard_p2p(const P2PArgs& a, cudaStream_t s);
 // Skip-flag exchange over peer memory (one warp): publishes this rank's
 // non-finite count to every peer, waits for all of theirs and writes the
 // rank-ordered sum to *flag.  Also the step's first cross-rank barrier.
-int launch_p2p_flag(SamoPeerSlots* const* slots, int G, int rank, float* flag, cudaStream_t s);
+int launch_p2p_flag(SamoPeerSlots* const* slots, int G, int rank, float* flag, int phase, cudaStream_t s);
 // Waits (one warp) until every rank has published bucket `bucket`.
 int launch_p2p_wait(const SamoPeerSlots* mine, int G, int bucket, cudaStream_t s);
 // Advances the local epoch (after the step's last read of the slots).

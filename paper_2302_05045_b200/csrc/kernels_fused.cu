@@ -988,18 +988,22 @@ __device__ void spin_until(const uint64_t* p, uint64_t target) {
   }
 }
 
-__global__ void k_p2p_flag(P2PArgs a, float* flag) {
+// phase bit 0: publish this rank's skip indicator (and, by the fence, K1's
+// pushed gradients) to every rank; bit 1: wait for every rank's and sum them.
+__global__ void k_p2p_flag(P2PArgs a, float* flag, int phase) {
   SamoPeerSlots* mine = a.slots[a.rank];
   const uint64_t e = mine->epoch + 1;
   const int q = threadIdx.x;
   if (q < a.G) {
-    a.slots[q]->flag_val[a.rank] = *flag;
-    asm volatile("fence.sc.sys;" ::: "memory");  // K1's grad16 + the value before the signal
-    st_release_sys(&a.slots[q]->flag_epoch[a.rank], e);
-    spin_until(&mine->flag_epoch[q], e);
+    if (phase & 1) {
+      a.slots[q]->flag_val[a.rank] = *flag;
+      asm volatile("fence.sc.sys;" ::: "memory");  // K1's grad16 + the value before the signal
+      st_release_sys(&a.slots[q]->flag_epoch[a.rank], e);
+    }
+    if (phase & 2) spin_until(&mine->flag_epoch[q], e);
   }
   __syncwarp();
-  if (q == 0) {
+  if ((phase & 2) && q == 0) {
     float f = 0.0f;  // rank order: every rank computes the same value
     const volatile float* fv = mine->flag_val;
     for (int r = 0; r < a.G; ++r) f = __fadd_rn(f, fv[r]);
@@ -1222,13 +1226,13 @@ int launch_shard_p2p(const P2PArgs& a, cudaStream_t s) {
   return SAMO_OK;
 }
 
-int launch_p2p_flag(SamoPeerSlots* const* slots, int G, int rank, float* flag, cudaStream_t s) {
+int launch_p2p_flag(SamoPeerSlots* const* slots, int G, int rank, float* flag, int phase, cudaStream_t s) {
   if (G < 2 || G > kMaxP2PRanks) return fail(SAMO_E_PARAMETER, "peer-to-peer exchange supports 2..8 ranks");
   P2PArgs a{};
   for (int q = 0; q < G; ++q) a.slots[q] = slots[q];
   a.G = G;
   a.rank = rank;
-  k_p2p_flag<<<1, 32, 0, s>>>(a, flag);
+  k_p2p_flag<<<1, 32, 0, s>>>(a, flag, phase);
   SAMO_LAUNCH_CHECK("k_p2p_flag");
   return SAMO_OK;
 }

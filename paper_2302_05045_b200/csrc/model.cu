@@ -177,6 +177,7 @@ int samo_model_destroy(samo_model* md) {
   if (!md) return clear_ok();
   if (md->graph) cudaGraphExecDestroy(md->graph);
   close_peers(md);
+  delete md->own_comm;
   if (md->capture_stream) cudaStreamDestroy(md->capture_stream);
   if (md->s_comm) cudaStreamDestroy(md->s_comm);
   if (md->s_flag) cudaStreamDestroy(md->s_flag);
@@ -319,6 +320,8 @@ int samo_model_set_config(samo_model* md, const samo_optimizer_config* cfg) {
 int samo_model_attach_comm(samo_model* md, samo_comm* comm) {
   if (!md) return fail(SAMO_E_PARAMETER, "null model");
   close_peers(md);
+  delete md->own_comm;
+  md->own_comm = nullptr;
   md->comm = comm;
   md->cfg_dirty = true;  // the scales fold in 1/G
   if (comm && comm->nranks > 1) SAMO_TRY(open_peers(md));

@@ -342,6 +342,21 @@ class SamoModel:
 
     EXCHANGE_NONE, EXCHANGE_ALLREDUCE, EXCHANGE_SHARDED, EXCHANGE_P2P = 0, 1, 2, 3
 
+    @staticmethod
+    def attach_local_group(models: Sequence["SamoModel"]) -> None:
+        """Test harness (samo_model_attach_local_group): the models, all on the
+        current device, become the ranks of one peer-to-peer group with no
+        NCCL; step them together with local_group_step."""
+        hs = (C.c_void_p * len(models))(*[m._h.value for m in models])
+        _abi.call("samo_model_attach_local_group", hs, len(models))
+
+    @staticmethod
+    def local_group_step(models: Sequence["SamoModel"]) -> None:
+        """One pipelined peer-to-peer step of every rank of a local group,
+        phase by phase on the current stream (samo_local_group_step)."""
+        hs = (C.c_void_p * len(models))(*[m._h.value for m in models])
+        _abi.call("samo_local_group_step", hs, len(models), _stream())
+
     def set_exchange(self, mode: int) -> None:
         """EXCHANGE_ALLREDUCE (replicated state), EXCHANGE_SHARDED (ZeRO-1 on
         the compressed state, NCCL reduce-scatter / all-gather) or EXCHANGE_P2P

@@ -141,3 +141,71 @@ def test_dp_four_gpus_p2p_stress(tmp_path, oracle):
     if torch.cuda.device_count() < 4:
         pytest.skip("needs 4 GPUs")
     _check(_run(tmp_path, "p2p", 4, steps=40), oracle, 4, "p2p", steps=40)
+
+
+def _local_group_run(oracle, G, steps=4):
+    """G models on cuda:0 as the ranks of one peer-to-peer group
+    (samo_model_attach_local_group + samo_local_group_step): the same inputs
+    and outputs as dp_worker.py."""
+    sys.path.insert(0, str(HERE))
+    os.environ["SAMO_DP_STEPS"] = str(steps)
+    import importlib
+    import dp_worker as W
+    W = importlib.reload(W)
+    from paper_2302_05045_b200 import samo
+    vals, sets, grads = W.inputs(oracle, G)
+    L = len(W.DENSE_LEN)
+    psets = [samo.PrunedIndexSet(f"l{l}", d, torch.from_numpy(s.view(np.int32)).cuda())
+             for l, (d, s) in enumerate(zip(W.DENSE_LEN, sets))]
+    models = []
+    for _ in range(G):
+        m = samo.SamoModel.from_index_sets(psets, [(d,) for d in W.DENSE_LEN], tile_elems=1024)
+        for l, v in enumerate(vals):
+            m.init_layer(l, torch.from_numpy(v).cuda())
+        m.set_config(samo.OptimizerConfig(learning_rate=1e-2))
+        models.append(m)
+    samo.SamoModel.attach_local_group(models)
+    dev = {(r, s): [torch.from_numpy(grads[(r, s, l)].view(np.int16)).cuda() for l in range(L)]
+           for r in range(G) for s in range(W.STEPS)}
+    torch.cuda.synchronize()
+    for s in range(W.STEPS):
+        for r in range(G):
+            models[r].set_grads(dev[(r, s)])
+        samo.SamoModel.local_group_step(models)
+    torch.cuda.synchronize()
+    out = []
+    for m in models:
+        rec = m.step_record()
+        rr = {"t": np.array([rec.t]), "skipped": np.array([rec.skipped_steps]),
+              "shard": np.array(m.shard_ranges(), np.uint64).reshape(-1, 2),
+              "k_off": np.array([m.view(l).k_offset for l in range(L)], np.uint64)}
+        for l in range(L):
+            for k in ("theta32", "adam_m", "adam_v"):
+                rr[f"{k}{l}"] = m.read(l, k).cpu().numpy()
+            rr[f"theta16_{l}"] = m.read(l, "theta16").cpu().numpy().view(np.uint16)
+        out.append(rr)
+    for m in models:
+        m.close()
+    return out
+
+
+@pytest.mark.parametrize("G,env", [(3, {}), (5, {}), (8, {}), (8, {"SAMO_P2P_TMA": "1"}),
+                                   (8, {"SAMO_P2P_PUSH": "0"}), (8, {"SAMO_P2P_PULL": "1"}),
+                                   (2, {"SAMO_P2P_BUCKETS": "5"}), (7, {"SAMO_P2P_BUCKETS": "3"})],
+                         ids=lambda x: str(x) if isinstance(x, int) else "-".join(f"{k[9:]}{v}" for k, v in x.items()) or "default")
+def test_local_group_p2p_bit_exact(cuda, oracle, monkeypatch, G, env):
+    """The pipelined peer-to-peer step at G up to 8 on ONE GPU: G models on
+    cuda:0 are the ranks (peers mapped directly, no NCCL), stepped phase by
+    phase on one stream.  The same kernels, peer stores, signals and bucket
+    plans as across GPUs, so every replica must equal the oracle bit for bit
+    — including G = 5, 7, 8, which the pool's 2- and 4-GPU boxes cannot run
+    as processes."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    _check(_local_group_run(oracle, G), oracle, G, "p2p")
+
+
+def test_local_group_eight_ranks_stress(cuda, oracle):
+    """40 steps of an 8-rank local group: the signal epochs advance through
+    many steps and every replica still equals the oracle bit for bit."""
+    _check(_local_group_run(oracle, 8, steps=40), oracle, 8, "p2p", steps=40)
