@@ -288,6 +288,41 @@ def fused_sink_probe(reps: int = 10) -> dict:
             "fused_saving": 1 - t_fused / t_unfused}
 
 
+class gpu_local_cpus:
+    """Runs the block bound to the CPUs NVML reports as local to `dev`
+    (nvmlDeviceGetCpuAffinity), then restores the affinity.  A pinned host
+    buffer allocated inside is placed on the GPU's NUMA node, so its
+    host->device copies do not cross the socket interconnect.  No-op where
+    NVML or the mapping is unavailable, or with SAMO_BENCH_NUMA=0."""
+
+    def __init__(self, dev):
+        self.dev, self.saved = dev, None
+
+    def __enter__(self):
+        if os.environ.get("SAMO_BENCH_NUMA", "1") == "0" or not hasattr(os, "sched_setaffinity"):
+            return self
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            uuid = str(torch.cuda.get_device_properties(self.dev).uuid)
+            h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            words = pynvml.nvmlDeviceGetCpuAffinity(h, 64)
+            cpus = {64 * w + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+            cpus &= os.sched_getaffinity(0)
+            if cpus:
+                self.saved = os.sched_getaffinity(0)
+                os.sched_setaffinity(0, cpus)
+        except Exception:  # noqa: BLE001  (no NVML / no mapping: leave placement to the OS)
+            self.saved = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.saved:
+            os.sched_setaffinity(0, self.saved)
+        return False
+
+
 def fc_sweep_probe(reps: int = 200, cpu: bool = True) -> list:
     """BASELINE config 2 (config 1 = its 4096 row): one [n, n]
     FC layer, 90% magnitude mask (K0), loss-scaled binary16 gradients.  The
@@ -618,7 +653,8 @@ def run_samo(args) -> None:
         # The pinned staging buffer (5.3 GB per rank) is the one allocation
         # that can fail on a small host; every rank agrees before going on.
         try:
-            host = torch.empty(off, dtype=torch.float16, pin_memory=True)
+            with gpu_local_cpus(dev):  # pages placed on the GPU's NUMA node
+                host = torch.empty(off, dtype=torch.float16, pin_memory=True)
         except Exception as ex:  # noqa: BLE001
             host, e2e_err = None, str(ex)
         ok = torch.tensor([1 if host is not None else 0], device=dev, dtype=torch.int32)
