@@ -288,6 +288,23 @@ def fused_sink_probe(reps: int = 10) -> dict:
             "fused_saving": 1 - t_fused / t_unfused}
 
 
+def mix_ceiling(k: dict):
+    """The measured streaming ceiling of the HBM read:write mix nearest to
+    the kernel's own (tools/bw_probe.cu on B200, profiles/r01b_bw_mix.jsonl):
+    the copy peak is a 1:1 mix, but K23 writes twice what it reads and HBM3e
+    writes are slower.  Reported beside `frac`, never instead of it."""
+    if "write_bytes" not in k:
+        return None
+    try:
+        pts = [json.loads(l) for l in (ROOT / "profiles" / "r01b_bw_mix.jsonl").read_text().splitlines() if l.strip()]
+    except OSError:
+        return None
+    w = k["write_bytes"] / k["bytes"]
+    best = min(pts, key=lambda p: abs(p["write_streams"] / (p["read_streams"] + p["write_streams"]) - w))
+    return {"mix": best["mix"], "write_fraction": round(w, 3), "GBps": best["GBps"],
+            "frac": k["GBps"] / best["GBps"], "src": "tools/bw_probe.cu"}
+
+
 class gpu_local_cpus:
     """Runs the block bound to the CPUs NVML reports as local to `dev`
     (nvmlDeviceGetCpuAffinity), then restores the affinity.  A pinned host
@@ -586,9 +603,11 @@ def run_samo(args) -> None:
         bytes_k23 = 2 * phi + 2 * nnz + gb * nnz + 24 * nnz
         kern = {
             "K1_gather_unscale": {"ms": k1_ms, "bytes": bytes_k1,
-                                  "GBps": bytes_k1 / (k1_ms * 1e-3) / 1e9},
+                                  "GBps": bytes_k1 / (k1_ms * 1e-3) / 1e9,
+                                  "write_bytes": gb * nnz},
             "K23_adam_downcast_expand": {"ms": k23_ms, "bytes": bytes_k23,
-                                         "GBps": bytes_k23 / (k23_ms * 1e-3) / 1e9},
+                                         "GBps": bytes_k23 / (k23_ms * 1e-3) / 1e9,
+                                         "write_bytes": 12 * nnz + 2 * phi},
         }
         hbm_kernels = list(kern)
     else:
@@ -640,7 +659,9 @@ def run_samo(args) -> None:
             traffic = json.loads(tp.read_text()).get(wl.name, {}).get(dom)
         except (ValueError, AttributeError):
             traffic = None
+    mix = mix_ceiling(kern[dom])
     roofline = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["GBps"], "peak": pk["hbm_gbs"],
+                "mix_ceiling": mix,
                 "peak_src": pk["src"], "unit": "GB/s", "frac": kern[dom]["frac"], "traffic": traffic,
                 "algorithmic_bytes_per_launch": kern[dom]["bytes"],
                 "step_bytes": bytes_k1 + bytes_k23,
