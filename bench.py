@@ -233,7 +233,7 @@ def run_reference(args) -> None:
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ---------------------------------------------------------------------------
@@ -808,7 +808,7 @@ def run_samo(args) -> None:
             "setup": {"seconds": setup_s, "k0_prune_ms": prune_ms,
                       "model_device_bytes": model.device_bytes()},
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     model.close()
     if comm is not None:
         comm.close()
@@ -816,8 +816,27 @@ def run_samo(args) -> None:
         dist.destroy_process_group()
 
 
+_RESULT_FD = None  # the process's real stdout: only the JSON line goes there
+
+
+def emit(line: dict) -> None:
+    """Writes the one JSON result line to the real stdout."""
+    text = (json.dumps(line) + "\n").encode()
+    if _RESULT_FD is None:
+        sys.stdout.write(text.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_RESULT_FD, text)
+
+
 def main() -> None:
+    global _RESULT_FD
     args = parse_args()
+    # Everything else that reaches fd 1 — NCCL's version banner, library
+    # chatter — goes to stderr, so stdout carries exactly one JSON line.
+    sys.stdout.flush()
+    _RESULT_FD = os.dup(1)
+    os.dup2(2, 1)
     if args.impl == "reference":
         run_reference(args)
     else:
