@@ -289,9 +289,10 @@ int samo_model_p2p_features(const samo_model* model);
  * all flag waits, all shard updates, all bucket waits + expands, all
  * finalizes — so every wait finds its signal already written.  The kernels,
  * peer stores and signals are those of the cross-process step; only the
- * cross-rank concurrency differs.  samo_model_attach_comm (or destroying a
- * model) leaves the group.  Not part of the reference's API; it lets
- * tests/test_gpu_dp.py check G = 5..8 on a single GPU. */
+ * cross-rank concurrency differs.  The members' own step calls fail with
+ * SAMO_E_STATE.  Re-attach (samo_model_attach_comm) or destroy all members
+ * together: each maps the others' memory.  Not part of the reference's API;
+ * it lets tests/test_gpu_dp.py check G = 5..8 on a single GPU. */
 int samo_model_attach_local_group(samo_model* const* models, int G);
 int samo_local_group_step(samo_model* const* models, int G, samo_stream_t stream);
 /* Compressed-arena elements this rank updates: for b in [0, buckets) the

@@ -462,9 +462,11 @@ static void set_pull_args(samo_model* md, const ShardPlan& p, StepArgs& a);
 
 int step_p2p(samo_model* md, cudaStream_t S, bool gather) {
   const int G = md->comm->nranks, r = md->comm->rank;
-  if (p2p_buckets(G) > 1) return step_p2p_pipelined(md, S, p2p_buckets(G), gather);
+  // A local group's ranks share one host thread: stepped one at a time they
+  // would wait for each other forever.
   if (md->comm->local_group)
-    return fail(SAMO_E_STATE, "a local group has no NCCL: it needs the pipelined exchange (SAMO_P2P_BUCKETS >= 2)");
+    return fail(SAMO_E_STATE, "a local-group member steps through samo_local_group_step");
+  if (p2p_buckets(G) > 1) return step_p2p_pipelined(md, S, p2p_buckets(G), gather);
   const uint64_t c = align_up((md->n_tot + G - 1) / G, 8);
   if (static_cast<uint64_t>(G) * c + 8 > md->n_al + kFlagOff)
     return fail(SAMO_E_PARAMETER, "too many ranks for the arena padding");

@@ -209,3 +209,24 @@ def test_local_group_eight_ranks_stress(cuda, oracle):
     """40 steps of an 8-rank local group: the signal epochs advance through
     many steps and every replica still equals the oracle bit for bit."""
     _check(_local_group_run(oracle, 8, steps=40), oracle, 8, "p2p", steps=40)
+
+
+def test_local_group_member_step_is_refused(cuda):
+    """A local group's ranks share one host thread: stepping one member on
+    its own would wait for the others forever, so it fails at once."""
+    from paper_2302_05045_b200 import samo
+    idx = torch.arange(0, 4096, 3, dtype=torch.int32, device="cuda")
+    models = [samo.SamoModel.from_index_sets([samo.PrunedIndexSet("w", 4096, idx)], [(4096,)]) for _ in range(3)]
+    for m in models:
+        m.init_layer(0, torch.zeros(4096, device="cuda"))
+    samo.SamoModel.attach_local_group(models)
+    g = torch.zeros(4096, dtype=torch.float16, device="cuda")
+    for m in models:
+        m.set_grads([g])
+    with pytest.raises(samo.StateError):
+        models[0].step()
+    samo.SamoModel.local_group_step(models)  # the group step still works
+    torch.cuda.synchronize()
+    assert all(m.step_record().t == 1 for m in models)
+    for m in models:
+        m.close()
