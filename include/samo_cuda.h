@@ -2,7 +2,7 @@
  * samo_cuda.h — C ABI of the B200-native SAMO per-step parameter-state path.
  *
  * Drop-in boundary for the hot path of the reference library
- * (/root/reference/proj/include/samo/*.hpp).  The reference is a header-only
+ * (the headers proj/include/samo/<name>.hpp).  The reference is a header-only
  * C++20 library whose "interface" is a set of free functions in namespace
  * `samo`; every entry point below names the reference symbol it replaces
  * (file:line).  The C++ mirror of the reference signatures lives in

@@ -97,3 +97,16 @@ def test_index_set_widening():
     s = samo.PrunedIndexSet("big", 2**32 - 1, raw)
     assert s.as_int64().tolist() == [0, 5, 2**31 - 1, 2**31, 2**32 - 2]
     assert s.count() == 5
+
+
+def test_header_is_plain_c99(tmp_path):
+    """cgo / JNI / ctypes hosts include the ABI header as C: it must compile as
+    strict C99 without warnings."""
+    import shutil
+    if not shutil.which("gcc"):
+        pytest.skip("no gcc")
+    src = tmp_path / "h.c"
+    src.write_text('#include "samo_cuda.h"\nint main(void) { return 0; }\n')
+    res = subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I", str(HEADER.parent),
+                          "-fsyntax-only", str(src)], capture_output=True, text=True)
+    assert res.returncode == 0, res.stderr
