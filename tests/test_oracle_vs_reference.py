@@ -114,9 +114,9 @@ def test_magnitude_prune_random(oracle, ref, sizes, seed, p, scope, levels, prun
         vals.append(v)
     prunable = [bool((prunable_mask >> i) & 1) for i in range(len(sizes))]
     rc, want = ref.magnitude_prune(vals, prunable, p, scope)
-    # rc 1: the reference's Tensor cannot hold an empty layer ("tensor extents
-    # must be positive", tensor.hpp:65) — not expressible there; the oracle and
-    # the device path accept empty layers (an extension).
+    # rc 1: the reference's Tensor cannot hold a zero-length layer ("tensor
+    # extents must be positive", tensor.hpp:65): not expressible there, so
+    # nothing to compare (the oracle returns an empty set for one).
     assume(rc != 1)
     if rc:  # ParameterError (sparsity outside [0, 1)): the oracle raises too
         with pytest.raises(ValueError):
