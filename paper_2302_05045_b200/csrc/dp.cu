@@ -51,11 +51,8 @@ struct NvlsApi {
   bool ok = false;
 };
 
-static const NvlsApi& nvls_api() {
-  static NvlsApi api;
-  static bool init = false;
-  if (init) return api;
-  init = true;
+static NvlsApi load_nvls_api() {
+  NvlsApi api;
   auto get = [](const char* name, auto& fn) {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q{};
@@ -74,6 +71,11 @@ static const NvlsApi& nvls_api() {
            get("cuMemImportFromShareableHandle", api.import_h) &&
            get("cuMemGetAllocationGranularity", api.mem_gran) && get("cuCtxGetDevice", api.ctx_device);
   cudaGetLastError();
+  return api;
+}
+
+static const NvlsApi& nvls_api() {
+  static const NvlsApi api = load_nvls_api();  // thread-safe one-time initialisation
   return api;
 }
 
