@@ -73,3 +73,20 @@ def test_reference_arm_other_ranks_exit_silently():
                          cwd=ROOT, env=env)
     assert res.returncode == 0, res.stderr[-2000:]
     assert res.stdout.strip() == ""
+
+
+@pytest.mark.parametrize("name,p,tensors,phi,nnz", [
+    ("gpt-2.7b", 0.9, 388, 2_651_553_280, 266_118_400),
+    ("gpt-1.3b", 0.8, 292, 1_315_723_264, 263_659_096),   # config 3
+    ("gpt-1.3b", 0.9, 292, 1_315_723_264, 132_151_096),
+    ("gpt-1.3b", 0.95, 292, 1_315_723_264, 66_397_096),
+])
+def test_workloads_match_the_survey(oracle, name, p, tensors, phi, nnz):
+    """The bench's synthetic GPT parameter sets: tensor
+    count, dense parameters and kept elements under the reference's
+    unpruned_count (prune.hpp:76-79; 1-D LN/bias tensors non-prunable)."""
+    from paper_2302_05045_b200 import workloads
+    wl = workloads.get(name, p)
+    assert len(wl.tensors) == tensors and wl.phi == phi
+    kept = sum(oracle.unpruned_count(p, t.numel) if t.prunable else t.numel for t in wl.tensors)
+    assert kept == nnz
