@@ -326,3 +326,25 @@ EXPORT int ref_dw_matmul(const uint16_t* x, const uint16_t* dy, uint64_t batch, 
     return status_of(e);
   }
 }
+
+#ifdef SAMO_REF_JSON
+// JSON checkpoints (serialize.hpp:121-190), when nlohmann's json.hpp is on
+// the include path: parse -> checkpoint_from_json -> checkpoint_to_json ->
+// dump, all of it the reference's own code.  98: not JSON; 100: `out` too small.
+#include "samo/serialize.hpp"
+
+EXPORT int ref_checkpoint_json_roundtrip(const char* in, char* out, uint64_t cap, uint64_t* need) {
+  try {
+    const samo::ModelState st = samo::checkpoint_from_json(nlohmann::json::parse(in));
+    const std::string s = samo::checkpoint_to_json(st).dump();
+    *need = s.size() + 1;
+    if (s.size() + 1 > cap) return 100;
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return 0;
+  } catch (const nlohmann::json::parse_error&) {
+    return 98;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
+#endif

@@ -1,0 +1,157 @@
+"""JSON checkpoints in the reference's schema (serialize.hpp:121-190).
+
+    {"layers": [{"layer_id": str, "shape": [...], "indices": [...],
+                 "theta32": [...], "adam_m": [...], "adam_v": [...]}]}
+
+The reference keeps JSON for small models and its tests
+(serialize_test.cpp:29-93); at GPT scale the binary checkpoint
+(samo_model_save / samo_model_load) carries the same fields.  This module is
+host-side format conversion only (numpy arrays in, numpy arrays out); the
+model glue is SamoModel.to_checkpoint_json / from_checkpoint_json.
+
+Compatibility with the reference, checked against its own
+checkpoint_from_json / checkpoint_to_json in tests/test_checkpoint_json.py:
+* values are fp32 widened to double and written with round-trip digits in
+  nlohmann's fixed/exponent layout.  Every value parses back to the same fp32
+  bits either way.  The texts match byte for byte except where nlohmann's
+  Grisu2 picks a different, equally round-tripping, last digit (about 0.7% of
+  random fp32 values);
+* non-finite values are written as null, as nlohmann writes them, and are
+  rejected on load, as the reference rejects them ("bad value");
+* load rejects exactly what checkpoint_from_json rejects, with ConfigError:
+  - a checkpoint that is not an object;
+  - unknown keys at either level;
+  - a missing key or a value of the wrong type;
+  - indices that are not strictly ascending or not below numel(shape);
+  - theta32 / adam_m / adam_v lengths that differ from the index count.
+  A zero shape extent is a DimensionError, as the reference's Tensor raises.
+* Keys are written in sorted order, as nlohmann's std::map stores them.
+"""
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import dataclass
+from decimal import Decimal
+
+import numpy as np
+
+from ._abi import ConfigError, DimensionError
+
+LAYER_KEYS = ("layer_id", "shape", "indices", "theta32", "adam_m", "adam_v")
+
+
+@dataclass
+class CheckpointLayer:
+    layer_id: str
+    shape: tuple[int, ...]
+    indices: np.ndarray  # uint32, strictly ascending, < numel(shape)
+    theta32: np.ndarray  # float32 [len(indices)]
+    adam_m: np.ndarray
+    adam_v: np.ndarray
+
+
+def _number(x: float) -> str:
+    """A double in nlohmann::json's layout (format_buffer): fixed notation
+    while the decimal point lies within (-4, 15] digits of the shortest
+    round-trip digits, else d.ddde+XX; integral values get '.0'; non-finite
+    values become null."""
+    if not math.isfinite(x):
+        return "null"
+    if x == 0.0:
+        return "-0.0" if math.copysign(1.0, x) < 0 else "0.0"
+    t = Decimal(repr(abs(x))).normalize().as_tuple()
+    d = "".join(map(str, t.digits))
+    k = len(d)
+    n = k + t.exponent  # value = 0.d x 10^n
+    sign = "-" if x < 0 else ""
+    if k <= n <= 15:
+        return f"{sign}{d}{'0' * (n - k)}.0"
+    if 0 < n <= 15:
+        return f"{sign}{d[:n]}.{d[n:]}"
+    if -4 < n <= 0:
+        return f"{sign}0.{'0' * (-n)}{d}"
+    e = n - 1
+    mant = d if k == 1 else f"{d[0]}.{d[1:]}"
+    return f"{sign}{mant}e{'-' if e < 0 else '+'}{abs(e):02d}"
+
+
+def _array(a: np.ndarray) -> str:
+    return "[" + ",".join(_number(float(x)) for x in np.asarray(a, dtype=np.float32).tolist()) + "]"
+
+
+def dumps(layers: list[CheckpointLayer]) -> str:
+    """checkpoint_to_json(state).dump() (serialize.hpp:124-135): keys sorted as
+    nlohmann's std::map holds them, no whitespace."""
+    out = []
+    for l in layers:
+        idx = ",".join(str(int(i)) for i in np.asarray(l.indices, dtype=np.uint32).tolist())
+        shape = ",".join(str(int(e)) for e in l.shape)
+        out.append(f'{{"adam_m":{_array(l.adam_m)},"adam_v":{_array(l.adam_v)},"indices":[{idx}],'
+                   f'"layer_id":{json.dumps(str(l.layer_id), ensure_ascii=False)},"shape":[{shape}],'
+                   f'"theta32":{_array(l.theta32)}}}')
+    return '{"layers":[' + ",".join(out) + "]}"
+
+
+def _required(obj: dict, key: str, where: str):
+    if key not in obj:
+        raise ConfigError(f"missing key '{key}' in {where}")
+    return obj[key]
+
+
+def _uints(v, key: str, bits: int) -> list[int]:
+    if not isinstance(v, list) or not all(isinstance(x, int) and not isinstance(x, bool) for x in v):
+        raise ConfigError(f"bad value for '{key}' in layer")
+    if any(x < 0 or x >= (1 << bits) for x in v):
+        raise ConfigError(f"bad value for '{key}' in layer")
+    return v
+
+
+def _f32s(v, key: str) -> np.ndarray:
+    if not isinstance(v, list) or not all(isinstance(x, (int, float)) and not isinstance(x, bool) for x in v):
+        raise ConfigError(f"bad value for '{key}' in layer")
+    return np.array(v, dtype=np.float64).astype(np.float32)
+
+
+def loads(text: str) -> list[CheckpointLayer]:
+    """checkpoint_from_json(json::parse(text)) (serialize.hpp:137-190)."""
+    def no_constants(name):  # NaN / Infinity are not JSON
+        raise ConfigError(f"checkpoint is not valid JSON: {name}")
+    try:
+        j = json.loads(text, parse_constant=no_constants)
+    except json.JSONDecodeError as e:
+        raise ConfigError(f"checkpoint is not valid JSON: {e}") from None
+    if not isinstance(j, dict):
+        raise ConfigError("checkpoint must be a JSON object")
+    for k in j:
+        if k != "layers":
+            raise ConfigError(f"unknown key '{k}' in checkpoint")
+    if not isinstance(j.get("layers"), list):
+        raise ConfigError("checkpoint must contain a layers array")
+    out = []
+    for lj in j["layers"]:
+        if not isinstance(lj, dict):
+            raise ConfigError("checkpoint layer must be a JSON object")
+        for k in lj:
+            if k not in LAYER_KEYS:
+                raise ConfigError(f"unknown key '{k}' in checkpoint layer")
+        layer_id = _required(lj, "layer_id", "layer")
+        if not isinstance(layer_id, str):
+            raise ConfigError("bad value for 'layer_id' in layer")
+        shape = _uints(_required(lj, "shape", "layer"), "shape", 64)
+        dense_len = 1
+        for e in shape:
+            dense_len *= e
+        idx = _uints(_required(lj, "indices", "layer"), "indices", 32)
+        for k in range(len(idx)):
+            if idx[k] >= dense_len or (k > 0 and idx[k] <= idx[k - 1]):
+                raise ConfigError(f"checkpoint indices must be strictly ascending and in range: {layer_id}")
+        theta = _f32s(_required(lj, "theta32", "layer"), "theta32")
+        m = _f32s(_required(lj, "adam_m", "layer"), "adam_m")
+        v = _f32s(_required(lj, "adam_v", "layer"), "adam_v")
+        if not (theta.size == m.size == v.size == len(idx)):
+            raise ConfigError(f"checkpoint buffer length mismatch: {layer_id}")
+        if any(e == 0 for e in shape):  # Tensor extents must be positive (tensor.hpp:65)
+            raise DimensionError("tensor extents must be positive")
+        out.append(CheckpointLayer(layer_id, tuple(shape), np.array(idx, dtype=np.uint32), theta, m, v))
+    return out

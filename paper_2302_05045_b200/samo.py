@@ -17,6 +17,7 @@ import ctypes as C
 from dataclasses import dataclass, field
 from typing import Iterable, Sequence
 
+import numpy as np
 import torch
 
 from . import _abi
@@ -499,6 +500,45 @@ class SamoModel:
                 layers.append(LayerSpec(f"l{l}", (int(v.dense_len),), int(v.nnz)))
         model.layers = list(layers)
         return model
+
+    def to_checkpoint_json(self) -> str:
+        """checkpoint_to_json(state).dump() (serialize.hpp:124-135): per layer
+        its id, shape, indices, theta32, adam_m, adam_v.  For small models —
+        the binary save() carries the same fields at any scale."""
+        from . import checkpoint_json as cj
+        layers = []
+        for l, spec in enumerate(self.layers):
+            idx = self.read(l, "indices").cpu().numpy().view(np.uint32)
+            layers.append(cj.CheckpointLayer(spec.layer_id, tuple(spec.shape), idx,
+                                             *(self.read(l, k).cpu().numpy() for k in ("theta32", "adam_m", "adam_v"))))
+        return cj.dumps(layers)
+
+    @classmethod
+    def from_checkpoint_json(cls, text: str, tile_elems: int = 0) -> "SamoModel":
+        """checkpoint_from_json (serialize.hpp:137-190), validated as the
+        reference does (ConfigError), theta16 rebuilt by downcast + expand.
+        The JSON has no Adam scalars, so the step counter and beta powers start
+        afresh, as a SamoTrainer built on the loaded state does.  Goes through
+        the binary loader (samo_model_load)."""
+        import os
+        import struct
+        import tempfile
+        from . import checkpoint_json as cj
+        layers = cj.loads(text)
+        head = struct.pack("<8sIIII", b"SAMOCKPT", 1, len(layers), int(tile_elems) or 16384, 0)
+        head += struct.pack("<QQfffI", 0, 0, 1.0, 1.0, 0.0, 0)  # samo_step_record: a fresh trainer
+        body = b"".join(struct.pack("<QQ", int(np.prod(l.shape)), l.indices.size) for l in layers)
+        fd, path = tempfile.mkstemp(suffix=".samockpt")
+        try:
+            with os.fdopen(fd, "wb") as f:
+                f.write(head + body)
+                for k in ("indices", "theta32", "adam_m", "adam_v"):
+                    for l in layers:
+                        f.write(np.ascontiguousarray(getattr(l, k)).tobytes())
+            specs = [LayerSpec(l.layer_id, tuple(l.shape), int(l.indices.size)) for l in layers]
+            return cls.load(path, layers=specs, tile_elems=tile_elems)
+        finally:
+            os.unlink(path)
 
     _FIELDS = {"theta16": (torch.float16, "dense"), "theta32": (torch.float32, "nnz"),
                "adam_m": (torch.float32, "nnz"), "adam_v": (torch.float32, "nnz"),

@@ -1,0 +1,95 @@
+"""CPU: JSON checkpoints in the reference's schema (serialize.hpp:121-190)
+against the reference's own checkpoint_from_json / checkpoint_to_json
+(oracle/_ref, built with nlohmann/json when available):
+
+* our dump loads in the reference, and the reference's re-dump loads in ours
+  with every value bit-identical; the texts agree except for Grisu2's
+  occasional alternative last digit, so values are compared, not bytes;
+* every malformed checkpoint the reference rejects, we reject with the
+  same error class (ConfigError / DimensionError), and vice versa.
+"""
+from __future__ import annotations
+
+import json
+
+import numpy as np
+import pytest
+
+from oracle.oracle import REF_SO, RefLib
+from paper_2302_05045_b200 import checkpoint_json as cj
+from paper_2302_05045_b200._abi import ConfigError, DimensionError
+
+
+@pytest.fixture(scope="module")
+def ref():
+    if not REF_SO.exists():
+        pytest.skip("oracle/_ref not built")
+    r = RefLib()
+    if not r.has_json:
+        pytest.skip("oracle/_ref built without nlohmann/json")
+    return r
+
+
+def _layers(seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    for l, shape in enumerate([(7, 5), (64,), (3, 4, 5)]):
+        n = int(np.prod(shape))
+        idx = np.flatnonzero(rng.random(n) < 0.4).astype(np.uint32)
+        k = idx.size
+        vals = [(rng.standard_normal(k) * 10.0 ** rng.integers(-30, 30, k)).astype(np.float32) for _ in range(3)]
+        vals[0][:3] = np.array([0.1, -0.0, 1e-45], dtype=np.float32)[: min(3, k)]
+        out.append(cj.CheckpointLayer(f"layer{l}", shape, idx, *vals))
+    return out
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_round_trip_through_the_reference(ref, seed):
+    layers = _layers(seed)
+    ours = cj.dumps(layers)
+    rc, theirs = ref.checkpoint_json_roundtrip(ours)
+    assert rc == 0
+    assert len(theirs) == pytest.approx(len(ours), rel=0.01)  # same layout, up to Grisu2 digits
+    back = cj.loads(theirs)
+    for a, b in zip(layers, back):
+        assert a.layer_id == b.layer_id and tuple(a.shape) == b.shape
+        assert np.array_equal(a.indices, b.indices)
+        for k in ("theta32", "adam_m", "adam_v"):
+            assert np.array_equal(getattr(a, k).view(np.uint32), getattr(b, k).view(np.uint32))
+
+
+def _mutations():
+    base = json.loads(cj.dumps(_layers(0)))
+    cases = {}
+
+    def case(name, fn):
+        j = json.loads(json.dumps(base))
+        fn(j)
+        cases[name] = json.dumps(j)
+
+    case("unknown_top_key", lambda j: j.update(extra=1))
+    case("unknown_layer_key", lambda j: j["layers"][0].update(grad16=[]))
+    case("missing_theta", lambda j: j["layers"][1].pop("theta32"))
+    case("descending_indices", lambda j: j["layers"][0].update(indices=j["layers"][0]["indices"][::-1]))
+    case("index_out_of_range", lambda j: j["layers"][1]["indices"].__setitem__(-1, 64))
+    case("length_mismatch", lambda j: j["layers"][2]["adam_m"].pop())
+    case("null_value", lambda j: j["layers"][0]["adam_v"].__setitem__(0, None))
+    case("string_value", lambda j: j["layers"][0]["theta32"].__setitem__(0, "x"))
+    case("layer_id_not_string", lambda j: j["layers"][0].update(layer_id=3))
+    case("layers_not_array", lambda j: j.update(layers={}))
+    case("not_object", lambda j: None)
+    cases["not_object"] = "[1, 2]"
+    case("zero_extent", lambda j: j["layers"][1].update(shape=[0], indices=[], theta32=[], adam_m=[], adam_v=[]))
+    case("empty_ok", lambda j: j.update(layers=[]))
+    return cases
+
+
+@pytest.mark.parametrize("name,text", sorted(_mutations().items()))
+def test_same_rejections_as_the_reference(ref, name, text):
+    rc, _ = ref.checkpoint_json_roundtrip(text)
+    if rc == 0:
+        cj.loads(text)  # accepted by both
+        return
+    want = {5: ConfigError, 1: DimensionError}[rc]
+    with pytest.raises(want):
+        cj.loads(text)

@@ -119,3 +119,33 @@ def test_memory_report_matches_reference_measured_bytes(S, golden):
     assert rep["reference_peak_bytes"] == sess.ref.lib.ref_session_measured_bytes(sess.h, 1) - dummy_peak
     assert rep["device_bytes"] >= rep["theta16_bytes"] + rep["compressed_state_bytes"]
     sess.close()
+
+
+def test_json_checkpoint_round_trip(S, golden):
+    """JSON checkpoint in the reference's schema (serialize.hpp:121-190):
+    to_checkpoint_json of a stepped model loads back (from_checkpoint_json)
+    with the same indices, theta32, m, v and the rebuilt theta16, bit for bit;
+    the step scalars start afresh, as a trainer built on loaded state does.
+    When oracle/_ref has the JSON entry point, the reference itself accepts
+    the text too."""
+    from paper_2302_05045_b200 import checkpoint_json as cj
+    g = golden("step")
+    m, L = _model(S, g)
+    for s in range(2):
+        m.set_grads([T(g[f"s{s}_grad{l}"]) for l in range(L)])
+        m.step()
+    text = m.to_checkpoint_json()
+    assert [l.layer_id for l in cj.loads(text)] == [f"l{l}" for l in range(L)]
+    m2 = S.SamoModel.from_checkpoint_json(text, tile_elems=1024)
+    a, b = _state(m, L), _state(m2, L)
+    for k in a:
+        if k != "rec":
+            assert np.array_equal(a[k], b[k]), k
+    assert b["rec"][0] == 0 and b["rec"][2] == 1.0 and b["rec"][3] == 1.0
+    m2.check_invariants()
+    from oracle.oracle import REF_SO, RefLib
+    if REF_SO.exists():
+        ref = RefLib()
+        if ref.has_json:
+            rc, back = ref.checkpoint_json_roundtrip(text)
+            assert rc == 0 and len(cj.loads(back)) == L
