@@ -239,20 +239,28 @@ class RefLib:
         lib.ref_dw_matmul.argtypes = [vp, vp, u64, u64, u64, vp]
         self.has_json = hasattr(lib, "ref_checkpoint_json_roundtrip")  # built with nlohmann/json
         if self.has_json:
-            lib.ref_checkpoint_json_roundtrip.argtypes = [C.c_char_p, C.c_char_p, u64, C.POINTER(u64)]
+            for n in ("ref_checkpoint_json_roundtrip", "ref_index_sets_json_roundtrip"):
+                getattr(lib, n).argtypes = [C.c_char_p, C.c_char_p, u64, C.POINTER(u64)]
 
-    def checkpoint_json_roundtrip(self, text: str):
-        """The reference's checkpoint_from_json + checkpoint_to_json + dump on
-        `text`: (status, output text)."""
+    def _json_roundtrip(self, fn, text: str):
         need = u64(0)
         cap = 2 * len(text) + 4096
         for _ in range(2):
             buf = C.create_string_buffer(cap)
-            rc = self.lib.ref_checkpoint_json_roundtrip(text.encode(), buf, cap, C.byref(need))
+            rc = fn(text.encode(), buf, cap, C.byref(need))
             if rc != 100:
                 return rc, buf.value.decode() if rc == 0 else None
             cap = int(need.value)
         return rc, None
+
+    def checkpoint_json_roundtrip(self, text: str):
+        """The reference's checkpoint_from_json + checkpoint_to_json + dump on
+        `text`: (status, output text)."""
+        return self._json_roundtrip(self.lib.ref_checkpoint_json_roundtrip, text)
+
+    def index_sets_json_roundtrip(self, text: str):
+        """index_sets_from_json + index_sets_to_json + dump: (status, text)."""
+        return self._json_roundtrip(self.lib.ref_index_sets_json_roundtrip, text)
 
     def f2h(self, x):
         x = np.ascontiguousarray(x, dtype=np.float32)

@@ -347,4 +347,20 @@ EXPORT int ref_checkpoint_json_roundtrip(const char* in, char* out, uint64_t cap
     return status_of(e);
   }
 }
+
+// Pruned index sets <-> JSON (serialize.hpp:84-119), the same way.
+EXPORT int ref_index_sets_json_roundtrip(const char* in, char* out, uint64_t cap, uint64_t* need) {
+  try {
+    const auto sets = samo::index_sets_from_json(nlohmann::json::parse(in));
+    const std::string s = samo::index_sets_to_json(sets).dump();
+    *need = s.size() + 1;
+    if (s.size() + 1 > cap) return 100;
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return 0;
+  } catch (const nlohmann::json::parse_error&) {
+    return 98;
+  } catch (const std::exception& e) {
+    return status_of(e);
+  }
+}
 #endif

@@ -93,6 +93,11 @@ def dumps(layers: list[CheckpointLayer]) -> str:
     return '{"layers":[' + ",".join(out) + "]}"
 
 
+def _no_constants(name: str):
+    """NaN / Infinity tokens are not JSON (Python's parser accepts them)."""
+    raise ConfigError(f"not valid JSON: {name}")
+
+
 def _required(obj: dict, key: str, where: str):
     if key not in obj:
         raise ConfigError(f"missing key '{key}' in {where}")
@@ -115,10 +120,8 @@ def _f32s(v, key: str) -> np.ndarray:
 
 def loads(text: str) -> list[CheckpointLayer]:
     """checkpoint_from_json(json::parse(text)) (serialize.hpp:137-190)."""
-    def no_constants(name):  # NaN / Infinity are not JSON
-        raise ConfigError(f"checkpoint is not valid JSON: {name}")
     try:
-        j = json.loads(text, parse_constant=no_constants)
+        j = json.loads(text, parse_constant=_no_constants)
     except json.JSONDecodeError as e:
         raise ConfigError(f"checkpoint is not valid JSON: {e}") from None
     if not isinstance(j, dict):
@@ -154,4 +157,50 @@ def loads(text: str) -> list[CheckpointLayer]:
         if any(e == 0 for e in shape):  # Tensor extents must be positive (tensor.hpp:65)
             raise DimensionError("tensor extents must be positive")
         out.append(CheckpointLayer(layer_id, tuple(shape), np.array(idx, dtype=np.uint32), theta, m, v))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Pruned index sets <-> JSON: [{layer_id, dense_len, indices}]
+# (serialize.hpp:84-119).
+
+def index_sets_dumps(sets) -> str:
+    """index_sets_to_json(sets).dump(): `sets` are PrunedIndexSet-like objects
+    (layer_id, dense_len, indices as uint32 values)."""
+    out = []
+    for st in sets:
+        idx = np.asarray(st.indices.cpu().numpy() if hasattr(st.indices, "cpu") else st.indices)
+        idx = ",".join(str(int(i)) for i in idx.view(np.uint32).tolist())
+        out.append(f'{{"dense_len":{int(st.dense_len)},"indices":[{idx}],'
+                   f'"layer_id":{json.dumps(str(st.layer_id), ensure_ascii=False)}}}')
+    return "[" + ",".join(out) + "]"
+
+
+def index_sets_loads(text: str) -> list[tuple[str, int, np.ndarray]]:
+    """index_sets_from_json(json::parse(text)): (layer_id, dense_len, uint32
+    indices) per set, validated as the reference does (ConfigError)."""
+    try:
+        arr = json.loads(text, parse_constant=_no_constants)
+    except json.JSONDecodeError as e:
+        raise ConfigError(f"index sets are not valid JSON: {e}") from None
+    if not isinstance(arr, list):
+        raise ConfigError("index sets must be a JSON array")
+    out = []
+    for j in arr:
+        if not isinstance(j, dict):
+            raise ConfigError("index set must be a JSON object")
+        for k in j:
+            if k not in ("layer_id", "dense_len", "indices"):
+                raise ConfigError(f"unknown key '{k}' in index set")
+        layer_id = _required(j, "layer_id", "index set")
+        if not isinstance(layer_id, str):
+            raise ConfigError("bad value for 'layer_id' in index set")
+        dense_len = _required(j, "dense_len", "index set")
+        if not isinstance(dense_len, int) or isinstance(dense_len, bool) or not 0 <= dense_len < (1 << 64):
+            raise ConfigError("bad value for 'dense_len' in index set")
+        idx = _uints(_required(j, "indices", "index set"), "indices", 32)
+        for k in range(len(idx)):
+            if idx[k] >= dense_len or (k > 0 and idx[k] <= idx[k - 1]):
+                raise ConfigError(f"indices must be strictly ascending and in range: {layer_id}")
+        out.append((layer_id, dense_len, np.array(idx, dtype=np.uint32)))
     return out

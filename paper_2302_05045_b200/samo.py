@@ -99,6 +99,20 @@ class LayerParams:
     prunable: bool = True
 
 
+def index_sets_to_json(sets: Sequence[PrunedIndexSet]) -> str:
+    """index_sets_to_json(sets).dump() (serialize.hpp:84-93)."""
+    from . import checkpoint_json as cj
+    return cj.index_sets_dumps(sets)
+
+
+def index_sets_from_json(text: str, device: str = "cuda") -> list[PrunedIndexSet]:
+    """index_sets_from_json (serialize.hpp:95-119), validated as the
+    reference does (ConfigError); indices land on `device`."""
+    from . import checkpoint_json as cj
+    return [PrunedIndexSet(lid, n, torch.from_numpy(idx.view(np.int32).copy()).to(device))
+            for lid, n, idx in cj.index_sets_loads(text)]
+
+
 def unpruned_count(p: float, n: int) -> int:
     """detail::unpruned_count (prune.hpp:76-79)."""
     return int(_abi.load().samo_unpruned_count(float(p), int(n)))

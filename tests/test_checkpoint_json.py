@@ -93,3 +93,43 @@ def test_same_rejections_as_the_reference(ref, name, text):
     want = {5: ConfigError, 1: DimensionError}[rc]
     with pytest.raises(want):
         cj.loads(text)
+
+
+def test_index_sets_round_trip_through_the_reference(ref, oracle):
+    """index_sets_to_json / index_sets_from_json (serialize.hpp:84-119): K0's
+    output format for masks, byte for byte (integers only) both ways."""
+    from types import SimpleNamespace
+    rng = np.random.default_rng(3)
+    vals = [rng.standard_normal(n).astype(np.float32) for n in (300, 1, 5000)]
+    sets = [SimpleNamespace(layer_id=f"w{l}", dense_len=v.size, indices=s)
+            for l, (v, s) in enumerate(zip(vals, oracle.magnitude_prune(vals, [True, False, True], 0.9)))]
+    ours = cj.index_sets_dumps(sets)
+    rc, theirs = ref.index_sets_json_roundtrip(ours)
+    assert rc == 0 and theirs == ours
+    back = cj.index_sets_loads(theirs)
+    assert [(b[0], b[1]) for b in back] == [(s.layer_id, s.dense_len) for s in sets]
+    for b, s in zip(back, sets):
+        assert np.array_equal(b[2], s.indices)
+
+
+@pytest.mark.parametrize("text", [
+    '{"layer_id":"a"}', '[{"layer_id":"a","dense_len":4,"indices":[0,2],"x":1}]',
+    '[{"layer_id":"a","dense_len":4,"indices":[2,0]}]', '[{"layer_id":"a","dense_len":4,"indices":[4]}]',
+    '[{"layer_id":"a","indices":[0]}]', '[{"layer_id":1,"dense_len":4,"indices":[0]}]',
+    '[{"layer_id":"a","dense_len":4,"indices":[0,1]}]', '[]'])
+def test_index_sets_same_rejections_as_the_reference(ref, text):
+    rc, _ = ref.index_sets_json_roundtrip(text)
+    if rc == 0:
+        cj.index_sets_loads(text)
+        return
+    with pytest.raises({5: ConfigError, 1: DimensionError}[rc]):
+        cj.index_sets_loads(text)
+
+
+def test_index_sets_python_api_on_cpu_tensors():
+    """samo.index_sets_from_json / index_sets_to_json round trip (host tensors)."""
+    from paper_2302_05045_b200 import samo
+    text = '[{"dense_len":10,"indices":[1,4,9],"layer_id":"a"},{"dense_len":3,"indices":[],"layer_id":"b"}]'
+    sets = samo.index_sets_from_json(text, device="cpu")
+    assert [s.layer_id for s in sets] == ["a", "b"] and sets[0].indices.tolist() == [1, 4, 9]
+    assert samo.index_sets_to_json(sets) == text
