@@ -61,6 +61,11 @@ def main() -> None:
     model.set_exchange({"sharded": model.EXCHANGE_SHARDED, "p2p": model.EXCHANGE_P2P,
                         "allreduce": model.EXCHANGE_ALLREDUCE}[mode])
     sink = os.environ.get("SAMO_DP_SINK") == "1"
+    # NCCL exchanges at G > 2: keep every step's exchanged fp32 gradient (the
+    # arena after the step: replicated for allreduce, the rank's shard for
+    # sharded) so the parent can bound the NCCL sum and replay the update.
+    save_g = os.environ.get("SAMO_DP_SAVE_G") == "1"
+    gsum = {}
     for s in range(STEPS):
         g = [torch.from_numpy(grads[(rank, s, l)].view(np.int16)).cuda() for l in range(len(DENSE_LEN))]
         if sink:  # per-layer backward sinks (last layer first), then exchange + update
@@ -70,12 +75,16 @@ def main() -> None:
         else:
             model.set_grads(g)
             model.step(graph=os.environ.get("SAMO_DP_GRAPH") == "1")
+        if save_g:
+            for l in range(len(DENSE_LEN)):
+                gsum[f"g32_{s}_{l}"] = model.read(l, "grad32").cpu().numpy()
     torch.cuda.synchronize()
     rec = model.step_record()
     ranges = np.array(model.shard_ranges(), np.uint64).reshape(-1, 2)
     out = {"t": np.array([rec.t]), "skipped": np.array([rec.skipped_steps]),
            "norm": np.array([rec.grad_norm], np.float32), "shard": ranges,
            "k_off": np.array([model.view(l).k_offset for l in range(len(DENSE_LEN))], np.uint64)}
+    out.update(gsum)
     for l in range(len(DENSE_LEN)):
         for k in ("theta32", "adam_m", "adam_v"):
             out[f"{k}{l}"] = model.read(l, k).cpu().numpy()
