@@ -280,21 +280,7 @@ enum samo_p2p_feature {
   SAMO_P2P_NVLS = 8
 };
 int samo_model_p2p_features(const samo_model* model);
-/* Test harness for the peer-to-peer step at any G <= 8 on ONE device:
- * models[0..G) (same layout, all on the current device) become the ranks of
- * one data-parallel group whose peers are mapped directly, with no NCCL
- * communicator and no IPC.  samo_local_group_step then runs one pipelined
- * P2P step of every rank (G >= 3 by default, or SAMO_P2P_BUCKETS >= 2),
- * queued phase by phase on one stream — all gathers, all skip-flag signals,
- * all flag waits, all shard updates, all bucket waits + expands, all
- * finalizes — so every wait finds its signal already written.  The kernels,
- * peer stores and signals are those of the cross-process step; only the
- * cross-rank concurrency differs.  The members' own step calls fail with
- * SAMO_E_STATE.  Re-attach (samo_model_attach_comm) or destroy all members
- * together: each maps the others' memory.  Not part of the reference's API;
- * it lets tests/test_gpu_dp.py check G = 5..8 on a single GPU. */
-int samo_model_attach_local_group(samo_model* const* models, int G);
-int samo_local_group_step(samo_model* const* models, int G, samo_stream_t stream);
+/* (The one-GPU local-group test harness is declared in samo_cuda_testing.h.) */
 /* Compressed-arena elements this rank updates: for b in [0, buckets) the
  * range [b*stride + rank*chunk, b*stride + (rank+1)*chunk) clipped to the
  * arena (chunk = stride = nnz, buckets = 1, rank = 0 unless sharded). */

@@ -18,6 +18,11 @@ checkpoint_from_json / checkpoint_to_json in tests/test_checkpoint_json.py:
   random fp32 values);
 * non-finite values are written as null, as nlohmann writes them, and are
   rejected on load, as the reference rejects them ("bad value");
+* integer fields are read as nlohmann's get<uintN_t>() reads them: floats
+  truncate, negative integers wrap modulo 2^N (then face the range checks),
+  booleans read as 0 / 1;
+  only values whose C++ conversion is undefined (non-finite, |x| >= 2^63)
+  are rejected where the reference's behaviour is unspecified;
 * load rejects exactly what checkpoint_from_json rejects, with ConfigError:
   - a checkpoint that is not an object;
   - unknown keys at either level;
@@ -36,7 +41,7 @@ from decimal import Decimal
 
 import numpy as np
 
-from ._abi import ConfigError, DimensionError
+from ._abi import ConfigError, DimensionError, ParameterError
 
 LAYER_KEYS = ("layer_id", "shape", "indices", "theta32", "adam_m", "adam_v")
 
@@ -104,12 +109,29 @@ def _required(obj: dict, key: str, where: str):
     return obj[key]
 
 
+def _uint(x, key: str, bits: int) -> int:
+    """One value as nlohmann's get<uintN_t>() reads it: a JSON integer is
+    static_cast (wraps modulo 2^bits, negatives included); a JSON float is
+    truncated toward zero, then wraps the same way (what gcc's x86-64
+    conversion does for |x| < 2^63); a JSON boolean reads as 0 / 1.  Beyond
+    that the C++ cast is undefined behaviour; those values — and
+    non-numbers — are rejected (ConfigError)."""
+    if isinstance(x, bool):
+        return int(x)
+    if not isinstance(x, (int, float)):
+        raise ConfigError(f"bad value for '{key}' in layer")
+    if isinstance(x, int) and -(1 << 63) <= x < (1 << 64):
+        return x % (1 << bits)
+    x = float(x)  # integers beyond 64 bits parse as floats in nlohmann
+    if not math.isfinite(x) or abs(x) >= 2.0**63:
+        raise ConfigError(f"bad value for '{key}' in layer")
+    return math.trunc(x) % (1 << bits)
+
+
 def _uints(v, key: str, bits: int) -> list[int]:
-    if not isinstance(v, list) or not all(isinstance(x, int) and not isinstance(x, bool) for x in v):
+    if not isinstance(v, list):
         raise ConfigError(f"bad value for '{key}' in layer")
-    if any(x < 0 or x >= (1 << bits) for x in v):
-        raise ConfigError(f"bad value for '{key}' in layer")
-    return v
+    return [_uint(x, key, bits) for x in v]
 
 
 def _f32s(v, key: str) -> np.ndarray:
@@ -156,6 +178,8 @@ def loads(text: str) -> list[CheckpointLayer]:
             raise ConfigError(f"checkpoint buffer length mismatch: {layer_id}")
         if any(e == 0 for e in shape):  # Tensor extents must be positive (tensor.hpp:65)
             raise DimensionError("tensor extents must be positive")
+        if dense_len > (1 << 32):  # u32 local indices (prune.hpp:24); the reference fails to allocate
+            raise DimensionError(f"layer too large for 32-bit indices: {layer_id}")
         out.append(CheckpointLayer(layer_id, tuple(shape), np.array(idx, dtype=np.uint32), theta, m, v))
     return out
 
@@ -170,7 +194,15 @@ def index_sets_dumps(sets) -> str:
     out = []
     for st in sets:
         idx = np.asarray(st.indices.cpu().numpy() if hasattr(st.indices, "cpu") else st.indices)
-        idx = ",".join(str(int(i)) for i in idx.view(np.uint32).tolist())
+        if idx.dtype.itemsize == 4 and idx.dtype.kind in "iu":
+            idx = idx.view(np.uint32)  # int32 storage of uint32 values (torch has no uint32)
+        elif idx.dtype.kind in "iu" or idx.size == 0:
+            idx = idx.astype(np.int64)  # wider integer storage: values, not bit patterns
+            if idx.size and (idx.min() < 0 or idx.max() >= (1 << 32)):
+                raise ParameterError("index values must fit uint32")
+        else:
+            raise ParameterError(f"indices must be an integer array, got {idx.dtype}")
+        idx = ",".join(str(int(i)) for i in idx.tolist())
         out.append(f'{{"dense_len":{int(st.dense_len)},"indices":[{idx}],'
                    f'"layer_id":{json.dumps(str(st.layer_id), ensure_ascii=False)}}}')
     return "[" + ",".join(out) + "]"
@@ -195,9 +227,7 @@ def index_sets_loads(text: str) -> list[tuple[str, int, np.ndarray]]:
         layer_id = _required(j, "layer_id", "index set")
         if not isinstance(layer_id, str):
             raise ConfigError("bad value for 'layer_id' in index set")
-        dense_len = _required(j, "dense_len", "index set")
-        if not isinstance(dense_len, int) or isinstance(dense_len, bool) or not 0 <= dense_len < (1 << 64):
-            raise ConfigError("bad value for 'dense_len' in index set")
+        dense_len = _uint(_required(j, "dense_len", "index set"), "dense_len", 64)
         idx = _uints(_required(j, "indices", "index set"), "indices", 32)
         for k in range(len(idx)):
             if idx[k] >= dense_len or (k > 0 and idx[k] <= idx[k - 1]):

@@ -10,7 +10,7 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 
-#include "samo_cuda.h"
+#include "samo_cuda_testing.h"
 
 namespace samo_dev {
 

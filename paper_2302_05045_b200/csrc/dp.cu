@@ -993,9 +993,13 @@ int samo_local_group_step(samo_model* const* models, int G, samo_stream_t stream
   for (int r = 0; r < G; ++r) {
     samo_model* md = models[r];
     SAMO_TRY(step_ready(md));
-    if (!md->comm || !md->comm->local_group || md->comm->nranks != G || md->comm->rank != r ||
-        md->peer_base[0] != models[0]->block)
+    if (!md->comm || !md->comm->local_group || md->comm->nranks != G || md->comm->rank != r)
       return fail(SAMO_E_STATE, "model %d is not rank %d of this local group", r, r);
+    // every rank's peer map must be exactly this list, in this order: the
+    // kernels address rank q's arena through peer_base[q]
+    for (int q = 0; q < G; ++q)
+      if (md->peer_base[q] != models[q]->block)
+        return fail(SAMO_E_STATE, "model %d: rank %d of its local group is not models[%d]", r, q, q);
     if (!md->grads_set) return fail(SAMO_E_STATE, "optimizer_step requires backward (no gradients set)");
   }
   SAMO_TRY(step_local_group(models, G, true, as_stream(stream)));

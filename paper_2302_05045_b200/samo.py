@@ -518,8 +518,12 @@ class SamoModel:
     def to_checkpoint_json(self) -> str:
         """checkpoint_to_json(state).dump() (serialize.hpp:124-135): per layer
         its id, shape, indices, theta32, adam_m, adam_v.  For small models —
-        the binary save() carries the same fields at any scale."""
+        the binary save() carries the same fields at any scale.  Refused, as
+        save() refuses it, when the state is sharded across ranks (theta32 /
+        m / v are then only authoritative on this rank's shard)."""
         from . import checkpoint_json as cj
+        if self.exchange_mode() in (self.EXCHANGE_SHARDED, self.EXCHANGE_P2P):
+            raise StateError("sharded state: theta32/m/v are only authoritative on each rank's shard")
         layers = []
         for l, spec in enumerate(self.layers):
             idx = self.read(l, "indices").cpu().numpy().view(np.uint32)

@@ -12,12 +12,21 @@ import pytest
 
 ROOT = Path(__file__).resolve().parents[1]
 HEADER = ROOT / "include" / "samo_cuda.h"
+TESTING = ROOT / "include" / "samo_cuda_testing.h"  # test harness, outside the boundary
 
 
-def declared_functions() -> list[str]:
-    text = HEADER.read_text()
-    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"\b(samo_[a-z0-9_]+)\s*\(", text)))
+def declared_functions(headers=(HEADER, TESTING)) -> list[str]:
+    out = set()
+    for h in headers:
+        text = re.sub(r"/\*.*?\*/", "", h.read_text(), flags=re.S)
+        out |= set(re.findall(r"\b(samo_[a-z0-9_]+)\s*\(", text))
+    return sorted(out)
+
+
+def test_boundary_header_has_no_test_harness():
+    product = declared_functions((HEADER,))
+    assert "samo_local_group_step" not in product and "samo_model_attach_local_group" not in product
+    assert {"samo_local_group_step", "samo_model_attach_local_group"} <= set(declared_functions((TESTING,)))
 
 
 @pytest.fixture(scope="module")
@@ -106,7 +115,7 @@ def test_header_is_plain_c99(tmp_path):
     if not shutil.which("gcc"):
         pytest.skip("no gcc")
     src = tmp_path / "h.c"
-    src.write_text('#include "samo_cuda.h"\nint main(void) { return 0; }\n')
+    src.write_text('#include "samo_cuda.h"\n#include "samo_cuda_testing.h"\nint main(void) { return 0; }\n')
     res = subprocess.run(["gcc", "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I", str(HEADER.parent),
                           "-fsyntax-only", str(src)], capture_output=True, text=True)
     assert res.returncode == 0, res.stderr

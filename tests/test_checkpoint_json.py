@@ -17,7 +17,7 @@ import pytest
 
 from oracle.oracle import REF_SO, RefLib
 from paper_2302_05045_b200 import checkpoint_json as cj
-from paper_2302_05045_b200._abi import ConfigError, DimensionError
+from paper_2302_05045_b200._abi import ConfigError, DimensionError, SamoError
 
 
 @pytest.fixture(scope="module")
@@ -81,16 +81,29 @@ def _mutations():
     cases["not_object"] = "[1, 2]"
     case("zero_extent", lambda j: j["layers"][1].update(shape=[0], indices=[], theta32=[], adam_m=[], adam_v=[]))
     case("empty_ok", lambda j: j.update(layers=[]))
+    # nlohmann's get<uintN_t>() casts: integral floats and truncated fractions
+    # are accepted, negative integers wrap (and then fail the range check)
+    case("float_shape", lambda j: j["layers"][0].update(shape=[7.0, 5.0]))
+    case("fractional_shape", lambda j: j["layers"][0].update(shape=[7.9, 5.2]))
+    case("float_index", lambda j: j["layers"][1]["indices"].__setitem__(0, float(j["layers"][1]["indices"][0])))
+    case("fractional_index", lambda j: j["layers"][1]["indices"].__setitem__(0, j["layers"][1]["indices"][0] + 0.5))
+    case("negative_index", lambda j: j["layers"][1]["indices"].__setitem__(0, -1))
+    case("negative_shape", lambda j: j["layers"][1].update(shape=[-64]))
+    case("bool_index", lambda j: j["layers"][1]["indices"].__setitem__(0, True))
     return cases
 
 
 @pytest.mark.parametrize("name,text", sorted(_mutations().items()))
 def test_same_rejections_as_the_reference(ref, name, text):
-    rc, _ = ref.checkpoint_json_roundtrip(text)
-    if rc == 0:
-        cj.loads(text)  # accepted by both
+    rc, theirs = ref.checkpoint_json_roundtrip(text)
+    if rc == 0:  # accepted by both, read to the same values
+        got, want = cj.loads(text), cj.loads(theirs)
+        assert [(a.layer_id, tuple(a.shape), a.indices.tolist()) for a in got] == \
+            [(b.layer_id, tuple(b.shape), b.indices.tolist()) for b in want]
         return
-    want = {5: ConfigError, 1: DimensionError}[rc]
+    # 99: the reference fails outside its own error classes (a wrapped
+    # negative extent makes a 2^64-element tensor); any SamoError will do
+    want = {5: ConfigError, 1: DimensionError, 99: SamoError}[rc]
     with pytest.raises(want):
         cj.loads(text)
 
@@ -116,14 +129,35 @@ def test_index_sets_round_trip_through_the_reference(ref, oracle):
     '{"layer_id":"a"}', '[{"layer_id":"a","dense_len":4,"indices":[0,2],"x":1}]',
     '[{"layer_id":"a","dense_len":4,"indices":[2,0]}]', '[{"layer_id":"a","dense_len":4,"indices":[4]}]',
     '[{"layer_id":"a","indices":[0]}]', '[{"layer_id":1,"dense_len":4,"indices":[0]}]',
-    '[{"layer_id":"a","dense_len":4,"indices":[0,1]}]', '[]'])
+    '[{"layer_id":"a","dense_len":4,"indices":[0,1]}]', '[]',
+    '[{"layer_id":"a","dense_len":4.7,"indices":[0,1]}]', '[{"layer_id":"a","dense_len":4,"indices":[1.0,2.5]}]',
+    '[{"layer_id":"a","dense_len":4,"indices":[-1]}]', '[{"layer_id":"a","dense_len":-1,"indices":[0,7]}]',
+    '[{"layer_id":"a","dense_len":4,"indices":[true]}]', '[{"layer_id":"a","dense_len":"4","indices":[0]}]'])
 def test_index_sets_same_rejections_as_the_reference(ref, text):
-    rc, _ = ref.index_sets_json_roundtrip(text)
-    if rc == 0:
-        cj.index_sets_loads(text)
+    rc, theirs = ref.index_sets_json_roundtrip(text)
+    if rc == 0:  # accepted by both, read to the same values
+        from types import SimpleNamespace
+        got = cj.index_sets_loads(text)
+        assert cj.index_sets_dumps([SimpleNamespace(layer_id=a, dense_len=d, indices=i) for a, d, i in got]) == theirs
         return
     with pytest.raises({5: ConfigError, 1: DimensionError}[rc]):
         cj.index_sets_loads(text)
+
+
+def test_index_sets_dump_takes_values_of_any_integer_dtype():
+    """int64 / Python-int indices are values: never split into
+    32-bit words; out-of-range and non-integer arrays are refused."""
+    from types import SimpleNamespace
+    from paper_2302_05045_b200._abi import ParameterError
+    want = '[{"dense_len":10,"indices":[1,4,9],"layer_id":"a"}]'
+    for idx in ([1, 4, 9], np.array([1, 4, 9], np.int64), np.array([1, 4, 9], np.uint32),
+                np.array([1, 4, 9], np.int32), np.array([1, 4, 9], np.uint16)):
+        assert cj.index_sets_dumps([SimpleNamespace(layer_id="a", dense_len=10, indices=idx)]) == want
+    big = np.array([0, 1 << 32], np.int64)
+    with pytest.raises(ParameterError):
+        cj.index_sets_dumps([SimpleNamespace(layer_id="a", dense_len=1 << 33, indices=big)])
+    with pytest.raises(ParameterError):
+        cj.index_sets_dumps([SimpleNamespace(layer_id="a", dense_len=10, indices=np.array([1.0]))])
 
 
 def test_index_sets_python_api_on_cpu_tensors():

@@ -347,6 +347,15 @@ def test_local_group_member_step_is_refused(cuda):
         m.set_grads([g])
     with pytest.raises(samo.StateError):
         models[0].step()
+    # the same members in another order are not this group (each rank's peer
+    # map must be exactly the list passed), nor is a list with a stranger
+    with pytest.raises(samo.StateError):
+        samo.SamoModel.local_group_step([models[0], models[2], models[1]])
+    other = samo.SamoModel.from_index_sets([samo.PrunedIndexSet("w", 4096, idx)], [(4096,)])
+    other.init_layer(0, torch.zeros(4096, device="cuda"))
+    with pytest.raises(samo.StateError):
+        samo.SamoModel.local_group_step([models[0], models[1], other])
+    other.close()
     samo.SamoModel.local_group_step(models)  # the group step still works
     torch.cuda.synchronize()
     assert all(m.step_record().t == 1 for m in models)
