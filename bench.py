@@ -54,6 +54,8 @@ def parse_args():
                     help="skip the side probes (fused dW-GEMM sink, FC-layer sweep of config 2)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-blocks", type=int, default=0, help="GPT blocks in the CPU sample")
+    ap.add_argument("--cpu-wte-rows", type=int, default=4096,
+                    help="rows of the token embedding in the CPU sample")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/CPU legs)")
     ap.add_argument("--graph", action="store_true",
                     help="time whole steps launched as one CUDA graph (small, launch-bound configs); "
@@ -140,7 +142,7 @@ def gpt_blocks_of(wl):
 
 
 def partition(sizes, nbins):
-    """Greedy LPT partition of layer indices into nbins by size."""
+    """Greedy LPT partition of item indices into nbins by size."""
     order = sorted(range(len(sizes)), key=lambda i: -sizes[i])
     bins = [[] for _ in range(nbins)]
     load = [0] * nbins
@@ -151,23 +153,61 @@ def partition(sizes, nbins):
     return [sorted(b) for b in bins if b]
 
 
-def cpu_reference_sample(dense_len, idx_sets, theta_sets, grad_sets, cfg_vals, reps, warm=1):
+def piece_cost(dense: int, kept: int) -> float:
+    """Relative CPU cost of the reference step on one layer: the dense passes
+    (sink gather read, theta16 zero-fill + expand) scale with dense_len, the
+    software half conversions, unscale and Adam with the kept count."""
+    return dense + 3.0 * kept
+
+
+def split_layers(dense_len, idx_sets, theta_sets, grad_sets, threads, per_thread=4):
+    """Element-range pieces of the layers for `threads` balanced trainers.
+
+    Every step operation of the reference is per element (sink gather,
+    unscale, Adam, downcast + expand), so a layer cut into contiguous dense
+    ranges [d0, d1) — indices rebased to d0, the matching theta32 range, the
+    dense gradient slice — does exactly the work of the whole layer.  Layers
+    are cut until no piece costs more than 1/(per_thread * threads) of the
+    total, then the pieces are LPT-partitioned over the threads.  Returns
+    (pieces, parts, balance = max thread load / mean thread load)."""
+    import numpy as np
+    total = sum(piece_cost(d, len(i)) for d, i in zip(dense_len, idx_sets))
+    target = total / max(1, threads * per_thread)
+    pieces = []
+    for d, idx, th, g in zip(dense_len, idx_sets, theta_sets, grad_sets):
+        k = max(1, int(np.ceil(piece_cost(d, len(idx)) / target))) if threads > 1 else 1
+        bounds = [d * j // k for j in range(k + 1)]
+        for d0, d1 in zip(bounds, bounds[1:]):
+            if d1 <= d0:
+                continue
+            a, b = np.searchsorted(idx, d0), np.searchsorted(idx, d1)
+            pieces.append((d1 - d0, (idx[a:b] - np.uint32(d0)).astype(np.uint32), th[a:b], g[d0:d1]))
+    costs = [piece_cost(p[0], len(p[1])) for p in pieces]
+    parts = partition(costs, min(threads, len(pieces)))
+    loads = [sum(costs[i] for i in part) for part in parts]
+    return pieces, parts, max(loads) / (sum(loads) / len(loads))
+
+
+def cpu_reference_sample(dense_len, idx_sets, theta_sets, grad_sets, cfg_vals, reps, warm=1,
+                         threads=None):
     """Times the UNMODIFIED reference (oracle/_ref) step — sink gather +
-    SamoTrainer::optimizer_step — on host threads, layers partitioned across
-    independent trainers (SURVEY §8(d) CPU baseline).  Returns (sec/step,
-    threads)."""
+    SamoTrainer::optimizer_step — on host threads (SURVEY §8(d) CPU
+    baseline).  threads = 1 is the reference as shipped: one trainer over the
+    layers as they are.  threads = T > 1 (default: every CPU this process may
+    use): the layers cut into balanced element ranges (split_layers) over T
+    independent trainers.  Returns {sec, threads, balance, pieces}."""
     from concurrent.futures import ThreadPoolExecutor
 
     from oracle.oracle import Cfg, RefLib, RefSession
     ref = RefLib()
     cfg = Cfg(*cfg_vals)
-    ncores = len(os.sched_getaffinity(0))
-    parts = partition(list(dense_len), min(ncores, len(dense_len)))
+    T = threads or len(os.sched_getaffinity(0))
+    pieces, parts, balance = split_layers(dense_len, idx_sets, theta_sets, grad_sets, T)
     sessions = []
     for part in parts:
-        s = RefSession(ref, [dense_len[i] for i in part], [idx_sets[i] for i in part],
-                       [theta_sets[i] for i in part], cfg)
-        s.wrap([grad_sets[i] for i in part])
+        s = RefSession(ref, [pieces[i][0] for i in part], [pieces[i][1] for i in part],
+                       [pieces[i][2] for i in part], cfg)
+        s.wrap([pieces[i][3] for i in part])
         sessions.append(s)
     with ThreadPoolExecutor(max_workers=len(sessions)) as ex:
         for _ in range(warm):
@@ -178,7 +218,40 @@ def cpu_reference_sample(dense_len, idx_sets, theta_sets, grad_sets, cfg_vals, r
         dt = (time.perf_counter() - t0) / reps
     for s in sessions:
         s.close()
-    return dt, len(sessions)
+    return {"sec": dt, "threads": len(sessions), "balance": balance, "pieces": len(pieces)}
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_sample_layers(wl, nb: int, wte_rows: int):
+    """The bounded CPU sample of a GPT workload: the first `nb` transformer
+    blocks plus the first `wte_rows` rows of the token embedding.  Returns
+    [(tensor index, dense offset, dense length)]."""
+    blocks = gpt_blocks_of(wl)
+    sel = [(i, 0, wl.tensors[i].numel) for b in blocks[:nb] for i in b]
+    names = [t.name for t in wl.tensors]
+    if wte_rows and "wte" in names:
+        i = names.index("wte")
+        sel.append((i, 0, min(wte_rows, wl.tensors[i].shape[0]) * wl.tensors[i].shape[1]))
+    return sel, len(blocks)
+
+
+def cpu_baseline_pair(dense_len, idx_sets, theta_sets, grad_sets, cfg_vals, reps, reps1):
+    """Both CPU baselines on one sample: the reference as shipped (1 thread)
+    and on every usable host thread with balanced element ranges."""
+    one = cpu_reference_sample(dense_len, idx_sets, theta_sets, grad_sets, cfg_vals, reps=reps1,
+                               warm=1, threads=1)
+    allt = cpu_reference_sample(dense_len, idx_sets, theta_sets, grad_sets, cfg_vals, reps=reps,
+                                warm=1)
+    return one, allt
 
 
 # ---------------------------------------------------------------------------
@@ -197,41 +270,51 @@ def run_reference(args) -> None:
     o = Oracle()
     ref = RefLib()
     ncores = len(os.sched_getaffinity(0))
-    blocks = gpt_blocks_of(wl)
-    nb = args.cpu_blocks or max(1, min(len(blocks), 8, ncores // 12 or 1))
-    sel = [i for b in blocks[:nb] for i in b]
-    dense_len = [wl.tensors[i].numel for i in sel]
-    # inputs: the same counter-hash synthetic values as the GPU arm
-    vals = [o.synth_f32(0, wl.tensors[i].numel, args.seed, 2 * i, wl.tensors[i].init_bound) for i in sel]
+    nb = args.cpu_blocks or (2 if ncores >= 8 else 1)
+    sel, nblocks = cpu_sample_layers(wl, nb, args.cpu_wte_rows)
+    dense_len = [n for _, _, n in sel]
+    # inputs: the same counter-hash synthetic values as the GPU arm (the
+    # embedding rows are the first rows of the GPU arm's wte)
+    vals = [o.synth_f32(off, n, args.seed, 2 * i, wl.tensors[i].init_bound) for i, off, n in sel]
     from concurrent.futures import ThreadPoolExecutor
 
-    def prune_one(j):
-        rc, s = ref.magnitude_prune([vals[j]], [wl.tensors[sel[j]].prunable], wl.sparsity, 0)
+    def prune_one(j):  # the reference's own magnitude_prune, per layer
+        rc, s = ref.magnitude_prune([vals[j]], [wl.tensors[sel[j][0]].prunable], wl.sparsity, 0)
         assert rc == 0
         return s[0]
     with ThreadPoolExecutor(max_workers=ncores) as ex:
         idx = list(ex.map(prune_one, range(len(sel))))
     theta = [o.compress(v, s) for v, s in zip(vals, idx)]
-    grads = [o.synth_f16(0, wl.tensors[i].numel, args.seed + 1, 2 * i + 1, 2.0**-7, 1024.0) for i in sel]
+    grads = [o.synth_f16(off, n, args.seed + 1, 2 * i + 1, 2.0**-7, 1024.0) for i, off, n in sel]
     del vals
     phi_s = sum(dense_len)
     cfg = (1e-3, 0.9, 0.999, 1e-8, 1024.0, 0.0)
     steps = max(1, args.steps)
-    dt, threads = cpu_reference_sample(dense_len, idx, theta, grads, cfg, reps=steps,
-                                       warm=max(1, min(args.warmup, 3)))
+    one, allt = cpu_baseline_pair(dense_len, idx, theta, grads, cfg, reps=steps, reps1=1)
+    dt = allt["sec"]
     value = phi_s / dt
-    sample = (f"{nb} of {len(blocks)} transformer blocks of {wl.name} "
-              f"({len(sel)} tensors, {phi_s} params) per step; layers split over {threads} "
-              f"independent reference trainers")
+    sample = (f"{nb} of {nblocks} transformer blocks of {wl.name} + the first {args.cpu_wte_rows} "
+              f"rows of wte (masked on their own) = {len(sel)} tensors, {phi_s} params per step; "
+              f"sink gather + SamoTrainer::optimizer_step of the unmodified reference, cut into "
+              f"{allt['pieces']} element ranges over {allt['threads']} independent trainers "
+              f"(max/mean thread load {allt['balance']:.3f})")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 * wl.phi / phi_s,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "ms_per_step_extrapolated": dt * 1e3 * wl.phi / phi_s,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": {"workload": wl.name, "sparsity": wl.sparsity,
-                                        "phi": wl.phi, "parallelism": "cpu-threads"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": sample},
+                                        "phi": wl.phi, "sample_params": phi_s,
+                                        "parallelism": "cpu-threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": allt["threads"], "kind": "reference",
+                         "sample": sample, "load_balance": allt["balance"], "cpu": cpu_model(),
+                         "single_thread": {"value": phi_s / one["sec"], "unit": UNIT,
+                                           "ms_per_step": one["sec"] * 1e3,
+                                           "note": "the reference as shipped: one trainer, "
+                                                   "layers whole (train.hpp:617-656)"}},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "ms_per_step is the measured sample step; ms_per_step_extrapolated scales it to "
+                "the whole workload (phi / sample params)",
     }
     emit(line)
 
@@ -379,8 +462,9 @@ def fc_sweep_probe(reps: int = 200, cpu: bool = True) -> list:
             try:
                 idx = sets[0].indices.cpu().numpy().view(np.uint32)
                 gh = g.cpu().numpy().view(np.uint16)
-                dt, _ = cpu_reference_sample([t.numel], [idx], [theta0], [gh],
-                                             (1e-3, 0.9, 0.999, 1e-8, 1024.0, 0.0), reps=ref_reps[n])
+                dt = cpu_reference_sample([t.numel], [idx], [theta0], [gh],
+                                          (1e-3, 0.9, 0.999, 1e-8, 1024.0, 0.0), reps=ref_reps[n],
+                                          threads=1)["sec"]
                 entry["reference_cpu_us"] = dt * 1e6
                 entry["speedup_vs_reference"] = dt * 1e6 / us
             except Exception as ex:  # no oracle/_ref on this host
@@ -435,14 +519,19 @@ def run_samo(args) -> None:
     torch.cuda.synchronize()
     cpu_sample = None
     if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.profile):
-        # keep what the CPU sample needs before freeing the dense init values
-        blocks = gpt_blocks_of(wl)
+        # keep what the CPU sample needs (the K0 masks, bit-exact with the
+        # reference's) before freeing the dense init values
         ncores = len(os.sched_getaffinity(0))
-        nb = args.cpu_blocks or max(1, min(len(blocks), 4, ncores // 16 or 1))
-        sel = [i for b in blocks[:nb] for i in b]
-        cpu_sample = {"sel": sel, "nb": nb, "nblocks": len(blocks),
-                      "idx": [sets[i].indices.cpu().numpy().view(np.uint32) for i in sel],
-                      "theta": [model.read(i, "theta32").cpu().numpy() for i in sel]}
+        nb = args.cpu_blocks or (2 if ncores >= 8 else 1)
+        sel, nblocks = cpu_sample_layers(wl, nb, args.cpu_wte_rows)
+        cs_idx, cs_theta = [], []
+        for i, off, n in sel:
+            idx = sets[i].indices.cpu().numpy().view(np.uint32)
+            th = model.read(i, "theta32").cpu().numpy()
+            a, b = np.searchsorted(idx, off), np.searchsorted(idx, off + n)
+            cs_idx.append((idx[a:b] - np.uint32(off)).astype(np.uint32))
+            cs_theta.append(th[a:b].copy())
+        cpu_sample = {"sel": sel, "nb": nb, "nblocks": nblocks, "idx": cs_idx, "theta": cs_theta}
     del init_vals, sets
     torch.cuda.empty_cache()
 
@@ -482,6 +571,14 @@ def run_samo(args) -> None:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = samo.kernel_launch_count()
+    nvl = nvl0 = None
+    if world > 1:  # NVLink bytes this GPU sent / received over the timed region
+        try:
+            from paper_2302_05045_b200.nvlink import NvlinkBytes
+            nvl = NvlinkBytes(int(smi_index))
+            nvl0 = nvl.read()
+        except Exception as ex:  # noqa: BLE001  (no NVML counter: reported as unavailable)
+            nvl, nvl0 = None, str(ex)
     with ClockSampler(smi_index) as clk:
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
@@ -514,6 +611,21 @@ def run_samo(args) -> None:
             time.sleep(0.35)
     launches = samo.kernel_launch_count() - launches0
     total_ms = t0.elapsed_time(t1)
+    nvlink_measured = None
+    if world > 1:  # every rank joins the gather (NaN where NVML has no counter)
+        nvl1 = nvl.read() if nvl is not None else None
+        per = torch.tensor([(nvl1[0] - nvl0[0]) / K, (nvl1[1] - nvl0[1]) / K] if nvl1 else
+                           [float("nan")] * 2, device=dev, dtype=torch.float64)
+        allr = [torch.zeros_like(per) for _ in range(world)]
+        dist.all_gather(allr, per)
+        if nvl is not None:
+            nvlink_measured = {"source": f"NVML {nvl.source} counters, {len(nvl.links)} links",
+                               "tx_bytes_per_step_per_rank": [float(x[0]) for x in allr],
+                               "rx_bytes_per_step_per_rank": [float(x[1]) for x in allr],
+                               "note": "whole device over the timed region (all kernels, NCCL "
+                                       "barriers included), divided by the steps"}
+        else:
+            nvlink_measured = {"unavailable": nvl0}
     phases = pipeline = None
     if world == 1 and args.graph:  # per-kernel breakdown from a staged pass
         for s in range(K):
@@ -739,18 +851,23 @@ def run_samo(args) -> None:
     cpu = None
     if cpu_sample is not None:
         sel = cpu_sample["sel"]
-        dl = [wl.tensors[i].numel for i in sel]
-        gr = [grads[i].cpu().numpy().view(np.uint16) for i in sel]
+        dl = [n for _, _, n in sel]
+        gr = [grads[i][off:off + n].cpu().numpy().view(np.uint16) for i, off, n in sel]
         cfgv = (cfg.learning_rate, cfg.beta1, cfg.beta2, cfg.epsilon, cfg.loss_scale, cfg.weight_decay)
         try:
-            dt, threads = cpu_reference_sample(dl, cpu_sample["idx"], cpu_sample["theta"], gr, cfgv,
-                                               reps=3, warm=1)
+            one, allt = cpu_baseline_pair(dl, cpu_sample["idx"], cpu_sample["theta"], gr, cfgv,
+                                          reps=3, reps1=1)
             phi_s = sum(dl)
-            cpu = {"value": phi_s / dt, "unit": UNIT, "cores": threads, "kind": "reference",
-                   "sample": f"{cpu_sample['nb']} of {cpu_sample['nblocks']} transformer blocks "
-                             f"({len(sel)} tensors, {phi_s} params), sink gather + "
-                             f"SamoTrainer::optimizer_step of the unmodified reference, layers "
-                             f"split over {threads} host threads, 3 reps"}
+            cpu = {"value": phi_s / allt["sec"], "unit": UNIT, "cores": allt["threads"], "kind": "reference",
+                   "sample": f"{cpu_sample['nb']} of {cpu_sample['nblocks']} transformer blocks + the "
+                             f"first {args.cpu_wte_rows} rows of wte ({len(sel)} tensors, {phi_s} params), "
+                             f"sink gather + SamoTrainer::optimizer_step of the unmodified reference, "
+                             f"cut into {allt['pieces']} element ranges over {allt['threads']} "
+                             f"independent trainers, 3 reps",
+                   "load_balance": allt["balance"], "cpu": cpu_model(), "ms_per_sample_step": allt["sec"] * 1e3,
+                   "single_thread": {"value": phi_s / one["sec"], "unit": UNIT,
+                                     "ms_per_sample_step": one["sec"] * 1e3,
+                                     "note": "the reference as shipped: one trainer, layers whole"}}
         except Exception as ex:  # the baseline must not kill the GPU measurement
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                    "sample": f"failed: {ex}"}
@@ -793,6 +910,8 @@ def run_samo(args) -> None:
                           "NCCL all-gather of binary16 weights || expand"
                           if model.exchange_mode() == model.EXCHANGE_SHARDED
                           else "allreduce: bucketed NCCL allreduce overlapped with K1/K23"),
+            "model_params_per_s": phi / (ms_step * 1e-3),
+            "nvlink_measured": nvlink_measured,
             "phases_ms": phases,
             "pipeline_phases_ms": pipeline,
             "p2p_features": model.p2p_features() if world > 1 else None,
