@@ -583,20 +583,11 @@ def run_samo(args) -> None:
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record()
-        if world == 1 and args.graph:
+        if world == 1:
+            # the production single-GPU step: K123 (+ the skip-repair no-op),
+            # eager launches or one captured graph per step
             for s in range(K):
-                model.step(graph=True)
-        elif world == 1:
-            # staged: K1 | K23 with events between (same work as model.step())
-            for s in range(K):
-                e = evs[s]
-                e[0].record()
-                model.gather()
-                e[1].record()
-                model.exchange()  # no-op without a communicator
-                e[2].record()
-                model.update()
-                e[3].record()
+                model.step(graph=args.graph)
         else:
             # the production data-parallel step: bucketed exchange overlapped
             # with the gather and update kernels
@@ -627,13 +618,29 @@ def run_samo(args) -> None:
         else:
             nvlink_measured = {"unavailable": nvl0}
     phases = pipeline = None
-    if world == 1 and args.graph:  # per-kernel breakdown from a staged pass
-        for s in range(K):
+    fused_ms = None
+    fused = world == 1 and os.environ.get("SAMO_FUSED_STEP", "1") != "0"
+    KB = min(K, 10)
+    if world == 1:
+        # Per-kernel breakdown (not the headline): the fused step's kernels
+        # timed by events inside the driver, one step at a time; then the
+        # K1 | K23 pair of the split path on the same state, for comparison.
+        if fused:
+            fused_ms = []
+            _abi.call("samo_model_enable_phase_timing", model.handle, 1)
+            for _ in range(KB):
+                model.step()
+                buf = (C.c_float * 4)()
+                cnt = _abi.load().samo_model_phase_times(model.handle, buf, 4)
+                fused_ms.append([buf[i] for i in range(max(0, cnt))])
+            _abi.call("samo_model_enable_phase_timing", model.handle, 0)
+        evs = evs[:KB]
+        for s in range(KB):
             e = evs[s]
             e[0].record()
             model.gather()
             e[1].record()
-            model.exchange()
+            model.exchange()  # no-op without a communicator
             e[2].record()
             model.update()
             e[3].record()
@@ -722,6 +729,20 @@ def run_samo(args) -> None:
                                          "write_bytes": 12 * nnz + 2 * phi},
         }
         hbm_kernels = list(kern)
+        if fused:
+            # K123: dense grad 2phi + off16 2n + theta/m/v read
+            # 12n + theta/m/v write 12n + theta16 2phi, one launch per step.
+            for v in kern.values():
+                v["role"] = "split path (SAMO_FUSED_STEP=0), timed for comparison"
+            f_ms = statistics.mean(x[0] for x in fused_ms)
+            r_ms = statistics.mean(x[1] for x in fused_ms)
+            b_f = 4 * phi + 26 * nnz
+            kern["K123_fused_step"] = {"ms": f_ms, "bytes": b_f, "GBps": b_f / (f_ms * 1e-3) / 1e9,
+                                       "write_bytes": 2 * phi + 12 * nnz}
+            kern["k123_repair"] = {"ms": r_ms, "bytes": 0, "GBps": 0.0,
+                                   "note": "skip repair: returns at once unless the step was skipped"}
+            hbm_kernels = ["K123_fused_step"]
+            bytes_k1, bytes_k23, k1_ms, k23_ms = 0, b_f, 0.0, f_ms
     else:
         # Production data-parallel step (fused P2P exchange), per rank
         # (DESIGN.md §7), push mode (default): K1 2phi + 2n off16 + 2n grad16,
@@ -896,10 +917,13 @@ def run_samo(args) -> None:
                               "L2; no flush needed") if 4 * phi + 32 * nnz > 2 * 126e6 else
                              "L2-resident working set: latency-bound configuration, reported as "
                              "time per step (no flush between steps)",
-                       "timing": "CUDA graph per step" if args.graph else "staged launches with events",
+                       "timing": ("CUDA graph per step" if args.graph else "eager launches") +
+                                 ", CUDA events around the timed region on the launching stream",
                        "gpu": gpu_name},
             "gpu_launches": int(launches),
-            "step_mode": "K1 | K23 (no exchange)" if world == 1 else
+            "step_mode": ("K123 fused step (gather + unscale + Adam + downcast + expand, one pass per "
+                          "tile, speculative on the skip flag) + skip-repair no-op" if fused else
+                          "K1 | K23 (no exchange)") if world == 1 else
                          ("p2p (ZeRO-1, exchange fused over NVLink, no NCCL): K1 pushes each kept "
                           "binary16 grad into its owner's receive buffer | peer-signalled flag "
                           "exchange | per k-bucket: shard kernel sums the G local contributions "

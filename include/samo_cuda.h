@@ -395,7 +395,7 @@ typedef struct samo_memory_report {
   uint64_t dense_params;           /* phi */
   uint64_t kept;                   /* n */
   uint64_t theta16_bytes;          /* dense binary16 weights */
-  uint64_t compressed_state_bytes; /* theta32, m, v, grad arenas */
+  uint64_t compressed_state_bytes; /* theta32, m, v (two sets), grad arenas */
   uint64_t index_bytes;            /* u32 index sets + off16 */
   uint64_t table_bytes;            /* tile table */
   uint64_t device_bytes;           /* everything the model allocated */

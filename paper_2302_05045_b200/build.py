@@ -42,7 +42,8 @@ def _stale() -> bool:
     if not LIB.exists():
         return True
     t = LIB.stat().st_mtime
-    deps = [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "samo_cuda.h", Path(__file__)]
+    deps = [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "samo_cuda.h",
+                                                    ROOT / "include" / "samo_cuda_testing.h", Path(__file__)]
     return any(d.stat().st_mtime > t for d in deps)
 
 

@@ -935,10 +935,7 @@ int samo_model_set_exchange(samo_model* md, int mode) {
       mode != SAMO_EXCHANGE_P2P)
     return fail(SAMO_E_PARAMETER, "unknown exchange mode %d", mode);
   md->exchange = mode;
-  if (md->graph) {
-    cudaGraphExecDestroy(md->graph);
-    md->graph = nullptr;
-  }
+  drop_graphs(md);
   return clear_ok();
 }
 
@@ -975,10 +972,7 @@ int samo_model_attach_local_group(samo_model* const* models, int G) {
     md->exchange = SAMO_EXCHANGE_P2P;
     for (int q = 0; q < G; ++q) md->peer_base[q] = models[q]->block;
     md->p2p_ok = true;
-    if (md->graph) {
-      cudaGraphExecDestroy(md->graph);
-      md->graph = nullptr;
-    }
+    drop_graphs(md);
   }
   const int B = p2p_buckets(G);
   for (int r = 0; r < G && B > 1; ++r) {

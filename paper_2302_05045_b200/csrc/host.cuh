@@ -90,6 +90,16 @@ struct samo_model {
   bool finalized = false;
   bool grads_set = false;
   int grid_gather16 = 0, grid_gather32 = 0, grid_update16 = 0, grid_update32 = 0;
+  // Fused single-GPU step (K123): the second set of theta/m/v buffers the
+  // step writes; the host swaps the sets after every step (`parity` = which
+  // set theta/m/v point at), so everything else always sees the live state.
+  float* theta_alt = nullptr;
+  float* m_alt = nullptr;
+  float* v_alt = nullptr;
+  int parity = 0;
+  int grid_fused = 0;
+  cudaGraphExec_t fgraph[2] = {nullptr, nullptr};  // captured fused steps, one per parity
+  uint64_t fgraph_kernels = 0;
   // CUDA graph of one step
   cudaGraphExec_t graph = nullptr;
   samo_comm* graph_comm = nullptr;
@@ -163,6 +173,20 @@ inline int env_int(const char* name, int dflt) {
 }
 
 inline int comm_size(const samo_model* md) { return md->comm ? md->comm->nranks : 1; }
+
+// Drops every captured step graph (the step plan changed).
+inline void drop_graphs(samo_model* md) {
+  if (md->graph) cudaGraphExecDestroy(md->graph);
+  md->graph = nullptr;
+  for (auto& g : md->fgraph) {
+    if (g) cudaGraphExecDestroy(g);
+    g = nullptr;
+  }
+}
+
+// The fused single-GPU step (K123) is the default without a communicator;
+// SAMO_FUSED_STEP=0 selects the K1 | K23 pair.
+inline bool fused_step(const samo_model* md) { return comm_size(md) <= 1 && env_int("SAMO_FUSED_STEP", 1) != 0; }
 
 inline int step_ready(samo_model* md) {
   if (!md) return fail(SAMO_E_PARAMETER, "null model");

@@ -46,6 +46,11 @@ struct StepArgs {
   float* theta;
   float* m;
   float* v;
+  // K123 (fused single-GPU step): theta/m/v are read from the buffers above
+  // and the updated values written to these (the model's other buffer set).
+  float* theta_o;
+  float* m_o;
+  float* v_o;
   float inv_scale;             // 1/loss_scale (and 1/G when exchanging fp32)
   SamoAdamParams prm;
   SamoStepState* st;
@@ -73,6 +78,15 @@ struct StepArgs {
 int launch_gather(const StepArgs& a, bool out_f32, int grid, cudaStream_t s);
 // K23 update: g_f32 selects the gradient arena type written by K1.
 int launch_update(const StepArgs& a, bool g_f32, int grid, cudaStream_t s);
+// K123, the fused single-GPU step (gather + unscale + Adam + downcast +
+// expand in one pass per tile), speculative on the global skip flag: reads
+// theta/m/v, writes theta_o/m_o/v_o and theta16 in place; the last CTA
+// advances the scalars or records the skip.  k123_repair, launched after it,
+// restores theta16 and copies theta/m/v -> theta_o/m_o/v_o when the step was
+// skipped (a no-op otherwise).  The host then swaps the two buffer sets.
+int launch_step_fused(const StepArgs& a, int grid, cudaStream_t s);
+int launch_step_repair(const StepArgs& a, cudaStream_t s);
+int fused_grid(uint32_t tile_elems);
 // which: 0 = gather, 1 = update; wide = fp32 gradient arena.
 int step_grid(int which, bool wide, uint32_t tile_elems);
 // Fused peer-to-peer exchange + shard update (kernels_fused.cu, k_shard_p2p):

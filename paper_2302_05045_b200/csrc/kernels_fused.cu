@@ -573,6 +573,344 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// K123: the whole single-GPU step in one pass per tile (train.hpp:598-654:
+// sink gather, unscale + finite check, Adam, downcast + expand).
+//
+// The skip decision (train.hpp:632-639) depends on every gradient of the
+// step, so the pass is speculative: it reads theta/m/v and writes the updated
+// values to the model's other buffer set (theta_o/m_o/v_o), and writes the
+// new binary16 weights straight into theta16.  The last CTA then either
+// advances the Adam scalars (the host swaps the buffer sets) or records the
+// skip, after which k123_repair copies theta/m/v into the other set and
+// rebuilds theta16 from theta — theta16 == expand(half(theta32)) is the
+// state invariant (store.hpp:171-197), so the repair restores it bit for bit.
+//
+// Per tile: the producer warp brings the dense binary16 gradient tile into
+// shared memory with one 1-D TMA copy (two tiles in flight), and theta/m/v/
+// off16 of the tile's kept range in <= CH-element chunks (NS-stage ring).
+// Consumers gather g = half(grad[off]) * 2^-s through off16, run the IEEE
+// Adam, store theta/m/v with streaming stores, and write half(theta) back
+// into the gradient tile at the same offset (each offset belongs to one kept
+// element, so no other element's gradient is overwritten), marking it in a
+// per-tile bitmap.  The copy-out writes the tile to theta16 with 128-bit
+// stores, zeroing the positions the bitmap does not mark (the pruned ones),
+// and clears the bitmap.  HBM bytes per step: 2 phi (grad) + 2 n (off16) +
+// 24 n (theta/m/v read + write) + 2 phi (theta16) = 4 phi + 26 n, against
+// 4 phi + 32 n for K1 + K23 (grad16 written and read back, off16 read twice).
+
+struct TileFull {
+  uint32_t layer, dense_begin, dense_count;
+  uint64_t k_begin, k_end, out_off;
+};
+
+__device__ __forceinline__ TileFull load_tile_full(const SamoTile* p) {
+  const uint4* q = reinterpret_cast<const uint4*>(p);
+  const uint4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+  TileFull r;
+  r.layer = a.x;
+  r.dense_begin = a.y;
+  r.dense_count = a.z;
+  r.k_begin = (static_cast<uint64_t>(b.y) << 32) | b.x;
+  r.k_end = (static_cast<uint64_t>(b.w) << 32) | b.z;
+  r.out_off = (static_cast<uint64_t>(c.y) << 32) | c.x;
+  return r;
+}
+
+template <int CH>
+struct K123Layout {
+  static constexpr uint32_t kF32 = (CH + 8) * 4;   // theta / m / v slot
+  static constexpr uint32_t kOff = (CH + 16) * 2;  // off16 slot
+  static constexpr uint32_t kStage = 3 * kF32 + kOff;
+  static_assert(kStage % 16 == 0, "stages stay 16-byte aligned");
+};
+constexpr int kK123Tiles = 2;  // dense gradient tiles in flight per CTA
+
+// Lane masks of 8 binary16 values from 8 bitmap bits (bit e -> lane e).
+__device__ __forceinline__ uint32_t lane_mask2(uint32_t bits, int e) {
+  return ((0u - ((bits >> (2 * e)) & 1u)) & 0x0000FFFFu) | ((0u - ((bits >> (2 * e + 1)) & 1u)) & 0xFFFF0000u);
+}
+
+template <int CH, int NS, bool CFG>
+__global__ void __launch_bounds__(kThreads + 32) k123_step(StepArgs a) {
+  using L = K123Layout<CH>;
+  constexpr uint32_t kConsumerWarps = kThreads / 32;
+  constexpr int NSG = kK123Tiles;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ __align__(8) uint64_t full[NS];
+  __shared__ __align__(8) uint64_t empty[NS];
+  __shared__ __align__(8) uint64_t gfull[NSG];
+  __shared__ __align__(8) uint64_t gempty[NSG];
+  __shared__ float red[kConsumerWarps];
+  __shared__ int last_cta;
+  __shared__ int cta_bad;
+
+  const uint32_t T = a.tile_elems;
+  uint8_t* const gst = smem + NS * L::kStage;                                 // NSG x T halves
+  uint32_t* const bm0 = reinterpret_cast<uint32_t*>(gst + NSG * T * 2u);     // NSG x T bits
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  for (uint32_t i = tid; i < NSG * (T / 32u); i += blockDim.x) bm0[i] = 0u;
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    for (int s = 0; s < NSG; ++s) {
+      mbar_init(&gfull[s], 1);
+      mbar_init(&gempty[s], kConsumerWarps);
+    }
+    cta_bad = 0;
+    fence_mbar_init();
+  }
+  __syncthreads();  // the only CTA-wide barrier
+  // PDL: the previous step's kernels may still be running until here.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  if (warp == kConsumerWarps) {
+    // ---- producer warp (one elected lane): per tile, the dense gradient
+    // tile, then theta/m/v/off16 of its kept range chunk by chunk.
+    if (lane == 0) {
+      const uint64_t policy = policy_evict_first();
+      uint32_t it = 0, tt = 0;
+      for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++tt) {
+        const TileFull td = load_tile_full(a.tiles + t);
+        const int sg = static_cast<int>(tt % NSG);
+        if (tt >= static_cast<uint32_t>(NSG)) mbar_wait(&gempty[sg], ((tt / NSG) - 1) & 1u);
+        const uint32_t bytes = (td.dense_count * 2u) & ~15u;
+        if (bytes) {
+          mbar_arrive_expect_tx(&gfull[sg], bytes);
+          bulk_g2s(gst + static_cast<size_t>(sg) * T * 2u, a.layers[td.layer].grad + td.dense_begin, bytes,
+                   &gfull[sg], policy);
+        } else {
+          mbar_arrive(&gfull[sg]);
+        }
+        const uint32_t nch = tile_chunks<CH>(td.k_begin, td.k_end);
+        for (uint32_t j = 0; j < nch; ++j, ++it) {
+          const int s = static_cast<int>(it % NS);
+          if (it >= static_cast<uint32_t>(NS)) mbar_wait(&empty[s], ((it / NS) - 1) & 1u);
+          const uint64_t kc0 = td.k_begin + static_cast<uint64_t>(j) * CH;
+          const uint64_t kc1 = min(td.k_end, kc0 + CH);
+          if (kc1 == kc0) {
+            mbar_arrive(&full[s]);
+            continue;
+          }
+          uint8_t* st = smem + s * L::kStage;
+          const uint64_t f0 = kc0 & ~3ull;
+          const uint32_t fb = static_cast<uint32_t>((((kc1 + 3) & ~3ull) - f0) * 4);
+          const uint64_t h0 = kc0 & ~7ull;
+          const uint32_t hb = static_cast<uint32_t>((((kc1 + 7) & ~7ull) - h0) * 2);
+          mbar_arrive_expect_tx(&full[s], 3 * fb + hb);
+          bulk_g2s(st, a.theta + f0, fb, &full[s], policy);
+          bulk_g2s(st + L::kF32, a.m + f0, fb, &full[s], policy);
+          bulk_g2s(st + 2 * L::kF32, a.v + f0, fb, &full[s], policy);
+          bulk_g2s(st + 3 * L::kF32, a.off16 + h0, hb, &full[s], policy);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumer warps ------------------------------------------------------
+  SamoAdamParams cprm = a.prm;
+  if constexpr (CFG) cprm = step_prm(a.cfg, a.prm);
+  const float b1p = __fmul_rn(a.st->beta1_pow, cprm.beta1);  // train.hpp:325-329, 640-642
+  const float b2p = __fmul_rn(a.st->beta2_pow, cprm.beta2);
+  const float bias1 = __fsub_rn(1.0f, b1p), bias2 = __fsub_rn(1.0f, b2p);
+  const float omb1 = __fsub_rn(1.0f, cprm.beta1);  // train.hpp:335
+  const float omb2 = __fsub_rn(1.0f, cprm.beta2);  // train.hpp:336
+  const float lrwd = __fmul_rn(cprm.lr, cprm.wd);
+  const float p_beta1 = pin_f32(cprm.beta1), p_beta2 = pin_f32(cprm.beta2);
+  const float p_lr = pin_f32(cprm.lr), p_eps = pin_f32(cprm.eps), p_wd = pin_f32(cprm.wd);
+  float inv_scale = a.inv_scale;
+  if constexpr (CFG) inv_scale = a.cfg ? a.cfg->inv_scale : a.inv_scale;
+  const float p_inv = pin_f32(inv_scale);
+  float* const p_to = pin_ptr(a.theta_o);
+  float* const p_mo = pin_ptr(a.m_o);
+  float* const p_vo = pin_ptr(a.v_o);
+  uint16_t* const p_t16 = pin_ptr(a.theta16);
+
+  float nacc = 0.0f;
+  bool bad = false;
+  uint32_t it = 0, tt = 0;
+  for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++tt) {
+    const TileFull td = load_tile_full(a.tiles + t);
+    const int sg = static_cast<int>(tt % NSG);
+    uint16_t* const sgr = reinterpret_cast<uint16_t*>(gst + static_cast<size_t>(sg) * T * 2u);
+    uint32_t* const bm = bm0 + sg * (T / 32u);
+    const uint32_t staged = ((td.dense_count * 2u) & ~15u) >> 1;
+    const uint16_t* const gsrc = a.layers[td.layer].grad + td.dense_begin;  // unstaged tail (< 8 elements)
+    const uint32_t nch = tile_chunks<CH>(td.k_begin, td.k_end);
+    mbar_wait(&gfull[sg], (tt / NSG) & 1u);
+    for (uint32_t j = 0; j < nch; ++j, ++it) {
+      const int s = static_cast<int>(it % NS);
+      const uint8_t* st = smem + s * L::kStage;
+      const uint64_t kc0 = td.k_begin + static_cast<uint64_t>(j) * CH;
+      const uint64_t kc1 = min(td.k_end, kc0 + CH);
+      const uint32_t n = static_cast<uint32_t>(kc1 - kc0);
+      const uint32_t fo = static_cast<uint32_t>(kc0 & 3ull);
+      const uint32_t ho = static_cast<uint32_t>(kc0 & 7ull);
+      const float* sth = reinterpret_cast<const float*>(st) + fo;
+      const float* smv = reinterpret_cast<const float*>(st + L::kF32) + fo;
+      const float* svv = reinterpret_cast<const float*>(st + 2 * L::kF32) + fo;
+      const uint16_t* soff = reinterpret_cast<const uint16_t*>(st + 3 * L::kF32) + ho;
+      mbar_wait(&full[s], (it / NS) & 1u);
+#pragma unroll 1
+      for (uint32_t ib = tid; ib < n; ib += kU * kThreads) {
+        float gv[kU], tv[kU], mv[kU], vv[kU];
+        uint32_t ov[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const uint32_t i = ib + u * kThreads;
+          if (i < n) {
+            ov[u] = soff[i];
+            const uint16_t h = ov[u] < staged ? sgr[ov[u]] : gsrc[ov[u]];
+            bad |= (h & 0x7C00u) == 0x7C00u;  // |h * 2^-s| is finite iff h is
+            gv[u] = mul_x86(f16_bits_to_f32(h), p_inv);
+            tv[u] = sth[i];
+            mv[u] = smv[i];
+            vv[u] = svv[i];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const uint32_t i = ib + u * kThreads;
+          if (i < n) {
+            const float gk = gv[u];
+            nacc = __fadd_rn(nacc, __fmul_rn(gk, gk));
+            // adam_update (train.hpp:338-345): IEEE per op, no contraction.
+            const float mk = __fadd_rn(__fmul_rn(p_beta1, mv[u]), __fmul_rn(omb1, gk));
+            const float vk = __fadd_rn(__fmul_rn(p_beta2, vv[u]), __fmul_rn(omb2, __fmul_rn(gk, gk)));
+            const float mh = __fdiv_rn(mk, bias1);
+            const float vh = __fdiv_rn(vk, bias2);
+            float tk = __fsub_rn(tv[u], __fmul_rn(p_lr, __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), p_eps))));
+            if (p_wd != 0.0f) tk = __fsub_rn(tk, __fmul_rn(lrwd, tk));
+            const uint64_t k = kc0 + i;
+            st_na_f32(p_mo + k, mk);
+            st_na_f32(p_vo + k, vk);
+            st_na_f32(p_to + k, tk);
+            sgr[ov[u]] = f32_to_f16_bits(tk);
+            atomicOr(&bm[ov[u] >> 5], 1u << (ov[u] & 31u));
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    // Every consumer warp has written its weights into the tile.
+    asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+    // Copy-out: 128-bit stores of the tile, pruned positions zeroed by the
+    // bitmap (layer segments are 256-byte aligned, tiles start at multiples
+    // of T); each thread clears the bitmap bytes it read.
+    {
+      const uint4* o4 = reinterpret_cast<const uint4*>(sgr);
+      uint8_t* b8 = reinterpret_cast<uint8_t*>(bm);
+      uint16_t* dst = p_t16 + td.out_off;
+      uint4* d4 = reinterpret_cast<uint4*>(dst);
+      const uint32_t full16 = td.dense_count >> 3;
+      for (uint32_t i0 = tid; i0 < full16; i0 += 4 * kThreads) {
+        uint4 v[4];
+        uint32_t bits[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t i = i0 + u * kThreads;
+          if (i < full16) {
+            v[u] = o4[i];
+            bits[u] = b8[i];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t i = i0 + u * kThreads;
+          if (i < full16) {
+            uint4 w = v[u];
+            w.x &= lane_mask2(bits[u], 0);
+            w.y &= lane_mask2(bits[u], 1);
+            w.z &= lane_mask2(bits[u], 2);
+            w.w &= lane_mask2(bits[u], 3);
+            if (bits[u]) b8[i] = 0;
+            st_na_v4u(d4 + i, w.x, w.y, w.z, w.w);
+          }
+        }
+      }
+      if (tid == 0 && (td.dense_count & 7u)) {
+        const uint32_t base = full16 * 8u;
+        const uint32_t bits = b8[full16];
+        for (uint32_t e = 0; e < (td.dense_count & 7u); ++e) dst[base + e] = ((bits >> e) & 1u) ? sgr[base + e] : 0;
+        b8[full16] = 0;
+      }
+    }
+    // The next TMA copy into this tile's buffer follows generic-proxy writes.
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&gempty[sg]);
+  }
+  // The repair kernel may start its (waiting) CTAs now.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+  // Grad norm partial and skip indicator per CTA; the last CTA finalises.
+  float x = nacc;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = __fadd_rn(x, __shfl_xor_sync(0xFFFFFFFFu, x, o));
+  if (lane == 0) red[warp] = x;
+  if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(&cta_bad, 1);
+  asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+  if (tid == 0) {
+    float sacc = 0.f;
+    for (uint32_t w = 0; w < kConsumerWarps; ++w) sacc = __fadd_rn(sacc, red[w]);
+    a.norm_partials[blockIdx.x] = sacc;
+    if (cta_bad) atomicAdd(a.flag_slot, 1.0f);
+    __threadfence();
+    const uint32_t ticket = atomicAdd(&a.st->done_ctas, 1u);
+    last_cta = (ticket == gridDim.x - 1);
+  }
+  asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+  if (!last_cta) return;
+  __shared__ double dred[kConsumerWarps];
+  if (tid == 0) __threadfence();
+  asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+  const double acc = sum_partials<kThreads>(a.norm_partials, gridDim.x, dred);
+  if (tid == 0) {
+    SamoStepState* stt = a.st;
+    stt->grad_norm = static_cast<float>(sqrt(acc));
+    if (*reinterpret_cast<volatile float*>(a.flag_slot) != 0.0f) {  // train.hpp:632-639
+      stt->skipped_steps += 1;
+      stt->last_skipped = 1u;
+    } else {  // AdamScalars::advance, train.hpp:325-329
+      stt->t += 1;
+      stt->beta1_pow = b1p;
+      stt->beta2_pow = b2p;
+      stt->last_skipped = 0u;
+    }
+    *a.flag_slot = 0.0f;
+    stt->done_ctas = 0u;
+    __threadfence();
+  }
+}
+
+// After K123: a no-op unless the step was skipped; then theta/m/v are copied
+// into the other buffer set (the host swaps the sets after every step) and
+// theta16 is rebuilt as expand(half(theta)) — the state before the step.
+__global__ void __launch_bounds__(kThreads) k123_repair(StepArgs a) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (*reinterpret_cast<volatile uint32_t*>(&a.st->last_skipped) == 0u) return;
+  for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+    const TileFull td = load_tile_full(a.tiles + t);
+    uint16_t* dst = a.theta16 + td.out_off;
+    for (uint32_t i = threadIdx.x; i < td.dense_count; i += blockDim.x) dst[i] = 0;
+    __syncthreads();
+    for (uint64_t k = td.k_begin + threadIdx.x; k < td.k_end; k += blockDim.x) {
+      const float th = a.theta[k];
+      a.theta_o[k] = th;
+      a.m_o[k] = a.m[k];
+      a.v_o[k] = a.v[k];
+      dst[a.off16[k]] = f32_to_f16_bits(th);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Sharded data-parallel step (ZeRO-1 on the compressed state): Adam on this
 // rank's shard of the reduce-scattered gradient, writing the updated weights
 // both as fp32 master copy and as compressed binary16 (theta16c) for the
@@ -1173,6 +1511,41 @@ int launch_update(const StepArgs& a, bool g_f32, int grid, cudaStream_t s) {
   };
   if (a.cfg) return g_f32 ? with_k23<false, true>(a.tile_elems, go) : with_k23<true, true>(a.tile_elems, go);
   return g_f32 ? with_k23<false, false>(a.tile_elems, go) : with_k23<true, false>(a.tile_elems, go);
+}
+
+// K123: 1024-element chunks, three stages when two CTAs still fit per SM.
+template <int CH, int NS>
+static size_t k123_smem(uint32_t tile_elems) {
+  return NS * K123Layout<CH>::kStage + kK123Tiles * (tile_elems * 2u + tile_elems / 8u);
+}
+
+template <bool CFG, typename F>
+static int with_k123(uint32_t tile_elems, F f) {
+  if (k123_smem<1024, 3>(tile_elems) <= 111u * 1024u)
+    return f(k123_step<1024, 3, CFG>, k123_smem<1024, 3>(tile_elems));
+  return f(k123_step<1024, 2, CFG>, k123_smem<1024, 2>(tile_elems));
+}
+
+int fused_grid(uint32_t tile_elems) {
+  return with_k123<false>(tile_elems, [](auto fn, size_t sm) { return grid_for(fn, sm, kThreads + 32); });
+}
+
+int launch_step_fused(const StepArgs& a, int grid, cudaStream_t s) {
+  if (a.ntiles == 0) return SAMO_OK;
+  if (grid <= 0) grid = fused_grid(a.tile_elems);
+  const char* e = getenv("SAMO_PDL");
+  const bool pdl = !(e && *e && atoi(e) == 0);
+  auto go = [&](auto fn, size_t sm) {
+    return launch_persistent(fn, a, sm, grid, s, kThreads + 32, "k123_step", pdl);
+  };
+  return a.cfg ? with_k123<true>(a.tile_elems, go) : with_k123<false>(a.tile_elems, go);
+}
+
+int launch_step_repair(const StepArgs& a, cudaStream_t s) {
+  if (a.ntiles == 0) return SAMO_OK;
+  const char* e = getenv("SAMO_PDL");
+  const bool pdl = !(e && *e && atoi(e) == 0);
+  return launch_persistent(k123_repair, a, 0, num_sms(), s, kThreads, "k123_repair", pdl);
 }
 
 template <int G>

@@ -73,7 +73,8 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   md->grid_update16 = step_grid(1, false, tile_elems);
   md->grid_update32 = step_grid(1, true, tile_elems);
   md->grid_expand = expand_grid(tile_elems);
-  const int max_grid = std::max(md->grid_update16, md->grid_update32);
+  md->grid_fused = fused_grid(tile_elems);
+  const int max_grid = std::max(std::max(md->grid_update16, md->grid_update32), md->grid_fused);
 
   // Carve one allocation.
   // +64 elements of slack: the update kernel's 16-byte aligned bulk loads may
@@ -87,6 +88,8 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
     return o;
   };
   const uint64_t o_theta = carve(n_al * 4), o_m = carve(n_al * 4), o_v = carve(n_al * 4);
+  // the fused step's second theta/m/v set (K123)
+  const uint64_t o_theta_b = carve(n_al * 4), o_m_b = carve(n_al * 4), o_v_b = carve(n_al * 4);
   // grad arena: n_al floats (the sharded exchange pads it to G * shard size,
   // G <= 128) + the skip-indicator slot at n_al + kFlagOff.
   const uint64_t o_g = carve((n_al + kArenaSlack) * 4), o_idx = carve(n_al * 4);
@@ -112,6 +115,9 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   md->theta = reinterpret_cast<float*>(b + o_theta);
   md->m = reinterpret_cast<float*>(b + o_m);
   md->v = reinterpret_cast<float*>(b + o_v);
+  md->theta_alt = reinterpret_cast<float*>(b + o_theta_b);
+  md->m_alt = reinterpret_cast<float*>(b + o_m_b);
+  md->v_alt = reinterpret_cast<float*>(b + o_v_b);
   md->g = reinterpret_cast<float*>(b + o_g);
   md->idx = reinterpret_cast<uint32_t*>(b + o_idx);
   md->off16 = reinterpret_cast<uint16_t*>(b + o_off);
@@ -175,7 +181,7 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
 
 int samo_model_destroy(samo_model* md) {
   if (!md) return clear_ok();
-  if (md->graph) cudaGraphExecDestroy(md->graph);
+  drop_graphs(md);
   close_peers(md);
   delete md->own_comm;
   if (md->capture_stream) cudaStreamDestroy(md->capture_stream);
@@ -268,10 +274,7 @@ int samo_model_finalize(samo_model* md, samo_stream_t stream) {
   }
   SAMO_CUDA_TRY(cudaStreamSynchronize(s));
   md->finalized = true;
-  if (md->graph) {
-    cudaGraphExecDestroy(md->graph);
-    md->graph = nullptr;
-  }
+  drop_graphs(md);
   return clear_ok();
 }
 
@@ -500,10 +503,46 @@ int samo_model_step_sunk(samo_model* md, samo_stream_t stream) {
   return clear_ok();
 }
 
+// The fused single-GPU step on `s`: K123 from the live theta/m/v set into the
+// other one, then the skip repair.  The caller swaps the sets once the work
+// is enqueued (not while capturing: a captured graph runs later).
+static int enqueue_fused(samo_model* md, cudaStream_t s) {
+  StepArgs a = step_args(md);
+  a.theta_o = md->theta_alt;
+  a.m_o = md->m_alt;
+  a.v_o = md->v_alt;
+  const int grid = std::min<int>(md->grid_fused, md->ntiles);
+  a.norm_count = static_cast<uint32_t>(grid);
+  SAMO_TRY(phase_mark(md, 0, s));
+  SAMO_TRY(launch_step_fused(a, grid, s));
+  SAMO_TRY(phase_mark(md, 1, s));
+  SAMO_TRY(launch_step_repair(a, s));
+  SAMO_TRY(phase_mark(md, 2, s));
+  if (md->phase_timing) md->phase_count = 2;
+  return SAMO_OK;
+}
+
+static void swap_sets(samo_model* md) {
+  if (md->graph) {  // a K1 | K23 graph captured the other set's pointers
+    cudaGraphExecDestroy(md->graph);
+    md->graph = nullptr;
+  }
+  std::swap(md->theta, md->theta_alt);
+  std::swap(md->m, md->m_alt);
+  std::swap(md->v, md->v_alt);
+  md->parity ^= 1;
+}
+
 int samo_model_step(samo_model* md, samo_stream_t stream) {
   SAMO_TRY(step_ready(md));
   if (!md->grads_set) return fail(SAMO_E_STATE, "optimizer_step requires backward (no gradients set)");
   SAMO_TRY(flush_cfg(md, as_stream(stream)));  // (never inside a capture: step_graph flushes first)
+  if (fused_step(md)) {
+    if (md->ntiles == 0) return clear_ok();
+    SAMO_TRY(enqueue_fused(md, as_stream(stream)));
+    if (!md->capturing) swap_sets(md);
+    return clear_ok();
+  }
   if (comm_size(md) > 1 && exchange_mode(md) == SAMO_EXCHANGE_P2P) {
     if (!md->p2p_ok) return fail(SAMO_E_STATE, "peer-to-peer exchange unavailable (IPC mapping failed)");
     SAMO_TRY(step_p2p(md, as_stream(stream)));
@@ -528,6 +567,40 @@ int samo_model_step_graph(samo_model* md, samo_stream_t stream) {
   if (!md->grads_set) return fail(SAMO_E_STATE, "optimizer_step requires backward (no gradients set)");
   cudaStream_t s = as_stream(stream);
   SAMO_TRY(flush_cfg(md, s));  // outside the graph: new scalars without a re-capture
+  if (fused_step(md)) {
+    // One graph per buffer parity: the step of parity p reads set p and
+    // writes set 1 - p.
+    if (md->ntiles == 0) return clear_ok();
+    cudaGraphExec_t& ge = md->fgraph[md->parity];
+    if (!ge) {
+      if (!md->capture_stream)
+        SAMO_CUDA_TRY(cudaStreamCreateWithFlags(&md->capture_stream, cudaStreamNonBlocking));
+      const uint64_t before = samo_kernel_launch_count();
+      SAMO_CUDA_TRY(cudaStreamBeginCapture(md->capture_stream, cudaStreamCaptureModeThreadLocal));
+      md->capturing = true;
+      int rc = enqueue_fused(md, md->capture_stream);
+      md->capturing = false;
+      cudaGraph_t graph = nullptr;
+      cudaError_t e = cudaStreamEndCapture(md->capture_stream, &graph);
+      if (rc != SAMO_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+      }
+      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+      e = cudaGraphInstantiate(&ge, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) {
+        ge = nullptr;
+        return cuda_fail(e, "cudaGraphInstantiate");
+      }
+      md->fgraph_kernels = samo_kernel_launch_count() - before;
+      unnote_launch(md->fgraph_kernels);  // captured, not launched
+    }
+    SAMO_CUDA_TRY(cudaGraphLaunch(ge, s));
+    note_launch(md->fgraph_kernels);
+    swap_sets(md);
+    return clear_ok();
+  }
   if (md->graph && md->graph_comm != md->comm) {
     cudaGraphExecDestroy(md->graph);
     md->graph = nullptr;
@@ -779,7 +852,7 @@ int samo_model_memory(const samo_model* md, samo_memory_report* out) {
   out->dense_params = phi;
   out->kept = n;
   out->theta16_bytes = md->d_tot * 2;
-  out->compressed_state_bytes = 4 * md->n_al * 4;          // theta32, m, v, grad
+  out->compressed_state_bytes = 7 * md->n_al * 4;          // theta32, m, v (x2: the fused step's two sets), grad
   out->index_bytes = md->n_al * (4 + 2);                    // u32 index set + off16
   out->table_bytes = static_cast<uint64_t>(md->ntiles) * sizeof(SamoTile);
   out->device_bytes = md->block_bytes;

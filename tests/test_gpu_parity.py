@@ -214,11 +214,15 @@ def _model_from_golden(S, g, tile_elems=0):
     return model, L
 
 
+@pytest.mark.parametrize("fused", ["1", "0"], ids=["K123", "K1+K23"])
 @pytest.mark.parametrize("graph", [False, True])
 @pytest.mark.parametrize("tile_elems", [0, 1024])
-def test_model_step_golden(S, golden, graph, tile_elems):
+def test_model_step_golden(S, golden, graph, tile_elems, fused, monkeypatch):
     """Five reference optimizer steps incl. one skipped on +inf: theta32/m/v/
-    theta16 bit-exact, skip counter exact, grad norm within rel 1e-5."""
+    theta16 bit-exact, skip counter exact, grad norm within rel 1e-5 — through
+    the fused single-GPU step (K123 + skip repair, speculative on the skip
+    flag) and through the K1 | K23 pair."""
+    monkeypatch.setenv("SAMO_FUSED_STEP", fused)
     g = golden("step")
     model, L = _model_from_golden(S, g, tile_elems)
     model.check_invariants()
@@ -275,9 +279,11 @@ def test_model_errors(S):
     m.close()
 
 
-def test_config1_fc4096_vs_oracle(S, oracle):
+@pytest.mark.parametrize("fused", ["1", "0"], ids=["K123", "K1+K23"])
+def test_config1_fc4096_vs_oracle(S, oracle, fused, monkeypatch):
     """BASELINE config 1: one 4096x4096 FC layer, init_params(seed 7), 90%
     magnitude mask, loss-scaled binary16 grads, three steps bit-exact."""
+    monkeypatch.setenv("SAMO_FUSED_STEP", fused)
     n = 4096 * 4096
     w = oracle.mt64_uniform(7, n, np.float32(1.0) / np.float32(64.0))  # 1/sqrt(4096)
     idx = oracle.magnitude_prune([w], [True], 0.9)[0]
@@ -323,12 +329,15 @@ def test_synth_matches_oracle(S, oracle):
     assert np.array_equal(h, oracle.synth_f16(0, 100_000, 3, 18, 2.0**-7, 1024.0))
 
 
+@pytest.mark.parametrize("fused", ["1", "0"], ids=["K123", "K1+K23"])
 @pytest.mark.parametrize("graph", [False, True])
-def test_model_step_empty_and_full_layers(S, oracle, graph):
+def test_model_step_empty_and_full_layers(S, oracle, graph, fused, monkeypatch):
     """Layers with no kept element (p = 1: unpruned_count = 0), every element
     kept (non-prunable / p = 0) and tiny odd sizes, stepped together through
-    K1 + K23 (empty tiles, tiles smaller than a chunk): bit-exact vs the
-    oracle's optimizer_step over two steps."""
+    K123 or K1 + K23 (empty tiles, tiles smaller than a chunk, an unstaged
+    tail of fewer than 8 elements): bit-exact vs the oracle's optimizer_step
+    over two steps."""
+    monkeypatch.setenv("SAMO_FUSED_STEP", fused)
     from oracle.oracle import Cfg, StepState
     dense_len = [5000, 7, 3 * 8192 + 3, 1, 40000]
     rng = np.random.default_rng(21)
@@ -398,3 +407,34 @@ def test_graph_follows_lr_schedule(S, golden):
         assert torch.equal(eager.read(l, "theta16"), graph.read(l, "theta16"))
     a, b = eager.step_record(), graph.step_record()
     assert (a.t, a.skipped_steps, a.beta1_pow) == (b.t, b.skipped_steps, b.beta1_pow)
+
+
+def test_fused_and_split_steps_interleave(S, golden, monkeypatch):
+    """The fused step swaps the model's two theta/m/v buffer sets after every
+    step; eager fused steps, captured fused steps of both parities, K1 | K23
+    steps, the staged gather/update calls and a backward sink + step_sunk
+    interleaved must equal the reference's five steps bit for bit (the skip
+    at step 2 included)."""
+    g = golden("step")
+    model, L = _model_from_golden(S, g, 1024)
+    plan = [("1", True), ("1", False), ("0", False), ("1", True), ("staged", False)]
+    for s in range(int(g["steps"][0])):
+        mode, graph = plan[s]
+        grads = [T(g[f"s{s}_grad{l}"]) for l in range(L)]
+        if mode == "staged":
+            monkeypatch.setenv("SAMO_FUSED_STEP", "1")
+            for l in reversed(range(L)):
+                model.sink_dense(l, grads[l])
+            model.step_sunk()
+        else:
+            monkeypatch.setenv("SAMO_FUSED_STEP", mode)
+            model.set_grads(grads)
+            model.step(graph=graph)
+        for l in range(L):
+            for k in ("theta32", "adam_m", "adam_v"):
+                assert np.array_equal(N(model.read(l, k), np.uint32), bits(g[f"s{s}_{k}{l}"])), (s, l, k)
+            assert np.array_equal(N(model.read(l, "theta16"), np.uint16), g[f"s{s}_theta16{l}"]), (s, l)
+    rec = model.step_record()
+    assert rec.skipped_steps == int(g[f"s{int(g['steps'][0]) - 1}_skipped"][0])
+    model.check_invariants()
+    model.close()
