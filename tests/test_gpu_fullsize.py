@@ -1,17 +1,25 @@
-"""GPU: the headline configuration at full size (GPT-2.7B set, p = 0.9, 388
-tensors, 2.65e9 parameters), through size-independent properties and
-sampled bit-exact layers (the oracle cannot run the whole model in a test):
+"""GPU: the headline configuration (GPT-2.7B set, p = 0.9, 388 tensors,
+2.65e9 parameters) and BASELINE config 3 (GPT-1.3B set, p = 0.8 / 0.95, 292
+tensors) at full size, EVERY tensor compared bit for bit with the oracle:
 
-* K0: every layer keeps exactly unpruned_count(p, n) indices (prune.hpp:76-79),
-  non-prunable layers keep all; sampled layers equal the oracle's mask;
-* two full device steps, then check_state_invariants over the whole model
-  (theta16 == expand(half(theta32)), zeros at every pruned position);
-* sampled layers (smallest, an attention projection, an MLP matrix) equal the
-  oracle's optimizer_step bit for bit after both steps;
-* the recorded grad norm equals an independent fp64 norm of all 2.66e8
-  kept gradients (rel 1e-5).
+* K0: every layer's kept index set equals the oracle's magnitude_prune
+  (prune.hpp:99-170, per-layer scope) on the same synthetic weights;
+* four device steps through the production single-GPU step (K123, eager then
+  graph): two finite steps, a step whose gradients hold +inf at one kept
+  element of one layer (global skip, train.hpp:632-639 -> K123's speculative
+  buffers are dropped and the skip-repair kernel restores theta16), then one
+  more finite step;
+* after them every layer's theta32 / adam_m / adam_v / theta16 equals the
+  oracle's optimizer_step (train.hpp:617-656) replayed on that layer, bit for
+  bit; the oracle runs one layer per host thread (ctypes releases the GIL);
+* check_state_invariants over the whole model, step counters (t = 3,
+  skipped = 1), and the recorded grad norm of step 1 against an independent
+  fp64 norm of all kept gradients (rel 1e-5).
 """
 from __future__ import annotations
+
+import os
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 import pytest
@@ -20,34 +28,57 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 SEED = 3
+F16_INF = 0x7C00
 
 
 def _bits32(t):
     return t.cpu().numpy().view(np.uint32)
 
 
-def test_gpt_2_7b_fullsize(cuda, oracle):
-    from paper_2302_05045_b200 import samo, workloads
+def _grad_sid(step: int, layer: int) -> int:
+    return 100 * step + layer
+
+
+def _oracle_layer(oracle, i, n, prunable, bound, sparsity, dev, steps, skip_step):
+    """Replays layer i on the CPU oracle; returns the names of mismatches."""
     from oracle.oracle import Cfg, StepState
-    wl = workloads.get("gpt-2.7b", 0.9)
-    assert len(wl.tensors) == 388
+    vals = oracle.synth_f32(0, n, SEED, 2 * i, bound)
+    idx = oracle.magnitude_prune([vals], [prunable], sparsity)[0]
+    bad = []
+    if not np.array_equal(dev["idx"], idx):
+        return ["mask"]
+    theta = oracle.compress(vals, idx)
+    del vals
+    m, v, g32 = (np.zeros_like(theta) for _ in range(3))
+    t16 = [np.zeros(n, np.uint16)]
+    cfg, st = Cfg(), StepState()
+    for s in range(steps):
+        gh = oracle.synth_f16(0, n, SEED + 1, _grad_sid(s, i), 2.0**-7, 1024.0)
+        if s == skip_step:
+            if idx.size == 0:
+                continue  # an empty layer sees no gradient; the global skip leaves it as is
+            gh[idx[0]] = F16_INF  # every layer skips, as the global flag makes the device do
+        oracle.optimizer_step([n], [idx.size], idx, [gh], theta, m, v, g32, t16, cfg, st)
+    if idx.size and (st.t, st.skipped) != (steps - 1, 1):
+        bad.append("counters")
+    for name, want in (("theta32", theta.view(np.uint32)), ("adam_m", m.view(np.uint32)),
+                       ("adam_v", v.view(np.uint32)), ("theta16", t16[0])):
+        if not np.array_equal(dev[name], want):
+            bad.append(name)
+    return bad
+
+
+@pytest.mark.parametrize("name,p", [("gpt-2.7b", 0.9), ("gpt-1.3b", 0.8), ("gpt-1.3b", 0.95)])
+def test_gpt_fullsize_every_tensor(cuda, oracle, name, p):
+    from paper_2302_05045_b200 import samo, workloads
+    wl = workloads.get(name, p)
+    assert len(wl.tensors) == {"gpt-2.7b": 388, "gpt-1.3b": 292}[name]
     vals = [samo.synth_uniform_f32(t.numel, SEED, 2 * i, t.init_bound) for i, t in enumerate(wl.tensors)]
     sets = samo.magnitude_prune([samo.LayerParams(t.name, v, t.prunable) for t, v in zip(wl.tensors, vals)],
                                 wl.sparsity)
     for t, s in zip(wl.tensors, sets):
         want = oracle.unpruned_count(wl.sparsity, t.numel) if t.prunable else t.numel
         assert s.count() == want, t.name
-    # sampled layers: the smallest, an attention projection, an MLP matrix
-    numel = [t.numel for t in wl.tensors]
-    small = int(np.argmin(numel))
-    attn = next(i for i, t in enumerate(wl.tensors) if t.prunable and t.shape == (2560, 2560))
-    mlp = next(i for i, t in enumerate(wl.tensors) if t.prunable and t.shape == (2560, 10240))
-    sample = [small, attn, mlp]
-    host_vals = {i: vals[i].cpu().numpy() for i in sample}
-    for i in sample:
-        want = oracle.magnitude_prune([host_vals[i]], [wl.tensors[i].prunable], wl.sparsity)[0]
-        assert np.array_equal(sets[i].indices.cpu().numpy().view(np.uint32), want), wl.tensors[i].name
-
     model = samo.SamoModel.from_index_sets(sets, [t.shape for t in wl.tensors], 0)
     for l, v in enumerate(vals):
         model.init_layer(l, v)
@@ -55,41 +86,48 @@ def test_gpt_2_7b_fullsize(cuda, oracle):
     del vals
     torch.cuda.empty_cache()
 
-    grads = [None] * len(wl.tensors)
+    steps, skip_step, inf_layer = 4, 2, len(wl.tensors) // 2
     kept_sq = torch.zeros((), dtype=torch.float64, device="cuda")
-    for s in range(2):
-        for i, t in enumerate(wl.tensors):
-            grads[i] = samo.synth_uniform_f16(t.numel, SEED + 1, 100 * s + i, 2.0**-7, 1024.0)
+    for s in range(steps):
+        grads = [samo.synth_uniform_f16(t.numel, SEED + 1, _grad_sid(s, i), 2.0**-7, 1024.0)
+                 for i, t in enumerate(wl.tensors)]
+        if s == skip_step:
+            k = int(sets[inf_layer].as_int64()[0])
+            grads[inf_layer].view(torch.int16)[k] = F16_INF
         model.set_grads(grads)
-        model.step(graph=(s == 1))
+        model.step(graph=(s >= 1))
         if s == 1:  # independent fp64 norm of the unscaled kept gradients
             for i in range(len(wl.tensors)):
-                g = grads[i][sets[i].indices.long()].double() / 1024.0
+                g = grads[i][sets[i].as_int64()].double() / 1024.0
                 kept_sq += (g * g).sum()
+            torch.cuda.synchronize()
+            rec = model.step_record()
+            exact = float(kept_sq.sqrt())
+            assert abs(rec.grad_norm - exact) <= 1e-5 * exact
+        del grads
     torch.cuda.synchronize()
     model.check_invariants()
     rec = model.step_record()
-    assert rec.t == 2 and rec.skipped_steps == 0
-    exact = float(kept_sq.sqrt())
-    assert abs(rec.grad_norm - exact) <= 1e-5 * exact
+    assert rec.t == steps - 1 and rec.skipped_steps == 1
 
-    cfg, st = Cfg(), StepState()
-    for i in sample:
-        idx = sets[i].indices.cpu().numpy().view(np.uint32)
-        n = wl.tensors[i].numel
-        theta = oracle.compress(host_vals[i], idx)
-        m, v, g32 = (np.zeros_like(theta) for _ in range(3))
-        t16 = [np.zeros(n, np.uint16)]
-        st = StepState()
-        for s in range(2):
-            gh = oracle.synth_f16(0, n, SEED + 1, 100 * s + i, 2.0**-7, 1024.0)
-            oracle.optimizer_step([n], [idx.size], idx, [gh], theta, m, v, g32, t16, cfg, st)
-        name = wl.tensors[i].name
-        assert np.array_equal(_bits32(model.read(i, "theta32")), theta.view(np.uint32)), name
-        assert np.array_equal(_bits32(model.read(i, "adam_m")), m.view(np.uint32)), name
-        assert np.array_equal(_bits32(model.read(i, "adam_v")), v.view(np.uint32)), name
-        assert np.array_equal(model.read(i, "theta16").reshape(-1).cpu().numpy().view(np.uint16), t16[0]), name
+    workers = max(1, min(32, os.cpu_count() or 1))
+    failures, pending = [], []
+    with ThreadPoolExecutor(workers) as pool:
+        for i, t in enumerate(wl.tensors):
+            dev = {"idx": sets[i].indices.cpu().numpy().view(np.uint32),
+                   "theta32": _bits32(model.read(i, "theta32")),
+                   "adam_m": _bits32(model.read(i, "adam_m")),
+                   "adam_v": _bits32(model.read(i, "adam_v")),
+                   "theta16": model.read(i, "theta16").reshape(-1).cpu().numpy().view(np.uint16)}
+            pending.append((t.name, pool.submit(_oracle_layer, oracle, i, t.numel, t.prunable,
+                                                t.init_bound, wl.sparsity, dev, steps, skip_step)))
+            while len(pending) > 2 * workers:  # bound the host copies in flight
+                nm, f = pending.pop(0)
+                failures += [f"{nm}:{b}" for b in f.result()]
+        for nm, f in pending:
+            failures += [f"{nm}:{b}" for b in f.result()]
     model.close()
+    assert not failures, failures[:20]
 
 
 def test_max_layer_size(cuda, oracle):
