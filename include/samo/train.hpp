@@ -1,0 +1,4 @@
+// Forwarding header: the reference name samo/train.hpp resolves to the
+// CUDA-backed mirror (include/samo_b200/samo.hpp).
+#pragma once
+#include "samo_b200/samo.hpp"

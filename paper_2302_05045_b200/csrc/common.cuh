@@ -296,7 +296,7 @@ struct SamoStepState {
   float grad_norm;
   uint32_t last_skipped;
   uint32_t done_ctas;  // arrival counter for the last-CTA finalisation
-  uint32_t pad_;
+  uint32_t tile_next;  // K123's dynamic tile claims (rewound by its last CTA)
 };
 
 struct SamoAdamParams {

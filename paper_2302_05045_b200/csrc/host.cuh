@@ -83,6 +83,8 @@ struct samo_model {
   uint64_t* k_off_dev = nullptr;
   SamoStepState* st = nullptr;
   float* norm_partials = nullptr;
+  float* tile_norm = nullptr;         // K123: per-tile grad-norm partials
+  double* norm_dpartials = nullptr;   // k123_repair: per-CTA sums of them
   std::vector<SamoLayerDev> layers_host;
   std::vector<SamoTile> tiles_host;
   samo_optimizer_config cfg{};
@@ -186,7 +188,9 @@ inline void drop_graphs(samo_model* md) {
 
 // The fused single-GPU step (K123) is the default without a communicator;
 // SAMO_FUSED_STEP=0 selects the K1 | K23 pair.
-inline bool fused_step(const samo_model* md) { return comm_size(md) <= 1 && env_int("SAMO_FUSED_STEP", 1) != 0; }
+inline bool fused_step(const samo_model* md) {
+  return comm_size(md) <= 1 && md->grid_fused > 0 && env_int("SAMO_FUSED_STEP", 1) != 0;
+}
 
 inline int step_ready(samo_model* md) {
   if (!md) return fail(SAMO_E_PARAMETER, "null model");

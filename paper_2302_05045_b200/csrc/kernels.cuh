@@ -56,6 +56,8 @@ struct StepArgs {
   SamoStepState* st;
   float* flag_slot;            // non-finite indicator (summed across ranks)
   float* norm_partials;        // this launch's per-CTA grad-norm partials
+  float* tile_norm;            // K123: one grad-norm partial per tile
+  double* norm_dpartials;      // k123_repair: one per CTA
   const float* norm_all;       // every partial of the step (read when finalize)
   uint32_t norm_count;
   uint32_t finalize;           // 1 on the step's last update launch

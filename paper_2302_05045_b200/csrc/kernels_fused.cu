@@ -585,18 +585,27 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
 // rebuilds theta16 from theta — theta16 == expand(half(theta32)) is the
 // state invariant (store.hpp:171-197), so the repair restores it bit for bit.
 //
-// Per tile: the producer warp brings the dense binary16 gradient tile into
-// shared memory with one 1-D TMA copy (two tiles in flight), and theta/m/v/
-// off16 of the tile's kept range in <= CH-element chunks (NS-stage ring).
-// Consumers gather g = half(grad[off]) * 2^-s through off16, run the IEEE
-// Adam, store theta/m/v with streaming stores, and write half(theta) back
-// into the gradient tile at the same offset (each offset belongs to one kept
-// element, so no other element's gradient is overwritten), marking it in a
-// per-tile bitmap.  The copy-out writes the tile to theta16 with 128-bit
-// stores, zeroing the positions the bitmap does not mark (the pruned ones),
-// and clears the bitmap.  HBM bytes per step: 2 phi (grad) + 2 n (off16) +
-// 24 n (theta/m/v read + write) + 2 phi (theta16) = 4 phi + 26 n, against
-// 4 phi + 32 n for K1 + K23 (grad16 written and read back, off16 read twice).
+// Scheduling: tiles are claimed dynamically (one atomic per tile by the
+// producer lane), so SMs that run faster take more tiles; the producer hands
+// each claimed tile's descriptor to the consumers through shared memory.
+// Per tile: one 1-D TMA copy of the dense binary16 gradient tile into one of
+// NSG slots, then theta/m/v/off16 of the tile's kept range in <= CH-element
+// chunks (NS-stage ring).  Consumers gather g = half(grad[off]) * 2^-s
+// through off16, run the IEEE Adam, store theta/m/v with streaming stores,
+// and write half(theta) back into the gradient tile at the same offset (each
+// offset belongs to one kept element), marking it in a per-slot bitmap.
+// Each warp signals the slot's `done` barrier when its share of the tile is
+// computed and copies the tile out one tile LATER (after computing the next
+// one), so no warp waits for the slowest warp of a tile: 128-bit stores to
+// theta16, pruned positions zeroed by the bitmap, bitmap cleared.
+//
+// Grad norm: one partial per tile (lanes in element order, warps in order)
+// into tile_norm[t]; k123_repair sums them in tile order, so the norm does
+// not depend on which CTA took which tile.
+//
+// HBM bytes per step: 2 phi (grad) + 2 n (off16) + 24 n (theta/m/v read +
+// write) + 2 phi (theta16) = 4 phi + 26 n, against 4 phi + 32 n for K1 + K23
+// (grad16 written and read back, off16 read twice).
 
 struct TileFull {
   uint32_t layer, dense_begin, dense_count;
@@ -616,6 +625,15 @@ __device__ __forceinline__ TileFull load_tile_full(const SamoTile* p) {
   return r;
 }
 
+// A claimed tile as the producer hands it to the consumers.
+struct K123Slot {
+  uint64_t k_begin, k_end, out_off;
+  const uint16_t* grad;  // the layer's dense gradient at the tile's first element
+  uint32_t t;            // tile id, kNoTile once the tiles are exhausted
+  uint32_t dense_count;
+};
+constexpr uint32_t kNoTile = 0xFFFFFFFFu;
+
 template <int CH>
 struct K123Layout {
   static constexpr uint32_t kF32 = (CH + 8) * 4;   // theta / m / v slot
@@ -623,24 +641,30 @@ struct K123Layout {
   static constexpr uint32_t kStage = 3 * kF32 + kOff;
   static_assert(kStage % 16 == 0, "stages stay 16-byte aligned");
 };
-constexpr int kK123Tiles = 2;  // dense gradient tiles in flight per CTA
+// Dense gradient slots per CTA: one being computed and copied out, one being
+// filled.  (A deferred copy-out — each warp copying tile j out after
+// computing tile j + 1, no consumer barrier — needs a third slot; it measured
+// 25% slower at 16384-element tiles (one CTA per SM) and level at 8192, both
+// behind this form: tools/sweep_k123.sh, profiles/r02d_k123_sweep.jsonl.)
+constexpr int kK123Slots = 2;
 
 // Lane masks of 8 binary16 values from 8 bitmap bits (bit e -> lane e).
 __device__ __forceinline__ uint32_t lane_mask2(uint32_t bits, int e) {
   return ((0u - ((bits >> (2 * e)) & 1u)) & 0x0000FFFFu) | ((0u - ((bits >> (2 * e + 1)) & 1u)) & 0xFFFF0000u);
 }
 
-template <int CH, int NS, bool CFG>
-__global__ void __launch_bounds__(kThreads + 32) k123_step(StepArgs a) {
+template <int CH, int NS, int NT, bool CFG>
+__global__ void __launch_bounds__(NT + 32) k123_step(StepArgs a) {
   using L = K123Layout<CH>;
-  constexpr uint32_t kConsumerWarps = kThreads / 32;
-  constexpr int NSG = kK123Tiles;
+  constexpr uint32_t kConsumerWarps = NT / 32;
+  constexpr int NSG = kK123Slots;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[NS];
   __shared__ __align__(8) uint64_t empty[NS];
   __shared__ __align__(8) uint64_t gfull[NSG];
   __shared__ __align__(8) uint64_t gempty[NSG];
-  __shared__ float red[kConsumerWarps];
+  __shared__ __align__(16) K123Slot slot[NSG];
+  __shared__ float red[NSG][kConsumerWarps];
   __shared__ int last_cta;
   __shared__ int cta_bad;
 
@@ -667,20 +691,36 @@ __global__ void __launch_bounds__(kThreads + 32) k123_step(StepArgs a) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == kConsumerWarps) {
-    // ---- producer warp (one elected lane): per tile, the dense gradient
-    // tile, then theta/m/v/off16 of its kept range chunk by chunk.
+    // ---- producer warp (one elected lane): claim a tile, publish its
+    // descriptor, bring its dense gradient tile, then theta/m/v/off16 of its
+    // kept range chunk by chunk.  The next claim is issued a tile ahead.
     if (lane == 0) {
       const uint64_t policy = policy_evict_first();
-      uint32_t it = 0, tt = 0;
-      for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++tt) {
-        const TileFull td = load_tile_full(a.tiles + t);
+      uint32_t it = 0;
+      uint32_t t = atomicAdd(&a.st->tile_next, 1u);
+      for (uint32_t tt = 0;; ++tt) {
         const int sg = static_cast<int>(tt % NSG);
         if (tt >= static_cast<uint32_t>(NSG)) mbar_wait(&gempty[sg], ((tt / NSG) - 1) & 1u);
+        K123Slot& sl = slot[sg];
+        if (t >= a.ntiles) {
+          sl.t = kNoTile;
+          mbar_arrive(&gfull[sg]);
+          break;
+        }
+        const TileFull td = load_tile_full(a.tiles + t);
+        const uint16_t* grad = a.layers[td.layer].grad + td.dense_begin;
+        const uint32_t t_cur = t;
+        t = atomicAdd(&a.st->tile_next, 1u);
+        sl.k_begin = td.k_begin;
+        sl.k_end = td.k_end;
+        sl.out_off = td.out_off;
+        sl.grad = grad;
+        sl.t = t_cur;
+        sl.dense_count = td.dense_count;
         const uint32_t bytes = (td.dense_count * 2u) & ~15u;
         if (bytes) {
           mbar_arrive_expect_tx(&gfull[sg], bytes);
-          bulk_g2s(gst + static_cast<size_t>(sg) * T * 2u, a.layers[td.layer].grad + td.dense_begin, bytes,
-                   &gfull[sg], policy);
+          bulk_g2s(gst + static_cast<size_t>(sg) * T * 2u, grad, bytes, &gfull[sg], policy);
         } else {
           mbar_arrive(&gfull[sg]);
         }
@@ -729,23 +769,81 @@ __global__ void __launch_bounds__(kThreads + 32) k123_step(StepArgs a) {
   float* const p_vo = pin_ptr(a.v_o);
   uint16_t* const p_t16 = pin_ptr(a.theta16);
 
-  float nacc = 0.0f;
+  // Copy-out of this CTA's j-th claimed tile, once every warp has computed
+  // its share.
+  auto copy_out = [&](uint32_t j) {
+    const int sg = static_cast<int>(j % NSG);
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+    const K123Slot& sl = slot[sg];
+    const uint32_t dense_count = sl.dense_count;
+    const uint4* o4 = reinterpret_cast<const uint4*>(gst + static_cast<size_t>(sg) * T * 2u);
+    const uint16_t* o2 = reinterpret_cast<const uint16_t*>(o4);
+    uint8_t* b8 = reinterpret_cast<uint8_t*>(bm0 + sg * (T / 32u));
+    uint16_t* dst = p_t16 + sl.out_off;
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    const uint32_t full16 = dense_count >> 3;
+    for (uint32_t i0 = tid; i0 < full16; i0 += 4 * NT) {
+      uint4 v[4];
+      uint32_t bits[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t i = i0 + u * NT;
+        if (i < full16) {
+          v[u] = o4[i];
+          bits[u] = b8[i];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t i = i0 + u * NT;
+        if (i < full16) {
+          uint4 w = v[u];
+          w.x &= lane_mask2(bits[u], 0);
+          w.y &= lane_mask2(bits[u], 1);
+          w.z &= lane_mask2(bits[u], 2);
+          w.w &= lane_mask2(bits[u], 3);
+          if (bits[u]) b8[i] = 0;
+          st_na_v4u(d4 + i, w.x, w.y, w.z, w.w);
+        }
+      }
+    }
+    if (tid == 0) {
+      if (dense_count & 7u) {
+        const uint32_t base = full16 * 8u;
+        const uint32_t bits = b8[full16];
+        for (uint32_t e = 0; e < (dense_count & 7u); ++e) dst[base + e] = ((bits >> e) & 1u) ? o2[base + e] : 0;
+        b8[full16] = 0;
+      }
+      float s = 0.f;  // the tile's grad-norm partial, warps in order
+      for (uint32_t w = 0; w < kConsumerWarps; ++w) s = __fadd_rn(s, red[sg][w]);
+      a.tile_norm[sl.t] = s;
+    }
+    // The next TMA copy into this slot follows generic-proxy writes.
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&gempty[sg]);
+  };
+
   bool bad = false;
   uint32_t it = 0, tt = 0;
-  for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++tt) {
-    const TileFull td = load_tile_full(a.tiles + t);
+  for (;; ++tt) {
     const int sg = static_cast<int>(tt % NSG);
+    mbar_wait(&gfull[sg], (tt / NSG) & 1u);
+    const K123Slot& sl = slot[sg];
+    const uint32_t t = sl.t;
+    if (t == kNoTile) break;
+    const uint64_t k_begin = sl.k_begin, k_end = sl.k_end;
     uint16_t* const sgr = reinterpret_cast<uint16_t*>(gst + static_cast<size_t>(sg) * T * 2u);
     uint32_t* const bm = bm0 + sg * (T / 32u);
-    const uint32_t staged = ((td.dense_count * 2u) & ~15u) >> 1;
-    const uint16_t* const gsrc = a.layers[td.layer].grad + td.dense_begin;  // unstaged tail (< 8 elements)
-    const uint32_t nch = tile_chunks<CH>(td.k_begin, td.k_end);
-    mbar_wait(&gfull[sg], (tt / NSG) & 1u);
+    const uint32_t staged = ((sl.dense_count * 2u) & ~15u) >> 1;
+    const uint16_t* const gsrc = sl.grad;  // unstaged tail (< 8 elements)
+    const uint32_t nch = tile_chunks<CH>(k_begin, k_end);
+    float nacc = 0.0f;
     for (uint32_t j = 0; j < nch; ++j, ++it) {
       const int s = static_cast<int>(it % NS);
       const uint8_t* st = smem + s * L::kStage;
-      const uint64_t kc0 = td.k_begin + static_cast<uint64_t>(j) * CH;
-      const uint64_t kc1 = min(td.k_end, kc0 + CH);
+      const uint64_t kc0 = k_begin + static_cast<uint64_t>(j) * CH;
+      const uint64_t kc1 = min(k_end, kc0 + CH);
       const uint32_t n = static_cast<uint32_t>(kc1 - kc0);
       const uint32_t fo = static_cast<uint32_t>(kc0 & 3ull);
       const uint32_t ho = static_cast<uint32_t>(kc0 & 7ull);
@@ -755,12 +853,12 @@ __global__ void __launch_bounds__(kThreads + 32) k123_step(StepArgs a) {
       const uint16_t* soff = reinterpret_cast<const uint16_t*>(st + 3 * L::kF32) + ho;
       mbar_wait(&full[s], (it / NS) & 1u);
 #pragma unroll 1
-      for (uint32_t ib = tid; ib < n; ib += kU * kThreads) {
+      for (uint32_t ib = tid; ib < n; ib += kU * NT) {
         float gv[kU], tv[kU], mv[kU], vv[kU];
         uint32_t ov[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-          const uint32_t i = ib + u * kThreads;
+          const uint32_t i = ib + u * NT;
           if (i < n) {
             ov[u] = soff[i];
             const uint16_t h = ov[u] < staged ? sgr[ov[u]] : gsrc[ov[u]];
@@ -773,7 +871,7 @@ __global__ void __launch_bounds__(kThreads + 32) k123_step(StepArgs a) {
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-          const uint32_t i = ib + u * kThreads;
+          const uint32_t i = ib + u * NT;
           if (i < n) {
             const float gk = gv[u];
             nacc = __fadd_rn(nacc, __fmul_rn(gk, gk));
@@ -796,103 +894,83 @@ __global__ void __launch_bounds__(kThreads + 32) k123_step(StepArgs a) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    // Every consumer warp has written its weights into the tile.
-    asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
-    // Copy-out: 128-bit stores of the tile, pruned positions zeroed by the
-    // bitmap (layer segments are 256-byte aligned, tiles start at multiples
-    // of T); each thread clears the bitmap bytes it read.
-    {
-      const uint4* o4 = reinterpret_cast<const uint4*>(sgr);
-      uint8_t* b8 = reinterpret_cast<uint8_t*>(bm);
-      uint16_t* dst = p_t16 + td.out_off;
-      uint4* d4 = reinterpret_cast<uint4*>(dst);
-      const uint32_t full16 = td.dense_count >> 3;
-      for (uint32_t i0 = tid; i0 < full16; i0 += 4 * kThreads) {
-        uint4 v[4];
-        uint32_t bits[4];
+    // This warp's share of the tile is computed: its norm partial, then the
+    // slot's done barrier; the copy-out of the PREVIOUS tile follows.
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t i = i0 + u * kThreads;
-          if (i < full16) {
-            v[u] = o4[i];
-            bits[u] = b8[i];
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t i = i0 + u * kThreads;
-          if (i < full16) {
-            uint4 w = v[u];
-            w.x &= lane_mask2(bits[u], 0);
-            w.y &= lane_mask2(bits[u], 1);
-            w.z &= lane_mask2(bits[u], 2);
-            w.w &= lane_mask2(bits[u], 3);
-            if (bits[u]) b8[i] = 0;
-            st_na_v4u(d4 + i, w.x, w.y, w.z, w.w);
-          }
-        }
-      }
-      if (tid == 0 && (td.dense_count & 7u)) {
-        const uint32_t base = full16 * 8u;
-        const uint32_t bits = b8[full16];
-        for (uint32_t e = 0; e < (td.dense_count & 7u); ++e) dst[base + e] = ((bits >> e) & 1u) ? sgr[base + e] : 0;
-        b8[full16] = 0;
-      }
-    }
-    // The next TMA copy into this tile's buffer follows generic-proxy writes.
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&gempty[sg]);
+    for (int o = 16; o > 0; o >>= 1) nacc = __fadd_rn(nacc, __shfl_xor_sync(0xFFFFFFFFu, nacc, o));
+    if (lane == 0) red[sg][warp] = nacc;
+    copy_out(tt);
   }
   // The repair kernel may start its (waiting) CTAs now.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
-  // Grad norm partial and skip indicator per CTA; the last CTA finalises.
-  float x = nacc;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x = __fadd_rn(x, __shfl_xor_sync(0xFFFFFFFFu, x, o));
-  if (lane == 0) red[warp] = x;
+  // Skip indicator per CTA; the last CTA decides the step.
   if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicOr(&cta_bad, 1);
-  asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
   if (tid == 0) {
-    float sacc = 0.f;
-    for (uint32_t w = 0; w < kConsumerWarps; ++w) sacc = __fadd_rn(sacc, red[w]);
-    a.norm_partials[blockIdx.x] = sacc;
     if (cta_bad) atomicAdd(a.flag_slot, 1.0f);
     __threadfence();
     const uint32_t ticket = atomicAdd(&a.st->done_ctas, 1u);
     last_cta = (ticket == gridDim.x - 1);
   }
-  asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
-  if (!last_cta) return;
-  __shared__ double dred[kConsumerWarps];
-  if (tid == 0) __threadfence();
-  asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");
-  const double acc = sum_partials<kThreads>(a.norm_partials, gridDim.x, dred);
-  if (tid == 0) {
-    SamoStepState* stt = a.st;
-    stt->grad_norm = static_cast<float>(sqrt(acc));
-    if (*reinterpret_cast<volatile float*>(a.flag_slot) != 0.0f) {  // train.hpp:632-639
-      stt->skipped_steps += 1;
-      stt->last_skipped = 1u;
-    } else {  // AdamScalars::advance, train.hpp:325-329
-      stt->t += 1;
-      stt->beta1_pow = b1p;
-      stt->beta2_pow = b2p;
-      stt->last_skipped = 0u;
-    }
-    *a.flag_slot = 0.0f;
-    stt->done_ctas = 0u;
-    __threadfence();
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+  if (!last_cta || tid != 0) return;
+  __threadfence();
+  SamoStepState* stt = a.st;
+  if (*reinterpret_cast<volatile float*>(a.flag_slot) != 0.0f) {  // train.hpp:632-639
+    stt->skipped_steps += 1;
+    stt->last_skipped = 1u;
+  } else {  // AdamScalars::advance, train.hpp:325-329
+    stt->t += 1;
+    stt->beta1_pow = b1p;
+    stt->beta2_pow = b2p;
+    stt->last_skipped = 0u;
   }
+  *a.flag_slot = 0.0f;
+  // Every producer has made its last claim (its consumers saw kNoTile before
+  // their CTA took a ticket), so the claim counter can be rewound.
+  stt->tile_next = 0u;
+  stt->done_ctas = 0u;
+  __threadfence();
 }
 
-// After K123: a no-op unless the step was skipped; then theta/m/v are copied
-// into the other buffer set (the host swaps the sets after every step) and
-// theta16 is rebuilt as expand(half(theta)) — the state before the step.
+// After K123: the grad norm from the per-tile partials (train.hpp:627-630;
+// fixed order: tile ranges per CTA, CTAs in order), then — only if the step
+// was skipped — theta/m/v are copied into the other buffer set (the host
+// swaps the sets after every step) and theta16 is rebuilt as
+// expand(half(theta)), the state before the step.
 __global__ void __launch_bounds__(kThreads) k123_repair(StepArgs a) {
+  __shared__ double dred[kThreads / 32];
+  __shared__ int last_cta;
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const uint32_t tid = threadIdx.x;
+  {
+    const uint32_t per = (a.ntiles + gridDim.x - 1) / gridDim.x;
+    const uint32_t t0 = min(a.ntiles, blockIdx.x * per), t1 = min(a.ntiles, t0 + per);
+    double acc = 0.0;
+    for (uint32_t t = t0 + tid; t < t1; t += kThreads) acc += static_cast<double>(__ldcg(a.tile_norm + t));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+    if ((tid & 31) == 0) dred[tid >> 5] = acc;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < kThreads / 32; ++w) s += dred[w];
+      a.norm_dpartials[blockIdx.x] = s;
+      __threadfence();
+      last_cta = (atomicAdd(&a.st->done_ctas, 1u) == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last_cta && tid == 0) {
+      __threadfence();
+      double s = 0.0;
+      for (uint32_t b = 0; b < gridDim.x; ++b) s += __ldcg(a.norm_dpartials + b);
+      a.st->grad_norm = static_cast<float>(sqrt(s));
+      a.st->done_ctas = 0u;
+      __threadfence();
+    }
+  }
   if (*reinterpret_cast<volatile uint32_t*>(&a.st->last_skipped) == 0u) return;
   for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
     const TileFull td = load_tile_full(a.tiles + t);
@@ -1516,27 +1594,35 @@ int launch_update(const StepArgs& a, bool g_f32, int grid, cudaStream_t s) {
 // K123: 1024-element chunks, three stages when two CTAs still fit per SM.
 template <int CH, int NS>
 static size_t k123_smem(uint32_t tile_elems) {
-  return NS * K123Layout<CH>::kStage + kK123Tiles * (tile_elems * 2u + tile_elems / 8u);
+  return NS * K123Layout<CH>::kStage + kK123Slots * (tile_elems * 2u + tile_elems / 8u);
 }
+constexpr size_t kSmemTwoPerSM = 111u * 1024u, kSmemOnePerSM = 225u * 1024u;
 
+// Two CTAs of 256 consumer threads per SM when the slots fit twice, else one
+// CTA of 512; 0 when even two chunk stages do not fit (the split path runs).
 template <bool CFG, typename F>
 static int with_k123(uint32_t tile_elems, F f) {
-  if (k123_smem<1024, 3>(tile_elems) <= 111u * 1024u)
-    return f(k123_step<1024, 3, CFG>, k123_smem<1024, 3>(tile_elems));
-  return f(k123_step<1024, 2, CFG>, k123_smem<1024, 2>(tile_elems));
+  if (k123_smem<1024, 3>(tile_elems) <= kSmemTwoPerSM)
+    return f(k123_step<1024, 3, kThreads, CFG>, k123_smem<1024, 3>(tile_elems), kThreads + 32);
+  if (k123_smem<1024, 3>(tile_elems) <= kSmemOnePerSM)
+    return f(k123_step<1024, 3, 2 * kThreads, CFG>, k123_smem<1024, 3>(tile_elems), 2 * kThreads + 32);
+  if (k123_smem<1024, 2>(tile_elems) <= kSmemOnePerSM)
+    return f(k123_step<1024, 2, 2 * kThreads, CFG>, k123_smem<1024, 2>(tile_elems), 2 * kThreads + 32);
+  return 0;
 }
 
 int fused_grid(uint32_t tile_elems) {
-  return with_k123<false>(tile_elems, [](auto fn, size_t sm) { return grid_for(fn, sm, kThreads + 32); });
+  return with_k123<false>(tile_elems, [](auto fn, size_t sm, int nt) { return grid_for(fn, sm, nt); });
 }
 
 int launch_step_fused(const StepArgs& a, int grid, cudaStream_t s) {
   if (a.ntiles == 0) return SAMO_OK;
   if (grid <= 0) grid = fused_grid(a.tile_elems);
+  if (grid <= 0) return fail(SAMO_E_PARAMETER, "fused step: tile of %u elements does not fit in shared memory", a.tile_elems);
   const char* e = getenv("SAMO_PDL");
   const bool pdl = !(e && *e && atoi(e) == 0);
-  auto go = [&](auto fn, size_t sm) {
-    return launch_persistent(fn, a, sm, grid, s, kThreads + 32, "k123_step", pdl);
+  auto go = [&](auto fn, size_t sm, int nt) {
+    return launch_persistent(fn, a, sm, grid, s, nt, "k123_step", pdl);
   };
   return a.cfg ? with_k123<true>(a.tile_elems, go) : with_k123<false>(a.tile_elems, go);
 }

@@ -99,6 +99,7 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   const uint64_t o_koff = carve((nlayers + 1) * sizeof(uint64_t));
   const uint64_t o_st = carve(sizeof(SamoStepState));
   const uint64_t o_np = carve(static_cast<uint64_t>(max_grid) * kMaxBuckets * sizeof(float));
+  const uint64_t o_tn = carve(static_cast<uint64_t>(ntiles) * sizeof(float) + 1024 * sizeof(double));
   // Buffers of the sharded exchange last: the step kernels' streams keep the
   // relative placement measured best.
   const uint64_t o_c16 = carve((n_al + kArenaSlack) * 2);
@@ -132,6 +133,8 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   md->k_off_dev = reinterpret_cast<uint64_t*>(b + o_koff);
   md->st = reinterpret_cast<SamoStepState*>(b + o_st);
   md->norm_partials = reinterpret_cast<float*>(b + o_np);
+  md->norm_dpartials = reinterpret_cast<double*>(b + o_tn);  // <= 1024 repair CTAs
+  md->tile_norm = reinterpret_cast<float*>(b + o_tn + 1024 * sizeof(double));
   e = cudaMemset(md->block, 0, off);
   if (e != cudaSuccess) {
     cudaFree(md->block);
@@ -511,6 +514,8 @@ static int enqueue_fused(samo_model* md, cudaStream_t s) {
   a.theta_o = md->theta_alt;
   a.m_o = md->m_alt;
   a.v_o = md->v_alt;
+  a.tile_norm = md->tile_norm;
+  a.norm_dpartials = md->norm_dpartials;
   const int grid = std::min<int>(md->grid_fused, md->ntiles);
   a.norm_count = static_cast<uint32_t>(grid);
   SAMO_TRY(phase_mark(md, 0, s));

@@ -332,6 +332,103 @@ int main() {
     CHECK(throws<DimensionError>([&] { fused.sink_dw(0, dx.get(), dd.get(), batch, in, out - 8); }));
   });
 
+  // ---- train_test.cpp OptimizerStep KATs through SamoTrainer ---------------
+  // The reference drives them with a one-layer MLP forward/backward; here the
+  // dense gradient that backward would hand to the sink is sunk directly.
+  auto one_layer_state = [](Tensor<float> w) {
+    const std::vector<LayerParams> params = {{"w", w, true}};
+    auto sets = magnitude_prune(params, 0.0);
+    ModelState st;
+    st.layers.push_back(make_layer_state(w, std::make_shared<const PrunedIndexSet>(std::move(sets[0]))));
+    return st;
+  };
+  auto plain_adam = [](float loss_scale) {
+    OptimizerConfig cfg;
+    cfg.learning_rate = 0.1f;
+    cfg.loss_scale = loss_scale;
+    return cfg;
+  };
+  run("OptimizerStep.ZeroGradientLeavesStateUntouched (train_test.cpp:139-154)", [&] {
+    SamoTrainer tr(plain_adam(1.0f), one_layer_state(Tensor<float>({2, 2}, {1.0f, 0.0f, 0.0f, 1.0f})));
+    const auto before = tr.state().layers[0].comp.theta32;
+    tr.sink(0, Tensor<Half>({2, 2}));  // identity weights, y == x: dL/dW == 0
+    CHECK(tr.optimizer_step());
+    CHECK(tr.state().layers[0].comp.theta32 == before);
+    for (float m : tr.state().layers[0].comp.adam_m) CHECK(m == 0.0f);
+  });
+  run("OptimizerStep.ScalarAdamOracle (train_test.cpp:156-180)", [&] {
+    SamoTrainer tr(plain_adam(1.0f), one_layer_state(Tensor<float>({1, 1}, {0.5f})));
+    tr.sink(0, Tensor<Half>({1, 1}, {Half(1.0f)}));  // 2 * (0.5 - 0) * 1
+    CHECK(static_cast<float>(tr.state().layers[0].comp.grad16[0]) == 1.0f);
+    CHECK(tr.optimizer_step());
+    const double g = 1.0, lr = 0.1, b1 = 0.9, b2 = 0.999, eps = 1e-8;
+    const double m_hat = (1.0 - b1) * g / (1.0 - b1), v_hat = (1.0 - b2) * g * g / (1.0 - b2);
+    const double want = 0.5 - lr * m_hat / (std::sqrt(v_hat) + eps);
+    const float got = tr.state().layers[0].comp.theta32[0];
+    CHECK(std::fabs(got - want) <= 1e-6);
+    CHECK(std::fabs(got - 0.4) <= 1e-6);
+    CHECK(tr.state().layers[0].comp.grad16[0].bits() == 0);  // reset after the step
+    check_state_invariants(tr.state());
+  });
+  run("OptimizerStep.NonFiniteGradientSkipsAndCounts (train_test.cpp:182-199)", [&] {
+    SamoTrainer tr(plain_adam(65536.0f), one_layer_state(Tensor<float>({1, 1}, {0.5f})));
+    tr.sink(0, Tensor<Half>({1, 1}, {Half(2.0f * 40000.5f * 65536.0f)}));  // overflows binary16
+    CHECK(!tr.state().layers[0].comp.grad16[0].is_finite());
+    CHECK(!tr.optimizer_step());
+    CHECK(tr.skipped_steps() == 1u);
+    CHECK(tr.state().layers[0].comp.theta32[0] == 0.5f);
+    CHECK(tr.state().layers[0].comp.grad16[0].bits() == 0);
+    for (float m : tr.state().layers[0].comp.adam_m) CHECK(m == 0.0f);
+  });
+  run("OptimizerStep.RequiresBackward (train.hpp:618)", [&] {
+    SamoTrainer tr(plain_adam(1.0f), one_layer_state(Tensor<float>({1, 1}, {0.5f})));
+    CHECK(throws<StateError>([&] { tr.optimizer_step(); }));
+    CHECK(throws<IndexError>([&] { tr.sink(3, Tensor<Half>({1, 1})); }));
+    CHECK(throws<DimensionError>([&] { tr.sink(0, Tensor<Half>({2, 1})); }));
+  });
+  run("SamoTrainer.MultiLayerStepsMatchModel (train.hpp:617-656)", [&] {
+    // three layers, p = 0.5, two steps: the trainer's state equals a Model
+    // stepped on the same gradients, and the invariants hold.
+    std::vector<LayerParams> params;
+    for (int l = 0; l < 3; ++l) {
+      std::vector<float> v(64 + 8 * l);
+      for (std::size_t i = 0; i < v.size(); ++i) v[i] = 0.01f * static_cast<float>((i * 37 + l * 11) % 29) - 0.14f;
+      params.push_back(layer("l" + std::to_string(l), v));
+    }
+    auto sets = magnitude_prune(params, 0.5);
+    ModelState st;
+    for (int l = 0; l < 3; ++l)
+      st.layers.push_back(make_layer_state(params[l].values, std::make_shared<const PrunedIndexSet>(sets[l])));
+    check_state_invariants(st);
+    OptimizerConfig cfg;
+    SamoTrainer tr(cfg, st);
+    Model m(sets);
+    for (int l = 0; l < 3; ++l) m.init_layer(l, params[l].values);
+    m.set_config(cfg);
+    for (int step = 0; step < 2; ++step) {
+      std::vector<DeviceBuffer<std::uint16_t>> bufs;
+      std::vector<const std::uint16_t*> ptrs;
+      for (int l = 2; l >= 0; --l) {  // last layer first, as mlp_backward
+        std::vector<Half> g(params[l].values.size());
+        for (std::size_t i = 0; i < g.size(); ++i) g[i] = Half(static_cast<float>((i * 13 + step * 7 + l) % 17) - 8.0f);
+        tr.sink(l, Tensor<Half>({g.size()}, g));
+        bufs.emplace_back(reinterpret_cast<const std::uint16_t*>(g.data()), g.size());
+      }
+      for (int l = 0; l < 3; ++l) ptrs.push_back(bufs[2 - l].get());
+      m.set_grads(ptrs);
+      m.step();
+      CHECK(tr.optimizer_step());
+    }
+    for (int l = 0; l < 3; ++l) {
+      CHECK(tr.state().layers[l].comp.theta32 == m.theta32(l));
+      CHECK(tr.state().layers[l].comp.adam_v == m.adam_v(l));
+      CHECK(bit_equal(tr.state().layers[l].theta16, Tensor<Half>({params[l].values.size()}, m.theta16(l))));
+    }
+    check_state_invariants(tr.state());
+    CHECK(measured_bytes(tr.state(), Accounting::steady_state) ==
+          measured_bytes(tr.state(), Accounting::peak) - 2 * tr.state().total_unpruned());
+  });
+
   std::printf("%d passed, %d failed\n", g_pass, g_fail);
   return g_fail ? 1 : 0;
 }
