@@ -48,6 +48,8 @@ def parse_args():
     ap.add_argument("--sparsity", type=float, default=0.9)
     ap.add_argument("--tile", type=int, default=0, help="dense elements per tile (0 = default)")
     ap.add_argument("--seed", type=int, default=1234)
+    ap.add_argument("--grad-dtype", choices=["f16", "bf16"], default="f16",
+                    help="dense gradient type (bf16: north_star's other 16-bit type; no CPU reference)")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = min(steps, 10)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-fused", action="store_true",
@@ -518,7 +520,8 @@ def run_samo(args) -> None:
     phi, nnz, ntiles = model.totals()
     torch.cuda.synchronize()
     cpu_sample = None
-    if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.profile):
+    # (the reference is binary16-only: no CPU baseline for bf16 gradients)
+    if rank == 0 and world == 1 and not (args.no_cpu_baseline or args.profile or args.grad_dtype == "bf16"):
         # keep what the CPU sample needs (the K0 masks, bit-exact with the
         # reference's) before freeing the dense init values
         ncores = len(os.sched_getaffinity(0))
@@ -546,6 +549,10 @@ def run_samo(args) -> None:
         g = grad_arena[offs[i]:offs[i] + t.numel]
         samo.synth_uniform_f16(t.numel, args.seed + 1 + rank, 2 * i + 1, 2.0**-7, 1024.0, out=g)  # rank_seed
         grads.append(g)
+    if args.grad_dtype == "bf16":  # the same values rounded to bfloat16 (setup, untimed)
+        grad_arena = grad_arena.float().to(torch.bfloat16)
+        grads = [grad_arena[offs[i]:offs[i] + t.numel] for i, t in enumerate(wl.tensors)]
+        model.set_grad_dtype(torch.bfloat16)
     model.set_grads(grads)
 
     comm = None
@@ -808,7 +815,7 @@ def run_samo(args) -> None:
         # that can fail on a small host; every rank agrees before going on.
         try:
             with gpu_local_cpus(dev):  # pages placed on the GPU's NUMA node
-                host = torch.empty(off, dtype=torch.float16, pin_memory=True)
+                host = torch.empty(off, dtype=grad_arena.dtype, pin_memory=True)
         except Exception as ex:  # noqa: BLE001
             host, e2e_err = None, str(ex)
         ok = torch.tensor([1 if host is not None else 0], device=dev, dtype=torch.int32)
@@ -863,7 +870,7 @@ def run_samo(args) -> None:
         e2e = {"value": world * phi / (e2e_ms / E * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(host.numel() * 2), "d2h_bytes_per_step": 32,
                "steps": E, "ms_per_step": e2e_ms / E,
-               "note": "dense fp16 grads H2D from pinned host (double-buffered against the "
+               "note": f"dense {args.grad_dtype} grads H2D from pinned host (double-buffered against the "
                        "previous step; PCIe-bound: 55.5 GB/s with 1-8 copy streams, "
                        "tools/h2d_probe.py) + step + D2H of the step record (grad norm, skip flag)"}
         del host, dbuf, dgrads
@@ -909,10 +916,11 @@ def run_samo(args) -> None:
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (counter-hash weights and loss-scaled fp16 grads; K0-pruned mask)",
+            "data": f"synthetic (counter-hash weights and loss-scaled {'bf16' if args.grad_dtype == 'bf16' else 'fp16'} "
+                    "grads; K0-pruned mask)",
             "config": {"workload": wl.name, "description": wl.description,
                        "sparsity": wl.sparsity, "phi": phi, "nnz": nnz, "tensors": L,
-                       "tiles": ntiles, "parallelism": f"dp{world}",
+                       "tiles": ntiles, "parallelism": f"dp{world}", "grad_dtype": args.grad_dtype,
                        "l2": (f"inputs ({(4 * phi + 32 * nnz) / 1e9:.1f} GB per step) are larger than "
                               "L2; no flush needed") if 4 * phi + 32 * nnz > 2 * 126e6 else
                              "L2-resident working set: latency-bound configuration, reported as "

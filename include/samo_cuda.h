@@ -298,6 +298,16 @@ int samo_model_shard_layout(samo_model* model, uint64_t* chunk, uint64_t* stride
 int samo_model_enable_phase_timing(samo_model* model, int on);
 int samo_model_phase_times(samo_model* model, float* ms, int cap);
 
+/* Element type of the dense gradients the model consumes (set_grads, the
+ * backward sinks): binary16 (SAMO_GRAD_F16, the default — the reference's
+ * Half, half.hpp) or bfloat16 (SAMO_GRAD_BF16: widened exactly to binary32,
+ * bits << 16; then the same unscale, finite check and Adam).  The fused dW
+ * sink stays binary16-only (SAMO_E_STATE). */
+#define SAMO_GRAD_F16 0
+#define SAMO_GRAD_BF16 1
+int samo_model_set_grad_dtype(samo_model* model, int dtype);
+int samo_model_grad_dtype(const samo_model* model);
+
 /* Per-layer dense binary16 gradients (device pointers, 16-byte aligned,
  * dense_len elements each) consumed by the next step. `ptrs` is a host array
  * of nlayers device pointers; it is copied to the device on `stream`. */

@@ -81,6 +81,11 @@ class Oracle:
         lib.or_adam_update.argtypes = [vp, vp, vp, vp, u64, C.POINTER(Cfg), C.c_float, C.c_float]
         lib.or_optimizer_step.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                           C.POINTER(Cfg), C.POINTER(StepState)]
+        lib.or_optimizer_step_ex.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                             C.POINTER(Cfg), C.POINTER(StepState), C.c_int]
+        lib.or_bf16_to_float.restype = C.c_float
+        lib.or_bf16_to_float.argtypes = [C.c_uint16]
+        lib.or_bf16_to_float_n.argtypes = [vp, vp, u64]
         lib.or_unpruned_count.restype = u64
         lib.or_unpruned_count.argtypes = [C.c_double, u64]
         lib.or_magnitude_prune.argtypes = [vp, vp, vp, C.c_int, C.c_double, C.c_int, vp, vp]
@@ -138,14 +143,22 @@ class Oracle:
                                 C.c_float(bias1), C.c_float(bias2))
 
     def optimizer_step(self, dense_len, nnz, idx_arena, dense_grads, theta, m, v, g32, theta16,
-                       cfg: Cfg, st: StepState) -> bool:
+                       cfg: Cfg, st: StepState, grad_bf16: bool = False) -> bool:
+        """dense_grads: uint16 bit patterns, binary16 (the reference) or, with
+        grad_bf16, bfloat16."""
         dl = np.ascontiguousarray(dense_len, dtype=np.uint64)
         nz = np.ascontiguousarray(nnz, dtype=np.uint64)
         gp = _ptr_array(dense_grads)
         tp = _ptr_array(theta16)
-        return bool(self.lib.or_optimizer_step(len(dl), _p(dl), _p(nz), _p(idx_arena), gp,
-                                               _p(theta), _p(m), _p(v), _p(g32), tp,
-                                               C.byref(cfg), C.byref(st)))
+        return bool(self.lib.or_optimizer_step_ex(len(dl), _p(dl), _p(nz), _p(idx_arena), gp,
+                                                  _p(theta), _p(m), _p(v), _p(g32), tp,
+                                                  C.byref(cfg), C.byref(st), 1 if grad_bf16 else 0))
+
+    def bf16_to_float(self, h) -> np.ndarray:
+        h = np.ascontiguousarray(h, dtype=np.uint16)
+        out = np.empty(h.shape, dtype=np.float32)
+        self.lib.or_bf16_to_float_n(_p(h), _p(out), h.size)
+        return out
 
     # prune.hpp
     def unpruned_count(self, p: float, n: int) -> int:

@@ -151,10 +151,27 @@ typedef struct {
   uint32_t last_skipped;
 } or_step_state;
 
-EXPORT int or_optimizer_step(int nlayers, const uint64_t* dense_len, const uint64_t* nnz,
-                             const uint32_t* idx, const uint16_t* const* dense_grads,
-                             float* theta, float* m, float* v, float* g32,
-                             uint16_t* const* theta16, const or_cfg* c, or_step_state* st) {
+/* bfloat16 -> binary32 (the north_star's other 16-bit gradient type; no
+ * reference code — an extension paralleling half_bits_to_float,
+ * half.hpp:52-71): bfloat16 is the top half of a binary32, so the widening is
+ * exact for every input, NaN payloads included. */
+EXPORT float or_bf16_to_float(uint16_t h) {
+  const uint32_t w = (uint32_t)h << 16;
+  float f;
+  memcpy(&f, &w, 4);
+  return f;
+}
+
+EXPORT void or_bf16_to_float_n(const uint16_t* in, float* out, uint64_t n) {
+  for (uint64_t i = 0; i < n; ++i) out[i] = or_bf16_to_float(in[i]);
+}
+
+/* grad_bf16 = 0: binary16 dense gradients (the reference); 1: bfloat16. */
+EXPORT int or_optimizer_step_ex(int nlayers, const uint64_t* dense_len, const uint64_t* nnz,
+                                const uint32_t* idx, const uint16_t* const* dense_grads,
+                                float* theta, float* m, float* v, float* g32,
+                                uint16_t* const* theta16, const or_cfg* c, or_step_state* st,
+                                int grad_bf16) {
   const float inv_scale = 1.0f / c->loss_scale; /* train.hpp:619 */
   int finite = 1;
   float norm_acc = 0.0f;
@@ -162,7 +179,7 @@ EXPORT int or_optimizer_step(int nlayers, const uint64_t* dense_len, const uint6
   for (int l = 0; l < nlayers; ++l) { /* train.hpp:622-629, serial over layers then k */
     for (uint64_t k = 0; k < nnz[l]; ++k) {
       const uint16_t h = dense_grads[l][idx[k0 + k]];
-      const float gv = or_half_to_float(h) * inv_scale;
+      const float gv = (grad_bf16 ? or_bf16_to_float(h) : or_half_to_float(h)) * inv_scale;
       g32[k0 + k] = gv;
       finite = finite && isfinite(gv);
       norm_acc += gv * gv;
@@ -190,6 +207,13 @@ EXPORT int or_optimizer_step(int nlayers, const uint64_t* dense_len, const uint6
     k0 += nnz[l];
   }
   return 1;
+}
+
+EXPORT int or_optimizer_step(int nlayers, const uint64_t* dense_len, const uint64_t* nnz,
+                             const uint32_t* idx, const uint16_t* const* dense_grads,
+                             float* theta, float* m, float* v, float* g32,
+                             uint16_t* const* theta16, const or_cfg* c, or_step_state* st) {
+  return or_optimizer_step_ex(nlayers, dense_len, nnz, idx, dense_grads, theta, m, v, g32, theta16, c, st, 0);
 }
 
 /* ---------------------------------------------------------------------- */

@@ -123,6 +123,8 @@ _SIGS = {
     "samo_model_finalize": (C.c_int, [vp, vp]),
     "samo_model_init_layer": (C.c_int, [vp, C.c_int, vp, C.c_uint64, vp]),
     "samo_model_set_config": (C.c_int, [vp, C.POINTER(OptimizerConfig)]),
+    "samo_model_set_grad_dtype": (C.c_int, [vp, C.c_int]),
+    "samo_model_grad_dtype": (C.c_int, [vp]),
     "samo_model_attach_comm": (C.c_int, [vp, vp]),
     "samo_model_set_exchange": (C.c_int, [vp, C.c_int]),
     "samo_model_exchange_mode": (C.c_int, [vp]),

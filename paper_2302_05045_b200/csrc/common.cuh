@@ -237,6 +237,15 @@ __device__ __forceinline__ float f16_bits_to_f32(uint16_t h) {
   return f;
 }
 
+// Dense gradient element of either 16-bit type: binary16 (the reference's
+// Half, half_bits_to_float above) or bfloat16 (north_star's other gradient
+// type; bf16 -> binary32 widening is exact: the bits shifted up by 16).
+__device__ __forceinline__ float grad_to_f32(uint32_t h, bool bf16) {
+  return bf16 ? __uint_as_float(h << 16) : f16_bits_to_f32(static_cast<uint16_t>(h));
+}
+// Exponent field of the 16-bit gradient type: all ones <=> inf or NaN.
+__device__ __forceinline__ uint32_t grad_exp_mask(bool bf16) { return bf16 ? 0x7F80u : 0x7C00u; }
+
 // x86 SSE `mulss` semantics for one multiply whose second operand is a
 // non-NaN number: a NaN first operand is returned quieted (payload kept).
 __device__ __forceinline__ float mul_x86(float a, float b) {

@@ -504,6 +504,7 @@ int step_p2p(samo_model* md, cudaStream_t S, bool gather) {
   pa.k0 = std::min<uint64_t>(r * c, md->n_tot);
   pa.k1 = std::min<uint64_t>((r + 1) * c, md->n_tot);
   pa.scale = (1.0f / md->cfg.loss_scale) * (1.0f / static_cast<float>(G));
+  pa.grad_bf16 = md->grad_bf16;
   pa.prm = adam_params(&md->cfg);
   pa.cfg = md->capturing ? md->cfg_dev : nullptr;
   pa.st = md->st;
@@ -819,6 +820,7 @@ static int p2p_prepare(samo_model* md, int B, bool gather, P2PStep& sp) {
   pa.m = md->m;
   pa.v = md->v;
   pa.scale = (1.0f / md->cfg.loss_scale) * (1.0f / static_cast<float>(G));
+  pa.grad_bf16 = md->grad_bf16;
   pa.prm = adam_params(&md->cfg);
   pa.cfg = md->capturing ? md->cfg_dev : nullptr;
   pa.st = md->st;

@@ -83,6 +83,7 @@ struct samo_model {
   uint64_t* k_off_dev = nullptr;
   SamoStepState* st = nullptr;
   float* norm_partials = nullptr;
+  int grad_bf16 = 0;                  // dense gradients are bfloat16 (else binary16)
   float* tile_norm = nullptr;         // K123: per-tile grad-norm partials
   double* norm_dpartials = nullptr;   // k123_repair: per-CTA sums of them
   std::vector<SamoLayerDev> layers_host;

@@ -52,6 +52,7 @@ struct StepArgs {
   float* m_o;
   float* v_o;
   float inv_scale;             // 1/loss_scale (and 1/G when exchanging fp32)
+  uint32_t grad_bf16;          // dense (and compressed 16-bit) gradients are bfloat16
   SamoAdamParams prm;
   SamoStepState* st;
   float* flag_slot;            // non-finite indicator (summed across ranks)
@@ -118,6 +119,7 @@ struct P2PArgs {
   float* v;
   uint64_t k0, k1;                    // k0 a multiple of 8
   float scale;                        // (1/loss_scale) * (1/G)
+  int grad_bf16;                      // the 16-bit gradients are bfloat16
   SamoAdamParams prm;
   const SamoStepState* st;
   const float* flag_slot;             // global skip indicator (already reduced)

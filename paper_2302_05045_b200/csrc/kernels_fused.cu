@@ -150,6 +150,8 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
   }
 
   bool bad = false;
+  const bool bf16 = a.grad_bf16 != 0;
+  const uint32_t xm = grad_exp_mask(bf16);
   uint32_t it = 0;
   for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++it) {
     const int s = static_cast<int>(it % NS);
@@ -176,11 +178,11 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
       const uint16_t off = a.off16[k];
       const uint16_t h = off < staged ? sg[off] : gsrc[off];
       if constexpr (OUT_F32) {
-        const float gk = mul_x86(f16_bits_to_f32(h), inv_scale);
+        const float gk = mul_x86(grad_to_f32(h, bf16), inv_scale);
         bad |= !finite_f32(gk);
         st_na_f32(reinterpret_cast<float*>(a.g) + k, gk);
       } else {
-        bad |= (h & 0x7C00u) == 0x7C00u;  // |h * 2^-s| is finite iff h is
+        bad |= (h & xm) == xm;  // |h * 2^-s| is finite iff h is
         st_na_u16(g16 + k, h);
       }
     };
@@ -205,7 +207,7 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const uint16_t h = static_cast<uint16_t>((e & 1) ? (hw[e >> 1] >> 16) : (hw[e >> 1] & 0xFFFFu));
-          f[e] = mul_x86(f16_bits_to_f32(h), inv_scale);
+          f[e] = mul_x86(grad_to_f32(h, bf16), inv_scale);
           bad |= !finite_f32(f[e]);
         }
         float* dst = reinterpret_cast<float*>(a.g) + k;
@@ -214,7 +216,7 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
       } else {
 #pragma unroll
         for (int e = 0; e < 4; ++e)
-          bad |= ((hw[e] & 0x7C00u) == 0x7C00u) | ((hw[e] & 0x7C000000u) == 0x7C000000u);
+          bad |= ((hw[e] & xm) == xm) | ((hw[e] & (xm << 16)) == (xm << 16));
         st_na_v4u(g16 + k, hw[0], hw[1], hw[2], hw[3]);
       }
     }
@@ -455,7 +457,7 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
           if (i < n) {
             if constexpr (G16) {
               const uint16_t h = reinterpret_cast<const uint16_t*>(st + 3 * L::kF32)[ho + i];
-              gv[u] = mul_x86(f16_bits_to_f32(h), p_inv);
+              gv[u] = mul_x86(grad_to_f32(h, a.grad_bf16 != 0), p_inv);
             } else {
               gv[u] = reinterpret_cast<const float*>(st + 3 * L::kF32)[fo + i];
             }
@@ -825,6 +827,8 @@ __global__ void __launch_bounds__(NT + 32) k123_step(StepArgs a) {
   };
 
   bool bad = false;
+  const bool bf16 = a.grad_bf16 != 0;
+  const uint32_t xm = grad_exp_mask(bf16);
   uint32_t it = 0, tt = 0;
   for (;; ++tt) {
     const int sg = static_cast<int>(tt % NSG);
@@ -862,8 +866,8 @@ __global__ void __launch_bounds__(NT + 32) k123_step(StepArgs a) {
           if (i < n) {
             ov[u] = soff[i];
             const uint16_t h = ov[u] < staged ? sgr[ov[u]] : gsrc[ov[u]];
-            bad |= (h & 0x7C00u) == 0x7C00u;  // |h * 2^-s| is finite iff h is
-            gv[u] = mul_x86(f16_bits_to_f32(h), p_inv);
+            bad |= (h & xm) == xm;  // |h * 2^-s| is finite iff h is
+            gv[u] = mul_x86(grad_to_f32(h, bf16), p_inv);
             tv[u] = sth[i];
             mv[u] = smv[i];
             vv[u] = svv[i];
@@ -962,13 +966,18 @@ __global__ void __launch_bounds__(kThreads) k123_repair(StepArgs a) {
       last_cta = (atomicAdd(&a.st->done_ctas, 1u) == gridDim.x - 1);
     }
     __syncthreads();
-    if (last_cta && tid == 0) {
+    if (last_cta) {  // uniform: all threads fetch the partials, one sums them in order
+      __shared__ double part[1024];
       __threadfence();
-      double s = 0.0;
-      for (uint32_t b = 0; b < gridDim.x; ++b) s += __ldcg(a.norm_dpartials + b);
-      a.st->grad_norm = static_cast<float>(sqrt(s));
-      a.st->done_ctas = 0u;
-      __threadfence();
+      for (uint32_t b = tid; b < gridDim.x; b += kThreads) part[b] = __ldcg(a.norm_dpartials + b);
+      __syncthreads();
+      if (tid == 0) {
+        double s = 0.0;
+        for (uint32_t b = 0; b < gridDim.x; ++b) s += part[b];
+        a.st->grad_norm = static_cast<float>(sqrt(s));
+        a.st->done_ctas = 0u;
+        __threadfence();
+      }
     }
   }
   if (*reinterpret_cast<volatile uint32_t*>(&a.st->last_skipped) == 0u) return;
@@ -1206,7 +1215,7 @@ __global__ void __launch_bounds__(kThreads, SAMO_P2P_MINB) k_shard_p2p(P2PArgs a
     for (int e = 0; e < 8; ++e) {
       float g = 0.0f;  // rank-ascending fp32 sum, as the oracle's dp_sum
 #pragma unroll
-      for (int r = 0; r < G; ++r) g = __fadd_rn(g, mul_x86(f16_bits_to_f32(half_lane(h[r], e)), scale));
+      for (int r = 0; r < G; ++r) g = __fadd_rn(g, mul_x86(grad_to_f32(half_lane(h[r], e), a.grad_bf16 != 0), scale));
       if (e < cnt) nacc = __fadd_rn(nacc, __fmul_rn(g, g));
       float t = th[e];
       if (!skip && e < cnt) t = adam_one(g, mm[e], vv[e], t, prm, omb1, omb2, bias1, bias2, lrwd);
@@ -1347,7 +1356,7 @@ __global__ void __launch_bounds__(32 * (kShardConsumers + 1)) k_shard_p2p_tma(P2
       for (int e = 0; e < 8; ++e) {
         float g = 0.0f;  // rank-ascending fp32 sum, as the oracle's dp_sum
 #pragma unroll
-        for (int r = 0; r < G; ++r) g = __fadd_rn(g, mul_x86(f16_bits_to_f32(half_lane(h[r], e)), scale));
+        for (int r = 0; r < G; ++r) g = __fadd_rn(g, mul_x86(grad_to_f32(half_lane(h[r], e), a.grad_bf16 != 0), scale));
         if (e < ce) nacc = __fadd_rn(nacc, __fmul_rn(g, g));
         float t = th[e];
         if (!skip && e < ce) t = adam_one(g, mm[e], vv[e], t, prm, omb1, omb2, bias1, bias2, lrwd);

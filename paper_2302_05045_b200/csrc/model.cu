@@ -323,6 +323,18 @@ int samo_model_set_config(samo_model* md, const samo_optimizer_config* cfg) {
   return clear_ok();
 }
 
+int samo_model_set_grad_dtype(samo_model* md, int dtype) {
+  if (!md) return fail(SAMO_E_PARAMETER, "null model");
+  if (dtype != SAMO_GRAD_F16 && dtype != SAMO_GRAD_BF16)
+    return fail(SAMO_E_PARAMETER, "gradient dtype must be SAMO_GRAD_F16 or SAMO_GRAD_BF16");
+  const int bf16 = dtype == SAMO_GRAD_BF16;
+  if (bf16 != md->grad_bf16) drop_graphs(md);  // captured steps baked the decode in
+  md->grad_bf16 = bf16;
+  return clear_ok();
+}
+
+int samo_model_grad_dtype(const samo_model* md) { return md && md->grad_bf16 ? SAMO_GRAD_BF16 : SAMO_GRAD_F16; }
+
 int samo_model_attach_comm(samo_model* md, samo_comm* comm) {
   if (!md) return fail(SAMO_E_PARAMETER, "null model");
   close_peers(md);
@@ -377,6 +389,7 @@ StepArgs step_args(samo_model* md) {
   const int G = comm_size(md);
   if (G > 1) inv_scale = inv_scale * (1.0f / static_cast<float>(G));
   a.inv_scale = inv_scale;
+  a.grad_bf16 = md->grad_bf16 ? 1u : 0u;
   a.prm = adam_params(&md->cfg);
   a.st = md->st;
   a.flag_slot = flag_ptr(md);
@@ -424,6 +437,8 @@ int samo_model_sink_dense(samo_model* md, int l, const uint16_t* grad, samo_stre
 int samo_model_sink_dw(samo_model* md, int l, const uint16_t* x, const uint16_t* dy, uint64_t batch,
                        uint64_t in, uint64_t out, samo_stream_t stream) {
   SAMO_TRY(sink_ready(md, l));
+  if (md->grad_bf16)
+    return fail(SAMO_E_STATE, "sink_dw: the fused dW GEMM produces binary16 gradients (model expects bfloat16)");
   SAMO_TRY(dw_check(batch, in, out, x, dy));
   if (in * out != md->dense_len[l])
     return fail(SAMO_E_DIMENSION, "layer %d: in x out = %llu, dense_len = %llu", l,

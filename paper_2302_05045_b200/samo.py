@@ -352,6 +352,26 @@ class SamoModel:
     def set_config(self, cfg: OptimizerConfig) -> None:
         _abi.call("samo_model_set_config", self._h, C.byref(cfg))
 
+    GRAD_F16, GRAD_BF16 = 0, 1
+
+    def set_grad_dtype(self, dtype) -> None:
+        """Element type of the dense gradients: torch.float16 (binary16, the
+        reference's Half; default) or torch.bfloat16 (widened exactly)."""
+        code = {torch.float16: self.GRAD_F16, "f16": self.GRAD_F16, "fp16": self.GRAD_F16,
+                torch.bfloat16: self.GRAD_BF16, "bf16": self.GRAD_BF16}.get(dtype)
+        if code is None:
+            raise ParameterError(f"gradient dtype must be float16 or bfloat16, not {dtype}")
+        _abi.call("samo_model_set_grad_dtype", self._h, code)
+
+    @property
+    def grad_dtype(self) -> torch.dtype:
+        return torch.bfloat16 if _abi.load().samo_model_grad_dtype(self._h) == self.GRAD_BF16 else torch.float16
+
+    def _check_grad(self, g: torch.Tensor) -> None:
+        _bits16(g)
+        if g.dtype in (torch.float16, torch.bfloat16) and g.dtype != self.grad_dtype:
+            raise ParameterError(f"gradient is {g.dtype}, the model expects {self.grad_dtype} (set_grad_dtype)")
+
     def attach_comm(self, comm: Communicator | None) -> None:
         _abi.call("samo_model_attach_comm", self._h, comm.handle if comm else C.c_void_p())
 
@@ -399,12 +419,14 @@ class SamoModel:
 
     # -- step ----------------------------------------------------------------
     def set_grads(self, grads: Sequence[torch.Tensor]) -> None:
-        """Dense binary16 gradients of the step (the backward sink's input)."""
+        """Dense 16-bit gradients of the step (the backward sink's input):
+        binary16, or bfloat16 after set_grad_dtype(torch.bfloat16); int16
+        tensors pass raw bit patterns of the model's type."""
         if len(grads) != len(self.layers):
             raise DimensionError("one dense gradient per layer required")
         for g, l in zip(grads, self.layers):
             _require_cuda(g)
-            _bits16(g)
+            self._check_grad(g)
             if g.numel() != l.dense_len:
                 raise DimensionError(f"{l.layer_id}: gradient length does not match layer")
         ptrs = (C.c_void_p * max(1, len(grads)))(*[g.data_ptr() for g in grads])
@@ -418,7 +440,7 @@ class SamoModel:
         """Backward sink (train.hpp:596-611) of one layer's dense binary16
         gradient: K1 on that layer only.  Single-GPU models."""
         _require_cuda(grad)
-        _bits16(grad)
+        self._check_grad(grad)
         if grad.numel() != self.layers[layer].dense_len:
             raise DimensionError(f"{self.layers[layer].layer_id}: gradient length does not match layer")
         _abi.call("samo_model_sink_dense", self._h, layer, _vp(grad), _stream())

@@ -24,6 +24,12 @@ DENSE_LEN = [40000, 3000, 100003, 512]
 PRUNABLE = [True, True, True, False]
 STEPS = int(os.environ.get("SAMO_DP_STEPS", "4"))  # the stress variant runs 40
 INF_STEP, INF_RANK = 2, 1
+BF16 = os.environ.get("SAMO_DP_BF16") == "1"  # bfloat16 dense gradients
+
+
+def decode(o: Oracle, h):
+    """The oracle's widening of the dense gradient type."""
+    return o.bf16_to_float(h) if BF16 else o.h2f(h)
 
 
 def inputs(o: Oracle, world: int):
@@ -35,8 +41,11 @@ def inputs(o: Oracle, world: int):
         for s in range(STEPS):
             for l, d in enumerate(DENSE_LEN):
                 h = o.synth_f16(0, d, sdist.rank_seed(11, rank), 100 * s + l, 2.0**-7, 1024.0)
+                if BF16:  # the same values as bfloat16 patterns (truncated), wider exponents mixed in
+                    h = (o.h2f(h).view(np.uint32) >> 16).astype(np.uint16)
+                    h[::97] = (h[::97] & np.uint16(0x807F)) | np.uint16(0x4700)  # ~ 2^15 .. 2^16
                 if s == INF_STEP and rank == INF_RANK and l == 2:
-                    h[int(sets[2][5])] = 0x7C00
+                    h[int(sets[2][5])] = 0x7F80 if BF16 else 0x7C00
                 grads[(rank, s, l)] = h
     return vals, sets, grads
 
@@ -55,6 +64,8 @@ def main() -> None:
     for l, v in enumerate(vals):
         model.init_layer(l, torch.from_numpy(v).cuda())
     model.set_config(samo.OptimizerConfig(learning_rate=1e-2))
+    if BF16:
+        model.set_grad_dtype(torch.bfloat16)
     comm = sdist.make_communicator()
     model.attach_comm(comm)
     mode = os.environ.get("SAMO_DP_MODE", "sharded")

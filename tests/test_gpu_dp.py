@@ -47,7 +47,7 @@ def _expected(oracle, world, steps=4):
     for s in range(W.STEPS):
         g = []
         for l in range(L):
-            per_rank = [(oracle.h2f(oracle.compress(grads[(r, s, l)], sets[l])) * inv).astype(np.float32)
+            per_rank = [(W.decode(oracle, oracle.compress(grads[(r, s, l)], sets[l])) * inv).astype(np.float32)
                         for r in range(world)]
             g.append(oracle.dp_sum(per_rank)[0])
         if not all(np.all(np.isfinite(x)) for x in g):
@@ -78,6 +78,8 @@ def _run(tmp_path, mode, world, steps=4, save_g=False):
     env["SAMO_DP_SINK"] = "1" if mode == "p2p-sink" else "0"  # per-layer sinks + step_sunk
     env["SAMO_P2P_PULL"] = "1" if mode == "p2p-pull" else "0"  # expand pulls the weights
     env["SAMO_P2P_NVLS"] = "1" if mode == "p2p-nvls" else "0"  # multicast weight stores
+    env["SAMO_DP_BF16"] = "1" if mode.endswith("-bf16") else "0"  # bfloat16 dense gradients
+    os.environ["SAMO_DP_BF16"] = env["SAMO_DP_BF16"]  # the parent's oracle replay reads it too
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            str(HERE / "dp_worker.py"), str(tmp_path)]
@@ -111,7 +113,7 @@ def _check(r, oracle, world, mode, steps=4):
 
 @pytest.mark.parametrize("mode", ["p2p", "p2p-serial", "p2p-graph", "p2p-tma", "p2p-sink", "p2p-pull",
                                   "p2p-nvls", "sharded", "sharded-graph", "overlap",
-                                  "staged", "graph"])
+                                  "staged", "graph", "p2p-bf16", "sharded-bf16", "overlap-bf16"])
 def test_dp_two_gpus_bit_exact(tmp_path, oracle, mode):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
@@ -179,7 +181,7 @@ def _check_nccl_tolerance(r, oracle, world, mode, steps=4):
     for s in range(steps):
         g, gb = [], []
         for l in range(L):
-            per_rank = [(oracle.h2f(oracle.compress(grads[(q, s, l)], sets[l])) * inv).astype(np.float32)
+            per_rank = [(W.decode(oracle, oracle.compress(grads[(q, s, l)], sets[l])) * inv).astype(np.float32)
                         for q in range(world)]
             stack = np.stack(per_rank).astype(np.float64)
             exact = stack.sum(axis=0)
@@ -285,6 +287,8 @@ def _local_group_run(oracle, G, steps=4):
         for l, v in enumerate(vals):
             m.init_layer(l, torch.from_numpy(v).cuda())
         m.set_config(samo.OptimizerConfig(learning_rate=1e-2))
+        if W.BF16:
+            m.set_grad_dtype(torch.bfloat16)
         models.append(m)
     samo.SamoModel.attach_local_group(models)
     dev = {(r, s): [torch.from_numpy(grads[(r, s, l)].view(np.int16)).cuda() for l in range(L)]
@@ -313,7 +317,8 @@ def _local_group_run(oracle, G, steps=4):
 
 @pytest.mark.parametrize("G,env", [(3, {}), (5, {}), (8, {}), (8, {"SAMO_P2P_TMA": "1"}),
                                    (8, {"SAMO_P2P_PUSH": "0"}), (8, {"SAMO_P2P_PULL": "1"}),
-                                   (2, {"SAMO_P2P_BUCKETS": "5"}), (7, {"SAMO_P2P_BUCKETS": "3"})],
+                                   (2, {"SAMO_P2P_BUCKETS": "5"}), (7, {"SAMO_P2P_BUCKETS": "3"}),
+                                   (3, {"SAMO_DP_BF16": "1"}), (8, {"SAMO_DP_BF16": "1", "SAMO_P2P_TMA": "1"})],
                          ids=lambda x: str(x) if isinstance(x, int) else "-".join(f"{k[9:]}{v}" for k, v in x.items()) or "default")
 def test_local_group_p2p_bit_exact(cuda, oracle, monkeypatch, G, env):
     """The pipelined peer-to-peer step at G up to 8 on ONE GPU: G models on

@@ -438,3 +438,93 @@ def test_fused_and_split_steps_interleave(S, golden, monkeypatch):
     assert rec.skipped_steps == int(g[f"s{int(g['steps'][0]) - 1}_skipped"][0])
     model.check_invariants()
     model.close()
+
+
+# --------------------------------------------------------------------------
+# bfloat16 dense gradients (north_star's "bf16/fp16"; the reference is
+# binary16-only, so the oracle restates the exact bf16 -> binary32 widening)
+
+def _bf16_grads(rng, d, step):
+    """bf16 bit patterns: mostly N(0, 2^-7 * 1024) as the fp16 synth, plus
+    bf16-only magnitudes (beyond binary16's range and below its subnormals)
+    and, on step 1, a +inf at a kept element (global skip)."""
+    g = (rng.standard_normal(d).astype(np.float32) * np.float32(2.0**-7 * 1024.0))
+    b = (g.view(np.uint32) >> 16).astype(np.uint16)
+    j = rng.choice(d, size=min(d, 8), replace=False)
+    b[j[: len(j) // 2]] = np.array([0x4780, 0x5F00, 0x0080, 0x0001][: len(j) // 2], np.uint16)[: len(j) // 2]
+    return b
+
+
+@pytest.mark.parametrize("fused", ["1", "0"], ids=["K123", "K1+K23"])
+@pytest.mark.parametrize("graph", [False, True])
+def test_model_step_bf16_grads(S, oracle, graph, fused, monkeypatch):
+    """set_grad_dtype(bfloat16): three steps (the second skipped on a +inf)
+    through K123 or K1 + K23, eager or captured, bit-exact against the
+    oracle's optimizer_step with bf16 widening; bf16-only magnitudes (>65504,
+    tiny normals, subnormals) included."""
+    monkeypatch.setenv("SAMO_FUSED_STEP", fused)
+    from oracle.oracle import Cfg, StepState
+    dense_len = [3 * 8192 + 5, 4096, 777]
+    rng = np.random.default_rng(5)
+    vals = [(rng.standard_normal(d) * 0.05).astype(np.float32) for d in dense_len]
+    idx = [np.sort(rng.choice(d, d // 4, replace=False)).astype(np.uint32) for d in dense_len]
+    sets = [S.PrunedIndexSet(f"l{l}", d, T(i.view(np.int32))) for l, (d, i) in enumerate(zip(dense_len, idx))]
+    model = S.SamoModel.from_index_sets(sets, [(d,) for d in dense_len], 1024)
+    for l, v in enumerate(vals):
+        model.init_layer(l, T(v))
+    model.set_config(S.OptimizerConfig(learning_rate=1e-2))
+    model.set_grad_dtype(torch.bfloat16)
+    assert model.grad_dtype == torch.bfloat16
+    with pytest.raises(S.ParameterError):
+        model.set_grads([torch.zeros(d, dtype=torch.float16, device="cuda") for d in dense_len])
+    idx_arena = np.concatenate(idx).astype(np.uint32)
+    theta = np.concatenate([oracle.compress(v, i) for v, i in zip(vals, idx)])
+    m, v, g32 = (np.zeros_like(theta) for _ in range(3))
+    t16 = [np.zeros(d, np.uint16) for d in dense_len]
+    st = StepState()
+    for s in range(3):
+        grads = [_bf16_grads(rng, d, s) for d in dense_len]
+        if s == 1:
+            grads[1][idx[1][3]] = 0x7F80  # +inf at a kept element
+        model.set_grads([T(g).view(torch.bfloat16) for g in grads])
+        model.step(graph=graph)
+        oracle.optimizer_step(dense_len, [len(i) for i in idx], idx_arena, grads, theta, m, v, g32, t16,
+                              Cfg(lr=1e-2), st, grad_bf16=True)
+    k0 = 0
+    for l, d in enumerate(dense_len):
+        n = len(idx[l])
+        assert np.array_equal(N(model.read(l, "theta32"), np.uint32), bits(theta[k0:k0 + n])), l
+        assert np.array_equal(N(model.read(l, "adam_m"), np.uint32), bits(m[k0:k0 + n])), l
+        assert np.array_equal(N(model.read(l, "adam_v"), np.uint32), bits(v[k0:k0 + n])), l
+        assert np.array_equal(N(model.read(l, "theta16").reshape(-1), np.uint16), t16[l]), l
+        k0 += n
+    model.check_invariants()
+    rec = model.step_record()
+    assert (rec.t, rec.skipped_steps) == (2, 1) == (st.t, st.skipped)
+    model.close()
+
+
+def test_bf16_sinks_and_dw_refusal(S, oracle):
+    """Backward sinks take bf16 gradients the same way; the fused dW sink
+    (binary16 GEMM output) is refused for a bf16 model."""
+    from oracle.oracle import Cfg, StepState
+    d = 4096
+    rng = np.random.default_rng(8)
+    v0 = (rng.standard_normal(d) * 0.05).astype(np.float32)
+    idx = np.sort(rng.choice(d, 300, replace=False)).astype(np.uint32)
+    model = S.SamoModel.from_index_sets([S.PrunedIndexSet("w", d, T(idx.view(np.int32)))], [(64, 64)], 1024)
+    model.init_layer(0, T(v0))
+    model.set_config(S.OptimizerConfig())
+    model.set_grad_dtype("bf16")
+    g = _bf16_grads(rng, d, 0)
+    model.sink_dense(0, T(g).view(torch.bfloat16))
+    model.step_sunk()
+    theta = oracle.compress(v0, idx)
+    m, v, g32 = (np.zeros_like(theta) for _ in range(3))
+    t16 = [np.zeros(d, np.uint16)]
+    oracle.optimizer_step([d], [len(idx)], idx, [g], theta, m, v, g32, t16, Cfg(), StepState(), grad_bf16=True)
+    assert np.array_equal(N(model.read(0, "theta32"), np.uint32), bits(theta))
+    x = torch.zeros((16, 64), dtype=torch.float16, device="cuda")
+    with pytest.raises(S.StateError):
+        model.sink_dw(0, x, x)
+    model.close()

@@ -217,3 +217,38 @@ def test_dw_matmul_matches_reference(oracle, batch, n_in, n_out):
     rc, want = RefLib().dw_matmul(x, dy)
     assert rc == 0
     assert np.array_equal(oracle.dw_matmul(x, dy), want)
+
+
+def test_bf16_widening_exhaustive(oracle):
+    """or_bf16_to_float: every bf16 pattern is the top half of its binary32
+    (exact widening, NaN payloads kept)."""
+    h = np.arange(65536, dtype=np.uint32).astype(np.uint16)
+    got = oracle.bf16_to_float(h)
+    assert np.array_equal(got.view(np.uint32), h.astype(np.uint32) << 16)
+
+
+def test_bf16_step_equals_f16_step_on_common_values(oracle):
+    """Gradients representable in both 16-bit types (binary16 patterns with
+    the low 3 mantissa bits clear, normal range) give bit-identical steps
+    through the binary16 and the bfloat16 decode."""
+    from oracle.oracle import Cfg, StepState
+    rng = np.random.default_rng(4)
+    d = 5000
+    idx = np.sort(rng.choice(d, 900, replace=False)).astype(np.uint32)
+    v0 = (rng.standard_normal(d) * 0.05).astype(np.float32)
+    h16 = oracle.f2h((rng.standard_normal(d) * 8.0).astype(np.float32)) & np.uint16(0xFFF8)
+    h16[(h16 & 0x7C00) == 0] = 0  # no binary16 subnormals
+    f = oracle.h2f(h16)
+    hb = (f.view(np.uint32) >> 16).astype(np.uint16)
+    assert np.array_equal((hb.astype(np.uint32) << 16).view(np.float32), f)
+    out = []
+    for grads, bf in ((h16, False), (hb, True)):
+        theta = oracle.compress(v0, idx)
+        m, v, g32 = (np.zeros_like(theta) for _ in range(3))
+        t16 = [np.zeros(d, np.uint16)]
+        st = StepState()
+        for _ in range(2):
+            oracle.optimizer_step([d], [len(idx)], idx, [grads], theta, m, v, g32, t16, Cfg(), st, grad_bf16=bf)
+        out.append((theta.view(np.uint32).copy(), v.view(np.uint32).copy(), t16[0].copy()))
+    for a, b in zip(*out):
+        assert np.array_equal(a, b)
