@@ -624,7 +624,7 @@ def run_samo(args) -> None:
                                        "barriers included), divided by the steps"}
         else:
             nvlink_measured = {"unavailable": nvl0}
-    phases = pipeline = None
+    phases = pipeline = overlap = None
     fused_ms = None
     fused = world == 1 and os.environ.get("SAMO_FUSED_STEP", "1") != "0"
     KB = min(K, 10)
@@ -660,6 +660,7 @@ def run_samo(args) -> None:
         # sharded exchange only) — not the headline.
         phases = None
         pipeline = None
+        overlap = None
 
         def phase_pass():
             _abi.call("samo_model_enable_phase_timing", model.handle, 1)
@@ -687,6 +688,7 @@ def run_samo(args) -> None:
             phases = dict(zip(["K1_gather", "skip-flag allreduce (barrier)",
                                "shard update: fused NVLink exchange + Adam", "norm allreduce (barrier)",
                                "expand", "finalize"], ph))
+            overlap = sunk_pass(model, grads, stream, dev)
         elif model.exchange_mode() == model.EXCHANGE_SHARDED:
             phases = dict(zip(["K1_gather (reduce-scatter overlapped)",
                                "skip flag + shard Adam + first all-gather bucket",
@@ -946,6 +948,7 @@ def run_samo(args) -> None:
             "nvlink_measured": nvlink_measured,
             "phases_ms": phases,
             "pipeline_phases_ms": pipeline,
+            "backward_overlap": overlap,
             "p2p_features": model.p2p_features() if world > 1 else None,
             "roofline": roofline,
             "kernels": kern,
@@ -978,6 +981,40 @@ def emit(line: dict) -> None:
         sys.stdout.flush()
     else:
         os.write(_RESULT_FD, text)
+
+
+def sunk_pass(model, grads, stream, dev, reps: int = 3):
+    """The exchange sent during the backward (train.hpp:287-313): per-layer
+    sinks, last layer first, push each layer's kept binary16 gradients to
+    their owners; step_sunk is then only the flag exchange, the shard update
+    and the expand.  Times both parts (max over ranks): the sinks run back to
+    back here (no backward compute to hide under), so sinks_ms is what a
+    backward would absorb and step_after_sinks_ms what is left after it."""
+    import torch.distributed as dist
+    L = len(grads)
+    e = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(reps)]
+    for r in range(reps + 1):
+        dist.barrier()
+        torch.cuda.synchronize()
+        ev = e[r - 1] if r else None
+        if ev:
+            ev[0].record(stream)
+        for l in reversed(range(L)):
+            model.sink_dense(l, grads[l])
+        if ev:
+            ev[1].record(stream)
+        model.step_sunk()
+        if ev:
+            ev[2].record(stream)
+    torch.cuda.synchronize()
+    sk = statistics.median(x[0].elapsed_time(x[1]) for x in e)
+    st = statistics.median(x[1].elapsed_time(x[2]) for x in e)
+    t = torch.tensor([sk, st], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"sinks_ms": round(float(t[0]), 4), "step_after_sinks_ms": round(float(t[1]), 4),
+            "layers": L, "note": "per-layer K1 push sinks (backward order) then step_sunk (flag "
+                                 "exchange + shard update || expand); the sinks' NVLink traffic "
+                                 "rides under the backward in training"}
 
 
 def main() -> None:

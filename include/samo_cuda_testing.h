@@ -30,6 +30,9 @@ extern "C" {
  * it lets tests/test_gpu_dp.py check G = 5..8 on a single GPU. */
 int samo_model_attach_local_group(samo_model* const* models, int G);
 int samo_local_group_step(samo_model* const* models, int G, samo_stream_t stream);
+/* The same after every member's backward sinks (samo_model_sink_dense /
+ * samo_model_sink_dw on each rank): exchange + update only. */
+int samo_local_group_step_sunk(samo_model* const* models, int G, samo_stream_t stream);
 
 #ifdef __cplusplus
 }

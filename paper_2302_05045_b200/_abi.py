@@ -137,6 +137,7 @@ _SIGS = {
     "samo_model_p2p_features": (C.c_int, [vp]),
     "samo_model_attach_local_group": (C.c_int, [C.POINTER(C.c_void_p), C.c_int]),
     "samo_local_group_step": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, vp]),
+    "samo_local_group_step_sunk": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, vp]),
     "samo_model_step_sunk": (C.c_int, [vp, vp]),
     "samo_model_sink_dw": (C.c_int, [vp, C.c_int, vp, vp, C.c_uint64, C.c_uint64, C.c_uint64, vp]),
     "samo_dw_gemm_f16": (C.c_int, [vp, vp, C.c_uint64, C.c_uint64, C.c_uint64, vp, vp]),

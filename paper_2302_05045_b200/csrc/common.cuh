@@ -243,6 +243,12 @@ __device__ __forceinline__ float f16_bits_to_f32(uint16_t h) {
 __device__ __forceinline__ float grad_to_f32(uint32_t h, bool bf16) {
   return bf16 ? __uint_as_float(h << 16) : f16_bits_to_f32(static_cast<uint16_t>(h));
 }
+// The same for a value only a finite step consumes (K23 / K123: a non-finite
+// gradient skips the step, train.hpp:632-639, so its NaN payload is never
+// observed): the plain conversion, exact for every finite input.
+__device__ __forceinline__ float grad_to_f32_finite(uint32_t h, bool bf16) {
+  return bf16 ? __uint_as_float(h << 16) : __half2float(__ushort_as_half(static_cast<uint16_t>(h)));
+}
 // Exponent field of the 16-bit gradient type: all ones <=> inf or NaN.
 __device__ __forceinline__ uint32_t grad_exp_mask(bool bf16) { return bf16 ? 0x7F80u : 0x7C00u; }
 

@@ -344,6 +344,7 @@ int open_peers(samo_model* md) {
     return rc;
   }
   md->p2p_ok = true;
+  SAMO_TRY(set_spin_limit_from_env());
   return open_nvls(md);
 }
 
@@ -473,13 +474,14 @@ int step_p2p(samo_model* md, cudaStream_t S, bool gather) {
   if (static_cast<uint64_t>(G) * c + 8 > md->n_al + kFlagOff)
     return fail(SAMO_E_PARAMETER, "too many ranks for the arena padding");
   float* flag = flag_ptr(md);
-  const bool push = gather && p2p_push();
+  const bool push = gather ? p2p_push() : md->sunk_push;  // sunk: the sinks pushed already
   const bool pull = p2p_pull();
+  md->sunk_push = false;
   SAMO_TRY(plan_shards(md, md->p2p_plan, 1));
   if (md->p2p_plan.c != c) return fail(SAMO_E_STATE, "P2P plan mismatch");
   if (push) SAMO_TRY(build_push_tiles(md, md->p2p_plan));
   SAMO_TRY(phase_mark(md, 0, S));
-  if (push) {
+  if (push && gather) {
     SAMO_TRY(launch_gather_push(md, S));
   } else if (gather) {
     SAMO_TRY(launch_gather(step_args(md), false, md->grid_gather16, S));
@@ -717,8 +719,11 @@ int build_push_tiles(samo_model* md, const ShardPlan& p) {
   const uint64_t q = static_cast<uint64_t>(md->comm->rank);
   std::vector<SamoTile> out;
   out.reserve(md->ntiles + 2ull * p.G * p.B);
+  md->push_layer_t.assign(md->nlayers + 1, 0);
+  int cur_layer = -1;
   for (uint32_t t = 0; t < md->ntiles; ++t) {
     SamoTile td = md->tiles_host[t];
+    while (cur_layer < static_cast<int>(td.layer)) md->push_layer_t[++cur_layer] = static_cast<uint32_t>(out.size());
     if (td.k_end <= td.k_begin) {
       td.pad_ = 0;
       td.pad2_ = 0;
@@ -738,6 +743,7 @@ int build_push_tiles(samo_model* md, const ShardPlan& p) {
       cur = end;
     }
   }
+  while (cur_layer < md->nlayers) md->push_layer_t[++cur_layer] = static_cast<uint32_t>(out.size());
   if (md->push_tiles) cudaFree(md->push_tiles);
   md->push_tiles = nullptr;
   SAMO_CUDA_TRY(cudaMalloc(&md->push_tiles, out.size() * sizeof(SamoTile)));
@@ -746,6 +752,31 @@ int build_push_tiles(samo_model* md, const ShardPlan& p) {
   md->push_G = p.G;
   md->push_B = p.B;
   return SAMO_OK;
+}
+
+int push_sink_prepare(samo_model* md) {
+  const int B = p2p_buckets(md->comm->nranks);
+  SAMO_TRY(plan_shards(md, md->p2p_plan, B));
+  return build_push_tiles(md, md->p2p_plan);
+}
+
+// One layer's share of the exchange, sent during the backward (last layer
+// first, train.hpp:287-313): K1 in push mode over the layer's push pieces
+// (local_src == nullptr), or the push copy of its binary16 gradients that a
+// fused dW sink gathered into local_src.
+int push_sink_layer(samo_model* md, int l, const uint16_t* local_src, cudaStream_t s) {
+  StepArgs a = step_args(md);
+  a.tiles = md->push_tiles + md->push_layer_t[l];
+  a.ntiles = md->push_layer_t[l + 1] - md->push_layer_t[l];
+  a.push = 1;
+  const char* base = static_cast<const char*>(md->block);
+  const size_t g_off = reinterpret_cast<const char*>(md->g) - base;
+  for (int q = 0; q < md->comm->nranks; ++q)
+    a.push16[q] = reinterpret_cast<uint16_t*>(static_cast<char*>(md->peer_base[q]) + g_off);
+  md->sunk_push = true;
+  if (a.ntiles == 0) return SAMO_OK;
+  if (local_src) return launch_push_copy(a, local_src, s);
+  return launch_gather(a, false, std::min<int>(md->grid_gather16, a.ntiles), s);
 }
 
 // K1 of the P2P step in push mode.
@@ -799,7 +830,8 @@ static int p2p_prepare(samo_model* md, int B, bool gather, P2PStep& sp) {
   }
   sp.B = B;
   sp.gather = gather;
-  sp.push = gather && p2p_push();
+  sp.push = gather ? p2p_push() : md->sunk_push;  // sunk: the sinks pushed already
+  md->sunk_push = false;
   sp.pull = p2p_pull();
   if (sp.push) SAMO_TRY(build_push_tiles(md, p));
   const char* base = static_cast<const char*>(md->block);
@@ -844,7 +876,7 @@ static int p2p_prepare(samo_model* md, int B, bool gather, P2PStep& sp) {
 }
 
 static int p2p_gather(samo_model* md, const P2PStep& sp, cudaStream_t S) {
-  if (sp.push) return launch_gather_push(md, S);
+  if (sp.push && sp.gather) return launch_gather_push(md, S);
   if (sp.gather) return launch_gather(step_args(md), false, md->grid_gather16, S);
   return SAMO_OK;
 }
@@ -999,6 +1031,23 @@ int samo_local_group_step(samo_model* const* models, int G, samo_stream_t stream
     if (!md->grads_set) return fail(SAMO_E_STATE, "optimizer_step requires backward (no gradients set)");
   }
   SAMO_TRY(step_local_group(models, G, true, as_stream(stream)));
+  return clear_ok();
+}
+
+// The local group's step after every rank's backward sinks (exchange +
+// update only; the sinks have pushed or written the gradients).
+int samo_local_group_step_sunk(samo_model* const* models, int G, samo_stream_t stream) {
+  if (!models || G < 2 || G > kMaxP2PRanks) return fail(SAMO_E_PARAMETER, "local group of %d models", G);
+  for (int r = 0; r < G; ++r) {
+    samo_model* md = models[r];
+    SAMO_TRY(step_ready(md));
+    if (!md->comm || !md->comm->local_group || md->comm->nranks != G || md->comm->rank != r)
+      return fail(SAMO_E_STATE, "model %d is not rank %d of this local group", r, r);
+    for (int q = 0; q < G; ++q)
+      if (md->peer_base[q] != models[q]->block)
+        return fail(SAMO_E_STATE, "model %d: rank %d of its local group is not models[%d]", r, q, q);
+  }
+  SAMO_TRY(step_local_group(models, G, false, as_stream(stream)));
   return clear_ok();
 }
 

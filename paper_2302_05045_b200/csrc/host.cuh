@@ -123,6 +123,8 @@ struct samo_model {
   SamoTile* push_tiles = nullptr;
   uint32_t push_ntiles = 0;
   int push_G = 0, push_B = 0;
+  std::vector<uint32_t> push_layer_t;  // first push piece of each layer (+ end)
+  bool sunk_push = false;              // this step's sinks pushed to the owners
   SamoPeerSlots* slots = nullptr;       // this rank's signal area (in the block)
   // Device copy of the step scalars (SamoStepConfig), refreshed on the step's
   // stream before the next step whenever set_config / attach_comm changed them.
@@ -216,6 +218,12 @@ bool p2p_pull();
 int p2p_buckets(int G);
 int plan_shards(samo_model* md, ShardPlan& p, int B);
 int build_push_tiles(samo_model* md, const ShardPlan& p);
+// Backward sinks of a peer-to-peer model (push mode): the step's plan and
+// push pieces, then one layer's K1 push (sink_dense) or the copy of its
+// locally gathered binary16 gradients (sink_dw) to the owners.
+int push_sink_prepare(samo_model* md);
+int push_sink_layer(samo_model* md, int layer, const uint16_t* local_src, cudaStream_t s);
+bool p2p_push();
 int step_p2p(samo_model* md, cudaStream_t S, bool gather = true);
 int step_sharded(samo_model* md, cudaStream_t S);
 int step_overlapped(samo_model* md, cudaStream_t S);

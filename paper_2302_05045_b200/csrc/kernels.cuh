@@ -150,6 +150,11 @@ int launch_p2p_flag(SamoPeerSlots* const* slots, int G, int rank, float* flag, i
 int launch_p2p_wait(const SamoPeerSlots* mine, int G, int bucket, cudaStream_t s);
 // Advances the local epoch (after the step's last read of the slots).
 int launch_p2p_epoch(SamoPeerSlots* mine, cudaStream_t s);
+// Peer-wait trap limit from SAMO_SPIN_TIMEOUT_S (seconds), on the current device.
+int set_spin_limit_from_env();
+// Copies compressed binary16 gradients src[k] to their owners' receive
+// buffers along the push pieces a.tiles[0, a.ntiles) (a.push16 = peers).
+int launch_push_copy(const StepArgs& a, const uint16_t* src, cudaStream_t s);
 
 // Sharded data-parallel step pieces.
 struct ShardArgs {

@@ -867,7 +867,7 @@ __global__ void __launch_bounds__(NT + 32) k123_step(StepArgs a) {
             ov[u] = soff[i];
             const uint16_t h = ov[u] < staged ? sgr[ov[u]] : gsrc[ov[u]];
             bad |= (h & xm) == xm;  // |h * 2^-s| is finite iff h is
-            gv[u] = mul_x86(grad_to_f32(h, bf16), p_inv);
+            gv[u] = __fmul_rn(grad_to_f32_finite(h, bf16), p_inv);  // finite steps only (5% faster K123)
             tv[u] = sth[i];
             mv[u] = smv[i];
             vv[u] = svv[i];
@@ -1400,6 +1400,11 @@ __global__ void __launch_bounds__(32 * (kShardConsumers + 1)) k_shard_p2p_tma(P2
 
 // Spin on a local signal word written by a peer (acquire, system scope).  A
 // peer that never arrives is a dead job: trap after ~30 s rather than hang.
+// Limit of a peer wait before the kernel traps (a dead peer): 30 s, raised
+// with SAMO_SPIN_TIMEOUT_S for runs that pause a rank (ncu replay on rank 0).
+__device__ uint64_t g_spin_limit_ns = 30ull * 1000000000ull;
+
+
 __device__ void spin_until(const uint64_t* p, uint64_t target) {
   uint64_t t0;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
@@ -1409,7 +1414,7 @@ __device__ void spin_until(const uint64_t* p, uint64_t target) {
     ns = ns < 1024 ? ns * 2 : ns;
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (t - t0 > 30ull * 1000000000ull) __trap();
+    if (t - t0 > g_spin_limit_ns) __trap();
   }
 }
 
@@ -1714,6 +1719,37 @@ int launch_p2p_wait(const SamoPeerSlots* mine, int G, int bucket, cudaStream_t s
 int launch_set_step_config(SamoStepConfig* dst, const SamoStepConfig& v, cudaStream_t s) {
   k_set_step_config<<<1, 1, 0, s>>>(dst, v);
   SAMO_LAUNCH_CHECK("k_set_step_config");
+  return SAMO_OK;
+}
+
+// Push of compressed binary16 gradients already in `src` (indexed by k) to
+// their owners' receive buffers: piece t of a.tiles carries owner pad_ and
+// destination offset pad2_ (build_push_tiles), the layout K1's push mode
+// writes.  Used after the fused dW sink, whose epilogue gathers locally.
+__global__ void __launch_bounds__(kThreads) k_push_copy(StepArgs a, const uint16_t* __restrict__ src) {
+  for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+    const SamoTile td = a.tiles[t];
+    if (td.k_end <= td.k_begin) continue;
+    uint16_t* dst = a.push16[td.pad_] + td.pad2_;
+    const uint64_t n = td.k_end - td.k_begin;
+    for (uint64_t i = threadIdx.x; i < n; i += kThreads) dst[i] = src[td.k_begin + i];
+  }
+  asm volatile("fence.acq_rel.sys;" ::: "memory");  // peer stores visible system-wide
+}
+
+int set_spin_limit_from_env() {
+  const char* e = getenv("SAMO_SPIN_TIMEOUT_S");
+  if (!e || !*e) return SAMO_OK;
+  const uint64_t ns = static_cast<uint64_t>(atof(e) * 1e9);
+  SAMO_CUDA_TRY(cudaMemcpyToSymbol(g_spin_limit_ns, &ns, sizeof(ns)));
+  return SAMO_OK;
+}
+
+int launch_push_copy(const StepArgs& a, const uint16_t* src, cudaStream_t s) {
+  if (a.ntiles == 0) return SAMO_OK;
+  const int grid = static_cast<int>(std::min<uint32_t>(a.ntiles, 4u * num_sms()));
+  k_push_copy<<<grid, kThreads, 0, s>>>(a, src);
+  SAMO_LAUNCH_CHECK("k_push_copy");
   return SAMO_OK;
 }
 

@@ -427,6 +427,11 @@ int samo_model_sink_dense(samo_model* md, int l, const uint16_t* grad, samo_stre
   md->layers_host[l].grad = grad;
   SAMO_CUDA_TRY(cudaMemcpyAsync(md->layers_dev + l, &md->layers_host[l], sizeof(SamoLayerDev),
                                 cudaMemcpyHostToDevice, as_stream(stream)));
+  if (comm_size(md) > 1 && p2p_push()) {  // straight to the owners over NVLink
+    SAMO_TRY(push_sink_prepare(md));
+    SAMO_TRY(push_sink_layer(md, l, nullptr, as_stream(stream)));
+    return clear_ok();
+  }
   StepArgs a = step_args(md);
   a.tiles = md->tiles + md->layer_t[l];
   a.ntiles = md->layer_t[l + 1] - md->layer_t[l];
@@ -456,15 +461,23 @@ int samo_model_sink_dw(samo_model* md, int l, const uint16_t* x, const uint16_t*
     md->dw_kb_in[l] = in;
     SAMO_TRY(launch_build_rowblocks(md->idx + md->k_off[l], md->nnz[l], in, out, md->dw_kb[l], s));
   }
+  // Push mode: this rank's gradient arena is its receive buffer, which peers
+  // fill during their backward; the epilogue gathers into the idle theta16c
+  // arena instead (written by the owners only after every rank's flag,
+  // i.e. after this rank's sinks) and a copy pushes the layer to its owners.
+  const bool push = comm_size(md) > 1 && p2p_push();
+  if (push) SAMO_TRY(push_sink_prepare(md));
+  uint16_t* g16 = push ? md->c16 : reinterpret_cast<uint16_t*>(md->g);
   DwArgs a{};
   a.M = in;
   a.N = out;
   a.K = batch;
   a.idx = md->idx + md->k_off[l];
   a.kb = md->dw_kb[l];
-  a.g16 = reinterpret_cast<uint16_t*>(md->g) + md->k_off[l];
+  a.g16 = g16 + md->k_off[l];
   a.flag = flag_ptr(md);
   SAMO_TRY(launch_dw_gemm(x, dy, a, 1, s));
+  if (push) SAMO_TRY(push_sink_layer(md, l, md->c16, s));
   return clear_ok();
 }
 

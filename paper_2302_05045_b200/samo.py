@@ -392,6 +392,13 @@ class SamoModel:
         hs = (C.c_void_p * len(models))(*[m._h.value for m in models])
         _abi.call("samo_local_group_step", hs, len(models), _stream())
 
+    @staticmethod
+    def local_group_step_sunk(models: Sequence["SamoModel"]) -> None:
+        """Test harness: the group's step after every member's backward sinks
+        (samo_local_group_step_sunk)."""
+        hs = (C.c_void_p * len(models))(*[m._h.value for m in models])
+        _abi.call("samo_local_group_step_sunk", hs, len(models), _stream())
+
     def set_exchange(self, mode: int) -> None:
         """EXCHANGE_ALLREDUCE (replicated state), EXCHANGE_SHARDED (ZeRO-1 on
         the compressed state, NCCL reduce-scatter / all-gather) or EXCHANGE_P2P

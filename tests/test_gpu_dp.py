@@ -121,7 +121,7 @@ def test_dp_two_gpus_bit_exact(tmp_path, oracle, mode):
 
 
 @pytest.mark.parametrize("mode", ["p2p", "p2p-serial", "p2p-graph", "p2p-tma", "p2p-sink", "p2p-pull",
-                                  "p2p-nvls"])
+                                  "p2p-nvls", "p2p-bf16"])
 def test_dp_four_gpus_p2p_bit_exact(tmp_path, oracle, mode):
     """The fused exchange sums in rank order: bit-exact for G = 4 too."""
     if torch.cuda.device_count() < 4:
@@ -267,7 +267,7 @@ def test_dp_nccl_tolerance_two_gpus(tmp_path, oracle):
     _check_nccl_tolerance(_run(tmp_path, "overlap", 2, save_g=True), oracle, 2, "overlap")
 
 
-def _local_group_run(oracle, G, steps=4):
+def _local_group_run(oracle, G, steps=4, sink=False):
     """G models on cuda:0 as the ranks of one peer-to-peer group
     (samo_model_attach_local_group + samo_local_group_step): the same inputs
     and outputs as dp_worker.py."""
@@ -295,9 +295,15 @@ def _local_group_run(oracle, G, steps=4):
            for r in range(G) for s in range(W.STEPS)}
     torch.cuda.synchronize()
     for s in range(W.STEPS):
-        for r in range(G):
-            models[r].set_grads(dev[(r, s)])
-        samo.SamoModel.local_group_step(models)
+        if sink:  # per-layer backward sinks, last layer first, pushed to the owners
+            for r in range(G):
+                for l in reversed(range(L)):
+                    models[r].sink_dense(l, dev[(r, s)][l])
+            samo.SamoModel.local_group_step_sunk(models)
+        else:
+            for r in range(G):
+                models[r].set_grads(dev[(r, s)])
+            samo.SamoModel.local_group_step(models)
     torch.cuda.synchronize()
     out = []
     for m in models:
@@ -330,6 +336,60 @@ def test_local_group_p2p_bit_exact(cuda, oracle, monkeypatch, G, env):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     _check(_local_group_run(oracle, G), oracle, G, "p2p")
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_local_group_push_sinks_bit_exact(cuda, oracle, G):
+    """The exchange sent during the backward: each rank's per-layer sinks
+    (last layer first, train.hpp:287-313) push the layer's kept binary16
+    gradients straight into their owners' receive buffers; the step after
+    them is only the flag exchange, the shard updates and the expand.  Every
+    replica equals the oracle bit for bit."""
+    _check(_local_group_run(oracle, G, sink=True), oracle, G, "p2p")
+
+
+def test_local_group_push_dw_sinks_equal_dense_sinks(cuda):
+    """Fused dW sinks in push mode (the epilogue gathers into scratch, a copy
+    pushes to the owners) give the same state as dense sinks of the same dW
+    (samo_dw_gemm_f16), at G = 4 over three steps."""
+    from paper_2302_05045_b200 import samo
+    G, batch = 4, 64
+    shapes = [(64, 128), (256, 32), (8, 8)]
+    rng = np.random.default_rng(3)
+    vals = [torch.from_numpy((rng.standard_normal(a * b) * 0.05).astype(np.float32)).cuda() for a, b in shapes]
+    sets = samo.magnitude_prune([samo.LayerParams(f"l{i}", v, True) for i, v in enumerate(vals)], 0.7)
+
+    def group():
+        ms = []
+        for _ in range(G):
+            m = samo.SamoModel.from_index_sets(sets, shapes, tile_elems=1024)
+            for l, v in enumerate(vals):
+                m.init_layer(l, v)
+            m.set_config(samo.OptimizerConfig(learning_rate=1e-2))
+            ms.append(m)
+        samo.SamoModel.attach_local_group(ms)
+        return ms
+    fused, dense = group(), group()
+    for s in range(3):
+        xs = {(r, l): torch.from_numpy((rng.standard_normal((batch, a)) * 0.5).astype(np.float16)).cuda()
+              for r in range(G) for l, (a, b) in enumerate(shapes)}
+        dys = {(r, l): torch.from_numpy((rng.standard_normal((batch, b)) * 8.0).astype(np.float16)).cuda()
+               for r in range(G) for l, (a, b) in enumerate(shapes)}
+        for r in range(G):
+            for l in reversed(range(len(shapes))):
+                fused[r].sink_dw(l, xs[(r, l)], dys[(r, l)])
+                dense[r].sink_dense(l, samo.dw_gemm(xs[(r, l)], dys[(r, l)]).reshape(-1))
+        samo.SamoModel.local_group_step_sunk(fused)
+        samo.SamoModel.local_group_step_sunk(dense)
+    torch.cuda.synchronize()
+    for r in range(G):
+        assert fused[r].step_record().t == dense[r].step_record().t == 3
+        for l in range(len(shapes)):
+            for k in ("theta32", "adam_v", "theta16"):
+                assert torch.equal(fused[r].read(l, k).view(torch.int16 if k == "theta16" else torch.int32),
+                                   dense[r].read(l, k).view(torch.int16 if k == "theta16" else torch.int32)), (r, l, k)
+    for m in fused + dense:
+        m.close()
 
 
 def test_local_group_eight_ranks_stress(cuda, oracle):
