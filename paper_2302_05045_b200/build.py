@@ -19,6 +19,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libsamo_cuda.so"
+CHECKED_LIB = PKG / "libsamo_cuda_checked.so"
 SOURCES = ["abi.cu", "model.cu", "dp.cu", "kernels_step.cu", "kernels_fused.cu", "kernels_prune.cu", "kernels_gemm.cu"]
 HEADERS = ["common.cuh", "kernels.cuh", "host.cuh"]
 
@@ -38,45 +39,50 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
-def _stale() -> bool:
-    if not LIB.exists():
+def _stale(lib: Path = None) -> bool:
+    lib = lib or LIB
+    if not lib.exists():
         return True
-    t = LIB.stat().st_mtime
+    t = lib.stat().st_mtime
     deps = [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "samo_cuda.h",
                                                     ROOT / "include" / "samo_cuda_testing.h", Path(__file__)]
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
-        return LIB
-    objdir = PKG / "build"
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> Path:
+    """checked: device bounds checks + trapping waits (-DSAMO_CHECKED) into
+    libsamo_cuda_checked.so, for test runs with SAMO_LIB pointing at it."""
+    lib = CHECKED_LIB if checked else LIB
+    if not force and not _stale(lib):
+        return lib
+    objdir = PKG / ("build_checked" if checked else "build")
     objdir.mkdir(exist_ok=True)
     objs = []
     for src in SOURCES:
         obj = objdir / (Path(src).stem + ".o")
-        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-I", str(CSRC),
-               "-c", str(CSRC / src), "-o", str(obj)]
+        cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *(["-DSAMO_CHECKED"] if checked else []),
+               "-I", str(ROOT / "include"), "-I", str(CSRC), "-c", str(CSRC / src), "-o", str(obj)]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     link = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *objs,
             "-L/usr/lib/x86_64-linux-gnu", "-lnccl", "-cudart", "static",
             "-Xlinker", "--no-undefined"]
     if verbose:
         print(" ".join(link), flush=True)
     subprocess.run(link, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-v", "--verbose", action="store_true")
+    ap.add_argument("--checked", action="store_true", help="device bounds checks (libsamo_cuda_checked.so)")
     a = ap.parse_args()
-    print(build(force=a.force, verbose=a.verbose))
+    print(build(force=a.force, verbose=a.verbose, checked=a.checked))
     sys.exit(0)

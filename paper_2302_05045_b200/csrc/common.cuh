@@ -10,6 +10,8 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 
+#include <cstdio>
+
 #include "samo_cuda_testing.h"
 
 namespace samo_dev {
@@ -74,6 +76,39 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
+// Checked builds (python -m paper_2302_05045_b200.build --checked ->
+// libsamo_cuda_checked.so, loaded with SAMO_LIB): device-side bounds checks
+// on shared-memory and arena indices, and mbarrier waits that trap instead of
+// hanging.  The stand-in for compute-sanitizer, which this pool does not run.
+#ifdef SAMO_CHECKED
+#define SAMO_DCHECK(cond)                                                               \
+  do {                                                                                  \
+    if (!(cond)) {                                                                      \
+      printf("SAMO_DCHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,  \
+             static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x), #cond);        \
+      __trap();                                                                         \
+    }                                                                                   \
+  } while (0)
+#else
+#define SAMO_DCHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
+
+#ifdef SAMO_CHECKED
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  for (uint64_t spin = 0;; ++spin) {
+    uint32_t done;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    SAMO_DCHECK(spin < (1ull << 28));  // a lost arrival: fail instead of hanging
+  }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -85,6 +120,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+#endif
 
 // 1-D bulk copy global -> shared, completion signalled on `bar` (UBLKCP).
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,

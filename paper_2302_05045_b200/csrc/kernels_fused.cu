@@ -159,6 +159,8 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
     // binary16 destination of element k: the local arena, or (push) the
     // owner's receive buffer over NVLink (tile-constant shift, same k % 8)
     uint16_t* g16 = reinterpret_cast<uint16_t*>(a.g);
+    SAMO_DCHECK(td.k_begin <= td.k_end && td.dense_count <= T);
+    SAMO_DCHECK(!a.push || td.pad_ < static_cast<uint32_t>(kMaxP2PRanks));
     if (!OUT_F32 && a.push)
       g16 = reinterpret_cast<uint16_t*>(reinterpret_cast<uintptr_t>(a.push16[td.pad_]) +
                                         2 * (td.pad2_ - td.k_begin));
@@ -176,6 +178,7 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
     const uint64_t ke8 = ka + ((ke - ka) & ~7ull);
     auto gather_one = [&](uint64_t k) {
       const uint16_t off = a.off16[k];
+      SAMO_DCHECK(off < td.dense_count && k >= td.k_begin && k < td.k_end);
       const uint16_t h = off < staged ? sg[off] : gsrc[off];
       if constexpr (OUT_F32) {
         const float gk = mul_x86(grad_to_f32(h, bf16), inv_scale);
@@ -198,6 +201,7 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const uint32_t o0 = ow[e] & 0xFFFFu, o1 = ow[e] >> 16;
+        SAMO_DCHECK(o0 < td.dense_count && o1 < td.dense_count);
         const uint32_t h0 = o0 < staged ? sg[o0] : gsrc[o0];
         const uint32_t h1 = o1 < staged ? sg[o1] : gsrc[o1];
         hw[e] = h0 | (h1 << 16);
@@ -445,7 +449,10 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
       if constexpr (EXPAND) {
         const uint16_t* sval = reinterpret_cast<const uint16_t*>(st + 3 * L::kF32) + ho;
 #pragma unroll 4
-        for (uint32_t i = tid; i < n; i += kThreads) out[soff[i]] = sval[i];
+        for (uint32_t i = tid; i < n; i += kThreads) {
+          SAMO_DCHECK(soff[i] < p_T);
+          out[soff[i]] = sval[i];
+        }
       } else {
 #pragma unroll 1
       for (uint32_t ib = tid; ib < n; ib += kU * kThreads) {
@@ -465,6 +472,7 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
             mv[u] = smv[i];
             vv[u] = svv[i];
             ov[u] = soff[i];
+            SAMO_DCHECK(ov[u] < p_T);
           }
         }
 #pragma unroll
@@ -710,6 +718,7 @@ __global__ void __launch_bounds__(NT + 32) k123_step(StepArgs a) {
           break;
         }
         const TileFull td = load_tile_full(a.tiles + t);
+        SAMO_DCHECK(td.dense_count <= T && td.k_begin <= td.k_end);
         const uint16_t* grad = a.layers[td.layer].grad + td.dense_begin;
         const uint32_t t_cur = t;
         t = atomicAdd(&a.st->tile_next, 1u);
@@ -865,6 +874,7 @@ __global__ void __launch_bounds__(NT + 32) k123_step(StepArgs a) {
           const uint32_t i = ib + u * NT;
           if (i < n) {
             ov[u] = soff[i];
+            SAMO_DCHECK(ov[u] < sl.dense_count && n <= CH);
             const uint16_t h = ov[u] < staged ? sgr[ov[u]] : gsrc[ov[u]];
             bad |= (h & xm) == xm;  // |h * 2^-s| is finite iff h is
             gv[u] = __fmul_rn(grad_to_f32_finite(h, bf16), p_inv);  // finite steps only (5% faster K123)
@@ -1730,6 +1740,7 @@ __global__ void __launch_bounds__(kThreads) k_push_copy(StepArgs a, const uint16
   for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
     const SamoTile td = a.tiles[t];
     if (td.k_end <= td.k_begin) continue;
+    SAMO_DCHECK(td.pad_ < static_cast<uint32_t>(kMaxP2PRanks));
     uint16_t* dst = a.push16[td.pad_] + td.pad2_;
     const uint64_t n = td.k_end - td.k_begin;
     for (uint64_t i = threadIdx.x; i < n; i += kThreads) dst[i] = src[td.k_begin + i];

@@ -401,6 +401,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               if (j + u < cnt) {
+                SAMO_DCHECK(ix[u] >= colbase && ix[u] - colbase < L::kHalf);
                 const uint16_t hv = mine[ix[u] - colbase];
                 a.g16[ks + j + u] = hv;
                 bad |= (hv & 0x7C00u) == 0x7C00u;
