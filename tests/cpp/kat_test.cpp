@@ -1,5 +1,5 @@
 // kat_test.cpp — the reference's own known-answer tests, restated against the
-// CUDA-backed drop-in API (include/samo_b200/samo.hpp).  Each block names the
+// CUDA-backed drop-in API (namespace samo, include/samo_b200/samo.hpp).  Each block names the
 // reference test it ports (proj/tests/*.cpp).  Built by tests/test_cpp_kat.py;
 // prints one line per test and exits non-zero on the first failure group.
 #include <bit>
@@ -13,7 +13,7 @@
 
 #include "samo_b200/samo.hpp"
 
-using namespace samo_b200;
+using namespace samo;
 
 static int g_fail = 0, g_pass = 0;
 
