@@ -664,7 +664,7 @@ __device__ __forceinline__ uint32_t lane_mask2(uint32_t bits, int e) {
 }
 
 template <int CH, int NS, int NT, bool CFG>
-__global__ void __launch_bounds__(NT + 32) k123_step(StepArgs a) {
+__global__ void __launch_bounds__(NT + 32, 512 / NT) k123_step(StepArgs a) {
   using L = K123Layout<CH>;
   constexpr uint32_t kConsumerWarps = NT / 32;
   constexpr int NSG = kK123Slots;

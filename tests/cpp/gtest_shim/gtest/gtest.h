@@ -79,9 +79,31 @@ std::string cmp_text(const char* op, const char* ea, const char* eb, const A& a,
   return std::string("Expected: (") + ea + ") " + op + " (" + eb + "), actual: " + show(a) + " vs " + show(b);
 }
 
-inline int run_all() {
+// --gtest_filter=A.*:B.c (':'-separated patterns, '*' wildcard), as GoogleTest.
+inline bool glob_match(const char* p, const char* s) {
+  if (*p == '\0') return *s == '\0';
+  if (*p == '*') return glob_match(p + 1, s) || (*s && glob_match(p, s + 1));
+  return *s == *p && glob_match(p + 1, s + 1);
+}
+inline bool selected(const std::string& filter, const std::string& name) {
+  if (filter.empty()) return true;
+  std::size_t b = 0;
+  while (b <= filter.size()) {
+    const std::size_t e = filter.find(':', b);
+    const std::string pat = filter.substr(b, e == std::string::npos ? std::string::npos : e - b);
+    if (glob_match(pat.c_str(), name.c_str())) return true;
+    if (e == std::string::npos) break;
+    b = e + 1;
+  }
+  return false;
+}
+
+inline int run_all(const std::string& filter = "") {
   int failed = 0;
+  std::size_t ran = 0;
   for (const auto& t : registry()) {
+    if (!selected(filter, std::string(t.suite) + "." + t.name)) continue;
+    ++ran;
     current_failed() = false;
     std::printf("[ RUN      ] %s.%s\n", t.suite, t.name);
     try {
@@ -96,8 +118,8 @@ inline int run_all() {
     std::printf("%s %s.%s\n", current_failed() ? "[  FAILED  ]" : "[       OK ]", t.suite, t.name);
     failed += current_failed() ? 1 : 0;
   }
-  std::printf("[==========] %zu tests, %zu passed, %d failed\n", registry().size(),
-              registry().size() - static_cast<std::size_t>(failed), failed);
+  std::printf("[==========] %zu tests, %zu passed, %d failed\n", ran, ran - static_cast<std::size_t>(failed),
+              failed);
   return failed ? 1 : 0;
 }
 
@@ -166,4 +188,9 @@ inline int run_all() {
 #define EXPECT_NO_THROW(stmt) MG_NOTHROW_(stmt, )
 #define ASSERT_NO_THROW(stmt) MG_NOTHROW_(stmt, return)
 
-int main() { return ::mini_gtest::run_all(); }
+int main(int argc, char** argv) {
+  std::string filter;
+  for (int i = 1; i < argc; ++i)
+    if (std::string(argv[i]).rfind("--gtest_filter=", 0) == 0) filter = std::string(argv[i]).substr(15);
+  return ::mini_gtest::run_all(filter);
+}

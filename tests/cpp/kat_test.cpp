@@ -11,7 +11,7 @@
 #include <string>
 #include <vector>
 
-#include "samo_b200/samo.hpp"
+#include "samo/samo.hpp"  // the reference header name -> the CUDA-backed mirror
 
 using namespace samo;
 

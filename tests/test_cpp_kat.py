@@ -88,6 +88,20 @@ def test_reference_store_test_compiles_against_mirror():
     assert build_ref_store_test().exists()
 
 
+def test_reference_store_test_host_suites_on_cpu():
+    """The host-arithmetic suites of the reference's store_test.cpp
+    (MemoryModel's Rational arithmetic and analytical model, the empty-model
+    measured_bytes) run without a GPU; the rest needs the device."""
+    exe = build_ref_store_test()
+    if exe is None:
+        pytest.skip("no reference store_test binary")
+    res = subprocess.run([str(exe), "--gtest_filter=MemoryModel.PaperEndpoints:MemoryModel.ReportIdentities:"
+                          "MemoryModel.Savings*:MeasuredBytes.EmptyModel"],
+                         capture_output=True, text=True, timeout=120)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
+    assert "4 tests, 4 passed, 0 failed" in res.stdout, res.stdout[-2000:]
+
+
 @pytest.mark.gpu
 def test_reference_store_test_passes_on_device(cuda):
     exe = build_ref_store_test()
