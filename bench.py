@@ -990,6 +990,7 @@ def sunk_pass(model, grads, stream, dev, reps: int = 3):
     and the expand.  Times both parts (max over ranks): the sinks run back to
     back here (no backward compute to hide under), so sinks_ms is what a
     backward would absorb and step_after_sinks_ms what is left after it."""
+    import torch
     import torch.distributed as dist
     L = len(grads)
     e = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(reps)]

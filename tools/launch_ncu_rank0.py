@@ -30,6 +30,7 @@ def main() -> None:
     cmd = sys.argv[sys.argv.index("--") + 1:]
     kfilter = os.environ.get("NCU_KERNELS", "regex:k1_gather|k_shard_p2p")
     count = os.environ.get("NCU_COUNT", "6")
+    plain_first = os.environ.get("NCU_PLAIN_FIRST", "1") != "0"
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
@@ -41,6 +42,10 @@ def main() -> None:
         if r == 0:
             c = ["ncu", "--metrics", METRICS, "--clock-control", "none", "-k", kfilter, "-c", count,
                  "-f", "-o", out] + c
+        elif plain_first:
+            # the pool's ncu first runs rank 0's command once without ncu: the
+            # other ranks take part in that run and then in the profiled one
+            c = ["bash", "-c", " ".join(cmd) + " && " + " ".join(cmd)]
         procs.append(subprocess.Popen(c, env=env))
     rc = 0
     for p in procs:
