@@ -192,20 +192,14 @@ struct DwArgs {
   uint16_t* dw;          // epi 0
   const uint32_t* idx;   // epi 1: layer's ascending kept indices
   const uint32_t* kb;    // epi 1: [(col blocks + 1) x M] row/column-block k starts
-  const uint4* msk;      // epi 1: [col blocks x M] kept columns of each row's 128-column block
   uint16_t* g16;         // epi 1: layer's compressed binary16 gradient
   float* flag;           // epi 1: skip indicator
   uint32_t tail0;        // set by launch_dw_gemm: pair tiles >= tail0 run as two 256 x BN/2 halves
 };
 int dw_check(uint64_t batch, uint64_t in, uint64_t out, const void* x, const void* dy);
 uint32_t dw_col_blocks(uint64_t out);
-// kb: (col blocks + 1) x in u32 row/column-block k starts; msk: col blocks x
-// in 128-bit masks of the kept columns (16-byte aligned).  u32 entries of the
-// combined table: dw_table_entries(in, out).
 int launch_build_rowblocks(const uint32_t* idx, uint64_t n, uint64_t in, uint64_t out, uint32_t* kb,
-                           uint4* msk, cudaStream_t s);
-uint64_t dw_table_entries(uint64_t in, uint64_t out);
-uint64_t dw_mask_offset(uint64_t in, uint64_t out);  // u32 offset of msk in the table
+                           cudaStream_t s);
 int launch_dw_gemm(const uint16_t* x, const uint16_t* dy, const DwArgs& a, int epi, cudaStream_t s);
 
 template <int MODE, typename OutT>

@@ -303,13 +303,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
       for (uint32_t u = cid; u < nunits; u += ncl, ++i) {
         const uint32_t idesc = u < tail0 ? idesc_full : idesc_half;
         const uint32_t buf = i % NBUF;
-        // MS = 1: wait until both epilogues drained this buffer.  MS = 2 (one
-        // buffer, sub-tiles j = 0, 1 in acce[j]): the first k-block issues
-        // all of sub-tile 0's MMAs once sub-tile 0 is drained and only then
-        // waits for sub-tile 1, so the mainloop restarts while the epilogue
-        // still drains sub-tile 1 (each accumulator sees the same MMA order).
-        if (MS == 1 && i >= NBUF) mbar_wait_bounded(&acce[buf], ((i / NBUF) - 1) & 1u);
-        if (MS == 2 && i >= 1) mbar_wait_bounded(&acce[0], (i - 1) & 1u);
+        if (i >= NBUF) mbar_wait_bounded(&acce[buf], ((i / NBUF) - 1) & 1u);  // both epilogues drained it
         tc_fence_after();
         const uint32_t acc = tmem + buf * MS * BN;
         for (uint32_t kb = 0; kb < nk; ++kb, ++g) {
@@ -317,29 +311,13 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
           mbar_wait_bounded(&full[s], (g / NS) & 1u);
           tc_fence_after();
           const uint32_t sa = smem_addr(ring + s * L::kStage), sb = sa + L::kA;
-          if (MS == 2 && kb == 0) {
+#pragma unroll
+          for (uint32_t kk = 0; kk < kBK / 16; ++kk) {  // UMMA_K = 16: 16 K-rows of 128 bytes
+            const uint64_t db = umma_desc_mn_sw128(sb + kk * 2048, kBox, 1024);
 #pragma unroll
             for (uint32_t j = 0; j < static_cast<uint32_t>(MS); ++j) {
-              if (j == 1 && i >= 1) {
-                mbar_wait_bounded(&acce[1], (i - 1) & 1u);
-                tc_fence_after();
-              }
-#pragma unroll
-              for (uint32_t kk = 0; kk < kBK / 16; ++kk) {
-                const uint64_t db = umma_desc_mn_sw128(sb + kk * 2048, kBox, 1024);
-                const uint64_t da = umma_desc_mn_sw128(sa + 2 * j * kBox + kk * 2048, kBox, 1024);
-                umma_f16_pair(acc + j * BN, da, db, idesc, kk != 0u);
-              }
-            }
-          } else {
-#pragma unroll
-            for (uint32_t kk = 0; kk < kBK / 16; ++kk) {  // UMMA_K = 16: 16 K-rows of 128 bytes
-              const uint64_t db = umma_desc_mn_sw128(sb + kk * 2048, kBox, 1024);
-#pragma unroll
-              for (uint32_t j = 0; j < static_cast<uint32_t>(MS); ++j) {
-                const uint64_t da = umma_desc_mn_sw128(sa + 2 * j * kBox + kk * 2048, kBox, 1024);
-                umma_f16_pair(acc + j * BN, da, db, idesc, (kb | kk) != 0u);
-              }
+              const uint64_t da = umma_desc_mn_sw128(sa + 2 * j * kBox + kk * 2048, kBox, 1024);
+              umma_f16_pair(acc + j * BN, da, db, idesc, (kb | kk) != 0u);
             }
           }
           umma_commit_pair_mc(&empty[s], 0x3);  // frees the stage in both CTAs
@@ -361,16 +339,9 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
       const uint32_t nhalves = t.width / L::kHalf;
       mbar_wait_bounded(&accf[buf], (i / NBUF) & 1u);
       tc_fence_after();
-      if (gx >= nhalves) {  // nothing of this unit for this group: release the buffer(s) at once
+      if (gx >= nhalves) {  // nothing of this unit for this group: release the buffer at once
         __syncwarp();
-        if (lane == 0) {
-          if (MS == 2) {
-            mbar_arrive_cluster(mapa_shared(smem_addr(&acce[0]), 0));
-            mbar_arrive_cluster(mapa_shared(smem_addr(&acce[1]), 0));
-          } else {
-            mbar_arrive_cluster(mapa_shared(smem_addr(&acce[buf]), 0));
-          }
-        }
+        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_addr(&acce[buf]), 0));
         continue;
       }
 #pragma unroll 1
@@ -382,13 +353,11 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
       for (uint32_t h = gx; h < nhalves; h += EW) {
         const uint64_t nh = static_cast<uint64_t>(t.n0) + h * L::kHalf;  // first column of this half
         uint32_t ks = 0, cnt = 0;
-        uint4 mk = make_uint4(0u, 0u, 0u, 0u);
-        if constexpr (EPI == 1) {  // this row's kept range and columns in the half (128-column blocks)
+        if constexpr (EPI == 1) {  // this row's kept range in the column half (kb: 128-column blocks)
           if (row < a.M && nh < a.N) {
             const uint64_t cb = nh / L::kHalf;
             ks = a.kb[cb * a.M + row];
             cnt = a.kb[(cb + 1) * a.M + row] - ks;
-            mk = __ldg(a.msk + cb * a.M + row);
           }
         }
         // accumulator half -> binary16 -> staging row r: the four 32-column
@@ -413,40 +382,32 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
             }
           }
         }
-        if (h + EW >= nhalves && (MS == 2 || sub + 1 == MS)) {  // this group's last half of the sub-tile
+        if (sub + 1 == MS && h + EW >= nhalves) {  // this group's last half: TMEM drained for it
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_addr(&acce[MS == 2 ? sub : buf]), 0));
+          if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_addr(&acce[buf]), 0));
         }
         if constexpr (EPI == 1) {
-          // Gather.  Each thread compacts its own staged row (TMEM lane = tile
-          // row) in place to the kept columns of the half — the bits of its
-          // 128-bit mask, ascending, so the write never passes the read —
-          // then the warp writes its 32 rows' kept ranges [ks, ks + cnt) of
-          // the arena with coalesced stores, one row at a time.
-          uint16_t* mine = tile + r * L::kTileLd;
-          uint32_t bad = 0, j = 0;
-          const uint32_t mw[4] = {mk.x, mk.y, mk.z, mk.w};
+          // Gather of this thread's own row (TMEM lane = tile row): its kept
+          // elements in the half are the arena range [ks, ks + cnt), read
+          // back from the row it just staged, so no barrier is needed.
+          const uint16_t* mine = tile + r * L::kTileLd;
+          const uint32_t colbase = static_cast<uint32_t>(row * a.N + nh);
+          uint32_t bad = 0;
+          for (uint32_t j = 0; j < cnt; j += 4) {
+            uint32_t ix[4];
 #pragma unroll
-          for (int w = 0; w < 4; ++w) {
-            uint32_t bits = mw[w];
-            while (bits) {
-              const uint32_t c = 32u * w + (__ffs(bits) - 1);
-              bits &= bits - 1;
-              const uint16_t hv = mine[c];
-              bad |= (hv & 0x7C00u) == 0x7C00u;
-              mine[j++] = hv;
+            for (int u = 0; u < 4; ++u) ix[u] = j + u < cnt ? __ldg(a.idx + ks + j + u) : colbase;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (j + u < cnt) {
+                SAMO_DCHECK(ix[u] >= colbase && ix[u] - colbase < L::kHalf);
+                const uint16_t hv = mine[ix[u] - colbase];
+                a.g16[ks + j + u] = hv;
+                bad |= (hv & 0x7C00u) == 0x7C00u;
+              }
             }
           }
-          SAMO_DCHECK(j == cnt);
-          __syncwarp();
-          const uint16_t* wrows = tile + (q * 32u) * L::kTileLd;
-#pragma unroll 4
-          for (uint32_t rr = 0; rr < 32; ++rr) {
-            const uint32_t c_r = __shfl_sync(0xFFFFFFFFu, cnt, rr), s_r = __shfl_sync(0xFFFFFFFFu, ks, rr);
-            for (uint32_t e = lane; e < c_r; e += 32) a.g16[s_r + e] = wrows[rr * L::kTileLd + e];
-          }
-          __syncwarp();  // the staging rows are rewritten by the next half
           if (__any_sync(0xFFFFFFFFu, bad) && lane == 0) atomicAdd(a.flag, 1.0f);
         } else {
           asm volatile("bar.sync %0, 128;" ::"r"(1 + gx) : "memory");
@@ -471,16 +432,6 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kCols) : "memory");
-  }
-}
-
-// msk[b * M + i]: bit c of the 128-bit mask set when column b * 128 + c of
-// row i is kept (zeroed before).
-__global__ void k_build_colmask(const uint32_t* idx, uint64_t n, uint64_t N, uint64_t M, uint32_t* msk) {
-  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n;
-       k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t i = idx[k] / N, c = idx[k] % N;
-    atomicOr(msk + ((c >> 7) * M + i) * 4 + ((c >> 5) & 3u), 1u << (c & 31u));
   }
 }
 
@@ -548,22 +499,13 @@ int dw_check(uint64_t batch, uint64_t in, uint64_t out, const void* x, const voi
 
 uint32_t dw_col_blocks(uint64_t out) { return static_cast<uint32_t>((out + kKbCols - 1) / kKbCols); }
 
-uint64_t dw_mask_offset(uint64_t in, uint64_t out) { return ((dw_col_blocks(out) + 1ull) * in + 3) & ~3ull; }
-uint64_t dw_table_entries(uint64_t in, uint64_t out) { return dw_mask_offset(in, out) + 4ull * dw_col_blocks(out) * in; }
-
 int launch_build_rowblocks(const uint32_t* idx, uint64_t n, uint64_t in, uint64_t out, uint32_t* kb,
-                           uint4* msk, cudaStream_t s) {
+                           cudaStream_t s) {
   const uint32_t nb = dw_col_blocks(out);
   const uint64_t total = (nb + 1ull) * in;
   const int grid = static_cast<int>((total + 255) / 256);
   k_build_rowblocks<<<grid, 256, 0, s>>>(idx, n, in, out, kKbCols, nb, kb);
   SAMO_LAUNCH_CHECK("k_build_rowblocks");
-  SAMO_CUDA_TRY(cudaMemsetAsync(msk, 0, static_cast<size_t>(nb) * in * sizeof(uint4), s));
-  if (n) {
-    const int g2 = static_cast<int>(std::min<uint64_t>((n + 255) / 256, 4096));
-    k_build_colmask<<<g2, 256, 0, s>>>(idx, n, out, in, reinterpret_cast<uint32_t*>(msk));
-    SAMO_LAUNCH_CHECK("k_build_colmask");
-  }
   return SAMO_OK;
 }
 

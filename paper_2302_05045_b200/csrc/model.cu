@@ -456,11 +456,10 @@ int samo_model_sink_dw(samo_model* md, int l, const uint16_t* x, const uint16_t*
   if (!md->dw_kb[l] || md->dw_kb_in[l] != in) {
     if (md->dw_kb[l]) cudaFree(md->dw_kb[l]);
     md->dw_kb[l] = nullptr;
-    const uint64_t entries = dw_table_entries(in, out);  // kb starts + 128-column masks
+    const uint64_t entries = (dw_col_blocks(out) + 1ull) * in;
     SAMO_CUDA_TRY(cudaMalloc(&md->dw_kb[l], entries * sizeof(uint32_t)));
     md->dw_kb_in[l] = in;
-    SAMO_TRY(launch_build_rowblocks(md->idx + md->k_off[l], md->nnz[l], in, out, md->dw_kb[l],
-                                    reinterpret_cast<uint4*>(md->dw_kb[l] + dw_mask_offset(in, out)), s));
+    SAMO_TRY(launch_build_rowblocks(md->idx + md->k_off[l], md->nnz[l], in, out, md->dw_kb[l], s));
   }
   // Push mode: this rank's gradient arena is its receive buffer, which peers
   // fill during their backward; the epilogue gathers into the idle theta16c
@@ -475,7 +474,6 @@ int samo_model_sink_dw(samo_model* md, int l, const uint16_t* x, const uint16_t*
   a.K = batch;
   a.idx = md->idx + md->k_off[l];
   a.kb = md->dw_kb[l];
-  a.msk = reinterpret_cast<const uint4*>(md->dw_kb[l] + dw_mask_offset(md->dw_kb_in[l], out));
   a.g16 = g16 + md->k_off[l];
   a.flag = flag_ptr(md);
   SAMO_TRY(launch_dw_gemm(x, dy, a, 1, s));
