@@ -589,7 +589,7 @@ def run_samo(args) -> None:
     torch.cuda.synchronize()
     launches0 = samo.kernel_launch_count()
     nvl = nvl0 = None
-    if world > 1:  # NVLink bytes this GPU sent / received over the timed region
+    if world > 1 and os.environ.get("SAMO_BENCH_NVLINK") == "1":  # NVLink bytes sent / received (NVML)
         try:
             from paper_2302_05045_b200.nvlink import NvlinkBytes
             nvl = NvlinkBytes(int(smi_index))
@@ -633,7 +633,7 @@ def run_samo(args) -> None:
                                "note": "whole device over the timed region (all kernels, NCCL "
                                        "barriers included), divided by the steps"}
         else:
-            nvlink_measured = {"unavailable": nvl0}
+            nvlink_measured = {"unavailable": nvl0 or "NVML NVLink counters not read (SAMO_BENCH_NVLINK=1 reads them)"}
     phases = pipeline = overlap = None
     fused_ms = None
     fused = world == 1 and os.environ.get("SAMO_FUSED_STEP", "1") != "0"
