@@ -1005,7 +1005,7 @@ def sunk_pass(model, grads, stream, dev, reps: int = 3):
     import torch
     import torch.distributed as dist
     L = len(grads)
-    e = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(reps)]
+    e = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(reps)]
     for r in range(reps + 1):
         dist.barrier()
         torch.cuda.synchronize()
@@ -1016,12 +1016,19 @@ def sunk_pass(model, grads, stream, dev, reps: int = 3):
             model.sink_dense(l, grads[l])
         if ev:
             ev[1].record(stream)
-        model.step_sunk()
+        # every rank's backward (here: its sink launches) ends before the step
+        # after it, as in synchronous training, so the host-launch skew of 388
+        # Python calls per rank is not charged to the step
+        torch.cuda.synchronize()
+        dist.barrier()
         if ev:
             ev[2].record(stream)
+        model.step_sunk()
+        if ev:
+            ev[3].record(stream)
     torch.cuda.synchronize()
     sk = statistics.median(x[0].elapsed_time(x[1]) for x in e)
-    st = statistics.median(x[1].elapsed_time(x[2]) for x in e)
+    st = statistics.median(x[2].elapsed_time(x[3]) for x in e)
     t = torch.tensor([sk, st], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return {"sinks_ms": round(float(t[0]), 4), "step_after_sinks_ms": round(float(t[1]), 4),
