@@ -163,23 +163,6 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
     }
   }
 
-  // CLAIM: thread 0's finished pieces of its current bucket; reporting them
-  // makes them visible system-wide first, and the report completing the
-  // bucket tells every rank (bucket of a piece = the host's rule).
-  uint32_t sig_b = 0xFFFFFFFFu, sig_n = 0;
-  auto signal_bucket = [&](uint32_t b, uint32_t n) {
-    if (n == 0) return;
-    asm volatile("fence.acq_rel.sys;" ::: "memory");
-    const uint32_t done = atomicAdd(a.sig_ctl + 2 + b, n) + n;
-    if (done == a.sig_cnt[b]) {
-      asm volatile("fence.acq_rel.sys;" ::: "memory");
-      const uint64_t e = a.sig_slots[a.sig_rank]->epoch + 1;
-      const int slot = static_cast<int>(b) * kMaxP2PRanks + a.sig_rank;
-      for (int q = 0; q < a.sig_G; ++q) st_release_sys(&a.sig_slots[q]->push_epoch[slot], e);
-      a.sig_ctl[2 + b] = 0u;  // every piece of b is done: rewind for the next step
-    }
-  };
-
   bool bad = false;
   const bool bf16 = a.grad_bf16 != 0;
   const uint32_t xm = grad_exp_mask(bf16);
@@ -263,17 +246,19 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
     __syncthreads();  // every thread is done reading stage s (and storing its pushes)
     if (tid == 0) {
       if constexpr (CLAIM) {
-        // Pieces are claimed in k order, so this CTA's buckets only grow: it
-        // reports its finished pieces of a bucket once, when it moves on to
-        // the next bucket (one system fence per bucket, not per piece).
+        // this piece's pushes are visible system-wide; the CTA completing the
+        // bucket's last piece tells every rank (bucket = the host's rule)
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
         const uint64_t bq = td.k_begin / a.sig_C;
         const uint32_t b = bq < a.sig_B - 1 ? static_cast<uint32_t>(bq) : a.sig_B - 1;
-        if (b != sig_b) {
-          signal_bucket(sig_b, sig_n);
-          sig_b = b;
-          sig_n = 0;
+        const uint32_t done = atomicAdd(a.sig_ctl + 2 + b, 1u) + 1u;
+        if (done == a.sig_cnt[b]) {
+          asm volatile("fence.acq_rel.sys;" ::: "memory");
+          const uint64_t e = a.sig_slots[a.sig_rank]->epoch + 1;
+          const int slot = static_cast<int>(b) * kMaxP2PRanks + a.sig_rank;
+          for (int q = 0; q < a.sig_G; ++q) st_release_sys(&a.sig_slots[q]->push_epoch[slot], e);
+          a.sig_ctl[2 + b] = 0u;  // every piece of b is done: rewind for the next step
         }
-        ++sig_n;
         fence_proxy_async_smem();
         claim(s);
       } else {
@@ -284,9 +269,6 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
         }
       }
     }
-  }
-  if constexpr (CLAIM) {
-    if (tid == 0) signal_bucket(sig_b, sig_n);  // the last bucket this CTA worked on
   }
   if (!OUT_F32 && a.push) asm volatile("fence.acq_rel.sys;" ::: "memory");  // peer stores visible system-wide
   if (__syncthreads_or(bad) && tid == 0) atomicAdd(a.flag_slot, 1.0f);
