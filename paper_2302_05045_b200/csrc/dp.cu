@@ -1090,14 +1090,11 @@ int step_p2p_spec(samo_model* md, cudaStream_t S, bool gather) {
   SAMO_CUDA_TRY(cudaEventRecord(md->ev_fork, S));
   SAMO_CUDA_TRY(cudaStreamWaitEvent(E, md->ev_fork, 0));
   SAMO_CUDA_TRY(cudaStreamWaitEvent(E2, md->ev_fork, 0));
-  // K1 first in host order: streams of one process can share a hardware
-  // queue, and a spinning wait queued ahead of the kernel it waits for would
-  // never see it start
+  SAMO_TRY(spec_shards(md, sp, E2));
+  SAMO_TRY(p2p_expand(md, sp, E));
   SAMO_TRY(spec_gather(md, sp, S));
   SAMO_TRY(phase_mark(md, 1, S));
   SAMO_TRY(p2p_flag(md, sp, 1, S));  // publish now, sum at the end
-  SAMO_TRY(spec_shards(md, sp, E2));
-  SAMO_TRY(p2p_expand(md, sp, E));
   SAMO_CUDA_TRY(cudaEventRecord(md->ev_flag, E));
   SAMO_CUDA_TRY(cudaStreamWaitEvent(S, md->ev_flag, 0));
   SAMO_CUDA_TRY(cudaEventRecord(md->ev_spec, E2));
