@@ -1282,10 +1282,9 @@ int samo_model_shard_layout(samo_model* md, uint64_t* chunk, uint64_t* stride, i
     *rank = 0;
     return clear_ok();
   }
-  const int Bp = p2p_spec(md) ? std::max(2, p2p_buckets(comm_size(md))) : p2p_buckets(comm_size(md));
-  if (exchange_mode(md) == SAMO_EXCHANGE_P2P && Bp > 1) {
+  if (exchange_mode(md) == SAMO_EXCHANGE_P2P && p2p_buckets(comm_size(md)) > 1) {
     if (!md->finalized) return fail(SAMO_E_STATE, "model not finalized");
-    SAMO_TRY(plan_shards(md, md->p2p_plan, Bp));
+    SAMO_TRY(plan_shards(md, md->p2p_plan, p2p_buckets(comm_size(md))));
     *chunk = md->p2p_plan.c;
     *stride = md->p2p_plan.C;
     *buckets = md->p2p_plan.B;
