@@ -681,12 +681,7 @@ def run_samo(args) -> None:
             _abi.call("samo_model_enable_phase_timing", model.handle, 0)
             return [round(buf[i], 4) for i in range(max(0, cnt))]
 
-        if model.exchange_mode() == model.EXCHANGE_P2P and os.environ.get("SAMO_P2P_SPEC", "0") != "0":
-            ph = phase_pass()  # the speculative pipelined step
-            pipeline = dict(zip(["K1 with bucket signals || shard update || expand (until the last expand)",
-                                 "flag sum + finalize + repair no-op"], ph))
-            overlap = sunk_pass(model, grads, stream, dev)
-        elif model.exchange_mode() == model.EXCHANGE_P2P:
+        if model.exchange_mode() == model.EXCHANGE_P2P:
             ph = phase_pass()
             if len(ph) == 4:  # pipelined step (SAMO_P2P_BUCKETS > 1)
                 pipeline = dict(zip(["K1_gather", "skip-flag exchange (peer signals)",

@@ -469,8 +469,6 @@ int step_p2p(samo_model* md, cudaStream_t S, bool gather) {
   // would wait for each other forever.
   if (md->comm->local_group)
     return fail(SAMO_E_STATE, "a local-group member steps through samo_local_group_step");
-  if (p2p_spec(md)) return step_p2p_spec(md, S, gather);
-  md->spec_ready = false;  // the other schedules write c16 only
   if (p2p_buckets(G) > 1) return step_p2p_pipelined(md, S, p2p_buckets(G), gather);
   const uint64_t c = align_up((md->n_tot + G - 1) / G, 8);
   if (static_cast<uint64_t>(G) * c + 8 > md->n_al + kFlagOff)
@@ -746,16 +744,6 @@ int build_push_tiles(samo_model* md, const ShardPlan& p) {
     }
   }
   while (cur_layer < md->nlayers) md->push_layer_t[++cur_layer] = static_cast<uint32_t>(out.size());
-  // pieces per k-bucket (the speculative step's arrival counts; K1 applies
-  // the same rule to a piece's k_begin)
-  std::vector<uint32_t> cnt(kMaxP2PBuckets, 0u);
-  for (const SamoTile& piece : out) ++cnt[std::min<uint64_t>(piece.k_begin / p.C, p.B - 1)];
-  if (!md->sig_ctl) {
-    SAMO_CUDA_TRY(cudaMalloc(&md->sig_ctl, (2 + kMaxP2PBuckets) * sizeof(uint32_t)));
-    SAMO_CUDA_TRY(cudaMalloc(&md->sig_cnt, kMaxP2PBuckets * sizeof(uint32_t)));
-  }
-  SAMO_CUDA_TRY(cudaMemset(md->sig_ctl, 0, (2 + kMaxP2PBuckets) * sizeof(uint32_t)));
-  SAMO_CUDA_TRY(cudaMemcpy(md->sig_cnt, cnt.data(), kMaxP2PBuckets * sizeof(uint32_t), cudaMemcpyHostToDevice));
   if (md->push_tiles) cudaFree(md->push_tiles);
   md->push_tiles = nullptr;
   SAMO_CUDA_TRY(cudaMalloc(&md->push_tiles, out.size() * sizeof(SamoTile)));
@@ -953,193 +941,13 @@ static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather
   return SAMO_OK;
 }
 
-// ---------------------------------------------------------------------------
-// The speculative pipelined P2P step.
-//
-//   S  : K1 (claims tiles in k order; the CTA finishing a bucket's last push
-//        piece signals every rank)  -> publish flag | join -> flag sum ->
-//        finalize -> repair (no-op unless skipped) -> epoch++
-//   E2 :   wait_push[0] shard[0]  wait_push[1] shard[1] ...   (start while K1 runs)
-//   E  :       wait[0] expand[0]     wait[1] expand[1] ...
-//
-// The skip flag (train.hpp:632-639) needs every gradient of every rank, so
-// the shard updates run before it is known: Adam reads this step's theta/m/v
-// set and writes the other one, the binary16 weights go to the other c16
-// buffer of every rank, and the expand rebuilds theta16 from it.  Finalize
-// then advances the scalars, or records the skip and the repair puts back
-// the previous state: the rank's own theta/m/v ranges, c16 (every rank keeps
-// the previous step's weights in c16_alt, = compress(theta16)) and theta16
-// expanded from it.  The host swaps the theta/m/v sets and the c16 buffers
-// after every step, on every rank alike.
-bool p2p_spec(const samo_model* md) {
-  return env_int("SAMO_P2P_SPEC", 0) != 0 && p2p_push() && !p2p_pull() && !md->mc_c16;
-}
-
-int spec_init(samo_model* md) {
-  if (!md->s_spec) SAMO_CUDA_TRY(cudaStreamCreateWithFlags(&md->s_spec, cudaStreamNonBlocking));
-  if (!md->ev_spec) SAMO_CUDA_TRY(cudaEventCreateWithFlags(&md->ev_spec, cudaEventDisableTiming));
-  if (md->spec_ready) return SAMO_OK;
-  // c16_alt := compress(theta16): the previous weights a skip restores
-  SAMO_CUDA_TRY(cudaDeviceSynchronize());
-  for (int l = 0; l < md->nlayers; ++l) {
-    if (!md->nnz[l]) continue;
-    SAMO_TRY(samo_compress_u16(md->theta16 + md->d_off[l], md->dense_len[l], md->idx + md->k_off[l],
-                               md->nnz[l], md->dense_len[l], md->c16_alt + md->k_off[l], nullptr));
-  }
-  SAMO_CUDA_TRY(cudaDeviceSynchronize());
-  md->spec_ready = true;
-  return SAMO_OK;
-}
-
-// K1's CTAs per SM in the speculative step: fewer than its own optimum, so
-// the shard updates of the landed buckets find room on the SMs meanwhile.
-static int spec_k1_grid(const samo_model*) { return num_sms() * std::max(1, env_int("SAMO_P2P_SPEC_K1_CTAS", 2)); }
-
-static int spec_prepare(samo_model* md, int B, bool gather, P2PStep& sp) {
-  if (!md->capturing) SAMO_TRY(spec_init(md));
-  if (!md->spec_ready || !md->s_spec) return fail(SAMO_E_STATE, "speculative P2P step not initialised");
-  SAMO_TRY(p2p_prepare(md, B, gather, sp));
-  if (!sp.push) return fail(SAMO_E_STATE, "speculative P2P step needs push mode");
-  sp.pa.spec = 1;
-  sp.pa.theta_o = md->theta_alt;
-  sp.pa.m_o = md->m_alt;
-  sp.pa.v_o = md->v_alt;
-  sp.pa.tma = 0;
-  return SAMO_OK;
-}
-
-static int spec_gather(samo_model* md, const P2PStep& sp, cudaStream_t S) {
-  if (!sp.gather) {  // backward sinks pushed already: every bucket has landed
-    return launch_p2p_signal_all(sp.pa.slots, sp.pa.G, sp.pa.rank, sp.B, S);
-  }
-  StepArgs a = step_args(md);
-  a.tiles = md->push_tiles;
-  a.ntiles = md->push_ntiles;
-  a.push = 1;
-  const char* base = static_cast<const char*>(md->block);
-  const size_t g_off = reinterpret_cast<const char*>(md->g) - base;
-  for (int q = 0; q < md->comm->nranks; ++q)
-    a.push16[q] = reinterpret_cast<uint16_t*>(static_cast<char*>(md->peer_base[q]) + g_off);
-  a.sig_ctl = md->sig_ctl;
-  a.sig_cnt = md->sig_cnt;
-  for (int q = 0; q < sp.pa.G; ++q) a.sig_slots[q] = sp.pa.slots[q];
-  a.sig_G = sp.pa.G;
-  a.sig_rank = sp.pa.rank;
-  a.sig_C = md->p2p_plan.C;
-  a.sig_B = static_cast<uint32_t>(sp.B);
-  const int grid = std::max(1, std::min<int>(spec_k1_grid(md), a.ntiles));
-  return launch_gather_signal(a, grid, S);
-}
-
-static int spec_shards(samo_model* md, P2PStep& sp, cudaStream_t E2) {
-  const ShardPlan& p = md->p2p_plan;
-  const int r = md->comm->rank;
-  for (int b = 0; b < sp.B; ++b) {
-    SAMO_TRY(launch_p2p_wait_push(md->slots, sp.pa.G, b, E2));
-    sp.pa.k0 = std::min<uint64_t>(b * p.C + r * p.c, md->n_tot);
-    sp.pa.k1 = std::min<uint64_t>(b * p.C + (r + 1) * p.c, md->n_tot);
-    sp.pa.i0 = static_cast<uint64_t>(b) * p.c;
-    sp.pa.bucket = b;
-    SAMO_TRY(launch_shard_p2p(sp.pa, E2));  // also when empty: it signals
-  }
-  return SAMO_OK;
-}
-
-static int spec_repair(samo_model* md, const P2PStep& sp, cudaStream_t S) {
-  const ShardPlan& p = md->p2p_plan;
-  const int r = md->comm->rank;
-  RepairArgs a{};
-  a.st = md->st;
-  a.tiles = md->tiles;
-  a.ntiles = md->ntiles;
-  a.off16 = md->off16;
-  a.theta16 = md->theta16;
-  a.c16_old = md->c16_alt;
-  a.c16_new = md->c16;
-  a.n = md->n_tot;
-  a.theta = md->theta;
-  a.m = md->m;
-  a.v = md->v;
-  a.theta_o = md->theta_alt;
-  a.m_o = md->m_alt;
-  a.v_o = md->v_alt;
-  a.nranges = sp.B;
-  for (int b = 0; b < sp.B; ++b) {
-    a.k0[b] = std::min<uint64_t>(b * p.C + r * p.c, md->n_tot);
-    a.k1[b] = std::min<uint64_t>(b * p.C + (r + 1) * p.c, md->n_tot);
-  }
-  return launch_p2p_repair(a, S);
-}
-
-// After the step is enqueued (not while capturing): the sets swap on every
-// rank alike, skipped or not.
-void spec_swap(samo_model* md) {
-  std::swap(md->theta, md->theta_alt);
-  std::swap(md->m, md->m_alt);
-  std::swap(md->v, md->v_alt);
-  std::swap(md->c16, md->c16_alt);
-  md->parity ^= 1;
-}
-
-int step_p2p_spec(samo_model* md, cudaStream_t S, bool gather) {
-  const int B = std::max(2, p2p_buckets(md->comm->nranks));
-  P2PStep sp;
-  SAMO_TRY(spec_prepare(md, B, gather, sp));
-  cudaStream_t E = md->s_comm, E2 = md->s_spec;
-  SAMO_TRY(phase_mark(md, 0, S));
-  SAMO_CUDA_TRY(cudaEventRecord(md->ev_fork, S));
-  SAMO_CUDA_TRY(cudaStreamWaitEvent(E, md->ev_fork, 0));
-  SAMO_CUDA_TRY(cudaStreamWaitEvent(E2, md->ev_fork, 0));
-  SAMO_TRY(spec_shards(md, sp, E2));
-  SAMO_TRY(p2p_expand(md, sp, E));
-  SAMO_TRY(spec_gather(md, sp, S));
-  SAMO_TRY(phase_mark(md, 1, S));
-  SAMO_TRY(p2p_flag(md, sp, 1, S));  // publish now, sum at the end
-  SAMO_CUDA_TRY(cudaEventRecord(md->ev_flag, E));
-  SAMO_CUDA_TRY(cudaStreamWaitEvent(S, md->ev_flag, 0));
-  SAMO_CUDA_TRY(cudaEventRecord(md->ev_spec, E2));
-  SAMO_CUDA_TRY(cudaStreamWaitEvent(S, md->ev_spec, 0));
-  SAMO_TRY(phase_mark(md, 2, S));
-  SAMO_TRY(p2p_flag(md, sp, 2, S));
-  SAMO_TRY(launch_step_finalize(md->st, md->slots->norm, sp.B * kMaxP2PRanks, flag_ptr(md), md->cfg.beta1,
-                                md->cfg.beta2, md->capturing ? md->cfg_dev : nullptr, S));
-  SAMO_TRY(spec_repair(md, sp, S));
-  SAMO_TRY(launch_p2p_epoch(md->slots, S));
-  SAMO_TRY(phase_mark(md, 3, S));
-  md->phase_count = 3;
-  if (!md->capturing) spec_swap(md);
-  return SAMO_OK;
-}
-
 // One step of every rank of a local group, queued phase by phase on one
 // stream: each rank's waits (flag, buckets) find their signals already
 // written, so no kernel spins on another that is queued behind it.
 static int step_local_group(samo_model* const* models, int G, bool gather, cudaStream_t S) {
   const int B = p2p_buckets(G);
-  std::vector<P2PStep> sp(G);
-  if (p2p_spec(models[0])) {  // the speculative schedule, one phase at a time
-    const int Bs = std::max(2, B);
-    for (int r = 0; r < G; ++r) {
-      SAMO_TRY(flush_cfg(models[r], S));
-      SAMO_TRY(spec_prepare(models[r], Bs, gather, sp[r]));
-    }
-    for (int r = 0; r < G; ++r) SAMO_TRY(spec_gather(models[r], sp[r], S));
-    for (int r = 0; r < G; ++r) SAMO_TRY(p2p_flag(models[r], sp[r], 1, S));
-    for (int r = 0; r < G; ++r) SAMO_TRY(spec_shards(models[r], sp[r], S));
-    for (int r = 0; r < G; ++r) SAMO_TRY(p2p_expand(models[r], sp[r], S));
-    for (int r = 0; r < G; ++r) SAMO_TRY(p2p_flag(models[r], sp[r], 2, S));
-    for (int r = 0; r < G; ++r) {
-      samo_model* md = models[r];
-      SAMO_TRY(launch_step_finalize(md->st, md->slots->norm, sp[r].B * kMaxP2PRanks, flag_ptr(md), md->cfg.beta1,
-                                    md->cfg.beta2, nullptr, S));
-      SAMO_TRY(spec_repair(md, sp[r], S));
-      SAMO_TRY(launch_p2p_epoch(md->slots, S));
-    }
-    for (int r = 0; r < G; ++r) spec_swap(models[r]);
-    return SAMO_OK;
-  }
   if (B < 2) return fail(SAMO_E_STATE, "a local group needs the pipelined exchange (SAMO_P2P_BUCKETS >= 2)");
-  for (int r = 0; r < G; ++r) models[r]->spec_ready = false;
+  std::vector<P2PStep> sp(G);
   for (int r = 0; r < G; ++r) {
     SAMO_TRY(flush_cfg(models[r], S));
     SAMO_TRY(p2p_prepare(models[r], B, gather, sp[r]));

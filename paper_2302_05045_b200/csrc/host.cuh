@@ -71,10 +71,6 @@ struct samo_model {
   float* v = nullptr;
   float* g = nullptr;          // compressed gradient arena (+ skip-indicator slot)
   uint16_t* c16 = nullptr;     // compressed binary16 weights (sharded exchange)
-  uint16_t* c16_alt = nullptr; // speculative P2P step: the previous step's weights (swapped with c16)
-  bool spec_ready = false;     // c16_alt == compress(theta16) (speculative P2P step)
-  uint32_t* sig_ctl = nullptr; // K1 claim/signal counters of the speculative P2P step
-  uint32_t* sig_cnt = nullptr; // push pieces per k-bucket (device)
   double* norm2 = nullptr;     // this rank's / the global sum of g^2 (sharded exchange)
   uint32_t* done = nullptr;    // arrival counter of k_adam_shard
   uint64_t n_al = 0;
@@ -119,9 +115,6 @@ struct samo_model {
   cudaStream_t s_comm = nullptr, s_flag = nullptr;
   std::vector<cudaEvent_t> ev_k1, ev_ar;
   cudaEvent_t ev_fork = nullptr, ev_flag = nullptr;
-  cudaStream_t s_spec = nullptr;  // the speculative P2P step's shard stream
-  cudaEvent_t ev_spec = nullptr;
-  cudaGraphExec_t pgraph[2] = {nullptr, nullptr};  // speculative P2P step graphs, per buffer parity
   int reserve_sms = 16;                 // SMs left to NCCL while our kernels run
   ShardPlan shard_plan;
   ShardPlan p2p_plan;                   // peer-to-peer step (serial: 1 bucket)
@@ -190,10 +183,6 @@ inline int comm_size(const samo_model* md) { return md->comm ? md->comm->nranks 
 inline void drop_graphs(samo_model* md) {
   if (md->graph) cudaGraphExecDestroy(md->graph);
   md->graph = nullptr;
-  for (auto& g : md->pgraph) {
-    if (g) cudaGraphExecDestroy(g);
-    g = nullptr;
-  }
   for (auto& g : md->fgraph) {
     if (g) cudaGraphExecDestroy(g);
     g = nullptr;
@@ -225,14 +214,6 @@ void close_peers(samo_model* md);
 void close_nvls(samo_model* md);
 int exchange_mode(const samo_model* md);
 bool p2p_push();
-// The speculative pipelined P2P step (SAMO_P2P_SPEC): K1 signals each k-bucket
-// as its pushes land, the shard updates start per bucket while K1 runs on,
-// Adam writes the other theta/m/v set and the other c16 buffer, and the skip
-// flag is settled at the end (repair on a skip).
-bool p2p_spec(const samo_model* md);
-int step_p2p_spec(samo_model* md, cudaStream_t S, bool gather);
-void spec_swap(samo_model* md);
-int spec_init(samo_model* md);  // c16_alt := compress(theta16) once; side stream + event
 bool p2p_pull();
 int p2p_buckets(int G);
 int plan_shards(samo_model* md, ShardPlan& p, int B);

@@ -34,8 +34,6 @@ int launch_tiles_fill(SamoTile* tiles, uint32_t ntiles, const uint64_t* k_off,
 
 constexpr int kMaxP2PRanks = 8;
 
-struct SamoPeerSlots;
-
 // Arguments of the two per-step kernels (kernels_fused.cu).
 struct StepArgs {
   const SamoTile* tiles;
@@ -73,17 +71,6 @@ struct StepArgs {
   // Expand-only pass with pulled weights (peer-to-peer step): the binary16
   // weights of element k live in its owner's theta16c arena, peer16c[owner],
   // owner = ((k - b*pC) / pc) with bucket b = min(k / pC, pB - 1).
-  // K1 of the speculative P2P step (k1_gather<.., CLAIM = true>): tiles are
-  // claimed in order (ctl[0]; ctl[1] counts finished CTAs), and the CTA that
-  // completes the last push piece of k-bucket b (ctl[2 + b] counts them
-  // against sig_cnt[b]) tells every rank that this rank's bucket-b pushes
-  // have landed (SamoPeerSlots::push_epoch).
-  uint32_t* sig_ctl;
-  const uint32_t* sig_cnt;
-  SamoPeerSlots* sig_slots[kMaxP2PRanks];
-  int sig_G, sig_rank;
-  uint64_t sig_C;
-  uint32_t sig_B;
   uint32_t pull;
   uint32_t pB;
   uint64_t pc, pC;
@@ -120,7 +107,6 @@ struct SamoPeerSlots {
   uint64_t flag_epoch[kMaxP2PRanks];
   float flag_val[kMaxP2PRanks];
   uint64_t bucket_epoch[kMaxP2PBuckets * kMaxP2PRanks];  // [bucket * 8 + rank]
-  uint64_t push_epoch[kMaxP2PBuckets * kMaxP2PRanks];    // speculative step: rank's K1 pushes of a bucket landed
   double norm[kMaxP2PBuckets * kMaxP2PRanks];             // [bucket * 8 + rank]
 };
 struct P2PArgs {
@@ -134,12 +120,6 @@ struct P2PArgs {
   uint64_t k0, k1;                    // k0 a multiple of 8
   float scale;                        // (1/loss_scale) * (1/G)
   int grad_bf16;                      // the 16-bit gradients are bfloat16
-  // Speculative step (spec = 1): Adam runs whatever the skip flag, reading
-  // theta/m/v and writing theta_o/m_o/v_o (the other buffer set).
-  int spec;
-  float* theta_o;
-  float* m_o;
-  float* v_o;
   SamoAdamParams prm;
   const SamoStepState* st;
   const float* flag_slot;             // global skip indicator (already reduced)
@@ -172,36 +152,6 @@ int launch_p2p_wait(const SamoPeerSlots* mine, int G, int bucket, cudaStream_t s
 int launch_p2p_epoch(SamoPeerSlots* mine, cudaStream_t s);
 // Peer-wait trap limit from SAMO_SPIN_TIMEOUT_S (seconds), on the current device.
 int set_spin_limit_from_env();
-// K1 of the speculative P2P step: push mode with in-order tile claims and
-// per-bucket arrival signals (StepArgs::sig_*).
-int launch_gather_signal(const StepArgs& a, int grid, cudaStream_t s);
-// Waits (one warp) until every rank's K1 pushes of `bucket` have landed.
-int launch_p2p_wait_push(const SamoPeerSlots* mine, int G, int bucket, cudaStream_t s);
-// Tells every rank that this rank's pushes of buckets [0, B) have landed
-// (after backward sinks, which pushed without signals).
-int launch_p2p_signal_all(SamoPeerSlots* const* slots, int G, int rank, int B, cudaStream_t s);
-// After a speculative P2P step: a no-op unless the step was skipped; then the
-// rank's own shard ranges of theta/m/v are copied back (old -> new set), the
-// binary16 weights restored (c16 old -> new) and theta16 rebuilt from them.
-struct RepairArgs {
-  const SamoStepState* st;
-  const SamoTile* tiles;
-  uint32_t ntiles;
-  const uint16_t* off16;
-  uint16_t* theta16;
-  const uint16_t* c16_old;
-  uint16_t* c16_new;
-  uint64_t n;
-  const float* theta;  // the step's input set
-  const float* m;
-  const float* v;
-  float* theta_o;      // the step's output set
-  float* m_o;
-  float* v_o;
-  uint64_t k0[kMaxP2PBuckets], k1[kMaxP2PBuckets];
-  int nranges;
-};
-int launch_p2p_repair(const RepairArgs& a, cudaStream_t s);
 // Copies compressed binary16 gradients src[k] to their owners' receive
 // buffers along the push pieces a.tiles[0, a.ntiles) (a.push16 = peers).
 int launch_push_copy(const StepArgs& a, const uint16_t* src, cudaStream_t s);

@@ -114,14 +114,10 @@ k_build_off16(const SamoTile* __restrict__ tiles, uint32_t ntiles, const uint32_
 // ---------------------------------------------------------------------------
 // K1
 
-// CLAIM (speculative P2P step, push mode): tiles are claimed in order by
-// thread 0 (StepArgs::sig_ctl), and completing the last push piece of a
-// k-bucket signals every rank (StepArgs::sig_*).
-template <bool OUT_F32, int NS, bool CLAIM = false>
+template <bool OUT_F32, int NS>
 __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[NS];
-  __shared__ uint32_t tq[NS];  // CLAIM: the tile of each stage (>= ntiles: none)
 
   const uint32_t T = a.tile_elems;
   const uint32_t tid = threadIdx.x;
@@ -146,20 +142,10 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
       mbar_arrive(&full[s]);
     }
   };
-  auto claim = [&](int s) {  // CLAIM: thread 0 takes the next tile for stage s
-    const uint32_t t = atomicAdd(a.sig_ctl, 1u);
-    tq[s] = t;
-    if (t < a.ntiles) issue(t, s);
-    else mbar_arrive(&full[s]);
-  };
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
-      if constexpr (CLAIM) {
-        claim(s);
-      } else {
-        const uint64_t t = blockIdx.x + static_cast<uint64_t>(s) * gridDim.x;
-        if (t < a.ntiles) issue(static_cast<uint32_t>(t), s);
-      }
+      const uint64_t t = blockIdx.x + static_cast<uint64_t>(s) * gridDim.x;
+      if (t < a.ntiles) issue(static_cast<uint32_t>(t), s);
     }
   }
 
@@ -167,13 +153,8 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
   const bool bf16 = a.grad_bf16 != 0;
   const uint32_t xm = grad_exp_mask(bf16);
   uint32_t it = 0;
-  for (uint32_t t = blockIdx.x; CLAIM || t < a.ntiles; t += gridDim.x, ++it) {
+  for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++it) {
     const int s = static_cast<int>(it % NS);
-    if constexpr (CLAIM) {
-      mbar_wait(&full[s], (it / NS) & 1u);  // also publishes tq[s]
-      t = tq[s];
-      if (t >= a.ntiles) break;  // claims ascend: no later stage holds a tile
-    }
     const SamoTile td = a.tiles[t];
     // binary16 destination of element k: the local arena, or (push) the
     // owner's receive buffer over NVLink (tile-constant shift, same k % 8)
@@ -186,7 +167,7 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
     const uint16_t* gsrc = a.layers[td.layer].grad + td.dense_begin;
     const uint32_t staged = ((td.dense_count * 2u) & ~15u) >> 1;
     const uint16_t* sg = reinterpret_cast<const uint16_t*>(smem + static_cast<size_t>(s) * T * 2);
-    if constexpr (!CLAIM) mbar_wait(&full[s], (it / NS) & 1u);
+    mbar_wait(&full[s], (it / NS) & 1u);
 
     // Kept elements: 8-wide vectors on the 16-byte aligned middle of the
     // tile's k range (one 16-byte off16 load and one 16/32-byte store per 8),
@@ -243,42 +224,17 @@ __global__ void __launch_bounds__(kThreads) k1_gather(StepArgs a) {
         st_na_v4u(g16 + k, hw[0], hw[1], hw[2], hw[3]);
       }
     }
-    __syncthreads();  // every thread is done reading stage s (and storing its pushes)
+    __syncthreads();  // every thread is done reading stage s
     if (tid == 0) {
-      if constexpr (CLAIM) {
-        // this piece's pushes are visible system-wide; the CTA completing the
-        // bucket's last piece tells every rank (bucket = the host's rule)
-        asm volatile("fence.acq_rel.sys;" ::: "memory");
-        const uint64_t bq = td.k_begin / a.sig_C;
-        const uint32_t b = bq < a.sig_B - 1 ? static_cast<uint32_t>(bq) : a.sig_B - 1;
-        const uint32_t done = atomicAdd(a.sig_ctl + 2 + b, 1u) + 1u;
-        if (done == a.sig_cnt[b]) {
-          asm volatile("fence.acq_rel.sys;" ::: "memory");
-          const uint64_t e = a.sig_slots[a.sig_rank]->epoch + 1;
-          const int slot = static_cast<int>(b) * kMaxP2PRanks + a.sig_rank;
-          for (int q = 0; q < a.sig_G; ++q) st_release_sys(&a.sig_slots[q]->push_epoch[slot], e);
-          a.sig_ctl[2 + b] = 0u;  // every piece of b is done: rewind for the next step
-        }
+      const uint64_t tn = t + static_cast<uint64_t>(NS) * gridDim.x;
+      if (tn < a.ntiles) {
         fence_proxy_async_smem();
-        claim(s);
-      } else {
-        const uint64_t tn = t + static_cast<uint64_t>(NS) * gridDim.x;
-        if (tn < a.ntiles) {
-          fence_proxy_async_smem();
-          issue(static_cast<uint32_t>(tn), s);
-        }
+        issue(static_cast<uint32_t>(tn), s);
       }
     }
   }
   if (!OUT_F32 && a.push) asm volatile("fence.acq_rel.sys;" ::: "memory");  // peer stores visible system-wide
   if (__syncthreads_or(bad) && tid == 0) atomicAdd(a.flag_slot, 1.0f);
-  if constexpr (CLAIM) {
-    if (tid == 0 && atomicAdd(a.sig_ctl + 1, 1u) == gridDim.x - 1) {  // every CTA has made its last claim
-      a.sig_ctl[0] = 0u;
-      a.sig_ctl[1] = 0u;
-      __threadfence();
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1217,11 +1173,7 @@ template <int G, bool PUSH>
 __global__ void __launch_bounds__(kThreads, SAMO_P2P_MINB) k_shard_p2p(P2PArgs a) {
   __shared__ float red[kThreads / 32];
   __shared__ int last_cta;
-  // speculative step: the flag is not known yet; Adam writes the other set
-  const bool skip = !a.spec && *reinterpret_cast<const volatile float*>(a.flag_slot) != 0.0f;
-  float* const t_out = a.spec ? a.theta_o : a.theta;
-  float* const m_out = a.spec ? a.m_o : a.m;
-  float* const v_out = a.spec ? a.v_o : a.v;
+  const bool skip = *reinterpret_cast<const volatile float*>(a.flag_slot) != 0.0f;
   const SamoAdamParams prm = step_prm(a.cfg, a.prm);
   const float b1p = __fmul_rn(a.st->beta1_pow, prm.beta1);
   const float b2p = __fmul_rn(a.st->beta2_pow, prm.beta2);
@@ -1283,17 +1235,17 @@ __global__ void __launch_bounds__(kThreads, SAMO_P2P_MINB) k_shard_p2p(P2PArgs a
     }
     if (!skip) {
       if (cnt == 8) {
-        *reinterpret_cast<float4*>(t_out + k) = make_float4(th[0], th[1], th[2], th[3]);
-        *reinterpret_cast<float4*>(t_out + k + 4) = make_float4(th[4], th[5], th[6], th[7]);
-        *reinterpret_cast<float4*>(m_out + k) = make_float4(mm[0], mm[1], mm[2], mm[3]);
-        *reinterpret_cast<float4*>(m_out + k + 4) = make_float4(mm[4], mm[5], mm[6], mm[7]);
-        *reinterpret_cast<float4*>(v_out + k) = make_float4(vv[0], vv[1], vv[2], vv[3]);
-        *reinterpret_cast<float4*>(v_out + k + 4) = make_float4(vv[4], vv[5], vv[6], vv[7]);
+        *reinterpret_cast<float4*>(a.theta + k) = make_float4(th[0], th[1], th[2], th[3]);
+        *reinterpret_cast<float4*>(a.theta + k + 4) = make_float4(th[4], th[5], th[6], th[7]);
+        *reinterpret_cast<float4*>(a.m + k) = make_float4(mm[0], mm[1], mm[2], mm[3]);
+        *reinterpret_cast<float4*>(a.m + k + 4) = make_float4(mm[4], mm[5], mm[6], mm[7]);
+        *reinterpret_cast<float4*>(a.v + k) = make_float4(vv[0], vv[1], vv[2], vv[3]);
+        *reinterpret_cast<float4*>(a.v + k + 4) = make_float4(vv[4], vv[5], vv[6], vv[7]);
       } else {
         for (int e = 0; e < cnt; ++e) {
-          t_out[k + e] = th[e];
-          m_out[k + e] = mm[e];
-          v_out[k + e] = vv[e];
+          a.theta[k + e] = th[e];
+          a.m[k + e] = mm[e];
+          a.v[k + e] = vv[e];
         }
       }
     }
@@ -1508,47 +1460,6 @@ __global__ void k_p2p_wait(const SamoPeerSlots* mine, int G, int bucket) {
 }
 
 __global__ void k_p2p_epoch(SamoPeerSlots* mine) { mine->epoch += 1; }
-
-// One warp: wait until every rank's K1 pushes of `bucket` have landed here.
-__global__ void k_p2p_wait_push(const SamoPeerSlots* mine, int G, int bucket) {
-  const uint64_t e = mine->epoch + 1;
-  const int q = threadIdx.x;
-  if (q < G) spin_until(&mine->push_epoch[bucket * kMaxP2PRanks + q], e);
-  __syncwarp();
-}
-
-// One warp: this rank's pushes of every bucket have landed (they were made
-// by earlier kernels on this stream — the backward sinks).
-__global__ void k_p2p_signal_all(P2PArgs a, int B) {
-  asm volatile("fence.acq_rel.sys;" ::: "memory");
-  const uint64_t e = a.slots[a.rank]->epoch + 1;
-  for (int i = threadIdx.x; i < B * a.G; i += 32) {
-    const int b = i / a.G, q = i % a.G;
-    st_release_sys(&a.slots[q]->push_epoch[b * kMaxP2PRanks + a.rank], e);
-  }
-}
-
-// The skip repair of the speculative P2P step (see RepairArgs).
-__global__ void __launch_bounds__(kThreads) k_p2p_repair(RepairArgs a) {
-  if (*reinterpret_cast<const volatile uint32_t*>(&a.st->last_skipped) == 0u) return;
-  const uint64_t tid = blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x;
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kThreads;
-  for (int r = 0; r < a.nranges; ++r)
-    for (uint64_t k = a.k0[r] + tid; k < a.k1[r]; k += stride) {
-      a.theta_o[k] = a.theta[k];
-      a.m_o[k] = a.m[k];
-      a.v_o[k] = a.v[k];
-    }
-  for (uint64_t k = tid; k < a.n; k += stride) a.c16_new[k] = a.c16_old[k];
-  for (uint32_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
-    const TileFull td = load_tile_full(a.tiles + t);
-    uint16_t* dst = a.theta16 + td.out_off;
-    for (uint32_t i = threadIdx.x; i < td.dense_count; i += kThreads) dst[i] = 0;
-    __syncthreads();
-    for (uint64_t k = td.k_begin + threadIdx.x; k < td.k_end; k += kThreads) dst[a.off16[k]] = a.c16_old[k];
-    __syncthreads();
-  }
-}
 
 __global__ void k_set_step_config(SamoStepConfig* dst, SamoStepConfig v) { *dst = v; }
 
@@ -1851,39 +1762,6 @@ int launch_push_copy(const StepArgs& a, const uint16_t* src, cudaStream_t s) {
   k_push_copy<<<grid, kThreads, 0, s>>>(a, src);
   SAMO_LAUNCH_CHECK("k_push_copy");
   return SAMO_OK;
-}
-
-int launch_p2p_wait_push(const SamoPeerSlots* mine, int G, int bucket, cudaStream_t s) {
-  k_p2p_wait_push<<<1, 32, 0, s>>>(mine, G, bucket);
-  SAMO_LAUNCH_CHECK("k_p2p_wait_push");
-  return SAMO_OK;
-}
-
-int launch_p2p_signal_all(SamoPeerSlots* const* slots, int G, int rank, int B, cudaStream_t s) {
-  P2PArgs a{};
-  for (int q = 0; q < G; ++q) a.slots[q] = slots[q];
-  a.G = G;
-  a.rank = rank;
-  k_p2p_signal_all<<<1, 32, 0, s>>>(a, B);
-  SAMO_LAUNCH_CHECK("k_p2p_signal_all");
-  return SAMO_OK;
-}
-
-int launch_p2p_repair(const RepairArgs& a, cudaStream_t s) {
-  k_p2p_repair<<<num_sms(), kThreads, 0, s>>>(a);
-  SAMO_LAUNCH_CHECK("k_p2p_repair");
-  return SAMO_OK;
-}
-
-int launch_gather_signal(const StepArgs& a, int grid, cudaStream_t s) {
-  if (a.ntiles == 0) return SAMO_OK;
-  // the same ring depth rule as launch_gather (with_k1), claim mode
-  const size_t sm = gather_smem(a.tile_elems, false);
-  auto go = [&](auto fn) {
-    if (grid <= 0) grid = grid_for(fn, sm);
-    return launch_persistent(fn, a, sm, grid, s, kThreads, "k1_gather_signal");
-  };
-  return k1_stages(a.tile_elems) == 3 ? go(k1_gather<false, 3, true>) : go(k1_gather<false, 2, true>);
 }
 
 int launch_p2p_epoch(SamoPeerSlots* mine, cudaStream_t s) {

@@ -103,7 +103,6 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   // Buffers of the sharded exchange last: the step kernels' streams keep the
   // relative placement measured best.
   const uint64_t o_c16 = carve((n_al + kArenaSlack) * 2);
-  const uint64_t o_c16b = carve((n_al + kArenaSlack) * 2);  // the speculative P2P step's previous weights
   const uint64_t o_n2 = carve(256);  // 16 norm^2 slots + arrival counter
   const uint64_t o_slots = carve(sizeof(SamoPeerSlots));
   const uint64_t o_cfg = carve(sizeof(SamoStepConfig));
@@ -124,7 +123,6 @@ int samo_model_create(const samo_layer_desc* layers, int nlayers, uint32_t tile_
   md->idx = reinterpret_cast<uint32_t*>(b + o_idx);
   md->off16 = reinterpret_cast<uint16_t*>(b + o_off);
   md->c16 = reinterpret_cast<uint16_t*>(b + o_c16);
-  md->c16_alt = reinterpret_cast<uint16_t*>(b + o_c16b);
   md->norm2 = reinterpret_cast<double*>(b + o_n2);
   md->done = reinterpret_cast<uint32_t*>(b + o_n2 + 16 * sizeof(double));
   md->slots = reinterpret_cast<SamoPeerSlots*>(b + o_slots);
@@ -196,18 +194,12 @@ int samo_model_destroy(samo_model* md) {
   for (auto e : md->ev_ar) cudaEventDestroy(e);
   if (md->ev_fork) cudaEventDestroy(md->ev_fork);
   if (md->ev_flag) cudaEventDestroy(md->ev_flag);
-  if (md->s_spec) cudaStreamDestroy(md->s_spec);
-  if (md->ev_spec) cudaEventDestroy(md->ev_spec);
-  for (auto g : md->pgraph)
-    if (g) cudaGraphExecDestroy(g);
   for (auto e : md->ev_sh) cudaEventDestroy(e);
   for (auto e : md->phase_ev)
     if (e) cudaEventDestroy(e);
   for (auto p : md->dw_kb)
     if (p) cudaFree(p);
   if (md->push_tiles) cudaFree(md->push_tiles);
-  if (md->sig_ctl) cudaFree(md->sig_ctl);
-  if (md->sig_cnt) cudaFree(md->sig_cnt);
   if (md->block) cudaFree(md->block);
   delete md;
   return clear_ok();
@@ -640,42 +632,6 @@ int samo_model_step_graph(samo_model* md, samo_stream_t stream) {
     SAMO_CUDA_TRY(cudaGraphLaunch(ge, s));
     note_launch(md->fgraph_kernels);
     swap_sets(md);
-    return clear_ok();
-  }
-  if (comm_size(md) > 1 && exchange_mode(md) == SAMO_EXCHANGE_P2P && md->p2p_ok && p2p_spec(md)) {
-    // the speculative P2P step swaps buffer sets every step: one graph per parity
-    cudaGraphExec_t& ge = md->pgraph[md->parity];
-    if (!ge) {
-      if (!md->capture_stream)
-        SAMO_CUDA_TRY(cudaStreamCreateWithFlags(&md->capture_stream, cudaStreamNonBlocking));
-      // host-side planning (allocations, synchronous uploads) before capture
-      SAMO_TRY(plan_shards(md, md->p2p_plan, std::max(2, p2p_buckets(comm_size(md)))));
-      SAMO_TRY(build_push_tiles(md, md->p2p_plan));
-      SAMO_TRY(spec_init(md));  // one-time synchronous work, outside the capture
-      const uint64_t before = samo_kernel_launch_count();
-      SAMO_CUDA_TRY(cudaStreamBeginCapture(md->capture_stream, cudaStreamCaptureModeThreadLocal));
-      md->capturing = true;
-      int rc = step_p2p_spec(md, md->capture_stream, true);
-      md->capturing = false;
-      cudaGraph_t graph = nullptr;
-      cudaError_t e = cudaStreamEndCapture(md->capture_stream, &graph);
-      if (rc != SAMO_OK) {
-        if (graph) cudaGraphDestroy(graph);
-        return rc;
-      }
-      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
-      e = cudaGraphInstantiate(&ge, graph, 0);
-      cudaGraphDestroy(graph);
-      if (e != cudaSuccess) {
-        ge = nullptr;
-        return cuda_fail(e, "cudaGraphInstantiate");
-      }
-      md->fgraph_kernels = samo_kernel_launch_count() - before;
-      unnote_launch(md->fgraph_kernels);
-    }
-    SAMO_CUDA_TRY(cudaGraphLaunch(ge, s));
-    note_launch(md->fgraph_kernels);
-    spec_swap(md);
     return clear_ok();
   }
   if (md->graph && md->graph_comm != md->comm) {

@@ -79,10 +79,6 @@ def _run(tmp_path, mode, world, steps=4, save_g=False):
     env["SAMO_P2P_PULL"] = "1" if mode == "p2p-pull" else "0"  # expand pulls the weights
     env["SAMO_P2P_NVLS"] = "1" if mode == "p2p-nvls" else "0"  # multicast weight stores
     env["SAMO_DP_BF16"] = "1" if mode.endswith("-bf16") else "0"  # bfloat16 dense gradients
-    env["SAMO_P2P_SPEC"] = "1" if "-spec" in mode else "0"  # the speculative pipelined step
-    if "-spec" in mode:
-        env["SAMO_DP_SINK"] = "1" if mode.endswith("-sink") else "0"
-        env["SAMO_DP_GRAPH"] = "1" if mode.endswith("-graph") else "0"
     os.environ["SAMO_DP_BF16"] = env["SAMO_DP_BF16"]  # the parent's oracle replay reads it too
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
@@ -121,8 +117,7 @@ def _check(r, oracle, world, mode, steps=4):
 
 @pytest.mark.parametrize("mode", ["p2p", "p2p-serial", "p2p-graph", "p2p-tma", "p2p-sink", "p2p-pull",
                                   "p2p-nvls", "sharded", "sharded-graph", "overlap",
-                                  "staged", "graph", "p2p-bf16", "sharded-bf16", "overlap-bf16",
-                                  "p2p-spec", "p2p-spec-sink", "p2p-spec-graph"])
+                                  "staged", "graph", "p2p-bf16", "sharded-bf16", "overlap-bf16"])
 def test_dp_two_gpus_bit_exact(tmp_path, oracle, mode):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
@@ -130,7 +125,7 @@ def test_dp_two_gpus_bit_exact(tmp_path, oracle, mode):
 
 
 @pytest.mark.parametrize("mode", ["p2p", "p2p-serial", "p2p-graph", "p2p-tma", "p2p-sink", "p2p-pull",
-                                  "p2p-nvls", "p2p-bf16", "p2p-spec", "p2p-spec-sink", "p2p-spec-graph"])
+                                  "p2p-nvls", "p2p-bf16"])
 def test_dp_four_gpus_p2p_bit_exact(tmp_path, oracle, mode):
     """The fused exchange sums in rank order: bit-exact for G = 4 too."""
     if torch.cuda.device_count() < 4:
@@ -333,9 +328,7 @@ def _local_group_run(oracle, G, steps=4, sink=False):
 @pytest.mark.parametrize("G,env", [(3, {}), (5, {}), (8, {}), (8, {"SAMO_P2P_TMA": "1"}),
                                    (8, {"SAMO_P2P_PUSH": "0"}), (8, {"SAMO_P2P_PULL": "1"}),
                                    (2, {"SAMO_P2P_BUCKETS": "5"}), (7, {"SAMO_P2P_BUCKETS": "3"}),
-                                   (3, {"SAMO_DP_BF16": "1"}), (8, {"SAMO_DP_BF16": "1", "SAMO_P2P_TMA": "1"}),
-                                   (2, {"SAMO_P2P_SPEC": "1"}), (3, {"SAMO_P2P_SPEC": "1"}),
-                                   (8, {"SAMO_P2P_SPEC": "1"}), (5, {"SAMO_P2P_SPEC": "1", "SAMO_DP_BF16": "1"})],
+                                   (3, {"SAMO_DP_BF16": "1"}), (8, {"SAMO_DP_BF16": "1", "SAMO_P2P_TMA": "1"})],
                          ids=lambda x: str(x) if isinstance(x, int) else "-".join(f"{k[9:]}{v}" for k, v in x.items()) or "default")
 def test_local_group_p2p_bit_exact(cuda, oracle, monkeypatch, G, env):
     """The pipelined peer-to-peer step at G up to 8 on ONE GPU: G models on
@@ -357,16 +350,6 @@ def test_local_group_push_sinks_bit_exact(cuda, oracle, monkeypatch, G):
     them is only the flag exchange, the shard updates and the expand.  Every
     replica equals the oracle bit for bit."""
     if G == 2:  # a local group runs the pipelined schedule (one bucket is the G = 2 default)
-        monkeypatch.setenv("SAMO_P2P_BUCKETS", "5")
-    _check(_local_group_run(oracle, G, sink=True), oracle, G, "p2p")
-
-
-@pytest.mark.parametrize("G", [2, 4, 8])
-def test_local_group_spec_sinks_bit_exact(cuda, oracle, monkeypatch, G):
-    """The speculative step after backward sinks (every bucket signalled at
-    once), incl. the skipped step's repair: bit-exact vs the oracle."""
-    monkeypatch.setenv("SAMO_P2P_SPEC", "1")
-    if G == 2:
         monkeypatch.setenv("SAMO_P2P_BUCKETS", "5")
     _check(_local_group_run(oracle, G, sink=True), oracle, G, "p2p")
 
