@@ -635,6 +635,10 @@ __device__ __forceinline__ TileFull load_tile_full(const SamoTile* p) {
   return r;
 }
 
+// Up to this many tiles K123's last CTA sums the per-tile norm partials
+// itself; above, the repair kernel's CTAs share the sum.
+constexpr uint32_t kK123SmallNorm = 4096;
+
 // A claimed tile as the producer hands it to the consumers.
 struct K123Slot {
   uint64_t k_begin, k_end, out_off;
@@ -707,7 +711,10 @@ __global__ void __launch_bounds__(NT + 32, 512 / NT) k123_step(StepArgs a) {
     if (lane == 0) {
       const uint64_t policy = policy_evict_first();
       uint32_t it = 0;
-      uint32_t t = atomicAdd(&a.st->tile_next, 1u);
+      // the first tile of each CTA is its own index, the rest are claimed
+      // (the counter runs from gridDim.x): one atomic less on the critical
+      // path of short steps
+      uint32_t t = blockIdx.x;
       for (uint32_t tt = 0;; ++tt) {
         const int sg = static_cast<int>(tt % NSG);
         if (tt >= static_cast<uint32_t>(NSG)) mbar_wait(&gempty[sg], ((tt / NSG) - 1) & 1u);
@@ -721,7 +728,7 @@ __global__ void __launch_bounds__(NT + 32, 512 / NT) k123_step(StepArgs a) {
         SAMO_DCHECK(td.dense_count <= T && td.k_begin <= td.k_end);
         const uint16_t* grad = a.layers[td.layer].grad + td.dense_begin;
         const uint32_t t_cur = t;
-        t = atomicAdd(&a.st->tile_next, 1u);
+        t = gridDim.x + atomicAdd(&a.st->tile_next, 1u);
         sl.k_begin = td.k_begin;
         sl.k_end = td.k_end;
         sl.out_off = td.out_off;
@@ -928,9 +935,26 @@ __global__ void __launch_bounds__(NT + 32, 512 / NT) k123_step(StepArgs a) {
     last_cta = (ticket == gridDim.x - 1);
   }
   asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
-  if (!last_cta || tid != 0) return;
-  __threadfence();
+  if (!last_cta) return;
   SamoStepState* stt = a.st;
+  if (a.ntiles <= kK123SmallNorm) {  // short steps: the grad norm here, tiles in order
+    __shared__ double dsum[NT / 32];
+    if (tid == 0) __threadfence();
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+    double acc = 0.0;
+    for (uint32_t t = tid; t < a.ntiles; t += NT) acc += static_cast<double>(__ldcg(a.tile_norm + t));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xFFFFFFFFu, acc, o);
+    if (lane == 0) dsum[warp] = acc;
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+    if (tid == 0) {
+      double s2 = 0.0;
+      for (uint32_t w = 0; w < kConsumerWarps; ++w) s2 += dsum[w];
+      stt->grad_norm = static_cast<float>(sqrt(s2));
+    }
+  }
+  if (tid != 0) return;
+  __threadfence();
   if (*reinterpret_cast<volatile float*>(a.flag_slot) != 0.0f) {  // train.hpp:632-639
     stt->skipped_steps += 1;
     stt->last_skipped = 1u;
@@ -959,7 +983,7 @@ __global__ void __launch_bounds__(kThreads) k123_repair(StepArgs a) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const uint32_t tid = threadIdx.x;
-  {
+  if (a.ntiles > kK123SmallNorm) {  // (short steps: K123's last CTA summed them)
     const uint32_t per = (a.ntiles + gridDim.x - 1) / gridDim.x;
     const uint32_t t0 = min(a.ntiles, blockIdx.x * per), t1 = min(a.ntiles, t0 + per);
     double acc = 0.0;
