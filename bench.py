@@ -545,6 +545,10 @@ def run_samo(args) -> None:
             cs_idx.append((idx[a:b] - np.uint32(off)).astype(np.uint32))
             cs_theta.append(th[a:b].copy())
         cpu_sample = {"sel": sel, "nb": nb, "nblocks": nblocks, "idx": cs_idx, "theta": cs_theta}
+    # 32-byte theta16 sectors (16 values) holding a kept element: the sectors
+    # K123 writes (the others stay zero)
+    sectors16 = int(sum(int(torch.unique_consecutive(st.as_int64() >> 4).numel()) if st.count() else 0
+                        for st in sets))
     del init_vals, sets
     torch.cuda.empty_cache()
 
@@ -750,14 +754,17 @@ def run_samo(args) -> None:
         hbm_kernels = list(kern)
         if fused:
             # K123: dense grad 2phi + off16 2n + theta/m/v read
-            # 12n + theta/m/v write 12n + theta16 2phi, one launch per step.
+            # 12n + theta/m/v write 12n + the theta16 sectors holding a kept
+            # element (32 B each), one launch per step.
             for v in kern.values():
                 v["role"] = "split path (SAMO_FUSED_STEP=0), timed for comparison"
             f_ms = statistics.mean(x[0] for x in fused_ms)
             r_ms = statistics.mean(x[1] for x in fused_ms)
-            b_f = 4 * phi + 26 * nnz
+            b_f = 2 * phi + 26 * nnz + 32 * sectors16
             kern["K123_fused_step"] = {"ms": f_ms, "bytes": b_f, "GBps": b_f / (f_ms * 1e-3) / 1e9,
-                                       "write_bytes": 2 * phi + 12 * nnz}
+                                       "write_bytes": 32 * sectors16 + 12 * nnz,
+                                       "theta16_sectors_written": sectors16,
+                                       "theta16_sector_fraction": 32 * sectors16 / (2 * phi)}
             kern["k123_repair"] = {"ms": r_ms, "bytes": 0, "GBps": 0.0,
                                    "note": "skip repair: returns at once unless the step was skipped"}
             hbm_kernels = ["K123_fused_step"]
