@@ -1,7 +1,7 @@
 #!/bin/bash
 # 1-GPU: parity (incl. bf16 gradients, local-group P2P, the C++ mirror KATs and
 # the reference's store_test), bench lines for binary16 and bfloat16 grads.
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 O=gpurun_out
 T=${TAG:-r02f}

@@ -3,7 +3,7 @@
 # trapping waits; compute-sanitizer is closed on this pool), then the
 # BASELINE config-3 bench lines (GPT-1.3B at p = 0.8 / 0.9 / 0.95) and the
 # GPT-2.7B sparsity variants.
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 O=gpurun_out
 T=${TAG:-r02i}

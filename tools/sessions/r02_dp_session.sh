@@ -3,7 +3,7 @@
 # tolerance tests, NVLink counter calibration, bench lines at N = 1, 2, 4 and
 # the reference arm, ncu NVLink bytes of the fused kernels at G = 4, and the
 # config-5 allreduce sweep.  Outputs under gpurun_out/ (copied to profiles/).
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 O=gpurun_out
 timeout 900 python -m pytest tests/test_gpu_dp.py -q -rs -k "nccl or refused" > $O/r02_dp_nccl.log 2>&1; echo "rc=$?" >> $O/r02_dp_nccl.log

@@ -1,6 +1,6 @@
 #!/bin/bash
 # dW GEMM forms per shape: auto, MS=1 (256x256 + tail split), MS=2 (512x256).
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 : > gpurun_out/r02w_dw_forms.log
 for F in auto 1 2 auto; do

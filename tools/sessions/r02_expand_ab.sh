@@ -1,7 +1,7 @@
 #!/bin/bash
 # expand variants at N GPUs: HEAD (.), st.na stores (ab_x1), sector skip + st.na (ab_x2);
 # local-group parity of ab_x2 first.
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 O=gpurun_out
 N=${N:-2}

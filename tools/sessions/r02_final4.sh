@@ -1,7 +1,7 @@
 #!/bin/bash
 # Final 4-GPU evidence: the whole -m gpu suite, then bench lines at N = 1, 2, 4
 # and the reference arm.
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 O=gpurun_out
 T=${TAG:-r02q}

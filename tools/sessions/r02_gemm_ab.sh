@@ -1,7 +1,7 @@
 #!/bin/bash
 # GEMM epilogue + K123 launch-bound A/B: dW tests, bench_dw on the old tree
 # (ab_h) and the current one, then ab3 on the step.
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 O=gpurun_out
 timeout 900 python -m pytest tests/test_gpu_dw.py tests/test_gpu_parity.py -x -q > $O/r02j_pytest.log 2>&1; echo "rc=$?" >> $O/r02j_pytest.log

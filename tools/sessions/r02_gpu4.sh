@@ -3,7 +3,7 @@
 # DP test runs), bench lines N = 1, 2, 4 and the reference arm, NVLink link
 # counters of the fused P2P kernels (rank 0 under ncu, G = 2 and 4), NVLink
 # tools probe.  Outputs under gpurun_out/ (copied to profiles/).
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 O=gpurun_out
 T=${TAG:-r02h}

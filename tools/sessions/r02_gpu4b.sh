@@ -2,7 +2,7 @@
 # 4-GPU lease, second pass: the two tests fixed after r02h, bench lines at
 # N = 2 and 4 (binary16 and bfloat16), and one attempt at NVLink link
 # counters of the fused P2P kernels (rank 0 under ncu, G = 2, bounded).
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 O=gpurun_out
 T=${TAG:-r02k}

@@ -1,7 +1,7 @@
 #!/bin/bash
 # 1-GPU headline after the theta16 sector skip: full -m gpu suite, the bench
 # line, the ncu launch list and one --set full capture of K123.
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 O=gpurun_out
 T=${TAG:-r02v}

@@ -1,6 +1,6 @@
 #!/bin/bash
 # Quick K123 check: step parity tests + the bench's K123 line (f16, bf16).
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 O=gpurun_out
 T=${TAG:-r02g}

@@ -1,7 +1,7 @@
 #!/bin/bash
 # 1-GPU check of the fused K123 step: the -m gpu suite, the bench line, the
 # ncu launch list of the bench, and one ncu --set full capture of K123.
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 O=gpurun_out
 T=${TAG:-r02b}

@@ -1,6 +1,6 @@
 #!/bin/bash
 # K123 v2 (dynamic tiles, deferred copy-out): parity + bench at two tile sizes.
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 O=gpurun_out
 T=${TAG:-r02c}

@@ -1,7 +1,7 @@
 #!/bin/bash
 # 2-GPU: the data-parallel bench with and without the NVML NVLink reads, and
 # with the phase-timed pass only, to find the N > 1 regression.
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 O=gpurun_out
 : > $O/r02m_n2.log

@@ -1,6 +1,6 @@
 #!/bin/bash
 # 4-GPU: bench lines at N = 2 and 4 (binary16, default flags) and N = 4 bf16.
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 O=gpurun_out
 T=${TAG:-r02n}

@@ -1,7 +1,7 @@
 #!/bin/bash
 # K23 / expand sector skipping: split-path parity (K1+K23), checked suite of the
 # step tests, A/B of the split path against HEAD (ab_s), then (N GPUs) the DP tests.
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 O=gpurun_out
 timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_state.py -q -x > $O/r02t_pytest.log 2>&1; echo "rc=$?" >> $O/r02t_pytest.log

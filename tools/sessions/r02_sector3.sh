@@ -1,7 +1,7 @@
 #!/bin/bash
 # expand-pass sector skipping: local-group parity (normal + checked build),
 # then on N GPUs the cross-process P2P tests and a bench A/B against ab_s.
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 O=gpurun_out
 N=${N:-2}

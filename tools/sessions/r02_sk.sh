@@ -1,6 +1,6 @@
 #!/bin/bash
 # dW GEMM stream-K tail: correctness, then timings with SAMO_DW_SK=0/1.
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 O=gpurun_out
 timeout 900 python -m pytest tests/test_gpu_dw.py tests/test_cpp_kat.py -q -x > $O/r02sk_pytest.log 2>&1; echo "rc=$?" >> $O/r02sk_pytest.log

@@ -1,6 +1,6 @@
 #!/bin/bash
 # 1-GPU: K123 short-step changes — parity, the checked suite subset, the bench
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 O=gpurun_out
 T=${TAG:-r02r}
