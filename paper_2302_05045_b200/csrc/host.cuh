@@ -125,6 +125,7 @@ struct samo_model {
   int push_G = 0, push_B = 0;
   std::vector<uint32_t> push_layer_t;  // first push piece of each layer (+ end)
   bool sunk_push = false;              // this step's sinks pushed to the owners
+  uint16_t* sink16 = nullptr;          // fused dW sink's gather target in push mode (n halves)
   SamoPeerSlots* slots = nullptr;       // this rank's signal area (in the block)
   // Device copy of the step scalars (SamoStepConfig), refreshed on the step's
   // stream before the next step whenever set_config / attach_comm changed them.

@@ -200,6 +200,7 @@ int samo_model_destroy(samo_model* md) {
   for (auto p : md->dw_kb)
     if (p) cudaFree(p);
   if (md->push_tiles) cudaFree(md->push_tiles);
+  if (md->sink16) cudaFree(md->sink16);
   if (md->block) cudaFree(md->block);
   delete md;
   return clear_ok();
@@ -462,12 +463,16 @@ int samo_model_sink_dw(samo_model* md, int l, const uint16_t* x, const uint16_t*
     SAMO_TRY(launch_build_rowblocks(md->idx + md->k_off[l], md->nnz[l], in, out, md->dw_kb[l], s));
   }
   // Push mode: this rank's gradient arena is its receive buffer, which peers
-  // fill during their backward; the epilogue gathers into the idle theta16c
-  // arena instead (written by the owners only after every rank's flag,
-  // i.e. after this rank's sinks) and a copy pushes the layer to its owners.
+  // fill during their backward, and theta16c may still be read by a peer's
+  // expand of the previous step (pull mode): the epilogue gathers into a
+  // scratch arena of its own (2 n bytes, allocated on first use) and a copy
+  // pushes the layer to its owners.
   const bool push = comm_size(md) > 1 && p2p_push();
-  if (push) SAMO_TRY(push_sink_prepare(md));
-  uint16_t* g16 = push ? md->c16 : reinterpret_cast<uint16_t*>(md->g);
+  if (push) {
+    SAMO_TRY(push_sink_prepare(md));
+    if (!md->sink16) SAMO_CUDA_TRY(cudaMalloc(&md->sink16, (md->n_tot + 8) * sizeof(uint16_t)));
+  }
+  uint16_t* g16 = push ? md->sink16 : reinterpret_cast<uint16_t*>(md->g);
   DwArgs a{};
   a.M = in;
   a.N = out;
@@ -477,7 +482,7 @@ int samo_model_sink_dw(samo_model* md, int l, const uint16_t* x, const uint16_t*
   a.g16 = g16 + md->k_off[l];
   a.flag = flag_ptr(md);
   SAMO_TRY(launch_dw_gemm(x, dy, a, 1, s));
-  if (push) SAMO_TRY(push_sink_layer(md, l, md->c16, s));
+  if (push) SAMO_TRY(push_sink_layer(md, l, md->sink16, s));
   return clear_ok();
 }
 
