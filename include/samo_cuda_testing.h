@@ -27,7 +27,11 @@ extern "C" {
  * cross-rank concurrency differs.  The members' own step calls fail with
  * SAMO_E_STATE.  Re-attach (samo_model_attach_comm) or destroy all members
  * together: each maps the others' memory.  Not part of the reference's API;
- * it lets tests/test_gpu_dp.py check G = 5..8 on a single GPU. */
+ * it lets tests/test_gpu_dp.py check G = 5..8 on a single GPU.  Models on
+ * different devices (one per device, every pair peer-capable) form a group
+ * across GPUs in one process: each rank's phase runs on its own device,
+ * and the step waits for every device between phases (the harness
+ * tools/nvlink_group_ncu.py profiles the NVLink bytes with). */
 int samo_model_attach_local_group(samo_model* const* models, int G);
 int samo_local_group_step(samo_model* const* models, int G, samo_stream_t stream);
 /* The same after every member's backward sinks (samo_model_sink_dense /

@@ -944,20 +944,48 @@ static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather
 // One step of every rank of a local group, queued phase by phase on one
 // stream: each rank's waits (flag, buckets) find their signals already
 // written, so no kernel spins on another that is queued behind it.
+// A group spread over several devices (one model per device, peers mapped
+// directly: a single-process stand-in for G processes, e.g. to profile the
+// NVLink traffic of the fused kernels with one ncu) runs each rank's phase
+// on its own device and stream and waits for every device between phases.
 static int step_local_group(samo_model* const* models, int G, bool gather, cudaStream_t S) {
   const int B = p2p_buckets(G);
   if (B < 2) return fail(SAMO_E_STATE, "a local group needs the pipelined exchange (SAMO_P2P_BUCKETS >= 2)");
+  const bool multi = models[0]->group_dev >= 0;
+  int dev0 = 0;
+  SAMO_CUDA_TRY(cudaGetDevice(&dev0));
+  auto on = [&](int r) -> cudaStream_t {
+    if (!multi) return S;
+    cudaSetDevice(models[r]->group_dev);
+    return models[r]->s_group;
+  };
+  auto phase_end = [&]() -> int {
+    if (!multi) return SAMO_OK;
+    for (int r = 0; r < G; ++r) {
+      SAMO_CUDA_TRY(cudaSetDevice(models[r]->group_dev));
+      SAMO_CUDA_TRY(cudaStreamSynchronize(models[r]->s_group));
+    }
+    return SAMO_OK;
+  };
   std::vector<P2PStep> sp(G);
   for (int r = 0; r < G; ++r) {
-    SAMO_TRY(flush_cfg(models[r], S));
+    cudaStream_t s = on(r);
+    SAMO_TRY(flush_cfg(models[r], s));
     SAMO_TRY(p2p_prepare(models[r], B, gather, sp[r]));
   }
-  for (int r = 0; r < G; ++r) SAMO_TRY(p2p_gather(models[r], sp[r], S));
-  for (int r = 0; r < G; ++r) SAMO_TRY(p2p_flag(models[r], sp[r], 1, S));
-  for (int r = 0; r < G; ++r) SAMO_TRY(p2p_flag(models[r], sp[r], 2, S));
-  for (int r = 0; r < G; ++r) SAMO_TRY(p2p_shards(models[r], sp[r], S));
-  for (int r = 0; r < G; ++r) SAMO_TRY(p2p_expand(models[r], sp[r], S));
-  for (int r = 0; r < G; ++r) SAMO_TRY(p2p_finish(models[r], sp[r], S));
+  for (int r = 0; r < G; ++r) SAMO_TRY(p2p_gather(models[r], sp[r], on(r)));
+  SAMO_TRY(phase_end());
+  for (int r = 0; r < G; ++r) SAMO_TRY(p2p_flag(models[r], sp[r], 1, on(r)));
+  SAMO_TRY(phase_end());
+  for (int r = 0; r < G; ++r) SAMO_TRY(p2p_flag(models[r], sp[r], 2, on(r)));
+  SAMO_TRY(phase_end());
+  for (int r = 0; r < G; ++r) SAMO_TRY(p2p_shards(models[r], sp[r], on(r)));
+  SAMO_TRY(phase_end());
+  for (int r = 0; r < G; ++r) SAMO_TRY(p2p_expand(models[r], sp[r], on(r)));
+  SAMO_TRY(phase_end());
+  for (int r = 0; r < G; ++r) SAMO_TRY(p2p_finish(models[r], sp[r], on(r)));
+  SAMO_TRY(phase_end());
+  if (multi) SAMO_CUDA_TRY(cudaSetDevice(dev0));
   return SAMO_OK;
 }
 
@@ -982,6 +1010,8 @@ int samo_model_attach_local_group(samo_model* const* models, int G) {
     return fail(SAMO_E_PARAMETER, "local group of %d models (2..%d)", G, kMaxP2PRanks);
   int dev = -1;
   SAMO_CUDA_TRY(cudaGetDevice(&dev));
+  std::vector<int> devs(G);
+  bool multi = false;
   for (int r = 0; r < G; ++r) {
     samo_model* md = models[r];
     if (!md) return fail(SAMO_E_PARAMETER, "null model %d", r);
@@ -991,7 +1021,28 @@ int samo_model_attach_local_group(samo_model* const* models, int G) {
       return fail(SAMO_E_DIMENSION, "model %d: layout differs from model 0", r);
     cudaPointerAttributes pa{};
     SAMO_CUDA_TRY(cudaPointerGetAttributes(&pa, md->block));
-    if (pa.device != dev) return fail(SAMO_E_PARAMETER, "model %d is not on the current device", r);
+    devs[r] = pa.device;
+    multi = multi || pa.device != dev;
+  }
+  if (multi) {  // one model per device, every pair of devices peer-capable
+    for (int r = 0; r < G; ++r)
+      for (int q = 0; q < G; ++q) {
+        if (q == r) continue;
+        if (devs[q] == devs[r]) return fail(SAMO_E_PARAMETER, "a multi-device group takes one model per device");
+        int ok = 0;
+        SAMO_CUDA_TRY(cudaDeviceCanAccessPeer(&ok, devs[r], devs[q]));
+        if (!ok) return fail(SAMO_E_PARAMETER, "device %d cannot access device %d", devs[r], devs[q]);
+        SAMO_CUDA_TRY(cudaSetDevice(devs[r]));
+        const cudaError_t e = cudaDeviceEnablePeerAccess(devs[q], 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+        cudaGetLastError();
+      }
+    for (int r = 0; r < G; ++r) {
+      SAMO_CUDA_TRY(cudaSetDevice(devs[r]));
+      models[r]->group_dev = devs[r];
+      if (!models[r]->s_group) SAMO_CUDA_TRY(cudaStreamCreateWithFlags(&models[r]->s_group, cudaStreamNonBlocking));
+    }
+    SAMO_CUDA_TRY(cudaSetDevice(dev));
   }
   for (int r = 0; r < G; ++r) {
     samo_model* md = models[r];
@@ -1010,9 +1061,11 @@ int samo_model_attach_local_group(samo_model* const* models, int G) {
   }
   const int B = p2p_buckets(G);
   for (int r = 0; r < G && B > 1; ++r) {
+    if (multi) SAMO_CUDA_TRY(cudaSetDevice(devs[r]));
     SAMO_TRY(plan_shards(models[r], models[r]->p2p_plan, B));
     if (p2p_push()) SAMO_TRY(build_push_tiles(models[r], models[r]->p2p_plan));
   }
+  if (multi) SAMO_CUDA_TRY(cudaSetDevice(dev));
   return clear_ok();
 }
 

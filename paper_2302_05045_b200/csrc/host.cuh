@@ -126,6 +126,8 @@ struct samo_model {
   std::vector<uint32_t> push_layer_t;  // first push piece of each layer (+ end)
   bool sunk_push = false;              // this step's sinks pushed to the owners
   uint16_t* sink16 = nullptr;          // fused dW sink's gather target in push mode (n halves)
+  int group_dev = -1;                  // local group across devices: this model's device
+  cudaStream_t s_group = nullptr;      // ... and its stream for the group step
   SamoPeerSlots* slots = nullptr;       // this rank's signal area (in the block)
   // Device copy of the step scalars (SamoStepConfig), refreshed on the step's
   // stream before the next step whenever set_config / attach_comm changed them.

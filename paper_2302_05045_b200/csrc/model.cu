@@ -201,6 +201,7 @@ int samo_model_destroy(samo_model* md) {
     if (p) cudaFree(p);
   if (md->push_tiles) cudaFree(md->push_tiles);
   if (md->sink16) cudaFree(md->sink16);
+  if (md->s_group) cudaStreamDestroy(md->s_group);
   if (md->block) cudaFree(md->block);
   delete md;
   return clear_ok();

@@ -271,10 +271,11 @@ def test_dp_nccl_tolerance_two_gpus(tmp_path, oracle):
     _check_nccl_tolerance(_run(tmp_path, "overlap", 2, save_g=True), oracle, 2, "overlap")
 
 
-def _local_group_run(oracle, G, steps=4, sink=False):
+def _local_group_run(oracle, G, steps=4, sink=False, devices=None):
     """G models on cuda:0 as the ranks of one peer-to-peer group
     (samo_model_attach_local_group + samo_local_group_step): the same inputs
-    and outputs as dp_worker.py."""
+    and outputs as dp_worker.py.  devices: model r on cuda:devices[r] (a
+    group across GPUs in one process)."""
     sys.path.insert(0, str(HERE))
     os.environ["SAMO_DP_STEPS"] = str(steps)
     import importlib
@@ -283,10 +284,12 @@ def _local_group_run(oracle, G, steps=4, sink=False):
     from paper_2302_05045_b200 import samo
     vals, sets, grads = W.inputs(oracle, G)
     L = len(W.DENSE_LEN)
-    psets = [samo.PrunedIndexSet(f"l{l}", d, torch.from_numpy(s.view(np.int32)).cuda())
-             for l, (d, s) in enumerate(zip(W.DENSE_LEN, sets))]
     models = []
-    for _ in range(G):
+    for r in range(G):
+        if devices:
+            torch.cuda.set_device(devices[r])
+        psets = [samo.PrunedIndexSet(f"l{l}", d, torch.from_numpy(s.view(np.int32)).cuda())
+                 for l, (d, s) in enumerate(zip(W.DENSE_LEN, sets))]
         m = samo.SamoModel.from_index_sets(psets, [(d,) for d in W.DENSE_LEN], tile_elems=1024)
         for l, v in enumerate(vals):
             m.init_layer(l, torch.from_numpy(v).cuda())
@@ -294,8 +297,13 @@ def _local_group_run(oracle, G, steps=4, sink=False):
         if W.BF16:
             m.set_grad_dtype(torch.bfloat16)
         models.append(m)
+    if devices:
+        torch.cuda.set_device(devices[0])
+        for r in range(G):
+            torch.cuda.synchronize(devices[r])
     samo.SamoModel.attach_local_group(models)
-    dev = {(r, s): [torch.from_numpy(grads[(r, s, l)].view(np.int16)).cuda() for l in range(L)]
+    dev = {(r, s): [torch.from_numpy(grads[(r, s, l)].view(np.int16)).cuda(devices[r] if devices else None)
+                    for l in range(L)]
            for r in range(G) for s in range(W.STEPS)}
     torch.cuda.synchronize()
     for s in range(W.STEPS):
@@ -396,6 +404,19 @@ def test_local_group_push_dw_sinks_equal_dense_sinks(cuda):
                                    dense[r].read(l, k).view(torch.int16 if k == "theta16" else torch.int32)), (r, l, k)
     for m in fused + dense:
         m.close()
+
+
+def test_local_group_across_devices_bit_exact(cuda, oracle, monkeypatch):
+    """One process, one model per GPU, peers mapped directly (the harness
+    the NVLink profile uses, tools/nvlink_group_ncu.py): every phase of a
+    rank runs on its own device, the kernels move the gradients and weights
+    over NVLink, and every replica equals the oracle bit for bit."""
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs 2 GPUs")
+    G = min(n, 4)
+    monkeypatch.setenv("SAMO_P2P_BUCKETS", "5")
+    _check(_local_group_run(oracle, G, devices=list(range(G))), oracle, G, "p2p")
 
 
 def test_local_group_eight_ranks_stress(cuda, oracle):
