@@ -254,8 +254,7 @@ int samo_model_attach_comm(samo_model* model, samo_comm* comm);
  *    From G = 3 the step is pipelined over k-buckets (shard update || expand)
  *    with release/acquire signals in peer memory as its only barriers — no
  *    NCCL call at all; at G = 2 two 4/8-byte NCCL allreduces are the
- *    barriers.  Tuning: SAMO_P2P_BUCKETS, SAMO_P2P_PUSH, SAMO_P2P_PULL,
- *    SAMO_P2P_TMA.
+ *    barriers.  Tuning: SAMO_P2P_BUCKETS, SAMO_P2P_PUSH.
  * The default is P2P when the peer mappings succeeded on every rank, else
  * SHARDED (environment SAMO_EXCHANGE=allreduce|sharded overrides); mode -1
  * restores the default. */
@@ -269,15 +268,11 @@ int samo_model_set_exchange(samo_model* model, int mode);
 /* SAMO_EXCHANGE_NONE without a communicator of size > 1. */
 int samo_model_exchange_mode(const samo_model* model);
 /* Which peer-to-peer mechanisms this model's step uses (bitmask): peer
- * mappings made, K1 push, expand pull, NVLS multicast of the binary16
- * weights (opt-in with SAMO_P2P_NVLS=1 before samo_model_attach_comm; set
- * up at attach time, agreed by every rank, otherwise the weights are stored
- * to each peer). */
+ * mappings made (agreed by every rank at samo_model_attach_comm), K1 pushes
+ * the gradients to their owners (else the shard update pulls them). */
 enum samo_p2p_feature {
   SAMO_P2P_MAPPED = 1,
-  SAMO_P2P_PUSH = 2,
-  SAMO_P2P_PULL = 4,
-  SAMO_P2P_NVLS = 8
+  SAMO_P2P_PUSH = 2
 };
 int samo_model_p2p_features(const samo_model* model);
 /* (The one-GPU local-group test harness is declared in samo_cuda_testing.h.) */

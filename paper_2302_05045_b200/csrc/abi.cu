@@ -367,7 +367,6 @@ int samo_comm_create(const uint8_t id[SAMO_UNIQUE_ID_BYTES], int nranks, int ran
   auto* c = new samo_comm();
   c->nranks = nranks;
   c->rank = rank;
-  std::memcpy(c->uid, id, SAMO_UNIQUE_ID_BYTES);
   ncclResult_t r = ncclCommInitRank(&c->comm, nranks, uid, rank);
   if (r != ncclSuccess) {
     delete c;

@@ -132,15 +132,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// The same without an L2 cache hint (peer / NVLink sources).
-__device__ __forceinline__ void bulk_g2s_peer(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
-}
-
 // 1-D bulk copy shared -> global, tracked by the bulk async-group.
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
@@ -166,17 +157,6 @@ __device__ __forceinline__ void bulk_wait() {
 // async-proxy (bulk copy) accesses.
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-// NVLS multicast store: one 16-byte store through a multicast mapping lands
-// in every GPU bound to the multicast object (replicated by the NVSwitch).
-__device__ __forceinline__ void multimem_st_v4(void* mc, const uint4& v) {
-  // weak: ordered for the readers by the fence.proxy.alias + fence.acq_rel.sys
-  // + release signal that follow the kernel's stores
-  asm volatile("multimem.st.weak.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc),
-               "f"(__uint_as_float(v.x)), "f"(__uint_as_float(v.y)), "f"(__uint_as_float(v.z)),
-               "f"(__uint_as_float(v.w))
-               : "memory");
 }
 
 // Cross-GPU signalling over NVLink peer memory (system scope).

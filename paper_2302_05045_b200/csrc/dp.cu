@@ -1,274 +1,21 @@
 // dp.cu — the data-parallel machinery of the model: CUDA IPC peer mappings
-// and the optional NVLS multicast object (set up by samo_model_attach_comm),
-// the bucket / shard / push-tile plans, and the step drivers — the fused
-// peer-to-peer step (serial and pipelined, push / pull), the NCCL sharded and
-// overlapped-allreduce steps — plus the exchange-related C entry points.
-#include <poll.h>
-#include <sys/socket.h>
-#include <sys/un.h>
-#include <unistd.h>
-
+// (set up by samo_model_attach_comm), the bucket / shard / push-tile plans,
+// and the step drivers — the fused peer-to-peer step (serial and pipelined,
+// push / pull of the gradients), the NCCL sharded and overlapped-allreduce
+// steps — plus the exchange-related C entry points.
 #include <cstdio>
 #include <cstring>
 #include <string>
-#include <type_traits>
 
 #include "host.cuh"
 
 void close_peers(samo_model* md) {
-  close_nvls(md);
   const bool ipc = !(md->comm && md->comm->local_group);  // a local group maps its peers directly
   for (int q = 0; q < kMaxP2PRanks; ++q) {
     if (ipc && md->peer_base[q] && md->peer_base[q] != md->block) cudaIpcCloseMemHandle(md->peer_base[q]);
     md->peer_base[q] = nullptr;
   }
   md->p2p_ok = false;
-}
-
-// ---------------------------------------------------------------------------
-// NVLS multicast for the P2P weight push (SAMO_P2P_NVLS=1; off by default:
-// measured at G = 4 the shard update takes 0.82 ms with one multimem.st per
-// vector against 0.63 ms with G peer stores).  Driver API through
-// cudaGetDriverEntryPoint (the runtime is linked statically).
-
-struct NvlsApi {
-  decltype(&cuMulticastCreate) mc_create = nullptr;
-  decltype(&cuMulticastAddDevice) mc_add = nullptr;
-  decltype(&cuMulticastBindMem) mc_bind = nullptr;
-  decltype(&cuMulticastUnbind) mc_unbind = nullptr;
-  decltype(&cuMulticastGetGranularity) mc_gran = nullptr;
-  decltype(&cuMemCreate) mem_create = nullptr;
-  decltype(&cuMemRelease) mem_release = nullptr;
-  decltype(&cuMemAddressReserve) va_reserve = nullptr;
-  decltype(&cuMemAddressFree) va_free = nullptr;
-  decltype(&cuMemMap) mem_map = nullptr;
-  decltype(&cuMemUnmap) mem_unmap = nullptr;
-  decltype(&cuMemSetAccess) set_access = nullptr;
-  decltype(&cuMemExportToShareableHandle) export_h = nullptr;
-  decltype(&cuMemImportFromShareableHandle) import_h = nullptr;
-  decltype(&cuMemGetAllocationGranularity) mem_gran = nullptr;
-  decltype(&cuCtxGetDevice) ctx_device = nullptr;
-  bool ok = false;
-};
-
-static NvlsApi load_nvls_api() {
-  NvlsApi api;
-  auto get = [](const char* name, auto& fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q{};
-    if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
-      return false;
-    fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(p);
-    return true;
-  };
-  api.ok = get("cuMulticastCreate", api.mc_create) && get("cuMulticastAddDevice", api.mc_add) &&
-           get("cuMulticastBindMem", api.mc_bind) && get("cuMulticastUnbind", api.mc_unbind) &&
-           get("cuMulticastGetGranularity", api.mc_gran) && get("cuMemCreate", api.mem_create) &&
-           get("cuMemRelease", api.mem_release) && get("cuMemAddressReserve", api.va_reserve) &&
-           get("cuMemAddressFree", api.va_free) && get("cuMemMap", api.mem_map) &&
-           get("cuMemUnmap", api.mem_unmap) && get("cuMemSetAccess", api.set_access) &&
-           get("cuMemExportToShareableHandle", api.export_h) &&
-           get("cuMemImportFromShareableHandle", api.import_h) &&
-           get("cuMemGetAllocationGranularity", api.mem_gran) && get("cuCtxGetDevice", api.ctx_device);
-  cudaGetLastError();
-  return api;
-}
-
-static const NvlsApi& nvls_api() {
-  static const NvlsApi api = load_nvls_api();  // thread-safe one-time initialisation
-  return api;
-}
-
-// min over ranks of `ok` (a barrier as well).
-static int agree(samo_comm* c, int* ok) {
-  int* d = nullptr;
-  cudaStream_t s = nullptr;
-  SAMO_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-  int rc = SAMO_OK;
-  cudaError_t e = cudaMalloc(&d, sizeof(int));
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d, ok, sizeof(int), cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) {
-    const ncclResult_t nr = ncclAllReduce(d, d, 1, ncclInt32, ncclMin, c->comm, s);
-    if (nr != ncclSuccess) rc = nccl_fail(nr, "ncclAllReduce(agree)");
-  }
-  if (rc == SAMO_OK && e == cudaSuccess) e = cudaMemcpyAsync(ok, d, sizeof(int), cudaMemcpyDeviceToHost, s);
-  if (rc == SAMO_OK && e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (rc == SAMO_OK && e != cudaSuccess) rc = cuda_fail(e, "agree");
-  if (d) cudaFree(d);
-  cudaStreamDestroy(s);
-  return rc;
-}
-
-// Rank 0 hands the multicast object's file descriptor to the other ranks of
-// this node over an abstract Unix socket named after the communicator id.
-static void nvls_sock_name(const samo_comm* c, int seq, sockaddr_un* a, socklen_t* len) {
-  std::memset(a, 0, sizeof(*a));
-  a->sun_family = AF_UNIX;
-  char name[96];
-  int n = std::snprintf(name, sizeof(name), "samo-nvls-");
-  for (int i = 0; i < 12; ++i) n += std::snprintf(name + n, sizeof(name) - n, "%02x", c->uid[i]);
-  n += std::snprintf(name + n, sizeof(name) - n, "-%d", seq);
-  std::memcpy(a->sun_path + 1, name, n);  // leading NUL: abstract namespace
-  *len = static_cast<socklen_t>(offsetof(sockaddr_un, sun_path) + 1 + n);
-}
-
-static bool send_fd(int sock, int fd) {
-  char byte = 0;
-  iovec iov{&byte, 1};
-  char ctl[CMSG_SPACE(sizeof(int))] = {};
-  msghdr msg{};
-  msg.msg_iov = &iov;
-  msg.msg_iovlen = 1;
-  msg.msg_control = ctl;
-  msg.msg_controllen = sizeof(ctl);
-  cmsghdr* cm = CMSG_FIRSTHDR(&msg);
-  cm->cmsg_level = SOL_SOCKET;
-  cm->cmsg_type = SCM_RIGHTS;
-  cm->cmsg_len = CMSG_LEN(sizeof(int));
-  std::memcpy(CMSG_DATA(cm), &fd, sizeof(int));
-  return sendmsg(sock, &msg, 0) == 1;
-}
-
-static int recv_fd(int sock) {
-  char byte = 0;
-  iovec iov{&byte, 1};
-  char ctl[CMSG_SPACE(sizeof(int))] = {};
-  msghdr msg{};
-  msg.msg_iov = &iov;
-  msg.msg_iovlen = 1;
-  msg.msg_control = ctl;
-  msg.msg_controllen = sizeof(ctl);
-  if (recvmsg(sock, &msg, 0) != 1) return -1;
-  cmsghdr* cm = CMSG_FIRSTHDR(&msg);
-  if (!cm || cm->cmsg_type != SCM_RIGHTS) return -1;
-  int fd = -1;
-  std::memcpy(&fd, CMSG_DATA(cm), sizeof(int));
-  return fd;
-}
-
-void close_nvls(samo_model* md) {
-  const NvlsApi& api = nvls_api();
-  if (!api.ok) return;
-  if (md->mc_c16) {
-    api.mem_unmap(reinterpret_cast<CUdeviceptr>(md->mc_c16), md->nvls_bytes);
-    api.va_free(reinterpret_cast<CUdeviceptr>(md->mc_c16), md->nvls_bytes);
-  }
-  if (md->uc_c16) {
-    api.mem_unmap(reinterpret_cast<CUdeviceptr>(md->uc_c16), md->nvls_bytes);
-    api.va_free(reinterpret_cast<CUdeviceptr>(md->uc_c16), md->nvls_bytes);
-  }
-  if (md->nvls_mem) api.mem_release(md->nvls_mem);
-  if (md->nvls_mc) api.mem_release(md->nvls_mc);
-  md->mc_c16 = md->uc_c16 = nullptr;
-  md->nvls_mem = md->nvls_mc = 0;
-  md->nvls_bytes = 0;
-}
-
-// Collective (after open_peers succeeded).  Any failure on any rank leaves
-// every rank on the peer-store path.
-static int open_nvls(samo_model* md) {
-  samo_comm* c = md->comm;
-  const int G = c->nranks, r = c->rank;
-  const NvlsApi& api = nvls_api();
-  const bool dbg = env_int("SAMO_NVLS_DEBUG", 0) != 0;
-  auto chk = [&](const char* what, CUresult e) {
-    if (e != CUDA_SUCCESS && dbg) std::fprintf(stderr, "[samo nvls] rank %d: %s failed (%d)\n", r, what, int(e));
-    return e == CUDA_SUCCESS;
-  };
-  if (dbg && !api.ok) std::fprintf(stderr, "[samo nvls] rank %d: driver entry points missing\n", r);
-  int ok = (api.ok && env_int("SAMO_P2P_NVLS", 0) != 0) ? 1 : 0;
-  SAMO_TRY(agree(c, &ok));
-  if (!ok) return SAMO_OK;
-  const int seq = c->nvls_seq++;
-  CUdevice dev = 0;
-  CUmulticastObjectProp mp{};
-  CUmemAllocationProp ap{};
-  size_t gran = 0, g2 = 0;
-  int fd = -1;
-  ok = chk("cuCtxGetDevice", api.ctx_device(&dev));
-  if (ok) {
-    ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
-    ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-    ap.location.id = static_cast<int>(dev);
-    ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;  // bindable to the multicast object
-    mp.numDevices = static_cast<unsigned>(G);
-    mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
-    mp.size = 2 * (md->n_al + kArenaSlack) * sizeof(uint16_t);
-    ok = chk("cuMulticastGetGranularity", api.mc_gran(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED)) &&
-         chk("cuMemGetAllocationGranularity", api.mem_gran(&g2, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
-    gran = std::max(gran, g2);
-    if (ok) mp.size = (mp.size + gran - 1) / gran * gran;
-  }
-  if (ok && r == 0) {
-    ok = chk("cuMulticastCreate", api.mc_create(&md->nvls_mc, &mp)) &&
-         chk("cuMemExportToShareableHandle", api.export_h(&fd, md->nvls_mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
-  }
-  SAMO_TRY(agree(c, &ok));
-  // file descriptor hand-over (rank 0 serves G - 1 connections)
-  if (ok) {
-    sockaddr_un addr;
-    socklen_t alen;
-    nvls_sock_name(c, seq, &addr, &alen);
-    if (r == 0) {
-      const int ls = socket(AF_UNIX, SOCK_STREAM, 0);
-      ok = ls >= 0 && bind(ls, reinterpret_cast<sockaddr*>(&addr), alen) == 0 && listen(ls, G) == 0;
-      for (int i = 1; ok && i < G; ++i) {
-        pollfd pf{ls, POLLIN, 0};
-        if (poll(&pf, 1, 30000) != 1) { ok = 0; break; }
-        const int cs = accept(ls, nullptr, nullptr);
-        ok = cs >= 0 && send_fd(cs, fd);
-        if (cs >= 0) close(cs);
-      }
-      if (ls >= 0) close(ls);
-    } else {
-      int got = -1;
-      for (int attempt = 0; attempt < 3000 && got < 0; ++attempt) {  // up to ~30 s for rank 0 to listen
-        const int cs = socket(AF_UNIX, SOCK_STREAM, 0);
-        if (cs < 0) break;
-        if (connect(cs, reinterpret_cast<sockaddr*>(&addr), alen) == 0) got = recv_fd(cs);
-        close(cs);
-        if (got < 0) usleep(10000);
-      }
-      if (got < 0 && dbg) std::fprintf(stderr, "[samo nvls] rank %d: no file descriptor from rank 0\n", r);
-      ok = got >= 0 && chk("cuMemImportFromShareableHandle",
-                           api.import_h(&md->nvls_mc, reinterpret_cast<void*>(static_cast<intptr_t>(got)),
-                                        CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR));
-      if (got >= 0) close(got);
-    }
-  }
-  if (fd >= 0) close(fd);
-  SAMO_TRY(agree(c, &ok));
-  if (ok) ok = chk("cuMulticastAddDevice", api.mc_add(md->nvls_mc, dev));
-  SAMO_TRY(agree(c, &ok));  // every device added before any bind
-  if (ok) {
-    md->nvls_bytes = mp.size;
-    CUdeviceptr uc = 0, mc = 0;
-    CUmemAccessDesc acc{};
-    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-    acc.location.id = static_cast<int>(dev);
-    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-    ok = chk("cuMemCreate", api.mem_create(&md->nvls_mem, mp.size, &ap, 0)) &&
-         chk("cuMulticastBindMem", api.mc_bind(md->nvls_mc, 0, md->nvls_mem, 0, mp.size, 0)) &&
-         chk("cuMemAddressReserve", api.va_reserve(&uc, mp.size, gran, 0, 0));
-    if (ok) {
-      ok = chk("cuMemMap(uc)", api.mem_map(uc, mp.size, 0, md->nvls_mem, 0)) &&
-           chk("cuMemSetAccess(uc)", api.set_access(uc, mp.size, &acc, 1));
-      if (ok) md->uc_c16 = reinterpret_cast<uint16_t*>(uc);
-      else api.va_free(uc, mp.size);
-    }
-    if (ok) ok = api.va_reserve(&mc, mp.size, gran, 0, 0) == CUDA_SUCCESS;
-    if (ok) {
-      ok = chk("cuMemMap(mc)", api.mem_map(mc, mp.size, 0, md->nvls_mc, 0)) &&
-           chk("cuMemSetAccess(mc)", api.set_access(mc, mp.size, &acc, 1));
-      if (ok) md->mc_c16 = reinterpret_cast<uint16_t*>(mc);
-      else api.va_free(mc, mp.size);
-    }
-  }
-  cudaGetLastError();
-  SAMO_TRY(agree(c, &ok));
-  if (!ok) close_nvls(md);
-  if (dbg) std::fprintf(stderr, "[samo nvls] rank %d: multicast %s\n", r, ok ? "on" : "off");
-  return SAMO_OK;
 }
 
 // Collective over the attached communicator: exchanges the CUDA IPC handles
@@ -344,8 +91,7 @@ int open_peers(samo_model* md) {
     return rc;
   }
   md->p2p_ok = true;
-  SAMO_TRY(set_spin_limit_from_env());
-  return open_nvls(md);
+  return set_spin_limit_from_env();
 }
 
 
@@ -461,7 +207,6 @@ int exchange_mode(const samo_model* md) {
 // local skip count) — the step starts at the exchange.
 static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather);
 static int launch_gather_push(samo_model* md, cudaStream_t S);
-static void set_pull_args(samo_model* md, const ShardPlan& p, StepArgs& a);
 
 int step_p2p(samo_model* md, cudaStream_t S, bool gather) {
   const int G = md->comm->nranks, r = md->comm->rank;
@@ -475,7 +220,6 @@ int step_p2p(samo_model* md, cudaStream_t S, bool gather) {
     return fail(SAMO_E_PARAMETER, "too many ranks for the arena padding");
   float* flag = flag_ptr(md);
   const bool push = gather ? p2p_push() : md->sunk_push;  // sunk: the sinks pushed already
-  const bool pull = p2p_pull();
   md->sunk_push = false;
   SAMO_TRY(plan_shards(md, md->p2p_plan, 1));
   if (md->p2p_plan.c != c) return fail(SAMO_E_STATE, "P2P plan mismatch");
@@ -515,14 +259,10 @@ int step_p2p(samo_model* md, cudaStream_t S, bool gather) {
   pa.norm2_out = md->norm2;
   pa.done = md->done;
   pa.bucket = -1;
-  pa.tma = env_int("SAMO_P2P_TMA", 0);
   pa.push = push ? 1 : 0;
   pa.recv = reinterpret_cast<const uint16_t*>(md->g);
   pa.rstride = c;  // one bucket: [G][c]
   pa.i0 = 0;
-  pa.local_c16 = pull ? 1 : 0;
-  const bool nvls = md->mc_c16 && !pull;
-  pa.mc16 = nvls ? md->mc_c16 : nullptr;
   if (pa.k1 > pa.k0) {
     SAMO_TRY(launch_shard_p2p(pa, S));
   } else {
@@ -533,8 +273,7 @@ int step_p2p(samo_model* md, cudaStream_t S, bool gather) {
   if (rr != ncclSuccess) return nccl_fail(rr, "ncclAllReduce(norm)");
   SAMO_TRY(phase_mark(md, 4, S));
   StepArgs a = step_args(md);
-  a.g = nvls ? md->uc_c16 : md->c16;
-  if (pull) set_pull_args(md, md->p2p_plan, a);
+  a.g = md->c16;
   SAMO_TRY(launch_expand_c16(a, std::min<int>(md->grid_expand, md->ntiles), S));
   SAMO_TRY(phase_mark(md, 5, S));
   SAMO_TRY(launch_step_finalize(md->st, md->norm2, 1, flag, md->cfg.beta1, md->cfg.beta2, md->capturing ? md->cfg_dev : nullptr, S));
@@ -696,24 +435,6 @@ int step_sharded(samo_model* md, cudaStream_t S) {
 // gradient arena as binary16, [G][B * c]: source q's element k (bucket b,
 // owner r) at q * B * c + b * c + (k - b * C - r * c).
 bool p2p_push() { return env_int("SAMO_P2P_PUSH", 1) != 0; }
-// Pull mode of the expand (SAMO_P2P_PULL=1, off by default): each owner keeps
-// its binary16 weights in its own theta16c arena and every rank's expand
-// pulls them over NVLink with its TMA loads.  Measured: the shard
-// update drops 0.62 -> 0.46 ms at G = 4 but the expand rises 1.03 -> 1.29 ms
-// (any ring depth), so pushing the weights stays the default.
-bool p2p_pull() { return env_int("SAMO_P2P_PULL", 0) != 0; }
-
-static void set_pull_args(samo_model* md, const ShardPlan& p, StepArgs& a) {
-  a.pull = 1;
-  a.pB = static_cast<uint32_t>(p.B);
-  a.pc = p.c;
-  a.pC = p.C;
-  const char* base = static_cast<const char*>(md->block);
-  const size_t c_off = reinterpret_cast<const char*>(md->c16) - base;
-  for (int q = 0; q < md->comm->nranks; ++q)
-    a.peer16c[q] = reinterpret_cast<const uint16_t*>(static_cast<const char*>(md->peer_base[q]) + c_off);
-}
-
 int build_push_tiles(samo_model* md, const ShardPlan& p) {
   if (md->push_tiles && md->push_G == p.G && md->push_B == p.B) return SAMO_OK;
   const uint64_t q = static_cast<uint64_t>(md->comm->rank);
@@ -813,7 +534,7 @@ struct P2PStep {
   P2PArgs pa{};
   StepArgs sbase{};
   int B = 1, ge = 0;
-  bool push = false, gather = true, nvls = false, pull = false;
+  bool push = false, gather = true;
 };
 
 static int p2p_prepare(samo_model* md, int B, bool gather, P2PStep& sp) {
@@ -832,7 +553,6 @@ static int p2p_prepare(samo_model* md, int B, bool gather, P2PStep& sp) {
   sp.gather = gather;
   sp.push = gather ? p2p_push() : md->sunk_push;  // sunk: the sinks pushed already
   md->sunk_push = false;
-  sp.pull = p2p_pull();
   if (sp.push) SAMO_TRY(build_push_tiles(md, p));
   const char* base = static_cast<const char*>(md->block);
   const size_t g_off = reinterpret_cast<const char*>(md->g) - base;
@@ -861,17 +581,12 @@ static int p2p_prepare(samo_model* md, int B, bool gather, P2PStep& sp) {
   pa.norm2_out = md->norm2;  // scratch: the bucket totals travel in the slots
   pa.done = md->done;
   const int sms = num_sms();
-  pa.tma = env_int("SAMO_P2P_TMA", 0);
-  pa.grid = sms * std::max(1, env_int("SAMO_P2P_SHARD_CTAS", pa.tma ? 1 : 2));
+  pa.grid = sms * std::max(1, env_int("SAMO_P2P_SHARD_CTAS", 2));
   sp.ge = std::min(md->grid_expand, sms * std::max(1, env_int("SAMO_P2P_EXPAND_CTAS", 2)));
   pa.push = sp.push ? 1 : 0;
   pa.recv = reinterpret_cast<const uint16_t*>(md->g);
   pa.rstride = static_cast<uint64_t>(B) * p.c;
-  pa.local_c16 = sp.pull ? 1 : 0;
-  sp.nvls = md->mc_c16 && !sp.pull;
-  pa.mc16 = sp.nvls ? md->mc_c16 : nullptr;
   sp.sbase = step_args(md);
-  if (sp.pull) set_pull_args(md, p, sp.sbase);
   return SAMO_OK;
 }
 
@@ -905,7 +620,7 @@ static int p2p_expand(samo_model* md, const P2PStep& sp, cudaStream_t E) {
   for (int b = 0; b < sp.B; ++b) {
     SAMO_TRY(launch_p2p_wait(md->slots, sp.pa.G, b, E));
     StepArgs a = sp.sbase;
-    a.g = sp.nvls ? md->uc_c16 : md->c16;
+    a.g = md->c16;
     a.tiles = md->tiles + p.ex_t[b];
     a.ntiles = p.ex_t[b + 1] - p.ex_t[b];
     if (a.ntiles) SAMO_TRY(launch_expand_c16(a, std::min<int>(sp.ge, a.ntiles), E));
@@ -1125,8 +840,6 @@ int samo_model_p2p_features(const samo_model* md) {
   int f = 0;
   if (md->p2p_ok) f |= SAMO_P2P_MAPPED;
   if (md->p2p_ok && p2p_push()) f |= SAMO_P2P_PUSH;
-  if (md->p2p_ok && p2p_pull()) f |= SAMO_P2P_PULL;
-  if (md->mc_c16 && !p2p_pull()) f |= SAMO_P2P_NVLS;
   return f;
 }
 

@@ -22,8 +22,6 @@ struct samo_comm {
   ncclComm_t flag = nullptr;  // the skip indicator, concurrently with the buckets
   int nranks = 1;
   int rank = 0;
-  uint8_t uid[SAMO_UNIQUE_ID_BYTES] = {};  // names the local rendezvous socket of the NVLS setup
-  int nvls_seq = 0;                        // one multicast object per attached model
   bool local_group = false;  // samo_model_attach_local_group: peers are models on this device, no NCCL
 };
 
@@ -144,13 +142,6 @@ struct samo_model {
   void* peer_base[kMaxP2PRanks] = {};
   bool p2p_ok = false;
   samo_comm* own_comm = nullptr;  // the virtual communicator of a local group (owned)
-  // NVLS multicast of the binary16 weights (P2P step): every rank's theta16c
-  // lives in VMM memory bound to one multicast object; the shard kernel
-  // stores each vector once through mc_c16 and the switch replicates it.
-  uint16_t* mc_c16 = nullptr;        // multicast mapping
-  uint16_t* uc_c16 = nullptr;        // this rank's unicast mapping of the bound memory
-  uint64_t nvls_bytes = 0;
-  CUmemGenericAllocationHandle nvls_mem = 0, nvls_mc = 0;
   std::vector<cudaEvent_t> ev_sh;       // sharded pipeline: K1 and all-gather events
   int grid_expand = 0;
   // Phase timing of the data-parallel step.
@@ -212,12 +203,10 @@ StepArgs step_args(samo_model* md);
 int flush_cfg(samo_model* md, cudaStream_t s);  // stream-ordered update of cfg_dev if dirty
 
 // dp.cu — data-parallel machinery
-int open_peers(samo_model* md);   // collective: CUDA IPC peer mappings (+ optional NVLS)
+int open_peers(samo_model* md);   // collective: CUDA IPC peer mappings
 void close_peers(samo_model* md);
-void close_nvls(samo_model* md);
 int exchange_mode(const samo_model* md);
 bool p2p_push();
-bool p2p_pull();
 int p2p_buckets(int G);
 int plan_shards(samo_model* md, ShardPlan& p, int B);
 int build_push_tiles(samo_model* md, const ShardPlan& p);

@@ -68,13 +68,6 @@ struct StepArgs {
   // instead of g + k (binary16 output only).
   uint32_t push;
   uint16_t* push16[kMaxP2PRanks];
-  // Expand-only pass with pulled weights (peer-to-peer step): the binary16
-  // weights of element k live in its owner's theta16c arena, peer16c[owner],
-  // owner = ((k - b*pC) / pc) with bucket b = min(k / pC, pB - 1).
-  uint32_t pull;
-  uint32_t pB;
-  uint64_t pc, pC;
-  const uint16_t* peer16c[kMaxP2PRanks];
 };
 
 // K1 gather: out_f32 -> unscaled fp32 for the exchange, else raw binary16.
@@ -131,15 +124,12 @@ struct P2PArgs {
   SamoPeerSlots* slots[kMaxP2PRanks];
   int bucket;
   int grid;                           // 0 = default
-  int tma;                            // 1: k_shard_p2p_tma (TMA ring), 0: register loads
   // Push mode: every rank's K1 already wrote its contribution for [k0, k1)
   // into this rank's receive buffer: rank q's at recv[q * rstride + i0 + (k - k0)].
   int push;
   const uint16_t* recv;
   uint64_t rstride, i0;
-  int local_c16;                      // store the binary16 weights only locally (pulled by the expand)
   const SamoStepConfig* cfg;          // device scalars: override prm / scale
-  uint16_t* mc16;                     // NVLS: store each weight vector once through this multicast mapping
 };
 int launch_shard_p2p(const P2PArgs& a, cudaStream_t s);
 // Skip-flag exchange over peer memory (one warp): publishes this rank's

@@ -32,8 +32,8 @@
 //   Adam scalars.  EXPAND = true is the expand-only pass of the data-
 //   parallel steps (binary16 weights in, no Adam).
 //
-// Data-parallel pieces: k_adam_shard (NCCL sharded exchange), k_shard_p2p /
-// k_shard_p2p_tma (fused peer-to-peer exchange: rank-ordered sum of the G
+// Data-parallel pieces: k_adam_shard (NCCL sharded exchange), k_shard_p2p
+// (fused peer-to-peer exchange: rank-ordered sum of the G
 // contributions, Adam, binary16 weights stored to every rank, bucket
 // signals), the peer-signal kernels (flag exchange, bucket wait, epoch) and
 // k_step_finalize.
@@ -365,23 +365,7 @@ __global__ void __launch_bounds__(kThreads + 32) k23_update(StepArgs a) {
                                  : static_cast<const void*>(reinterpret_cast<const float*>(a.g) + f0);
           if constexpr (EXPAND) {  // theta/m/v slots unused; hb > 0 here
             mbar_arrive_expect_tx(&full[s], 2 * hb);
-            if (a.pull) {
-              // pull each owner's part of [h0, h0 + hb/2) over NVLink; owner
-              // boundaries are multiples of 8 elements, so pieces stay 16-byte aligned
-              const uint64_t h1 = h0 + hb / 2;
-              for (uint64_t cur = h0; cur < h1;) {
-                uint64_t b = cur / a.pC;
-                if (b >= a.pB) b = a.pB - 1;
-                const uint64_t r = (cur - b * a.pC) / a.pc;
-                uint64_t end = b * a.pC + (r + 1) * a.pc;
-                if (end > h1) end = h1;
-                bulk_g2s_peer(st + 3 * L::kF32 + (cur - h0) * 2, a.peer16c[r] + cur,
-                              static_cast<uint32_t>((end - cur) * 2), &full[s]);
-                cur = end;
-              }
-            } else {
-              bulk_g2s(st + 3 * L::kF32, gsrc, hb, &full[s], policy);
-            }
+            bulk_g2s(st + 3 * L::kF32, gsrc, hb, &full[s], policy);
             bulk_g2s(st + 3 * L::kF32 + L::kG, a.off16 + h0, hb, &full[s], policy);
           } else {
             // kc1 > kc0, so every range rounded out to 16 bytes is non-empty.
@@ -1164,9 +1148,8 @@ __device__ __forceinline__ uint16_t half_lane(const uint4& v, int e) {
 // pipelined step, publishes bucket completion + norm^2 to every rank.
 template <int G, int NT>
 __device__ __forceinline__ void shard_finish(const P2PArgs& a, float nacc, float* red, int* last_cta) {
-  // Make the peer (or multicast) stores visible system-wide before the
-  // kernel retires and before the completion signals below.
-  if (a.mc16) asm volatile("fence.proxy.alias;" ::: "memory");
+  // Make the peer stores visible system-wide before the kernel retires and
+  // before the completion signals below.
   asm volatile("fence.acq_rel.sys;" ::: "memory");
   float x = nacc;
 #pragma unroll
@@ -1283,162 +1266,10 @@ __global__ void __launch_bounds__(kThreads, SAMO_P2P_MINB) k_shard_p2p(P2PArgs a
       }
     }
     const uint4 pv = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-    if (a.mc16) {
-      multimem_st_v4(a.mc16 + k, pv);
-    } else {
 #pragma unroll
-      for (int r = 0; r < G; ++r)
-        if (!a.local_c16 || r == a.rank) *reinterpret_cast<uint4*>(a.c16[r] + k) = pv;  // arenas are padded
-    }
+    for (int r = 0; r < G; ++r) *reinterpret_cast<uint4*>(a.c16[r] + k) = pv;  // arenas are padded
   }
   shard_finish<G, kThreads>(a, nacc, red, &last_cta);
-}
-
-// The same shard update fed by TMA: one producer lane streams 1024-element
-// chunks — every rank's binary16 gradient (bulk copies straight from peer
-// memory over NVLink) and the local theta/m/v — into an NS-deep shared-memory
-// ring; four consumer warps run the rank-ordered sum + Adam from shared
-// memory and store theta/m/v locally and the binary16 weights to every rank.
-// Bytes in flight come from the ring, not from registers, so one small CTA
-// per SM saturates the links and leaves the SMs to the concurrent expand.
-constexpr int kShardCH = 1024;
-constexpr int kShardConsumers = 4;  // warps; 8 elements per thread per chunk
-template <int G>
-constexpr uint32_t shard_stage_bytes() { return G * kShardCH * 2u + 3u * kShardCH * 4u; }
-
-__device__ __forceinline__ void bulk_g2s_plain(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar))
-      : "memory");
-}
-
-template <int G, int NS>
-__global__ void __launch_bounds__(32 * (kShardConsumers + 1)) k_shard_p2p_tma(P2PArgs a) {
-  constexpr int NT = 32 * kShardConsumers;
-  constexpr uint32_t kStage = shard_stage_bytes<G>();
-  extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ __align__(8) uint64_t full[NS];
-  __shared__ __align__(8) uint64_t empty[NS];
-  __shared__ float red[kShardConsumers];
-  __shared__ int last_cta;
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kShardConsumers);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-  const uint64_t n = a.k1 > a.k0 ? a.k1 - a.k0 : 0;
-  const uint64_t nch = (n + kShardCH - 1) / kShardCH;
-
-  if (warp == kShardConsumers) {
-    if (lane == 0) {
-      const uint64_t policy = policy_evict_first();
-      uint32_t it = 0;
-      for (uint64_t c = blockIdx.x; c < nch; c += gridDim.x, ++it) {
-        const int s = static_cast<int>(it % NS);
-        if (it >= static_cast<uint32_t>(NS)) mbar_wait(&empty[s], ((it / NS) - 1) & 1u);
-        const uint64_t k = a.k0 + c * kShardCH;  // a multiple of 8
-        const uint32_t cnt = static_cast<uint32_t>(min(static_cast<uint64_t>(kShardCH), a.k1 - k));
-        const uint32_t hb = ((cnt + 7u) & ~7u) * 2u, fb = ((cnt + 3u) & ~3u) * 4u;
-        uint8_t* st = smem + s * kStage;
-        mbar_arrive_expect_tx(&full[s], G * hb + 3u * fb);
-#pragma unroll
-        for (int r = 0; r < G; ++r) bulk_g2s_plain(st + r * kShardCH * 2, a.g16[r] + k, hb, &full[s]);
-        uint8_t* f = st + G * kShardCH * 2;
-        bulk_g2s(f, a.theta + k, fb, &full[s], policy);
-        bulk_g2s(f + kShardCH * 4, a.m + k, fb, &full[s], policy);
-        bulk_g2s(f + 2 * kShardCH * 4, a.v + k, fb, &full[s], policy);
-      }
-    }
-    return;
-  }
-
-  const bool skip = *reinterpret_cast<const volatile float*>(a.flag_slot) != 0.0f;
-  const SamoAdamParams prm = step_prm(a.cfg, a.prm);
-  const float b1p = __fmul_rn(a.st->beta1_pow, prm.beta1);
-  const float b2p = __fmul_rn(a.st->beta2_pow, prm.beta2);
-  const float bias1 = __fsub_rn(1.0f, b1p), bias2 = __fsub_rn(1.0f, b2p);
-  const float omb1 = __fsub_rn(1.0f, prm.beta1), omb2 = __fsub_rn(1.0f, prm.beta2);
-  const float lrwd = __fmul_rn(prm.lr, prm.wd);
-  const float scale = pin_f32(a.cfg ? a.cfg->p2p_scale : a.scale);
-  float* const p_theta = pin_ptr(a.theta);
-  float* const p_m = pin_ptr(a.m);
-  float* const p_v = pin_ptr(a.v);
-  float nacc = 0.0f;
-  const uint32_t e0 = tid * 8u;
-  uint32_t it = 0;
-  for (uint64_t c = blockIdx.x; c < nch; c += gridDim.x, ++it) {
-    const int s = static_cast<int>(it % NS);
-    mbar_wait(&full[s], (it / NS) & 1u);
-    const uint64_t k = a.k0 + c * kShardCH;
-    const uint32_t cnt = static_cast<uint32_t>(min(static_cast<uint64_t>(kShardCH), a.k1 - k));
-    if (e0 < cnt) {
-      const int ce = cnt - e0 < 8u ? static_cast<int>(cnt - e0) : 8;
-      const uint8_t* st = smem + s * kStage;
-      uint4 h[G];
-#pragma unroll
-      for (int r = 0; r < G; ++r) h[r] = *reinterpret_cast<const uint4*>(st + r * kShardCH * 2 + e0 * 2);
-      const float* f = reinterpret_cast<const float*>(st + G * kShardCH * 2);
-      float th[8], mm[8], vv[8];
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const float4 t4 = *reinterpret_cast<const float4*>(f + e0 + 4 * q);
-        const float4 m4 = *reinterpret_cast<const float4*>(f + kShardCH + e0 + 4 * q);
-        const float4 v4 = *reinterpret_cast<const float4*>(f + 2 * kShardCH + e0 + 4 * q);
-        th[4 * q] = t4.x; th[4 * q + 1] = t4.y; th[4 * q + 2] = t4.z; th[4 * q + 3] = t4.w;
-        mm[4 * q] = m4.x; mm[4 * q + 1] = m4.y; mm[4 * q + 2] = m4.z; mm[4 * q + 3] = m4.w;
-        vv[4 * q] = v4.x; vv[4 * q + 1] = v4.y; vv[4 * q + 2] = v4.z; vv[4 * q + 3] = v4.w;
-      }
-      uint32_t packed[4];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        float g = 0.0f;  // rank-ascending fp32 sum, as the oracle's dp_sum
-#pragma unroll
-        for (int r = 0; r < G; ++r) g = __fadd_rn(g, mul_x86(grad_to_f32(half_lane(h[r], e), a.grad_bf16 != 0), scale));
-        if (e < ce) nacc = __fadd_rn(nacc, __fmul_rn(g, g));
-        float t = th[e];
-        if (!skip && e < ce) t = adam_one(g, mm[e], vv[e], t, prm, omb1, omb2, bias1, bias2, lrwd);
-        th[e] = t;
-        const uint32_t hbits = f32_to_f16_bits(t);
-        packed[e >> 1] = (e & 1) ? (packed[e >> 1] | (hbits << 16)) : hbits;
-      }
-      const uint64_t kk = k + e0;
-      if (!skip) {
-        if (ce == 8) {
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            *reinterpret_cast<float4*>(p_theta + kk + 4 * q) =
-                make_float4(th[4 * q], th[4 * q + 1], th[4 * q + 2], th[4 * q + 3]);
-            *reinterpret_cast<float4*>(p_m + kk + 4 * q) =
-                make_float4(mm[4 * q], mm[4 * q + 1], mm[4 * q + 2], mm[4 * q + 3]);
-            *reinterpret_cast<float4*>(p_v + kk + 4 * q) =
-                make_float4(vv[4 * q], vv[4 * q + 1], vv[4 * q + 2], vv[4 * q + 3]);
-          }
-        } else {
-          for (int e = 0; e < ce; ++e) {
-            p_theta[kk + e] = th[e];
-            p_m[kk + e] = mm[e];
-            p_v[kk + e] = vv[e];
-          }
-        }
-      }
-      const uint4 pv = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-      if (a.mc16) {
-        multimem_st_v4(a.mc16 + kk, pv);
-      } else {
-        for (int r = 0; r < G; ++r)
-          if (!a.local_c16 || r == a.rank) *reinterpret_cast<uint4*>(a.c16[r] + kk) = pv;  // arenas are padded
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
-  shard_finish<G, NT>(a, nacc, red, &last_cta);
 }
 
 // Spin on a local signal word written by a peer (acquire, system scope).  A
@@ -1691,33 +1522,8 @@ int launch_step_repair(const StepArgs& a, cudaStream_t s) {
   return launch_persistent(k123_repair, a, 0, num_sms(), s, kThreads, "k123_repair", pdl);
 }
 
-template <int G>
-static int launch_shard_tma(const P2PArgs& a, cudaStream_t s) {
-  constexpr int NS = G <= 4 ? 3 : 2;
-  const size_t sm = NS * shard_stage_bytes<G>();
-  const uint64_t nch = (a.k1 > a.k0) ? (a.k1 - a.k0 + kShardCH - 1) / kShardCH : 0;
-  const uint64_t cap = a.grid > 0 ? a.grid : static_cast<uint64_t>(num_sms()) * 2;
-  const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(cap, nch)));
-  SAMO_CUDA_TRY(cudaFuncSetAttribute(k_shard_p2p_tma<G, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(sm)));
-  k_shard_p2p_tma<G, NS><<<grid, 32 * (kShardConsumers + 1), sm, s>>>(a);
-  SAMO_LAUNCH_CHECK("k_shard_p2p_tma");
-  return SAMO_OK;
-}
-
 int launch_shard_p2p(const P2PArgs& a, cudaStream_t s) {
   if (a.G < 2 || a.G > kMaxP2PRanks) return fail(SAMO_E_PARAMETER, "peer-to-peer exchange supports 2..8 ranks");
-  if (a.tma && !a.push) {
-    switch (a.G) {
-      case 2: return launch_shard_tma<2>(a, s);
-      case 3: return launch_shard_tma<3>(a, s);
-      case 4: return launch_shard_tma<4>(a, s);
-      case 5: return launch_shard_tma<5>(a, s);
-      case 6: return launch_shard_tma<6>(a, s);
-      case 7: return launch_shard_tma<7>(a, s);
-      default: return launch_shard_tma<8>(a, s);
-    }
-  }
   const uint64_t nv = (a.k1 > a.k0) ? (a.k1 - a.k0 + 7) / 8 : 0;
   const uint64_t cap = a.grid > 0 ? a.grid : static_cast<uint64_t>(num_sms()) * SAMO_P2P_GRID;
   const int grid = static_cast<int>(
@@ -1817,11 +1623,6 @@ int launch_step_finalize(SamoStepState* st, const double* norm2, int nslots, flo
   return SAMO_OK;
 }
 
-static int env_ns() {
-  const char* e = getenv("SAMO_EXPAND_PULL_NS");
-  return (e && *e) ? atoi(e) : 6;
-}
-
 int expand_grid(uint32_t tile_elems) {
   return grid_for(k23_update<true, 1024, 3, true>, k23_smem<true, 1024, 3, true>(tile_elems),
                   kThreads + 32);
@@ -1830,14 +1631,6 @@ int expand_grid(uint32_t tile_elems) {
 int launch_expand_c16(const StepArgs& a, int grid, cudaStream_t s) {
   if (a.ntiles == 0) return SAMO_OK;
   if (grid <= 0) grid = expand_grid(a.tile_elems);
-  // Pulled weights (NVLink latency) get a deeper ring (SAMO_EXPAND_PULL_NS).
-  const int ns = a.pull ? env_ns() : 3;
-  if (ns >= 8)
-    return launch_persistent(k23_update<true, 1024, 8, true>, a, k23_smem<true, 1024, 8, true>(a.tile_elems),
-                             grid, s, kThreads + 32, "k23_expand");
-  if (ns >= 6)
-    return launch_persistent(k23_update<true, 1024, 6, true>, a, k23_smem<true, 1024, 6, true>(a.tile_elems),
-                             grid, s, kThreads + 32, "k23_expand");
   return launch_persistent(k23_update<true, 1024, 3, true>, a, k23_smem<true, 1024, 3, true>(a.tile_elems),
                            grid, s, kThreads + 32, "k23_expand");
 }

@@ -469,9 +469,9 @@ class SamoModel:
         _abi.call("samo_model_exchange", self._h, _stream())
 
     def p2p_features(self) -> dict:
-        """Peer-to-peer mechanisms in use: mapped, push, pull, nvls."""
+        """Peer-to-peer mechanisms in use: mapped, push (K1 pushes the gradients to their owners)."""
         f = int(_abi.load().samo_model_p2p_features(self._h))
-        return {"mapped": bool(f & 1), "push": bool(f & 2), "pull": bool(f & 4), "nvls": bool(f & 8)}
+        return {"mapped": bool(f & 1), "push": bool(f & 2)}
 
     def step_sunk(self) -> None:
         """The step after the backward sinks: exchange (peer-to-peer) + update."""

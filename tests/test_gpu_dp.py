@@ -74,10 +74,8 @@ def _run(tmp_path, mode, world, steps=4, save_g=False):
     # p2p: the pipelined peer-signalled step (5 buckets, some empty on some
     # ranks); p2p-serial: one shard launch between two NCCL barriers.
     env["SAMO_P2P_BUCKETS"] = "1" if mode == "p2p-serial" else "5"
-    env["SAMO_P2P_TMA"] = "1" if mode == "p2p-tma" else "0"  # TMA-fed shard kernel
     env["SAMO_DP_SINK"] = "1" if mode == "p2p-sink" else "0"  # per-layer sinks + step_sunk
-    env["SAMO_P2P_PULL"] = "1" if mode == "p2p-pull" else "0"  # expand pulls the weights
-    env["SAMO_P2P_NVLS"] = "1" if mode == "p2p-nvls" else "0"  # multicast weight stores
+    env["SAMO_P2P_PUSH"] = "0" if mode == "p2p-pull" else "1"  # the shard update pulls the gradients
     env["SAMO_DP_BF16"] = "1" if mode.endswith("-bf16") else "0"  # bfloat16 dense gradients
     os.environ["SAMO_DP_BF16"] = env["SAMO_DP_BF16"]  # the parent's oracle replay reads it too
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
@@ -115,8 +113,8 @@ def _check(r, oracle, world, mode, steps=4):
     assert covered == (n if mode.split("-")[0] in ("sharded", "p2p") else world * n)
 
 
-@pytest.mark.parametrize("mode", ["p2p", "p2p-serial", "p2p-graph", "p2p-tma", "p2p-sink", "p2p-pull",
-                                  "p2p-nvls", "sharded", "sharded-graph", "overlap",
+@pytest.mark.parametrize("mode", ["p2p", "p2p-serial", "p2p-graph", "p2p-sink", "p2p-pull",
+                                  "sharded", "sharded-graph", "overlap",
                                   "staged", "graph", "p2p-bf16", "sharded-bf16", "overlap-bf16"])
 def test_dp_two_gpus_bit_exact(tmp_path, oracle, mode):
     if torch.cuda.device_count() < 2:
@@ -124,8 +122,7 @@ def test_dp_two_gpus_bit_exact(tmp_path, oracle, mode):
     _check(_run(tmp_path, mode, 2), oracle, 2, mode)
 
 
-@pytest.mark.parametrize("mode", ["p2p", "p2p-serial", "p2p-graph", "p2p-tma", "p2p-sink", "p2p-pull",
-                                  "p2p-nvls", "p2p-bf16"])
+@pytest.mark.parametrize("mode", ["p2p", "p2p-serial", "p2p-graph", "p2p-sink", "p2p-pull", "p2p-bf16"])
 def test_dp_four_gpus_p2p_bit_exact(tmp_path, oracle, mode):
     """The fused exchange sums in rank order: bit-exact for G = 4 too."""
     if torch.cuda.device_count() < 4:
@@ -333,10 +330,9 @@ def _local_group_run(oracle, G, steps=4, sink=False, devices=None):
     return out
 
 
-@pytest.mark.parametrize("G,env", [(3, {}), (5, {}), (8, {}), (8, {"SAMO_P2P_TMA": "1"}),
-                                   (8, {"SAMO_P2P_PUSH": "0"}), (8, {"SAMO_P2P_PULL": "1"}),
+@pytest.mark.parametrize("G,env", [(3, {}), (5, {}), (8, {}), (8, {"SAMO_P2P_PUSH": "0"}),
                                    (2, {"SAMO_P2P_BUCKETS": "5"}), (7, {"SAMO_P2P_BUCKETS": "3"}),
-                                   (3, {"SAMO_DP_BF16": "1"}), (8, {"SAMO_DP_BF16": "1", "SAMO_P2P_TMA": "1"})],
+                                   (3, {"SAMO_DP_BF16": "1"}), (8, {"SAMO_DP_BF16": "1", "SAMO_P2P_PUSH": "0"})],
                          ids=lambda x: str(x) if isinstance(x, int) else "-".join(f"{k[9:]}{v}" for k, v in x.items()) or "default")
 def test_local_group_p2p_bit_exact(cuda, oracle, monkeypatch, G, env):
     """The pipelined peer-to-peer step at G up to 8 on ONE GPU: G models on

@@ -1,9 +1,9 @@
 # P2P step variants at NGPU GPUs: each VARIANT is a list of env assignments
-# (SAMO_P2P_BUCKETS, SAMO_P2P_TMA, SAMO_P2P_SHARD_CTAS, SAMO_P2P_EXPAND_CTAS).
+# (SAMO_P2P_BUCKETS, SAMO_P2P_PUSH, SAMO_P2P_SHARD_CTAS, SAMO_P2P_EXPAND_CTAS).
 mkdir -p gpurun_out
 N=${NGPU:-4}
 OUT=gpurun_out/sweep_p2p_pipe_g$N.log
-IFS=';' read -ra VS <<< "${VARIANTS:-SAMO_P2P_BUCKETS=1 SAMO_P2P_TMA=0;SAMO_P2P_BUCKETS=1 SAMO_P2P_TMA=1;SAMO_P2P_BUCKETS=8 SAMO_P2P_TMA=0;SAMO_P2P_BUCKETS=8 SAMO_P2P_TMA=1}"
+IFS=';' read -ra VS <<< "${VARIANTS:-SAMO_P2P_BUCKETS=1 SAMO_P2P_PUSH=1;SAMO_P2P_BUCKETS=1 SAMO_P2P_PUSH=0;SAMO_P2P_BUCKETS=8 SAMO_P2P_PUSH=1;SAMO_P2P_BUCKETS=8 SAMO_P2P_PUSH=0}"
 for v in "${VS[@]}"; do
   echo "$v" >> $OUT
   env $v timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N \
