@@ -48,9 +48,6 @@ namespace samo_dev {
 namespace {
 
 constexpr int kU = 4;         // independent elements per thread and pass (ILP)
-#ifndef SAMO_P2P_MINB
-#define SAMO_P2P_MINB 1  // min resident CTAs/SM hint for k_shard_p2p (tuning)
-#endif
 #ifndef SAMO_P2P_GRID
 #define SAMO_P2P_GRID 8  // CTAs per SM launched for k_shard_p2p (tuning)
 #endif
@@ -1120,23 +1117,16 @@ __global__ void __launch_bounds__(kThreads) k_adam_shard(ShardArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Fused peer-to-peer exchange + shard update.  Every rank's K1 has written
-// its compressed binary16 gradient (raw grad16) into its own arena; the
-// skip-flag allreduce before this kernel is the cross-rank barrier.  For the
-// owned range, each thread loads 8 consecutive halves from every rank over
-// NVLink (16-byte peer loads), sums fl32(h * scale) in rank order — the
-// oracle's rank-ascending fp32 sum, so the result is bit-exact for any G —
-// runs Adam on its own fp32 state and stores the 8 new binary16 weights into
-// every rank's theta16c (16-byte peer stores).  Link bytes per rank:
-// 2n(G-1)/G in (gradients) + 2n(G-1)/G out (weights).
+// Fused peer-to-peer exchange + shard update.  The skip-flag exchange before
+// this kernel is the cross-rank barrier.  For the owned range, each thread
+// takes VE consecutive elements: it loads their binary16 gradient from every
+// rank — from the local receive buffer the ranks' K1 pushed into (push mode),
+// or from each rank's own arena over NVLink (pull mode) — sums fl32(h * scale)
+// in rank order (the oracle's rank-ascending fp32 sum, so the result is
+// bit-exact for any G), runs Adam on its own fp32 state and stores the VE new
+// binary16 weights into every rank's theta16c (peer stores).  Link bytes per
+// rank: 2n(G-1)/G in (gradients) + 2n(G-1)/G out (weights).
 
-__device__ __forceinline__ uint4 ld_peer_v4(const uint16_t* p) {
-  uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p));
-  return v;
-}
 
 __device__ __forceinline__ uint16_t half_lane(const uint4& v, int e) {
   const uint32_t w = e < 2 ? v.x : e < 4 ? v.y : e < 6 ? v.z : v.w;
@@ -1185,8 +1175,41 @@ __device__ __forceinline__ void shard_finish(const P2PArgs& a, float nacc, float
   }
 }
 
-template <int G, bool PUSH>
-__global__ void __launch_bounds__(kThreads, SAMO_P2P_MINB) k_shard_p2p(P2PArgs a) {
+// VE binary16 lanes (8 or 4) of a 16- or 8-byte vector.
+template <int VE>
+struct HalfVec;
+template <>
+struct HalfVec<8> {
+  uint4 v;
+  __device__ __forceinline__ void load(const uint16_t* p) { v = ld_stream_v4(p); }
+  __device__ __forceinline__ uint16_t lane(int e) const { return half_lane(v, e); }
+  __device__ __forceinline__ static void store(uint16_t* p, const uint32_t (&w)[4]) {
+    *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+template <>
+struct HalfVec<4> {
+  uint2 v;
+  __device__ __forceinline__ void load(const uint16_t* p) {
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  }
+  __device__ __forceinline__ uint16_t lane(int e) const {
+    const uint32_t w = e < 2 ? v.x : v.y;
+    return static_cast<uint16_t>((e & 1) ? (w >> 16) : (w & 0xFFFFu));
+  }
+  __device__ __forceinline__ static void store(uint16_t* p, const uint32_t (&w)[2]) {
+    *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+  }
+};
+
+// VE elements per thread and vector.  Alone (the serial step) the kernel is
+// latency-bound by the IEEE Adam's instruction count: VE = 4 at 4 CTAs/SM
+// (<= 64 registers) runs the G = 2 shard update in 0.72 ms against 0.87 ms
+// for VE = 8 at 2 CTAs/SM.  Overlapped with the expand (the pipelined step)
+// VE = 8 at 2 CTAs/SM is 1-2% faster: there it is NVLink-bound and more
+// resident warps only take issue slots from the expand.
+template <int G, bool PUSH, int VE>
+__global__ void __launch_bounds__(kThreads, VE == 4 ? 4 : 1) k_shard_p2p(P2PArgs a) {
   __shared__ float red[kThreads / 32];
   __shared__ int last_cta;
   const bool skip = *reinterpret_cast<const volatile float*>(a.flag_slot) != 0.0f;
@@ -1197,51 +1220,49 @@ __global__ void __launch_bounds__(kThreads, SAMO_P2P_MINB) k_shard_p2p(P2PArgs a
   const float omb1 = __fsub_rn(1.0f, prm.beta1), omb2 = __fsub_rn(1.0f, prm.beta2);
   const float lrwd = __fmul_rn(prm.lr, prm.wd);
   const float scale = pin_f32(a.cfg ? a.cfg->p2p_scale : a.scale);
+  const bool bf16 = a.grad_bf16 != 0;
   float nacc = 0.0f;
   const uint64_t n = a.k1 - a.k0;
-  const uint64_t nv = (n + 7) / 8;  // 8-element vectors (the last one may be partial)
+  const uint64_t nv = (n + VE - 1) / VE;  // VE-element vectors (the last one may be partial)
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kThreads;
   for (uint64_t q = blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x; q < nv; q += stride) {
-    const uint64_t k = a.k0 + 8 * q;
+    const uint64_t k = a.k0 + VE * q;
     const uint64_t left = a.k1 - k;
-    const int cnt = left < 8 ? static_cast<int>(left) : 8;
-    uint4 h[G];
+    const int cnt = left < VE ? static_cast<int>(left) : VE;
+    HalfVec<VE> h[G];
     if constexpr (PUSH) {  // every rank's contribution is already in the local receive buffer
       const uint16_t* src = a.recv + a.i0 + (k - a.k0);
 #pragma unroll
-      for (int r = 0; r < G; ++r) h[r] = ld_stream_v4(src + r * a.rstride);
+      for (int r = 0; r < G; ++r) h[r].load(src + r * a.rstride);
     } else {
 #pragma unroll
-      for (int r = 0; r < G; ++r) h[r] = ld_peer_v4(a.g16[r] + k);  // arenas are padded
+      for (int r = 0; r < G; ++r) h[r].load(a.g16[r] + k);  // peer loads; arenas are padded
     }
-    float th[8], mm[8], vv[8];
-    if (cnt == 8) {
-      const float4 t0 = *reinterpret_cast<const float4*>(a.theta + k);
-      const float4 t1 = *reinterpret_cast<const float4*>(a.theta + k + 4);
-      const float4 m0 = *reinterpret_cast<const float4*>(a.m + k);
-      const float4 m1 = *reinterpret_cast<const float4*>(a.m + k + 4);
-      const float4 v0 = *reinterpret_cast<const float4*>(a.v + k);
-      const float4 v1 = *reinterpret_cast<const float4*>(a.v + k + 4);
-      th[0] = t0.x; th[1] = t0.y; th[2] = t0.z; th[3] = t0.w;
-      th[4] = t1.x; th[5] = t1.y; th[6] = t1.z; th[7] = t1.w;
-      mm[0] = m0.x; mm[1] = m0.y; mm[2] = m0.z; mm[3] = m0.w;
-      mm[4] = m1.x; mm[5] = m1.y; mm[6] = m1.z; mm[7] = m1.w;
-      vv[0] = v0.x; vv[1] = v0.y; vv[2] = v0.z; vv[3] = v0.w;
-      vv[4] = v1.x; vv[5] = v1.y; vv[6] = v1.z; vv[7] = v1.w;
+    float th[VE], mm[VE], vv[VE];
+    if (cnt == VE) {
+#pragma unroll
+      for (int j = 0; j < VE / 4; ++j) {
+        const float4 t4 = *reinterpret_cast<const float4*>(a.theta + k + 4 * j);
+        const float4 m4 = *reinterpret_cast<const float4*>(a.m + k + 4 * j);
+        const float4 v4 = *reinterpret_cast<const float4*>(a.v + k + 4 * j);
+        th[4 * j] = t4.x; th[4 * j + 1] = t4.y; th[4 * j + 2] = t4.z; th[4 * j + 3] = t4.w;
+        mm[4 * j] = m4.x; mm[4 * j + 1] = m4.y; mm[4 * j + 2] = m4.z; mm[4 * j + 3] = m4.w;
+        vv[4 * j] = v4.x; vv[4 * j + 1] = v4.y; vv[4 * j + 2] = v4.z; vv[4 * j + 3] = v4.w;
+      }
     } else {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
+      for (int e = 0; e < VE; ++e) {
         th[e] = e < cnt ? a.theta[k + e] : 0.0f;
         mm[e] = e < cnt ? a.m[k + e] : 0.0f;
         vv[e] = e < cnt ? a.v[k + e] : 0.0f;
       }
     }
-    uint32_t packed[4];
+    uint32_t packed[VE / 2];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
+    for (int e = 0; e < VE; ++e) {
       float g = 0.0f;  // rank-ascending fp32 sum, as the oracle's dp_sum
 #pragma unroll
-      for (int r = 0; r < G; ++r) g = __fadd_rn(g, mul_x86(grad_to_f32(half_lane(h[r], e), a.grad_bf16 != 0), scale));
+      for (int r = 0; r < G; ++r) g = __fadd_rn(g, mul_x86(grad_to_f32(h[r].lane(e), bf16), scale));
       if (e < cnt) nacc = __fadd_rn(nacc, __fmul_rn(g, g));
       float t = th[e];
       if (!skip && e < cnt) t = adam_one(g, mm[e], vv[e], t, prm, omb1, omb2, bias1, bias2, lrwd);
@@ -1250,13 +1271,13 @@ __global__ void __launch_bounds__(kThreads, SAMO_P2P_MINB) k_shard_p2p(P2PArgs a
       packed[e >> 1] = (e & 1) ? (packed[e >> 1] | (hb << 16)) : hb;
     }
     if (!skip) {
-      if (cnt == 8) {
-        *reinterpret_cast<float4*>(a.theta + k) = make_float4(th[0], th[1], th[2], th[3]);
-        *reinterpret_cast<float4*>(a.theta + k + 4) = make_float4(th[4], th[5], th[6], th[7]);
-        *reinterpret_cast<float4*>(a.m + k) = make_float4(mm[0], mm[1], mm[2], mm[3]);
-        *reinterpret_cast<float4*>(a.m + k + 4) = make_float4(mm[4], mm[5], mm[6], mm[7]);
-        *reinterpret_cast<float4*>(a.v + k) = make_float4(vv[0], vv[1], vv[2], vv[3]);
-        *reinterpret_cast<float4*>(a.v + k + 4) = make_float4(vv[4], vv[5], vv[6], vv[7]);
+      if (cnt == VE) {
+#pragma unroll
+        for (int j = 0; j < VE / 4; ++j) {
+          *reinterpret_cast<float4*>(a.theta + k + 4 * j) = make_float4(th[4 * j], th[4 * j + 1], th[4 * j + 2], th[4 * j + 3]);
+          *reinterpret_cast<float4*>(a.m + k + 4 * j) = make_float4(mm[4 * j], mm[4 * j + 1], mm[4 * j + 2], mm[4 * j + 3]);
+          *reinterpret_cast<float4*>(a.v + k + 4 * j) = make_float4(vv[4 * j], vv[4 * j + 1], vv[4 * j + 2], vv[4 * j + 3]);
+        }
       } else {
         for (int e = 0; e < cnt; ++e) {
           a.theta[k + e] = th[e];
@@ -1265,9 +1286,8 @@ __global__ void __launch_bounds__(kThreads, SAMO_P2P_MINB) k_shard_p2p(P2PArgs a
         }
       }
     }
-    const uint4 pv = make_uint4(packed[0], packed[1], packed[2], packed[3]);
 #pragma unroll
-    for (int r = 0; r < G; ++r) *reinterpret_cast<uint4*>(a.c16[r] + k) = pv;  // arenas are padded
+    for (int r = 0; r < G; ++r) HalfVec<VE>::store(a.c16[r] + k, packed);  // arenas are padded
   }
   shard_finish<G, kThreads>(a, nacc, red, &last_cta);
 }
@@ -1524,14 +1544,21 @@ int launch_step_repair(const StepArgs& a, cudaStream_t s) {
 
 int launch_shard_p2p(const P2PArgs& a, cudaStream_t s) {
   if (a.G < 2 || a.G > kMaxP2PRanks) return fail(SAMO_E_PARAMETER, "peer-to-peer exchange supports 2..8 ranks");
-  const uint64_t nv = (a.k1 > a.k0) ? (a.k1 - a.k0 + 7) / 8 : 0;
+  const bool serial = a.bucket < 0;  // alone on the GPU (else overlapped with the expand)
+  const uint64_t ve = serial ? 4 : 8;
+  const uint64_t nv = (a.k1 > a.k0) ? (a.k1 - a.k0 + ve - 1) / ve : 0;
   const uint64_t cap = a.grid > 0 ? a.grid : static_cast<uint64_t>(num_sms()) * SAMO_P2P_GRID;
   const int grid = static_cast<int>(
       std::max<uint64_t>(1, std::min<uint64_t>(cap, (nv + kThreads - 1) / kThreads)));
-#define SAMO_SHARD_CASE(GG)                                                   \
-  case GG:                                                                    \
-    if (a.push) k_shard_p2p<GG, true><<<grid, kThreads, 0, s>>>(a);           \
-    else k_shard_p2p<GG, false><<<grid, kThreads, 0, s>>>(a);                 \
+#define SAMO_SHARD_CASE(GG)                                                                \
+  case GG:                                                                                 \
+    if (serial) {                                                                          \
+      if (a.push) k_shard_p2p<GG, true, 4><<<grid, kThreads, 0, s>>>(a);                   \
+      else k_shard_p2p<GG, false, 4><<<grid, kThreads, 0, s>>>(a);                         \
+    } else {                                                                               \
+      if (a.push) k_shard_p2p<GG, true, 8><<<grid, kThreads, 0, s>>>(a);                   \
+      else k_shard_p2p<GG, false, 8><<<grid, kThreads, 0, s>>>(a);                         \
+    }                                                                                      \
     break;
   switch (a.G) {
     SAMO_SHARD_CASE(2)
