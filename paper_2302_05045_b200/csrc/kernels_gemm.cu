@@ -23,11 +23,12 @@
 //   warp 1      TMEM allocation; MMA issue by one lane of the leader CTA
 //   warps 2..5  epilogue: tcgen05.ld (32 lanes x 32 columns per load), in two
 //               128-column halves; each thread owns one accumulator row
-// Long K uses 512 x 256 pair tiles (MS = 2, both accumulators in TMEM) where
-// they fill the waves; see launch_dw_gemm.  Measured (tools/bench_dw.py,
-// DESIGN.md §7c): 1.0-1.41 PFLOP/s on the GPT-2.7B layer shapes at 4096-8192
-// tokens, 70-95% of cuBLAS; the fused sink is within +-10% of the dense GEMM
-// followed by the K1 gather.
+// Long K uses 512 x 256 pair tiles (MS = 2, both accumulators in TMEM) or
+// 256 x 384 ones (BN = 384) where they fill the waves better; see
+// launch_dw_gemm.  Measured (tools/bench_dw.py): 1.09-1.39
+// PFLOP/s on the GPT-2.7B layer shapes at 4096-8192 tokens, 77-97% of
+// cuBLAS; the fused sink is within +-5% of the dense GEMM followed by the K1
+// gather.
 #include "kernels.cuh"
 
 #include <cuda.h>
@@ -223,12 +224,22 @@ struct GemmSmem {
 // operand bytes per flop, the bound of the MS = 1 form at 256 x 256, DESIGN
 // §7c).  Both accumulators fill the 512 TMEM columns, so there is one
 // buffer and the epilogue does not overlap the next tile's mainloop.
+// BN = 384 (MS = 1): a 256 x 384 pair tile, issued as two MMAs per k-step
+// that share the A operand — N = 128 (each SM holds 64 dY columns: one box)
+// then N = 256 (128 columns: two boxes) — so each SM's B is three whole
+// 64-column boxes and TMEM column c is output column n0 + c.  384 columns
+// leave no room for a second buffer: like MS = 2 the epilogue does not
+// overlap.  It fills the waves where neither 256-wide form does (2560 x 2560:
+// 70 tiles on 74 pairs against 50 or 100), at 40 KB of fill per SM and
+// k-block for 1.5x the MMAs of a 256 x 256 tile.
 template <int EPI, int BN, int NS, int EW, int MS>
 __global__ void __launch_bounds__(gemm_threads(EW), 1)
     k_dw_gemm(const __grid_constant__ CUtensorMap tx, const __grid_constant__ CUtensorMap tdy, DwArgs a) {
   using L = GemmSmem<BN, NS, EW, MS>;
   static_assert(MS == 1 || MS == 2, "one or two M sub-tiles");
-  constexpr uint32_t NBUF = MS == 1 ? 2 : 1;  // accumulator buffers
+  static_assert(BN == 256 || (BN == 384 && MS == 1), "256-wide tiles, or the 384-wide form with MS = 1");
+  constexpr bool kWide = BN == 384;
+  constexpr uint32_t NBUF = (MS == 1 && !kWide) ? 2 : 1;  // accumulator buffers
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ __align__(8) uint64_t full[NS];
   __shared__ __align__(8) uint64_t empty[NS];
@@ -244,8 +255,8 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
   const uint32_t tail0 = a.tail0 < ntiles ? a.tail0 : ntiles;
   const uint32_t nunits = tail0 + 2 * (ntiles - tail0);
   const uint32_t crank = cluster_ctarank(), cid = cluster_id_x(), ncl = ncluster_x();
-  constexpr uint32_t kCols = NBUF * MS * BN;
-  static_assert(kCols == 256 || kCols == 512, "TMEM allocation must be a power of two");
+  constexpr uint32_t kCols = NBUF * MS * BN <= 256 ? 256 : 512;  // a power of two
+  static_assert(NBUF * MS * BN <= 512, "accumulators exceed TMEM");
   uint8_t* ring = smem + EW * L::kTile;
   if (threadIdx.x == 0 && (smem_addr(ring) & 1023u)) __trap();  // swizzle atoms need 1024-byte alignment
 
@@ -279,6 +290,8 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
         const DwUnit t = dw_unit<BN>(u, tail0, mp);
         const int n0 = static_cast<int>(t.n0 + crank * (t.width / 2));  // my half of the columns
         const uint32_t boxes = t.width / 128;                          // 64-column dY boxes per CTA
+        // wide form: my 64 columns of the N = 128 MMA, then my 128 of the N = 256 one
+        const int nb0 = static_cast<int>(t.n0 + crank * 64), nb1 = static_cast<int>(t.n0 + 128 + crank * 128);
         for (uint32_t kb = 0; kb < nk; ++kb, ++g) {
           const uint32_t s = g % NS;
           if (g >= static_cast<uint32_t>(NS)) mbar_wait_bounded(&empty[s], ((g / NS) - 1) & 1u);
@@ -292,13 +305,20 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
             tma_load_2d_pair(st + 2 * j * kBox, &tx, m0, kc, fb);
             tma_load_2d_pair(st + (2 * j + 1) * kBox, &tx, m0 + 64, kc, fb);
           }
-          for (uint32_t c = 0; c < boxes; ++c) tma_load_2d_pair(st + L::kA + c * kBox, &tdy, n0 + 64 * c, kc, fb);
+          if constexpr (kWide) {
+            tma_load_2d_pair(st + L::kA, &tdy, nb0, kc, fb);
+            tma_load_2d_pair(st + L::kA + kBox, &tdy, nb1, kc, fb);
+            tma_load_2d_pair(st + L::kA + 2 * kBox, &tdy, nb1 + 64, kc, fb);
+          } else {
+            for (uint32_t c = 0; c < boxes; ++c) tma_load_2d_pair(st + L::kA + c * kBox, &tdy, n0 + 64 * c, kc, fb);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && crank == 0) {  // ---- MMA issue (leader)
-      constexpr uint32_t idesc_full = umma_idesc<2 * kBM, BN>(), idesc_half = umma_idesc<2 * kBM, BN / 2>();
+      constexpr uint32_t idesc_full = umma_idesc<2 * kBM, kWide ? 256 : BN>(),
+                         idesc_half = umma_idesc<2 * kBM, kWide ? 128 : BN / 2>();
       uint32_t g = 0, i = 0;
       for (uint32_t u = cid; u < nunits; u += ncl, ++i) {
         const uint32_t idesc = u < tail0 ? idesc_full : idesc_half;
@@ -313,11 +333,19 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
           const uint32_t sa = smem_addr(ring + s * L::kStage), sb = sa + L::kA;
 #pragma unroll
           for (uint32_t kk = 0; kk < kBK / 16; ++kk) {  // UMMA_K = 16: 16 K-rows of 128 bytes
-            const uint64_t db = umma_desc_mn_sw128(sb + kk * 2048, kBox, 1024);
+            if constexpr (kWide) {  // columns [0, 128) from box 0, [128, 384) from boxes 1-2
+              const uint64_t da = umma_desc_mn_sw128(sa + kk * 2048, kBox, 1024);
+              umma_f16_pair(acc, da, umma_desc_mn_sw128(sb + kk * 2048, kBox, 1024), idesc_half,
+                            (kb | kk) != 0u);
+              umma_f16_pair(acc + 128, da, umma_desc_mn_sw128(sb + kBox + kk * 2048, kBox, 1024), idesc_full,
+                            (kb | kk) != 0u);
+            } else {
+              const uint64_t db = umma_desc_mn_sw128(sb + kk * 2048, kBox, 1024);
 #pragma unroll
-            for (uint32_t j = 0; j < static_cast<uint32_t>(MS); ++j) {
-              const uint64_t da = umma_desc_mn_sw128(sa + 2 * j * kBox + kk * 2048, kBox, 1024);
-              umma_f16_pair(acc + j * BN, da, db, idesc, (kb | kk) != 0u);
+              for (uint32_t j = 0; j < static_cast<uint32_t>(MS); ++j) {
+                const uint64_t da = umma_desc_mn_sw128(sa + 2 * j * kBox + kk * 2048, kBox, 1024);
+                umma_f16_pair(acc + j * BN, da, db, idesc, (kb | kk) != 0u);
+              }
             }
           }
           umma_commit_pair_mc(&empty[s], 0x3);  // frees the stage in both CTAs
@@ -555,14 +583,27 @@ int launch_dw_gemm(const uint16_t* x, const uint16_t* dy, const DwArgs& a, int e
   const double fill2 = static_cast<double>(t2) / static_cast<double>(((t2 + P - 1) / P) * P);
   const bool auto2 = (fill2 >= 0.85 && nkb >= 48) || (t2 <= P && t1 > P);
   const int ms_env = env_on("SAMO_DW_MS", 0);
-  const int ms = short_k ? 1 : (ms_env == 1 || ms_env == 2) ? ms_env : (auto2 ? 2 : 1);
+  // ms 3: the 256 x 384 pair tile.  Taken when its waves cost less than the
+  // form picked above, in units of a 256 x 256 tile-time: MS = 2 tiles are 2
+  // units, MS = 1 tiles 1 unit at 0.91 of MS = 2's rate (a split tail half
+  // a wave), 384-wide tiles 1.5 units at 0.93 (measured rates).
+  // Interleaved A/B: -10% on qkv (2560 x 7680), -9% on attn out (2560 x 2560),
+  // never chosen where it lost (SAMO_DW_MS=3 forces it).
+  const uint64_t t3 = ((a.M + 2 * kBM - 1) / (2 * kBM)) * ((a.N + 383) / 384);
+  const bool tail_on = env_on("SAMO_DW_TAIL", 1) != 0;
+  const uint64_t r1 = t1 % P;
+  const double cost1 = (static_cast<double>(t1 / P) + (r1 ? (2 * r1 <= P && tail_on ? 0.5 : 1.0) : 0.0)) / 0.91;
+  const double cost2 = static_cast<double>((t2 + P - 1) / P) * 2.0;
+  const double cost3 = static_cast<double>((t3 + P - 1) / P) * 1.5 / 0.93;
+  int ms = short_k ? 1 : (ms_env >= 1 && ms_env <= 3) ? ms_env : (auto2 ? 2 : 1);
+  if (!short_k && ms_env == 0 && cost3 < (ms == 2 ? cost2 : cost1)) ms = 3;
   // Tail split (MS = 1): a last partial wave of r tiles with 2r <= #pairs
   // runs as 2r half tiles (SAMO_DW_TAIL=0 turns it off, for A/B).
-  const uint64_t tiles = ms == 2 ? t2 : t1;
+  const uint64_t tiles = ms == 2 ? t2 : ms == 3 ? t3 : t1;
   const uint64_t r = tiles % P;
   DwArgs args = a;
   args.tail0 = static_cast<uint32_t>(tiles);
-  if (ms == 1 && r > 0 && 2 * r <= P && env_on("SAMO_DW_TAIL", 1) != 0) args.tail0 = static_cast<uint32_t>(tiles - r);
+  if (ms == 1 && r > 0 && 2 * r <= P && tail_on) args.tail0 = static_cast<uint32_t>(tiles - r);
   const uint64_t units = args.tail0 + 2 * (tiles - args.tail0);
   const int grid = 2 * static_cast<int>(std::min<uint64_t>(units, P));
   using F = void (*)(CUtensorMap, CUtensorMap, DwArgs);
@@ -579,6 +620,16 @@ int launch_dw_gemm(const uint16_t* x, const uint16_t* dy, const DwArgs& a, int e
     smem = GemmSmem<kGemmBN, kGemmNS, 1>::kBytes;
     threads = gemm_threads(1);
     variant = 1;
+  } else if (ms == 3 && env_on("SAMO_DW_W_EW", 2) != 2) {
+    fn = epi == 0 ? k_dw_gemm<0, 384, 4, 1, 1> : k_dw_gemm<1, 384, 4, 1, 1>;
+    smem = GemmSmem<384, 4, 1, 1>::kBytes;
+    threads = gemm_threads(1);
+    variant = 4;
+  } else if (ms == 3) {
+    fn = epi == 0 ? k_dw_gemm<0, 384, 3, 2, 1> : k_dw_gemm<1, 384, 3, 2, 1>;
+    smem = GemmSmem<384, 3, 2, 1>::kBytes;
+    threads = gemm_threads(2);
+    variant = 5;
   } else if (env_on("SAMO_DW_MS2_EW", 2) != 2) {
     fn = epi == 0 ? k_dw_gemm<0, kGemmBN, 4, 1, 2> : k_dw_gemm<1, kGemmBN, 4, 1, 2>;
     smem = GemmSmem<kGemmBN, 4, 1, 2>::kBytes;
@@ -591,7 +642,7 @@ int launch_dw_gemm(const uint16_t* x, const uint16_t* dy, const DwArgs& a, int e
     variant = 3;
   }
   // The shared-memory opt-in is per device: remember it per (device, kernel).
-  static bool attr_set[64][8] = {};
+  static bool attr_set[64][16] = {};
   int dev = 0;
   SAMO_CUDA_TRY(cudaGetDevice(&dev));
   const int slot = (epi != 0) + 2 * variant;

@@ -74,10 +74,12 @@ def test_dw_gemm_vs_reference(S, oracle, batch, n_in, n_out):
 
 
 # Long-K shapes under each launch form (the launcher reads the knobs on every
-# call): MS = 1 / 2 (256 x 256 or 512 x 256 pair tiles), with and without
-# the tail-wave split; ragged M (520: a partly out-of-range sub-tile) and N.
+# call): MS = 1 / 2 / 3 (256 x 256, 512 x 256 or 256 x 384 pair tiles), with
+# and without the tail-wave split; ragged M (520: a partly out-of-range
+# sub-tile) and N (8, 1032: out-of-range dY boxes in the 384-wide form).
 FORMS = [{"SAMO_DW_MS": "1", "SAMO_DW_TAIL": "1"}, {"SAMO_DW_MS": "1", "SAMO_DW_TAIL": "0"},
-         {"SAMO_DW_MS": "2"}, {"SAMO_DW_MS": "2", "SAMO_DW_MS2_EW": "1"}]
+         {"SAMO_DW_MS": "2"}, {"SAMO_DW_MS": "2", "SAMO_DW_MS2_EW": "1"},
+         {"SAMO_DW_MS": "3"}, {"SAMO_DW_MS": "3", "SAMO_DW_W_EW": "1"}]  # 3: the 256 x 384 pair tile
 LONG_K = [(1100, 256, 384), (1100, 520, 1032), (1100, 2560, 2560), (3000, 136, 8)]
 
 

@@ -1,8 +1,9 @@
-"""A/B of a dW GEMM launch knob (an environment variable the launcher reads
-on every call, e.g. SAMO_DW_MS, SAMO_DW_TAIL) in one process, interleaved
-over rounds so clocks affect both alike.
+"""A/B of dW GEMM launch knobs (environment variables the launcher reads on
+every call, e.g. SAMO_DW_MS, SAMO_DW_TAIL) in one process, interleaved over
+rounds so clocks affect every variant alike; cuBLAS (x.T @ dy) alongside.
+Each argument is one variant: space-separated NAME=VALUE assignments.
 
-    python tools/ab_dw_env.py SAMO_DW_MS 2 1
+    python tools/ab_dw_env.py "SAMO_DW_MS=2" "SAMO_DW_MS=1" "SAMO_DW_MS=3 SAMO_DW_W_EW=1"
 """
 from __future__ import annotations
 
@@ -21,22 +22,27 @@ EXTRA = [(4096, 2048, 2048), (4096, 2048, 8192), (4096, 8192, 2048), (2048, 4096
 
 
 def main():
-    var, a, b = sys.argv[1], sys.argv[2], sys.argv[3]
+    variants = sys.argv[1:]
+    keys = sorted({kv.split("=")[0] for v in variants for kv in v.split()})
     torch.manual_seed(0)
     for batch, n_in, n_out in SHAPES + EXTRA:
         x = (torch.rand(batch, n_in, device="cuda") * 2 - 1).half()
         dy = (torch.rand(batch, n_out, device="cuda") * 2 - 1).half()
-        best = {a: float("inf"), b: float("inf")}
+        best = {v: float("inf") for v in variants + ["cublas"]}
         for _ in range(5):
-            for t in (a, b):
-                os.environ[var] = t
-                best[t] = min(best[t], timed(lambda: samo.dw_gemm(x, dy), 20))
+            for v in variants:
+                for k in keys:
+                    os.environ.pop(k, None)
+                for kv in v.split():
+                    k, val = kv.split("=")
+                    os.environ[k] = val
+                best[v] = min(best[v], timed(lambda: samo.dw_gemm(x, dy), 20))
+            best["cublas"] = min(best["cublas"], timed(lambda: torch.matmul(x.t(), dy), 20))
         fl = 2.0 * batch * n_in * n_out
-        tiles = ((n_in + 255) // 256) * ((n_out + 255) // 256)
-        print(json.dumps({"shape": [batch, n_in, n_out], "tiles256": tiles, var: [a, b],
-                          "ms": [round(best[a], 4), round(best[b], 4)],
-                          "tflops": [round(fl / best[a] / 1e9, 1), round(fl / best[b] / 1e9, 1)],
-                          "t_b_over_t_a_minus_1": round(best[b] / best[a] - 1, 3)}), flush=True)
+        print(json.dumps({"shape": [batch, n_in, n_out],
+                          "ms": {v: round(t, 4) for v, t in best.items()},
+                          "of_cublas": {v: round(best["cublas"] / t, 3) for v, t in best.items() if v != "cublas"},
+                          "tflops": {v: round(fl / t / 1e9, 1) for v, t in best.items()}}), flush=True)
 
 
 if __name__ == "__main__":
