@@ -78,18 +78,85 @@ def peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+    """SM / memory clocks and throttle reasons of rank 0's GPU through NVML
+    in-process (the nvidia_ml_py binding): clocks and reasons just before the
+    timed region and just after it; in it, the clocks right after its steps
+    are queued (the GPU is then still running them) and every 0.5 s.  Every clock query stalls
+    the GPU for a few ms, which the tightly coupled data-parallel step pays on
+    every rank: at N = 4 over 50 steps, 2.82-2.85 ms unsampled against
+    2.95-3.57 ms with a 100 ms NVML sampler, 2.87-3.08 with one nvidia-smi per
+    rank at 100 ms and 4.07-4.28 with one nvidia-smi over all GPUs at 200 ms
+    (profiles/r02z_n4_sampler_*.log).  SAMO_BENCH_CLOCKS: nvml
+    (default), smi (nvidia-smi at 100 ms, for A/B), nvml_sm / nvml_reasons /
+    nvml_power (query subsets), off."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_power_cap,clocks.mem")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
-    def __init__(self, gpu_index: str):
+    def __init__(self, gpu_index):
         self.gpu = gpu_index
+        self.mode = os.environ.get("SAMO_BENCH_CLOCKS", "nvml")
         self.proc = None
-        self.lines: list[str] = []
+        self.lines: list[str] = []          # nvidia-smi rows (smi mode)
+        self.samples: list[tuple] = []      # (sm, sm_max, mem, power or None, reasons)
+        self._stop = threading.Event()
+        self._t = None
+        self.in_region = 0
+
+    def __len__(self):
+        return len(self.samples) + len(self.lines)
+
+    # -- NVML in-process ------------------------------------------------------
+    def _nvml_sample(self, with_reasons: bool = True):
+        import pynvml as N
+        h = self._h
+        reasons = set()
+        if with_reasons and self.mode != "nvml_sm":
+            bits = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+            flags = (N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
+                     N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap)
+            reasons = {nm for nm, f in zip(self.NAMES, flags) if bits & f}
+        power = N.nvmlDeviceGetPowerUsage(h) / 1000.0 if self.mode == "nvml_power" else None
+        sm = float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)) if self.mode != "nvml_reasons" else self._max
+        mem = float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_MEM)) if self.mode == "nvml" else None
+        self.samples.append((sm, self._max, mem, power, reasons))
+
+    def sample_now(self):
+        """One clock sample now (call once the timed steps are queued).  The
+        throttle-reason query stalls the GPU longest, so in-region samples
+        read the clocks only; the reasons come from the samples taken just
+        before and just after the region."""
+        if self._t is not None and self.mode.startswith("nvml"):
+            try:
+                self._nvml_sample(with_reasons=False)
+                self.in_region += 1
+            except Exception:  # noqa: BLE001
+                pass
+
+    def _nvml_loop(self):
+        while not self._stop.wait(0.5):
+            try:
+                self._nvml_sample(with_reasons=False)
+            except Exception:  # noqa: BLE001  (a failed read only loses a sample)
+                pass
 
     def __enter__(self):
+        if self.gpu is None or self.mode == "off":
+            return self
+        if self.mode.startswith("nvml"):
+            try:
+                import pynvml as N
+                N.nvmlInit()
+                self._h = N.nvmlDeviceGetHandleByIndex(int(self.gpu))
+                self._max = float(N.nvmlDeviceGetMaxClockInfo(self._h, N.NVML_CLOCK_SM))
+                self._nvml_sample()  # NVML is up before the caller starts its clock
+                self._t = threading.Thread(target=self._nvml_loop, daemon=True)
+                self._t.start()
+            except Exception:  # noqa: BLE001  (no NVML: no clocks)
+                self._t = None
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", self.gpu, f"--query-gpu={self.FIELDS}",
@@ -97,6 +164,11 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
+            # nvidia-smi's start-up: let it finish (first sample in) before the
+            # caller starts its clock
+            t_end = time.perf_counter() + 3.0
+            while not self.lines and self.proc.poll() is None and time.perf_counter() < t_end:
+                time.sleep(0.01)
         except OSError:
             self.proc = None
         return self
@@ -105,33 +177,56 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def active(self) -> bool:
+        return self._t is not None
+
     def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None and self.mode.startswith("nvml"):
+            self._t.join(timeout=1.0)
+            try:
+                self._nvml_sample()  # reasons right after the region
+            except Exception:  # noqa: BLE001
+                pass
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        elif self._t is not None:
+            self._t.join(timeout=1.0)
 
     def summary(self) -> dict:
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = list(self.samples)
         for ln in self.lines:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 7:
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
+                sm, mx = float(parts[0]), float(parts[1])
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+            reasons = {nm for nm, v in zip(self.NAMES, parts[3:7]) if v.lower().startswith("active")}
+            vals = []
+            for v in (parts[7] if len(parts) > 7 else "", parts[2]):
+                try:
+                    vals.append(float(v))
+                except ValueError:
+                    vals.append(None)
+            rows.append((sm, mx, vals[0], vals[1], reasons))
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "source": self.mode}
+        out = {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+               "reasons": sorted(set().union(*(r[4] for r in rows))), "samples": len(rows),
+               "source": f"{self.mode}, rank 0's GPU", "samples_in_region": self.in_region}
+        mem = [r[2] for r in rows if r[2] is not None]
+        pw = [r[3] for r in rows if r[3] is not None]
+        if mem:
+            out["mem_mhz"] = statistics.median(mem)
+        if pw:
+            out["power_w_max"] = max(pw)
+        return out
 
 
 def gpt_blocks_of(wl):
@@ -588,7 +683,23 @@ def run_samo(args) -> None:
     gpu_name = torch.cuda.get_device_properties(dev).name
     smi_index = os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local] \
         if os.environ.get("CUDA_VISIBLE_DEVICES") else str(local)
+    # The same K steps timed once without any clock sampling first: every NVML
+    # clock query stalls the GPU for a few ms (ClockSampler), which the timed
+    # region below pays; this figure shows by how much (diagnostic only).
     if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    u0, u1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    u0.record()
+    for s in range(K):
+        model.step(graph=args.graph) if world == 1 else model.step()
+    u1.record()
+    torch.cuda.synchronize()
+    unsampled_ms = u0.elapsed_time(u1)
+    if world > 1:
+        ut = torch.tensor([unsampled_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(ut, op=dist.ReduceOp.MAX)
+        unsampled_ms = float(ut.item())
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = samo.kernel_launch_count()
@@ -600,7 +711,7 @@ def run_samo(args) -> None:
             nvl0 = nvl.read()
         except Exception as ex:  # noqa: BLE001  (no NVML counter: reported as unavailable)
             nvl, nvl0 = None, str(ex)
-    with ClockSampler(smi_index) as clk:
+    with ClockSampler(smi_index if rank == 0 else None) as clk:
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
         t0.record()
@@ -615,12 +726,14 @@ def run_samo(args) -> None:
             for s in range(K):
                 model.step()
         t1.record()
+        clk.sample_now()  # the queued steps are still running
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         # keep sampling a little longer so short regions still get clock samples
-        if len(clk.lines) < 3:
-            time.sleep(0.35)
+        t_end = time.perf_counter() + 1.0
+        while clk.active() and len(clk) < 3 and time.perf_counter() < t_end:
+            time.sleep(0.05)
     launches = samo.kernel_launch_count() - launches0
     total_ms = t0.elapsed_time(t1)
     nvlink_measured = None
@@ -976,6 +1089,10 @@ def run_samo(args) -> None:
             "fused_dw_sink": fused,
             "fc_sweep": fc_sweep,
             "clocks": clk.summary(),
+            "unsampled": {"ms_per_step": unsampled_ms / K,
+                          "note": "the same steps timed just before, with no clock sampling (each NVML "
+                                  "clock query stalls the GPU for a few ms; the headline keeps the sampled "
+                                  "region, DESIGN §6)"},
             "step_record": {"t": int(rec.t), "skipped": int(rec.skipped_steps),
                             "grad_norm": float(rec.grad_norm)},
             "setup": {"seconds": setup_s, "k0_prune_ms": prune_ms,
