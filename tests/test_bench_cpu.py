@@ -51,6 +51,26 @@ def test_numa_binding_is_a_no_op_without_nvml(monkeypatch):
     assert os.sched_getaffinity(0) == before
 
 
+def test_clock_sampler_summaries(monkeypatch):
+    """The clocks object: off / non-zero ranks sample nothing; nvidia-smi rows
+    and NVML samples reduce to the contract's keys, reasons as a union."""
+    monkeypatch.setenv("SAMO_BENCH_CLOCKS", "off")
+    with bench.ClockSampler("0") as clk:
+        pass
+    assert not clk.active() and clk.summary()["samples"] == 0
+    with bench.ClockSampler(None) as clk:  # ranks other than 0
+        clk.sample_now()
+    assert clk.summary()["samples"] == 0 and clk.in_region == 0
+    clk = bench.ClockSampler("0")
+    clk.lines = ["1965, 1965, 350.5, Not Active, Not Active, Not Active, Active, 3996",
+                 "1950, 1965, 360.0, Not Active, Not Active, Not Active, Not Active, 3996", "garbage"]
+    clk.samples = [(1965.0, 1965.0, 3996.0, None, {"hw_slowdown"})]
+    s = clk.summary()
+    assert s["sm_mhz"] == 1965.0 and s["sm_max_mhz"] == 1965.0 and s["samples"] == 3
+    assert s["reasons"] == ["hw_slowdown", "sw_power_cap"]
+    assert s["mem_mhz"] == 3996.0 and s["power_w_max"] == 360.0
+
+
 @pytest.mark.skipif(not _ref_built(), reason="oracle/_ref not built")
 def test_reference_arm_prints_one_json_line():
     res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "1",
