@@ -656,6 +656,12 @@ static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather
   return SAMO_OK;
 }
 
+// Sets the caller's device back on every return path (multi-device groups).
+struct RestoreDevice {
+  int dev;
+  ~RestoreDevice() { cudaSetDevice(dev); }
+};
+
 // One step of every rank of a local group, queued phase by phase on one
 // stream: each rank's waits (flag, buckets) find their signals already
 // written, so no kernel spins on another that is queued behind it.
@@ -669,6 +675,7 @@ static int step_local_group(samo_model* const* models, int G, bool gather, cudaS
   const bool multi = models[0]->group_dev >= 0;
   int dev0 = 0;
   SAMO_CUDA_TRY(cudaGetDevice(&dev0));
+  const RestoreDevice restore{dev0};
   auto on = [&](int r) -> cudaStream_t {
     if (!multi) return S;
     cudaSetDevice(models[r]->group_dev);
@@ -699,9 +706,7 @@ static int step_local_group(samo_model* const* models, int G, bool gather, cudaS
   for (int r = 0; r < G; ++r) SAMO_TRY(p2p_expand(models[r], sp[r], on(r)));
   SAMO_TRY(phase_end());
   for (int r = 0; r < G; ++r) SAMO_TRY(p2p_finish(models[r], sp[r], on(r)));
-  SAMO_TRY(phase_end());
-  if (multi) SAMO_CUDA_TRY(cudaSetDevice(dev0));
-  return SAMO_OK;
+  return phase_end();
 }
 
 extern "C" {
@@ -740,6 +745,7 @@ int samo_model_attach_local_group(samo_model* const* models, int G) {
     multi = multi || pa.device != dev;
   }
   if (multi) {  // one model per device, every pair of devices peer-capable
+    const RestoreDevice restore{dev};
     for (int r = 0; r < G; ++r)
       for (int q = 0; q < G; ++q) {
         if (q == r) continue;
@@ -757,7 +763,6 @@ int samo_model_attach_local_group(samo_model* const* models, int G) {
       models[r]->group_dev = devs[r];
       if (!models[r]->s_group) SAMO_CUDA_TRY(cudaStreamCreateWithFlags(&models[r]->s_group, cudaStreamNonBlocking));
     }
-    SAMO_CUDA_TRY(cudaSetDevice(dev));
   }
   for (int r = 0; r < G; ++r) {
     samo_model* md = models[r];
