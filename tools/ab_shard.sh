@@ -1,6 +1,12 @@
 #!/bin/bash
 # A/B of k_shard_p2p builds (ab_shard/lib_*.so) at NGPU ranks:
 # ms/step and the serial phase breakdown per run, alternating libraries.
+# A variant library: compile csrc/kernels_fused.cu with the build.py flags
+# plus its -D settings, then link it with the other in-tree objects, e.g.
+#   nvcc <build.py NVCC_FLAGS> -DX=1 -I include -I csrc -c csrc/kernels_fused.cu -o /tmp/kf_X.o
+#   nvcc -gencode arch=compute_100a,code=sm_100a -shared -o ab_shard/lib_X.so \
+#        $(ls build/*.o | grep -v kernels_fused) /tmp/kf_X.o -lnccl -cudart static
+# VARIANTS="A B:SAMO_P2P_SHARD_CTAS=4" runs lib_A, then lib_B with that env.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 N=${NGPU:-2}
