@@ -26,7 +26,7 @@
 // Long K uses 512 x 256 pair tiles (MS = 2, both accumulators in TMEM) or
 // 256 x 384 ones (BN = 384) where they fill the waves better; see
 // launch_dw_gemm.  Measured (tools/bench_dw.py): 1.09-1.39
-// PFLOP/s on the GPT-2.7B layer shapes at 4096-8192 tokens, 77-97% of
+// PFLOP/s on the GPT-2.7B layer shapes at 4096-8192 tokens, 77-102% of
 // cuBLAS; the fused sink is within +-5% of the dense GEMM followed by the K1
 // gather.
 #include "kernels.cuh"
@@ -388,17 +388,20 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
             cnt = a.kb[(cb + 1) * a.M + row] - ks;
           }
         }
-        // accumulator half -> binary16 -> staging row r: the four 32-column
-        // loads of the half are in flight together, one wait
-        {
-          uint32_t v[L::kHalf / 32][32];
+        // accumulator half -> binary16 -> staging row r: kLd 32-column loads
+        // in flight together, one wait (4 = the whole half; 2 with three
+        // epilogue groups, whose 448 threads get at most 128 registers)
+        constexpr uint32_t kLd = EW >= 3 ? 2 : 4;
 #pragma unroll
-          for (uint32_t cc = 0; cc < L::kHalf / 32; ++cc)
-            tmem_ld32_nowait(tmem + ((q * 32u) << 16) + tcol + h * L::kHalf + cc * 32, v[cc]);
+        for (uint32_t c0 = 0; c0 < L::kHalf / 32; c0 += kLd) {
+          uint32_t v[kLd][32];
 #pragma unroll
-          for (uint32_t cc = 0; cc < L::kHalf / 32; ++cc) {
+          for (uint32_t cc = 0; cc < kLd; ++cc)
+            tmem_ld32_nowait(tmem + ((q * 32u) << 16) + tcol + h * L::kHalf + (c0 + cc) * 32, v[cc]);
+#pragma unroll
+          for (uint32_t cc = 0; cc < kLd; ++cc) {
             tmem_wait32(v[cc]);
-            uint4* dst = reinterpret_cast<uint4*>(tile + r * L::kTileLd + cc * 32);
+            uint4* dst = reinterpret_cast<uint4*>(tile + r * L::kTileLd + (c0 + cc) * 32);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               uint32_t w[4];
@@ -620,7 +623,15 @@ int launch_dw_gemm(const uint16_t* x, const uint16_t* dy, const DwArgs& a, int e
     smem = GemmSmem<kGemmBN, kGemmNS, 1>::kBytes;
     threads = gemm_threads(1);
     variant = 1;
-  } else if (ms == 3 && env_on("SAMO_DW_W_EW", 2) != 2) {
+  } else if (ms == 3 && env_on("SAMO_DW_W_EW", 3) == 3) {
+    // three epilogue groups, one 128-column half each: the one-buffer
+    // epilogue drains in a third of the time (interleaved A/B: +6% on qkv,
+    // +10% on attn out over two groups; SAMO_DW_W_EW=1/2 for A/B)
+    fn = epi == 0 ? k_dw_gemm<0, 384, 3, 3, 1> : k_dw_gemm<1, 384, 3, 3, 1>;
+    smem = GemmSmem<384, 3, 3, 1>::kBytes;
+    threads = gemm_threads(3);
+    variant = 6;
+  } else if (ms == 3 && env_on("SAMO_DW_W_EW", 3) == 1) {
     fn = epi == 0 ? k_dw_gemm<0, 384, 4, 1, 1> : k_dw_gemm<1, 384, 4, 1, 1>;
     smem = GemmSmem<384, 4, 1, 1>::kBytes;
     threads = gemm_threads(1);

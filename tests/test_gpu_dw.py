@@ -79,7 +79,8 @@ def test_dw_gemm_vs_reference(S, oracle, batch, n_in, n_out):
 # sub-tile) and N (8, 1032: out-of-range dY boxes in the 384-wide form).
 FORMS = [{"SAMO_DW_MS": "1", "SAMO_DW_TAIL": "1"}, {"SAMO_DW_MS": "1", "SAMO_DW_TAIL": "0"},
          {"SAMO_DW_MS": "2"}, {"SAMO_DW_MS": "2", "SAMO_DW_MS2_EW": "1"},
-         {"SAMO_DW_MS": "3"}, {"SAMO_DW_MS": "3", "SAMO_DW_W_EW": "1"}]  # 3: the 256 x 384 pair tile
+         {"SAMO_DW_MS": "3"}, {"SAMO_DW_MS": "3", "SAMO_DW_W_EW": "1"},
+         {"SAMO_DW_MS": "3", "SAMO_DW_W_EW": "2"}]  # 3: the 256 x 384 pair tile (3 epilogue groups by default)
 LONG_K = [(1100, 256, 384), (1100, 520, 1032), (1100, 2560, 2560), (3000, 136, 8)]
 
 
