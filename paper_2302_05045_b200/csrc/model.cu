@@ -464,10 +464,10 @@ int samo_model_sink_dw(samo_model* md, int l, const uint16_t* x, const uint16_t*
     SAMO_TRY(launch_build_rowblocks(md->idx + md->k_off[l], md->nnz[l], in, out, md->dw_kb[l], s));
   }
   // Push mode: this rank's gradient arena is its receive buffer, which peers
-  // fill during their backward, and theta16c may still be read by a peer's
-  // expand of the previous step (pull mode): the epilogue gathers into a
-  // scratch arena of its own (2 n bytes, allocated on first use) and a copy
-  // pushes the layer to its owners.
+  // fill during their backward.  The epilogue gathers into a scratch arena
+  // of its own (2 n bytes, allocated on first use) rather than borrowing
+  // theta16c, so the sinks never touch the exchange's weight buffer, and a
+  // copy pushes the layer to its owners.
   const bool push = comm_size(md) > 1 && p2p_push();
   if (push) {
     SAMO_TRY(push_sink_prepare(md));
