@@ -656,11 +656,13 @@ static int step_p2p_pipelined(samo_model* md, cudaStream_t S, int B, bool gather
   return SAMO_OK;
 }
 
+namespace {
 // Sets the caller's device back on every return path (multi-device groups).
 struct RestoreDevice {
   int dev;
   ~RestoreDevice() { cudaSetDevice(dev); }
 };
+}  // namespace
 
 // One step of every rank of a local group, queued phase by phase on one
 // stream: each rank's waits (flag, buckets) find their signals already
